@@ -1,0 +1,343 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 parallel Boruvka MST (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1] [--impl ours|reference]
+
+One step = one complete MST of the configured synthetic graph (all rounds,
+sorted MST ids and total weight produced). Metric: graph edges/s =
+m / MST wall time (BASELINE.json), whole job over all ranks.
+
+* value: device-resident — edges already in HBM when the timed region
+  starts, ids left in HBM; CUDA events on the launching stream; L2 flushed
+  (a 512 MiB write) between timed steps; max over ranks.
+* e2e: the same MST through the public API with HOST (pinned) edge arrays:
+  H2D of src/dst/w and D2H of the sorted ids inside the timed region.
+* roofline: the edge-pass kernels (k_min_round1 + k_compact), algorithmic
+  bytes per SURVEY.md §8(d) (12 B/edge round 1, 16 B/live edge later,
+  +16 B/kept edge) over their CUDA-event time, against MEASURED_PEAKS.json.
+* cpu_baseline: the unchanged reference boruvka_cas (oracle/_ref) on the
+  host cores, rank 0 at N=1, on the same graph.
+
+--impl reference times the reference's own CPU implementation of the path
+(boruvka_cas through oracle/_ref, all host threads) on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "graph edges/sec (m / MST wall time)"
+UNIT = "edges/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default="c1", choices=["c0", "c1", "c2", "c3", "c4"])
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def peaks():
+    try:
+        d = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def hot_bytes(m: int, live_edges: list) -> int:
+    """Algorithmic bytes of the edge-pass kernels of one MST."""
+    b = 12 * m  # k_min_round1 reads (src, dst, w)
+    R = len(live_edges)
+    for r in range(1, R):  # k_compact(r) runs fully for r < rounds
+        m_r = live_edges[r - 1]
+        k_r = live_edges[r]
+        b += (12 if r == 1 else 16) * m_r + 16 * k_r
+    return b
+
+
+def reference_cpu(g, threads: int, runs: int):
+    """The unchanged reference boruvka_cas (oracle/_ref) on the host cores."""
+    from oracle import oracle as O
+
+    if not O.ref_available():
+        return None
+    times = []
+    res = None
+    for _ in range(runs):
+        res = O.ref_solve(g.n, g.src, g.dst, g.w, O.ALGO_CAS, threads=threads)
+        times.append(res.elapsed_ms)
+    return times, res
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+    from paper_2005_06913_b200 import configs as C
+
+    spec = C.CONFIGS[args.config]
+    g = C.generate_host(spec)
+    m = g.edge_count()
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libmstref.so not built"}))
+        return 0
+    threads = O.hardware_threads()
+    for _ in range(args.warmup):
+        O.ref_solve(g.n, g.src, g.dst, g.w, O.ALGO_CAS, threads=threads)
+    times = []
+    for _ in range(args.steps):
+        r = O.ref_solve(g.n, g.src, g.dst, g.w, O.ALGO_CAS, threads=threads)
+        times.append(r.elapsed_ms)
+    ms = float(np.mean(times))
+    value = m / (ms / 1e3)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded generator)",
+        "config": {"workload": spec.name, "n": g.n, "m": m, "seed": spec.seed,
+                   "path": "mst::boruvka_cas (unchanged reference, oracle/_ref) via SURVEY §8(c) adapter",
+                   "m_prime": r.m_prime, "timer": "reference MstResult::elapsed_ms"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"full {spec.name} graph, {args.steps} runs of boruvka_cas(T={threads})"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def run_ours(args):
+    import torch
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    import paper_2005_06913_b200 as P
+    from paper_2005_06913_b200 import configs as C
+    from paper_2005_06913_b200 import dist as D
+
+    spec = C.CONFIGS[args.config]
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    n, m, s_full, d_full, w_full = C.generate_torch(spec, device=f"cuda:{local}")
+    lo, hi = D.shard_range(m, rank, world)
+    s, d, w = s_full[lo:hi], d_full[lo:hi], w_full[lo:hi]
+    out = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    comm = D.RankComm.from_torch(local) if world > 1 else None
+
+    def one_step(info=None, hot=None):
+        if comm is None:
+            return P.boruvka_gpu_device(n, m, s.data_ptr(), d.data_ptr(), w.data_ptr(), out.data_ptr(),
+                                        stream.cuda_stream, info=info, hot=hot)
+        r = comm.boruvka_ptrs(n, m, lo, hi - lo, s.data_ptr(), d.data_ptr(), w.data_ptr(), True, info)
+        return len(r.mst_edges), r.total_weight
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    info = P.GpuRunInfo()
+    for _ in range(max(args.warmup, 3)):
+        one_step(info)
+    barrier()
+    step_ms, hot_ms, hot_launch, launches = [], 0.0, 0, 0
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        barrier()
+        for k in range(args.steps):
+            flush.zero_()
+            ev[k][0].record(stream)
+            hot = {} if comm is None else None
+            count, total = one_step(info, hot)
+            ev[k][1].record(stream)
+            if hot:
+                hot_ms += hot["ms"]
+                hot_launch += hot["launches"]
+            launches += info.kernel_launches
+        barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    t_local = float(np.sum(step_ms))
+    t = torch.tensor([t_local], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = m * args.steps / (total_ms / 1e3)
+
+    # ---- end to end through the public API with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        hs = torch.empty(hi - lo, dtype=torch.int32, pin_memory=True)
+        hd = torch.empty(hi - lo, dtype=torch.int32, pin_memory=True)
+        hw = torch.empty(hi - lo, dtype=torch.int32, pin_memory=True)
+        hs.copy_(s)
+        hd.copy_(d)
+        hw.copy_(w)
+        g = P.Graph(n, hs.numpy().view(np.uint32), hd.numpy().view(np.uint32), hw.numpy().view(np.uint32))
+        for _ in range(2):
+            (P.boruvka_gpu(g) if comm is None else comm.boruvka(n, m, lo, g.src, g.dst, g.w))
+        barrier()
+        e2e_t = []
+        for _ in range(args.steps):
+            flush.zero_()
+            barrier()
+            t0 = time.perf_counter()
+            r = P.boruvka_gpu(g) if comm is None else comm.boruvka(n, m, lo, g.src, g.dst, g.w)
+            e2e_t.append((time.perf_counter() - t0) * 1e3)
+        et = torch.tensor([float(np.sum(e2e_t))], dtype=torch.float64, device=dev)
+        if world > 1:
+            torch.distributed.all_reduce(et, op=torch.distributed.ReduceOp.MAX)
+        e2e = {"value": m * args.steps / (float(et.item()) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": 12 * (hi - lo), "d2h_bytes_per_step": 4 * len(r.mst_edges),
+               "ms_per_step": float(et.item()) / args.steps, "timer": "host wall clock around the call"}
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.barrier()
+            torch.distributed.destroy_process_group()
+        return 0
+
+    peak, peak_src = peaks()
+    roofline = None
+    if hot_launch:
+        per_mst = hot_bytes(m, info.live_edges)
+        achieved = per_mst * args.steps / (hot_ms / 1e3) / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": None,
+                    "kernel": "edge pass (k_min_round1 + k_compact), summed over rounds",
+                    "bytes_per_mst": per_mst, "launches_per_mst": hot_launch / args.steps,
+                    "kernel_ms_per_mst": hot_ms / args.steps, "peak_source": peak_src,
+                    "whole_mst_alg_bytes": info.alg_bytes,
+                    "whole_mst_frac": info.alg_bytes / (ms_per_step / 1e3) / 1e9 / peak}
+        tp = ROOT / "profiles" / "traffic.json"
+        if tp.exists():
+            try:
+                roofline["traffic"] = json.loads(tp.read_text()).get(args.config)
+            except Exception:
+                pass
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle import oracle as O
+            hg = g if e2e is not None else C.generate_host(spec)
+            threads = O.hardware_threads()
+            rr = reference_cpu(hg, threads, runs=1)
+            if rr is not None:
+                times, res = rr
+                cpu = {"value": m / (float(np.mean(times)) / 1e3), "unit": UNIT, "cores": threads,
+                       "kind": "reference",
+                       "sample": f"full {spec.name} graph, 1 run of unchanged boruvka_cas(T={threads}) "
+                                 f"(m'={res.m_prime} after the §8(c) adapter), reference elapsed_ms"}
+        except Exception as ex:  # reported, not fatal
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"failed: {ex}"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (seeded counter-based generator, BASELINE.json shape)",
+        "config": {"workload": spec.name, "n": n, "m": m, "seed": spec.seed,
+                   "rounds": info.rounds, "live_edges": info.live_edges, "live_comps": info.live_comps,
+                   "l2": "flushed (512 MiB write) between timed steps",
+                   "parallelism": f"edge-sharded x{world}" if world > 1 else "single GPU"},
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line))
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+    if comm is not None:
+        comm.close()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

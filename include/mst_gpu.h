@@ -1,0 +1,187 @@
+/*
+ * mst_gpu.h — C ABI of the B200-native parallel Boruvka MST (arXiv 2005.06913).
+ *
+ * This is the drop-in boundary for the reference's hot path
+ *   mst::boruvka_cas(Graph&, int, ParallelRunInfo*)
+ *     /root/reference/proj/include/mst/boruvka_parallel.hpp:70
+ *     /root/reference/proj/src/boruvka_parallel.cpp:85-291
+ * Plain pointers and sizes only; no C++ or torch types cross it. The C++
+ * wrapper with the reference's shape (Graph& in, MstResult out, exceptions)
+ * is include/mst/boruvka_gpu.hpp; the Python mirror is
+ * paper_2005_06913_b200/api.py. See INTEGRATION.md for the bindings.
+ *
+ * Types follow the reference: VertexId = uint32 (graph.hpp:12), EdgeId is
+ * int64 there (graph.hpp:13) and uint32 here (m < 2^32 - 1 is checked),
+ * Weight is uint64 there (graph.hpp:14) and uint32 here (checked at the AoS
+ * entry, which accepts the reference's 16-byte Edge directly).
+ *
+ * Result contract = mst::MstResult (mst_result.hpp:10-20): the MST edge ids
+ * sorted ascending, their total weight as uint64, the round count. Weights
+ * are expected to be distinct (the reference's build_graph contract,
+ * graph.cpp:118-125); on a single GPU ties are broken by lower edge id, which
+ * equals a stable Kruskal over (weight, id).
+ *
+ * Threading: calls are synchronous w.r.t. the host (like boruvka_cas) and
+ * may be made from several host threads on different devices. The last
+ * error string is thread-local.
+ */
+#ifndef MST_GPU_H_
+#define MST_GPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes. 0 = success. Mirrors the reference's error behaviour:
+ *   MST_ERR_INVALID_ARG  ~ std::invalid_argument (boruvka_parallel.cpp:86,
+ *                          graph.cpp:93)
+ *   MST_ERR_RANGE        ~ GraphError{EndpointOutOfRange} (graph.cpp:98-100)
+ *   MST_ERR_WEIGHT       weight does not fit the 32-bit device key
+ *   MST_ERR_DISCONNECTED ~ GraphError{Disconnected} (graph.cpp:127-134); the
+ *                          minimum spanning FOREST is still returned
+ *   MST_ERR_CUDA / _NCCL ~ WorkerPanic (boruvka_parallel.hpp:44-47)
+ */
+enum {
+  MST_OK = 0,
+  MST_ERR_INVALID_ARG = 1,
+  MST_ERR_RANGE = 2,
+  MST_ERR_WEIGHT = 3,
+  MST_ERR_DISCONNECTED = 4,
+  MST_ERR_CUDA = 5,
+  MST_ERR_NCCL = 6,
+  MST_ERR_NO_DEVICE = 7,
+  MST_ERR_OOM = 8,
+  MST_ERR_STALL = 9
+};
+
+#define MST_MAX_ROUNDS 48
+
+/* The reference's Edge, bit-for-bit (graph.hpp:41-45): 16 bytes. */
+typedef struct mst_edge {
+  uint32_t src;
+  uint32_t dest;
+  uint64_t weight;
+} mst_edge_t;
+
+/* SoA edge list: the device-native layout (12 bytes/edge). */
+typedef struct mst_edges_soa {
+  uint32_t n;            /* vertex count, >= 1 */
+  uint64_t m;            /* edge count, < 2^32 - 1 */
+  const uint32_t* src;   /* [m] */
+  const uint32_t* dst;   /* [m] */
+  const uint32_t* w;     /* [m] */
+  int on_device;         /* 1: pointers are device pointers on the run's GPU */
+} mst_edges_soa_t;
+
+/* Per-run statistics (ParallelRunInfo analogue, boruvka_parallel.hpp:52-56,
+ * plus the per-round counters the byte model of DESIGN.md needs). */
+typedef struct mst_stats {
+  uint32_t rounds;            /* Boruvka rounds (min-edge passes) */
+  uint32_t final_components;  /* 1 for a connected input */
+  double ms_total;            /* host wall time of the whole call */
+  double ms_device;           /* device time, first kernel .. result ready */
+  double ms_h2d;              /* host->device edge copy (0 for device input) */
+  double ms_d2h;              /* device->host result copy */
+  uint64_t alg_bytes;         /* algorithmic bytes over all rounds */
+  uint64_t live_edges[MST_MAX_ROUNDS]; /* m_r: live edges entering round r */
+  uint64_t live_comps[MST_MAX_ROUNDS]; /* n_r: live components in round r */
+  uint32_t kernel_launches;   /* kernels launched by this call */
+} mst_stats_t;
+
+/* Single-GPU (num_gpus == 1) or single-process multi-GPU (num_gpus in 2..8,
+ * devices 0..num_gpus-1 of the calling process, edge list sharded, one
+ * NCCL allreduce(min, uint64) per round). Device input requires
+ * num_gpus == 1 and pointers on the current CUDA device.
+ * out_ids must hold n-1 entries; they come back sorted ascending.
+ * out_count/out_total_weight/stats may be NULL. */
+int mst_gpu_boruvka(const mst_edges_soa_t* edges, int num_gpus, uint32_t* out_ids,
+                    uint64_t* out_count, uint64_t* out_total_weight, mst_stats_t* stats);
+
+/* Same, taking the reference's AoS Edge array unchanged (16 B/edge). Weights
+ * >= 2^32 give MST_ERR_WEIGHT. Single GPU. */
+int mst_gpu_boruvka_aos(uint32_t n, uint64_t m, const mst_edge_t* edges, int on_device,
+                        uint32_t* out_ids, uint64_t* out_count, uint64_t* out_total_weight,
+                        mst_stats_t* stats);
+
+/* Test hook: runs the sharded (multi-GPU) algorithm with `num_shards` edge
+ * shards emulated on the current device; the per-round allreduce becomes an
+ * on-device min over the shard buffers. Same result contract. */
+int mst_gpu_boruvka_emulated(const mst_edges_soa_t* edges, int num_shards, uint32_t* out_ids,
+                             uint64_t* out_count, uint64_t* out_total_weight,
+                             mst_stats_t* stats);
+
+/* Test hook: the round-1 minimum table alone (k_min_round1): for every
+ * vertex the key (w<<32 | edge id) of its lightest incident non-loop edge, ~0
+ * if none — the first pass of boruvka_seq.cpp:47-56. out_min: n entries
+ * (host memory). */
+int mst_gpu_round1_min(const mst_edges_soa_t* edges, uint64_t* out_min);
+
+/* ---- one process per GPU (torchrun) ----
+ * Rank r owns the contiguous edge slice [shard_base, shard_base + shard_m) of
+ * the global list (global ids are shard_base + local index). Every rank gets
+ * the full sorted result. The NCCL unique id is created on one rank and
+ * broadcast by the caller (paper_2005_06913_b200/dist.py uses torch.distributed). */
+typedef struct mst_comm* mst_comm_t;
+#define MST_UNIQUE_ID_BYTES 128
+int mst_comm_unique_id(uint8_t out_id[MST_UNIQUE_ID_BYTES]);
+int mst_comm_init(const uint8_t id[MST_UNIQUE_ID_BYTES], int nranks, int rank, int device,
+                  mst_comm_t* out_comm);
+int mst_comm_destroy(mst_comm_t comm);
+int mst_gpu_boruvka_rank(mst_comm_t comm, uint32_t n, uint64_t m_total, uint64_t shard_base,
+                         uint64_t shard_m, const uint32_t* src, const uint32_t* dst,
+                         const uint32_t* w, int on_device, uint32_t* out_ids,
+                         uint64_t* out_count, uint64_t* out_total_weight, mst_stats_t* stats);
+
+/* Device-resident timing entry (bench): edges already in HBM, result left in
+ * HBM (sorted ids in d_out_ids, count/total in host outputs). Runs `reps`
+ * back-to-back MSTs on `stream` (0 = legacy default stream) and returns the
+ * summed device time of the min-edge/compaction kernel family in
+ * *ms_hot and its launch count in *hot_launches (for the roofline). */
+int mst_gpu_boruvka_device(const mst_edges_soa_t* edges, uint32_t* d_out_ids, void* stream,
+                           uint64_t* out_count, uint64_t* out_total_weight,
+                           mst_stats_t* stats, double* ms_hot, uint32_t* hot_launches);
+
+/* Frees the cached device workspaces of the calling thread's devices. */
+int mst_gpu_release_workspace(void);
+
+/* Thread-local description of the last failure ("" if none). */
+const char* mst_gpu_last_error(void);
+
+/* Library version string and the number of visible CUDA devices (no GPU
+ * work; safe on a GPU-less host). */
+const char* mst_gpu_version(void);
+int mst_gpu_device_count(void);
+
+/* ---- seeded synthetic inputs for the BASELINE.json configs ----
+ * Counter-based (hash of seed and index), so the CPU and GPU generators
+ * produce identical bytes and any slice can be produced independently.
+ * kind: 0 uniform (spanning tree + uniform pairs, configs 0/3),
+ *       1 grid (rows x cols 4-neighbour, config 1; n = rows*cols),
+ *       2 R-MAT (scale, edgefactor; self-loops dropped, spanning tree added,
+ *         configs 2/4).
+ * mst_gen_count returns the edge count the generator will produce. */
+typedef struct mst_gen_spec {
+  int kind;
+  uint32_t n;            /* uniform: vertices; grid: rows*cols; rmat: 2^scale */
+  uint64_t m;            /* uniform: total edges (tree included) */
+  uint32_t rows, cols;   /* grid */
+  uint32_t scale;        /* rmat */
+  uint32_t edgefactor;   /* rmat */
+  double a, b, c;        /* rmat quadrant probabilities (d = 1-a-b-c) */
+  uint64_t seed;
+} mst_gen_spec_t;
+int mst_gen_count(const mst_gen_spec_t* spec, uint64_t* out_m);
+/* CPU generator (threads <= 0: all hardware threads). */
+int mst_gen_host(const mst_gen_spec_t* spec, uint32_t* src, uint32_t* dst, uint32_t* w,
+                 int threads);
+/* GPU generator into device arrays of mst_gen_count() entries. */
+int mst_gen_device(const mst_gen_spec_t* spec, uint32_t* d_src, uint32_t* d_dst, uint32_t* d_w);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MST_GPU_H_ */

@@ -1,0 +1,1 @@
+"""CPU checkers (test infrastructure only; see oracle/oracle.py)."""

@@ -1,0 +1,166 @@
+"""oracle/oracle.py — TEST INFRASTRUCTURE ONLY.
+
+ctypes access to the CPU checkers:
+  * liboracle.so  — plain-C restatement (mst_oracle.c), always built;
+  * _ref/libmstref.so — the unchanged reference library (+ ref_adapter.cpp),
+    built only where /root/reference exists, then shipped with the repo.
+
+Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline and
+--impl reference) may import this module. The product path never does.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+ORACLE_SO = HERE / "liboracle.so"
+REF_SO = HERE / "_ref" / "libmstref.so"
+
+_u32 = ctypes.c_uint32
+_u64 = ctypes.c_uint64
+_vp = ctypes.c_void_p
+_u64p = ctypes.POINTER(ctypes.c_uint64)
+_u32p = ctypes.POINTER(ctypes.c_uint32)
+
+_oracle = None
+_ref = None
+
+ALGO_KRUSKAL, ALGO_SEQ, ALGO_SEQ_OPT, ALGO_CAS, ALGO_LOCK = range(5)
+
+
+@dataclass
+class OracleResult:
+    ids: np.ndarray        # ascending uint32 edge ids
+    total_weight: int
+    rounds: int = 1
+    elapsed_ms: float = 0.0
+    m_prime: int = 0       # reference adapter: edges fed to build_graph
+
+
+def _load_oracle():
+    global _oracle
+    if _oracle is None:
+        if not ORACLE_SO.exists():
+            raise RuntimeError(f"{ORACLE_SO} missing: run `make -C oracle`")
+        lib = ctypes.CDLL(str(ORACLE_SO))
+        lib.oracle_kruskal.argtypes = [_u32, _u64, _vp, _vp, _vp, _vp, _u64p, _u64p]
+        lib.oracle_boruvka_seq.argtypes = [_u32, _u64, _vp, _vp, _vp, _vp, _u64p, _u64p, _u32p]
+        lib.oracle_min_edges.argtypes = [_u32, _u64, _vp, _vp, _vp, _vp]
+        lib.oracle_verify.argtypes = [_u32, _u64, _vp, _vp, _vp, _vp, _u64, _u32p, _u64p]
+        _oracle = lib
+    return _oracle
+
+
+def ref_available() -> bool:
+    return REF_SO.exists()
+
+
+def _load_ref():
+    global _ref
+    if _ref is None:
+        if not REF_SO.exists():
+            raise RuntimeError(f"{REF_SO} missing: build with `make -C oracle ref` where "
+                               "/root/reference exists")
+        lib = ctypes.CDLL(str(REF_SO))
+        lib.ref_last_error.restype = ctypes.c_char_p
+        lib.ref_generate_graph.argtypes = [_u32, ctypes.c_int, _u64, _vp, _vp, _vp, _u64p]
+        lib.ref_solve.argtypes = [ctypes.c_int, ctypes.c_int, _u32, _u64, _vp, _vp, _vp, _vp,
+                                  _u64p, _u64p, ctypes.POINTER(ctypes.c_double), _u32p, _u64p]
+        _ref = lib
+    return _ref
+
+
+def _arrs(src, dst, w):
+    return (np.ascontiguousarray(src, dtype=np.uint32), np.ascontiguousarray(dst, dtype=np.uint32),
+            np.ascontiguousarray(w, dtype=np.uint32))
+
+
+def _p(a: np.ndarray) -> int:
+    return a.ctypes.data if a.size else 0
+
+
+def kruskal(n: int, src, dst, w) -> OracleResult:
+    """Restated Kruskal oracle (boruvka_seq.cpp:121-143)."""
+    src, dst, w = _arrs(src, dst, w)
+    ids = np.empty(max(n - 1, 1), dtype=np.uint32)
+    cnt, tot = ctypes.c_uint64(), ctypes.c_uint64()
+    rc = _load_oracle().oracle_kruskal(n, src.size, _p(src), _p(dst), _p(w), _p(ids),
+                                       ctypes.byref(cnt), ctypes.byref(tot))
+    if rc:
+        raise ValueError(f"oracle_kruskal failed with status {rc}")
+    return OracleResult(ids[: cnt.value].copy(), int(tot.value))
+
+
+def boruvka_seq(n: int, src, dst, w) -> OracleResult:
+    """Restated sequential Boruvka (boruvka_seq.cpp:34-71)."""
+    src, dst, w = _arrs(src, dst, w)
+    ids = np.empty(max(n - 1, 1), dtype=np.uint32)
+    cnt, tot, rounds = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint32()
+    rc = _load_oracle().oracle_boruvka_seq(n, src.size, _p(src), _p(dst), _p(w), _p(ids),
+                                           ctypes.byref(cnt), ctypes.byref(tot), ctypes.byref(rounds))
+    if rc:
+        raise ValueError(f"oracle_boruvka_seq failed with status {rc}")
+    return OracleResult(ids[: cnt.value].copy(), int(tot.value), int(rounds.value))
+
+
+def min_edges(n: int, src, dst, w) -> np.ndarray:
+    """Round-1 lightest-edge key per vertex (boruvka_seq.cpp:47-56)."""
+    src, dst, w = _arrs(src, dst, w)
+    out = np.empty(n, dtype=np.uint64)
+    rc = _load_oracle().oracle_min_edges(n, src.size, _p(src), _p(dst), _p(w), _p(out))
+    if rc:
+        raise ValueError(f"oracle_min_edges failed with status {rc}")
+    return out
+
+
+def verify(n: int, src, dst, w, ids) -> dict:
+    """Structural checks of verify_mst (verify.cpp:15-57)."""
+    src, dst, w = _arrs(src, dst, w)
+    ids = np.ascontiguousarray(ids, dtype=np.uint32)
+    flags, total = ctypes.c_uint32(), ctypes.c_uint64()
+    rc = _load_oracle().oracle_verify(n, src.size, _p(src), _p(dst), _p(w), _p(ids), ids.size,
+                                      ctypes.byref(flags), ctypes.byref(total))
+    if rc:
+        raise IndexError("verify: edge id out of range")
+    f = flags.value
+    return {"edge_count_ok": bool(f & 1), "is_acyclic": bool(f & 2), "is_spanning": bool(f & 4),
+            "total_weight": int(total.value)}
+
+
+def ref_generate_graph(n: int, avg_degree: int, seed: int):
+    """The reference's own generate_graph (graph.cpp:143-194), unchanged."""
+    lib = _load_ref()
+    m = n * avg_degree // 2
+    src, dst, w = (np.empty(m, dtype=np.uint32) for _ in range(3))
+    mm = ctypes.c_uint64()
+    rc = lib.ref_generate_graph(n, avg_degree, seed, _p(src), _p(dst), _p(w), ctypes.byref(mm))
+    if rc:
+        raise ValueError(lib.ref_last_error().decode())
+    return src, dst, w
+
+
+def ref_solve(n: int, src, dst, w, algo: int = ALGO_KRUSKAL, threads: int = 1) -> OracleResult:
+    """Run the unchanged reference algorithm through the §8(c) adapter."""
+    lib = _load_ref()
+    src, dst, w = _arrs(src, dst, w)
+    ids = np.empty(max(n - 1, 1), dtype=np.uint32)
+    cnt, tot, mp = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+    ms, rounds = ctypes.c_double(), ctypes.c_uint32()
+    rc = lib.ref_solve(algo, threads, n, src.size, _p(src), _p(dst), _p(w), _p(ids),
+                       ctypes.byref(cnt), ctypes.byref(tot), ctypes.byref(ms), ctypes.byref(rounds),
+                       ctypes.byref(mp))
+    if rc:
+        raise ValueError(f"ref_solve status {rc}: {lib.ref_last_error().decode()}")
+    return OracleResult(ids[: cnt.value].copy(), int(tot.value), int(rounds.value), float(ms.value),
+                        int(mp.value))
+
+
+def hardware_threads() -> int:
+    if ref_available():
+        return int(_load_ref().ref_hardware_threads())
+    import os
+    return os.cpu_count() or 1

@@ -1,0 +1,145 @@
+// oracle/ref_adapter.cpp — TEST INFRASTRUCTURE / CPU BASELINE ONLY.
+//
+// C ABI over the UNCHANGED reference library, compiled from the sources where
+// they lie (/root/reference/proj/src/*.cpp) by oracle/Makefile into
+// oracle/_ref/libmstref.so. Nothing here is copied from the reference; this
+// file only calls its public API (graph.hpp, boruvka_seq.hpp,
+// boruvka_parallel.hpp).
+//
+// The BASELINE configs break the reference's input contract (weights start at
+// 0, duplicate pairs are kept; build_graph rejects both, graph.cpp:103-116),
+// so ref_solve applies the exact adapter of SURVEY.md §8(c):
+//   1. self-loops are dropped (never in an MST; graph.cpp:101-102 rejects),
+//   2. parallel edges collapse to their lightest (weight, id) representative
+//      (a heavier parallel edge is the maximum of a 2-cycle),
+//   3. if any weight is 0, every weight is fed as w+1 (order preserved).
+// Ids are mapped back and totals are reported in the caller's weight units.
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include <omp.h>
+
+#include "mst/boruvka_parallel.hpp"
+#include "mst/boruvka_seq.hpp"
+#include "mst/graph.hpp"
+
+namespace {
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+int ref_hardware_threads(void) {
+  const unsigned hc = std::thread::hardware_concurrency();
+  return hc ? (int)hc : 1;
+}
+
+int ref_omp_max_threads(void) { return omp_get_max_threads(); }
+
+// mst::generate_graph (graph.cpp:143-194): m = floor(n*deg/2) edges,
+// weights a permutation of 1..m. Arrays hold m entries.
+int ref_generate_graph(uint32_t n, int avg_degree, uint64_t seed, uint32_t* src, uint32_t* dst,
+                       uint32_t* w, uint64_t* out_m) {
+  try {
+    mst::Graph g = mst::generate_graph(n, avg_degree, seed);
+    const auto es = g.edges();
+    for (size_t i = 0; i < es.size(); ++i) {
+      src[i] = es[i].src;
+      dst[i] = es[i].dest;
+      if (es[i].weight > 0xFFFFFFFFull) return fail(3, "weight does not fit 32 bits");
+      w[i] = (uint32_t)es[i].weight;
+    }
+    *out_m = es.size();
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(1, e.what());
+  }
+}
+
+// algo: 0 kruskal_oracle, 1 boruvka_seq, 2 boruvka_seq_opt, 3 boruvka_cas(T),
+//       4 boruvka_lock(T). out_ids holds n-1 entries (ascending on return).
+// out_ms is the reference's own MstResult::elapsed_ms (computation only,
+// mst_result.hpp:13-14). out_mprime is the edge count fed to build_graph.
+int ref_solve(int algo, int threads, uint32_t n, uint64_t m, const uint32_t* src,
+              const uint32_t* dst, const uint32_t* w, uint32_t* out_ids, uint64_t* out_count,
+              uint64_t* out_total, double* out_ms, uint32_t* out_rounds, uint64_t* out_mprime) {
+  try {
+    if (n < 1) return fail(1, "n must be >= 1");
+    // (1)+(2): canonical pair key, keep the lightest (w, id) per pair.
+    std::vector<uint64_t> order;
+    order.reserve(m);
+    bool zero_weight = false;
+    for (uint64_t i = 0; i < m; ++i) {
+      if (src[i] >= n || dst[i] >= n) return fail(2, "endpoint out of range");
+      if (src[i] == dst[i]) continue;
+      if (w[i] == 0) zero_weight = true;
+      order.push_back(i);
+    }
+    auto pkey = [&](uint64_t i) {
+      uint64_t a = src[i], b = dst[i];
+      if (a > b) std::swap(a, b);
+      return (a << 32) | b;
+    };
+    std::sort(order.begin(), order.end(), [&](uint64_t x, uint64_t y) {
+      const uint64_t kx = pkey(x), ky = pkey(y);
+      if (kx != ky) return kx < ky;
+      if (w[x] != w[y]) return w[x] < w[y];
+      return x < y;
+    });
+    std::vector<uint64_t> keep;
+    keep.reserve(order.size());
+    for (size_t k = 0; k < order.size(); ++k)
+      if (k == 0 || pkey(order[k]) != pkey(order[k - 1])) keep.push_back(order[k]);
+    std::sort(keep.begin(), keep.end());  // original id order
+    const uint64_t shift = zero_weight ? 1 : 0;
+    std::vector<mst::Edge> edges(keep.size());
+    for (size_t k = 0; k < keep.size(); ++k)
+      edges[k] = mst::Edge{src[keep[k]], dst[keep[k]], (uint64_t)w[keep[k]] + shift};
+    mst::Graph g = mst::build_graph(n, edges);
+    mst::MstResult r;
+    switch (algo) {
+      case 0: r = mst::kruskal_oracle(g); break;
+      case 1: r = mst::boruvka_seq(g); break;
+      case 2: r = mst::boruvka_seq_opt(g); break;
+      case 3: r = mst::boruvka_cas(g, threads); break;
+      case 4: r = mst::boruvka_lock(g, threads); break;
+      default: return fail(1, "unknown algo");
+    }
+    std::vector<uint32_t> ids(r.mst_edges.size());
+    uint64_t total = 0;
+    for (size_t k = 0; k < ids.size(); ++k) {
+      ids[k] = (uint32_t)keep[(size_t)r.mst_edges[k]];
+      total += w[ids[k]];
+    }
+    std::sort(ids.begin(), ids.end());
+    if (r.total_weight != total + shift * ids.size())
+      return fail(5, "adapter total mismatch (reference total != mapped total + shift)");
+    std::memcpy(out_ids, ids.data(), ids.size() * sizeof(uint32_t));
+    *out_count = ids.size();
+    *out_total = total;
+    if (out_ms) *out_ms = r.elapsed_ms;
+    if (out_rounds) *out_rounds = r.rounds;
+    if (out_mprime) *out_mprime = keep.size();
+    return 0;
+  } catch (const mst::GraphError& e) {
+    return fail(e.kind() == mst::GraphErrorKind::Disconnected ? 4 : 1, e.what());
+  } catch (const std::invalid_argument& e) {
+    return fail(1, e.what());
+  } catch (const std::exception& e) {
+    return fail(5, e.what());
+  }
+}
+
+}  // extern "C"

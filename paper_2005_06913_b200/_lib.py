@@ -1,0 +1,146 @@
+"""ctypes binding of the C ABI declared in include/mst_gpu.h.
+
+The CUDA library is built in-tree (``paper_2005_06913_b200/libmstgpu.so``,
+see build.py). There is no CPU fallback: if the library is missing, every
+entry point raises ``RuntimeError`` loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+from pathlib import Path
+
+PKG_DIR = Path(__file__).resolve().parent
+REPO_ROOT = PKG_DIR.parent
+LIB_PATH = PKG_DIR / "libmstgpu.so"
+HEADER = REPO_ROOT / "include" / "mst_gpu.h"
+
+MST_OK = 0
+MST_ERR_INVALID_ARG = 1
+MST_ERR_RANGE = 2
+MST_ERR_WEIGHT = 3
+MST_ERR_DISCONNECTED = 4
+MST_ERR_CUDA = 5
+MST_ERR_NCCL = 6
+MST_ERR_NO_DEVICE = 7
+MST_ERR_OOM = 8
+MST_ERR_STALL = 9
+MST_MAX_ROUNDS = 48
+MST_UNIQUE_ID_BYTES = 128
+
+u32p = ctypes.POINTER(ctypes.c_uint32)
+u64p = ctypes.POINTER(ctypes.c_uint64)
+
+
+class MstEdgesSoa(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_uint32),
+        ("m", ctypes.c_uint64),
+        ("src", ctypes.c_void_p),
+        ("dst", ctypes.c_void_p),
+        ("w", ctypes.c_void_p),
+        ("on_device", ctypes.c_int),
+    ]
+
+
+class MstEdge(ctypes.Structure):
+    """The reference's ``mst::Edge`` (graph.hpp:41-45), 16 bytes."""
+
+    _fields_ = [("src", ctypes.c_uint32), ("dest", ctypes.c_uint32), ("weight", ctypes.c_uint64)]
+
+
+class MstStats(ctypes.Structure):
+    _fields_ = [
+        ("rounds", ctypes.c_uint32),
+        ("final_components", ctypes.c_uint32),
+        ("ms_total", ctypes.c_double),
+        ("ms_device", ctypes.c_double),
+        ("ms_h2d", ctypes.c_double),
+        ("ms_d2h", ctypes.c_double),
+        ("alg_bytes", ctypes.c_uint64),
+        ("live_edges", ctypes.c_uint64 * MST_MAX_ROUNDS),
+        ("live_comps", ctypes.c_uint64 * MST_MAX_ROUNDS),
+        ("kernel_launches", ctypes.c_uint32),
+    ]
+
+
+class MstGenSpec(ctypes.Structure):
+    _fields_ = [
+        ("kind", ctypes.c_int),
+        ("n", ctypes.c_uint32),
+        ("m", ctypes.c_uint64),
+        ("rows", ctypes.c_uint32),
+        ("cols", ctypes.c_uint32),
+        ("scale", ctypes.c_uint32),
+        ("edgefactor", ctypes.c_uint32),
+        ("a", ctypes.c_double),
+        ("b", ctypes.c_double),
+        ("c", ctypes.c_double),
+        ("seed", ctypes.c_uint64),
+    ]
+
+
+_SIGNATURES = {
+    "mst_gpu_boruvka": (ctypes.c_int, [ctypes.POINTER(MstEdgesSoa), ctypes.c_int, ctypes.c_void_p,
+                                       u64p, u64p, ctypes.POINTER(MstStats)]),
+    "mst_gpu_boruvka_aos": (ctypes.c_int, [ctypes.c_uint32, ctypes.c_uint64, ctypes.c_void_p,
+                                           ctypes.c_int, ctypes.c_void_p, u64p, u64p,
+                                           ctypes.POINTER(MstStats)]),
+    "mst_gpu_boruvka_emulated": (ctypes.c_int, [ctypes.POINTER(MstEdgesSoa), ctypes.c_int,
+                                                ctypes.c_void_p, u64p, u64p,
+                                                ctypes.POINTER(MstStats)]),
+    "mst_comm_unique_id": (ctypes.c_int, [ctypes.c_void_p]),
+    "mst_comm_init": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                     ctypes.POINTER(ctypes.c_void_p)]),
+    "mst_comm_destroy": (ctypes.c_int, [ctypes.c_void_p]),
+    "mst_gpu_boruvka_rank": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64,
+                                            ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p,
+                                            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                            ctypes.c_void_p, u64p, u64p,
+                                            ctypes.POINTER(MstStats)]),
+    "mst_gpu_boruvka_device": (ctypes.c_int, [ctypes.POINTER(MstEdgesSoa), ctypes.c_void_p,
+                                              ctypes.c_void_p, u64p, u64p,
+                                              ctypes.POINTER(MstStats),
+                                              ctypes.POINTER(ctypes.c_double), u32p]),
+    "mst_gpu_round1_min": (ctypes.c_int, [ctypes.POINTER(MstEdgesSoa), ctypes.c_void_p]),
+    "mst_gpu_release_workspace": (ctypes.c_int, []),
+    "mst_gpu_last_error": (ctypes.c_char_p, []),
+    "mst_gpu_version": (ctypes.c_char_p, []),
+    "mst_gpu_device_count": (ctypes.c_int, []),
+    "mst_gen_count": (ctypes.c_int, [ctypes.POINTER(MstGenSpec), u64p]),
+    "mst_gen_host": (ctypes.c_int, [ctypes.POINTER(MstGenSpec), ctypes.c_void_p, ctypes.c_void_p,
+                                    ctypes.c_void_p, ctypes.c_int]),
+    "mst_gen_device": (ctypes.c_int, [ctypes.POINTER(MstGenSpec), ctypes.c_void_p,
+                                      ctypes.c_void_p, ctypes.c_void_p]),
+}
+
+_lib = None
+
+
+def header_functions() -> list[str]:
+    """Every function the C header declares (for the export test)."""
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[\w ]+?\*?\s*\b(mst_\w+)\s*\(", text, flags=re.M)))
+
+
+def lib() -> ctypes.CDLL:
+    """The loaded CUDA library; raises if it was not built."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(there is no CPU fallback for the MST path)")
+        handle = ctypes.CDLL(str(LIB_PATH), mode=os.RTLD_NOW | getattr(os, "RTLD_GLOBAL", 0))
+        for name, (res, args) in _SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib
+
+
+def last_error() -> str:
+    return lib().mst_gpu_last_error().decode()

@@ -1,0 +1,251 @@
+"""Python mirror of the reference's MST entry point, backed by the CUDA library.
+
+Reference interface being replaced (one hot path, ``north_star``):
+
+    mst::MstResult mst::boruvka_cas(mst::Graph& g, int num_workers,
+                                    mst::ParallelRunInfo* info = nullptr);
+    -- /root/reference/proj/include/mst/boruvka_parallel.hpp:70
+       /root/reference/proj/src/boruvka_parallel.cpp:85-291
+
+Here ``boruvka_gpu(g, num_gpus=1, info=None)`` keeps that shape: a ``Graph``
+in, an ``MstResult`` out (``mst_result.hpp:15-20``: ids sorted ascending as
+int64, u64 total weight, rounds, elapsed_ms), errors as exceptions with the
+reference's meaning:
+
+* ``ValueError``   ~ std::invalid_argument (num_workers < 1,
+  boruvka_parallel.cpp:86; n < 1, graph.cpp:93)
+* ``GraphError``   ~ mst::GraphError (graph.hpp:19-38): EndpointOutOfRange,
+  Disconnected (raised after the run; ``err.forest`` holds the minimum
+  spanning forest), WeightOverflow (weight >= 2^32, a device-key limit)
+* ``WorkerPanic``  ~ mst::WorkerPanic (boruvka_parallel.hpp:44-47): CUDA,
+  NCCL or no-progress failures.
+
+Every call goes through the C ABI in include/mst_gpu.h; nothing falls back
+to the CPU.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib as L
+
+__all__ = [
+    "Graph", "MstResult", "GpuRunInfo", "GraphError", "WorkerPanic", "build_graph",
+    "boruvka_gpu", "boruvka_gpu_aos", "boruvka_gpu_emulated", "boruvka_gpu_device",
+    "EDGE_DTYPE",
+]
+
+# The reference's mst::Edge {u32 src, u32 dest, u64 weight} (graph.hpp:41-45).
+EDGE_DTYPE = np.dtype([("src", "<u4"), ("dest", "<u4"), ("weight", "<u8")])
+
+
+class GraphError(RuntimeError):
+    """Input-contract violation (mirrors mst::GraphError, graph.hpp:30-38)."""
+
+    def __init__(self, kind: str, what: str, forest: "MstResult | None" = None):
+        super().__init__(f"{kind}: {what}")
+        self.kind = kind
+        self.forest = forest
+
+
+class WorkerPanic(RuntimeError):
+    """Device/collective failure or stall (mirrors mst::WorkerPanic)."""
+
+
+@dataclass
+class MstResult:
+    """mst::MstResult (mst_result.hpp:15-20)."""
+
+    mst_edges: np.ndarray
+    total_weight: int
+    rounds: int
+    elapsed_ms: float
+
+
+@dataclass
+class GpuRunInfo:
+    """ParallelRunInfo analogue (boruvka_parallel.hpp:52-56) + round counters."""
+
+    final_components: int = 0
+    rounds: int = 0
+    ms_total: float = 0.0
+    ms_device: float = 0.0
+    ms_h2d: float = 0.0
+    ms_d2h: float = 0.0
+    alg_bytes: int = 0
+    live_edges: list = field(default_factory=list)
+    live_comps: list = field(default_factory=list)
+    kernel_launches: int = 0
+
+
+class Graph:
+    """Edge-list graph in the device-native SoA layout (u32 src/dst/weight).
+
+    Mirrors mst::Graph's accessors (graph.hpp:57-60). Unlike the reference's
+    build_graph, construction does not enforce the simple-graph contract:
+    duplicate pairs, zero weights and self-loops are legal input to the GPU
+    path (self-loops are skipped, parallel edges need no care). Endpoints are
+    range-checked on the device.
+    """
+
+    def __init__(self, n: int, src, dst, w):
+        self.n = int(n)
+        self.src = np.ascontiguousarray(src, dtype=np.uint32)
+        self.dst = np.ascontiguousarray(dst, dtype=np.uint32)
+        w = np.asarray(w)
+        if w.dtype != np.uint32:
+            if w.size and (w.min() < 0 or w.max() > 0xFFFFFFFF):
+                raise GraphError("WeightOverflow", "weights must fit in 32 bits")
+            w = w.astype(np.uint32)
+        self.w = np.ascontiguousarray(w)
+        if not (self.src.shape == self.dst.shape == self.w.shape) or self.src.ndim != 1:
+            raise ValueError("src, dst and w must be 1-D arrays of equal length")
+
+    @classmethod
+    def from_edges(cls, n: int, edges) -> "Graph":
+        arr = np.asarray(list(edges), dtype=np.uint64).reshape(-1, 3)
+        return cls(n, arr[:, 0], arr[:, 1], arr[:, 2])
+
+    def vertex_count(self) -> int:
+        return self.n
+
+    def edge_count(self) -> int:
+        return int(self.src.shape[0])
+
+    def to_aos(self) -> np.ndarray:
+        out = np.empty(self.edge_count(), dtype=EDGE_DTYPE)
+        out["src"], out["dest"], out["weight"] = self.src, self.dst, self.w
+        return out
+
+
+def build_graph(n: int, edges) -> Graph:
+    """Counterpart of mst::build_graph (graph.cpp:92-141) for list input."""
+    if n < 1:
+        raise ValueError("build_graph: vertex count must be >= 1")
+    return Graph.from_edges(n, edges)
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data if a.size else 0
+
+
+def _info_from(stats: L.MstStats, info: GpuRunInfo | None) -> None:
+    if info is None:
+        return
+    r = stats.rounds
+    info.final_components = stats.final_components
+    info.rounds = r
+    info.ms_total = stats.ms_total
+    info.ms_device = stats.ms_device
+    info.ms_h2d = stats.ms_h2d
+    info.ms_d2h = stats.ms_d2h
+    info.alg_bytes = stats.alg_bytes
+    info.live_edges = [int(stats.live_edges[i]) for i in range(min(r, L.MST_MAX_ROUNDS))]
+    info.live_comps = [int(stats.live_comps[i]) for i in range(min(r, L.MST_MAX_ROUNDS))]
+    info.kernel_launches = stats.kernel_launches
+
+
+def _raise_for(rc: int, result: MstResult | None = None) -> None:
+    if rc == L.MST_OK:
+        return
+    msg = L.last_error()
+    if rc == L.MST_ERR_INVALID_ARG:
+        raise ValueError(msg)
+    if rc == L.MST_ERR_RANGE:
+        raise GraphError("EndpointOutOfRange", msg)
+    if rc == L.MST_ERR_WEIGHT:
+        raise GraphError("WeightOverflow", msg)
+    if rc == L.MST_ERR_DISCONNECTED:
+        raise GraphError("Disconnected", msg, forest=result)
+    raise WorkerPanic(f"[status {rc}] {msg}")
+
+
+def _finish(rc, ids, count, total, stats, info):
+    res = None
+    if rc in (L.MST_OK, L.MST_ERR_DISCONNECTED):
+        res = MstResult(ids[: count.value].astype(np.int64), int(total.value), int(stats.rounds),
+                        float(stats.ms_total))
+    _info_from(stats, info)
+    _raise_for(rc, res)
+    return res
+
+
+def boruvka_gpu(g: Graph, num_gpus: int = 1, info: GpuRunInfo | None = None) -> MstResult:
+    """GPU replacement of boruvka_cas(g, num_workers, info).
+
+    num_gpus == 1: one B200. num_gpus in 2..8: this process drives devices
+    0..num_gpus-1, edge list sharded, one allreduce(min) per round.
+    """
+    if num_gpus < 1:
+        raise ValueError("boruvka: need num_gpus >= 1")
+    lib = L.lib()
+    e = L.MstEdgesSoa(g.n, g.edge_count(), _ptr(g.src), _ptr(g.dst), _ptr(g.w), 0)
+    ids = np.empty(max(g.n - 1, 1), dtype=np.uint32)
+    count, total = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    stats = L.MstStats()
+    rc = lib.mst_gpu_boruvka(ctypes.byref(e), num_gpus, ids.ctypes.data, ctypes.byref(count),
+                             ctypes.byref(total), ctypes.byref(stats))
+    return _finish(rc, ids, count, total, stats, info)
+
+
+def boruvka_gpu_aos(n: int, edges: np.ndarray, info: GpuRunInfo | None = None) -> MstResult:
+    """Same, fed the reference's AoS ``Edge`` array unchanged (EDGE_DTYPE)."""
+    edges = np.ascontiguousarray(edges, dtype=EDGE_DTYPE)
+    lib = L.lib()
+    ids = np.empty(max(n - 1, 1), dtype=np.uint32)
+    count, total = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    stats = L.MstStats()
+    rc = lib.mst_gpu_boruvka_aos(n, edges.shape[0], _ptr(edges), 0, ids.ctypes.data,
+                                 ctypes.byref(count), ctypes.byref(total), ctypes.byref(stats))
+    return _finish(rc, ids, count, total, stats, info)
+
+
+def boruvka_gpu_emulated(g: Graph, shards: int, info: GpuRunInfo | None = None) -> MstResult:
+    """The multi-GPU (sharded, partner-label key) algorithm with `shards` edge
+    shards emulated on the current GPU; used to test the sharded protocol."""
+    lib = L.lib()
+    e = L.MstEdgesSoa(g.n, g.edge_count(), _ptr(g.src), _ptr(g.dst), _ptr(g.w), 0)
+    ids = np.empty(max(g.n - 1, 1), dtype=np.uint32)
+    count, total = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    stats = L.MstStats()
+    rc = lib.mst_gpu_boruvka_emulated(ctypes.byref(e), shards, ids.ctypes.data, ctypes.byref(count),
+                                      ctypes.byref(total), ctypes.byref(stats))
+    return _finish(rc, ids, count, total, stats, info)
+
+
+def round1_min(g: Graph) -> np.ndarray:
+    """Test hook: the device's round-1 minimum table (k_min_round1 only)."""
+    lib = L.lib()
+    e = L.MstEdgesSoa(g.n, g.edge_count(), _ptr(g.src), _ptr(g.dst), _ptr(g.w), 0)
+    out = np.empty(g.n, dtype=np.uint64)
+    _raise_for(lib.mst_gpu_round1_min(ctypes.byref(e), out.ctypes.data))
+    return out
+
+
+def boruvka_gpu_device(n: int, m: int, src_ptr: int, dst_ptr: int, w_ptr: int, out_ptr: int,
+                       stream: int = 0, info: GpuRunInfo | None = None, hot: dict | None = None):
+    """Device-resident entry (edges already in HBM, ids left in HBM at out_ptr).
+
+    Returns (count, total_weight). With ``hot`` a dict, fills
+    ``hot['ms']``/``hot['launches']`` with the summed CUDA-event time and
+    launch count of the edge-pass kernels (k_min_round1 + k_compact).
+    """
+    lib = L.lib()
+    e = L.MstEdgesSoa(n, m, src_ptr, dst_ptr, w_ptr, 1)
+    count, total = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    stats = L.MstStats()
+    ms_hot = ctypes.c_double(0)
+    hot_n = ctypes.c_uint32(0)
+    rc = lib.mst_gpu_boruvka_device(ctypes.byref(e), out_ptr, stream, ctypes.byref(count),
+                                    ctypes.byref(total), ctypes.byref(stats),
+                                    ctypes.byref(ms_hot) if hot is not None else None,
+                                    ctypes.byref(hot_n) if hot is not None else None)
+    _info_from(stats, info)
+    if hot is not None:
+        hot["ms"] = ms_hot.value
+        hot["launches"] = hot_n.value
+    _raise_for(rc)
+    return int(count.value), int(total.value)

@@ -1,0 +1,1093 @@
+// Host engine + C ABI of the B200 parallel Boruvka MST.
+//
+// Replaces mst::boruvka_cas (reference: proj/src/boruvka_parallel.cpp:85-291)
+// with a device round loop. See kernels.cuh for the per-round kernels and
+// DESIGN.md for layouts, the byte model and the multi-GPU protocol.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace mstgpu {
+
+thread_local std::string t_last_error;
+void set_last_error(const std::string& m) { t_last_error = m; }
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+
+// ------------------------------- NCCL (dlopen) ------------------------------
+// Loaded lazily so the library has no hard NCCL dependency and reuses the
+// libnccl.so.2 torch already mapped, if any.
+struct NcclApi {
+  bool ok = false;
+  std::string why;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      api.why = std::string("dlopen(libnccl.so.2) failed: ") + dlerror();
+      return;
+    }
+#define MST_NCCL_SYM(field, name)                                         \
+  api.field = reinterpret_cast<decltype(api.field)>(dlsym(h, name));      \
+  if (!api.field) {                                                       \
+    api.why = std::string("NCCL symbol missing: ") + name;                \
+    return;                                                               \
+  }
+    MST_NCCL_SYM(GetUniqueId, "ncclGetUniqueId");
+    MST_NCCL_SYM(CommInitRank, "ncclCommInitRank");
+    MST_NCCL_SYM(CommInitAll, "ncclCommInitAll");
+    MST_NCCL_SYM(AllReduce, "ncclAllReduce");
+    MST_NCCL_SYM(GroupStart, "ncclGroupStart");
+    MST_NCCL_SYM(GroupEnd, "ncclGroupEnd");
+    MST_NCCL_SYM(CommDestroy, "ncclCommDestroy");
+    MST_NCCL_SYM(GetErrorString, "ncclGetErrorString");
+#undef MST_NCCL_SYM
+    api.ok = true;
+  });
+  if (!api.ok) throw MstError{MST_ERR_NCCL, api.why};
+  return api;
+}
+
+#define MST_NCCL_CHECK(expr)                                                                \
+  do {                                                                                      \
+    ncclResult_t _r = (expr);                                                               \
+    if (_r != ncclSuccess)                                                                  \
+      throw MstError{MST_ERR_NCCL, std::string(#expr " failed: ") + nccl().GetErrorString(_r)}; \
+  } while (0)
+
+// ------------------------------- workspace ----------------------------------
+// One per (device, slot): named grow-only device buffers, a stream, pinned
+// counter snapshots and the look-back epoch. Reused across calls like a
+// library handle; guarded by its mutex (one call at a time per workspace).
+struct Workspace {
+  int device = 0;
+  std::mutex mu;
+  cudaStream_t stream = nullptr;
+  struct Buf {
+    void* p = nullptr;
+    size_t bytes = 0;
+  };
+  std::map<std::string, Buf> bufs;
+  unsigned long long* status = nullptr;
+  size_t status_words = 0;
+  uint32_t epoch = 1;
+  DevCounters* h_snap = nullptr;  // pinned, kMaxR + 1 snapshots
+  std::vector<cudaEvent_t> ev;    // per-round events
+  std::vector<cudaEvent_t> tev;   // timing events (hot kernels)
+
+  void init(int dev) {
+    device = dev;
+    MST_CUDA_CHECK(cudaSetDevice(dev));
+    MST_CUDA_CHECK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    MST_CUDA_CHECK(cudaMallocHost(&h_snap, sizeof(DevCounters) * (kMaxR + 1)));
+    ev.resize(kMaxR + 1);
+    for (auto& e : ev) MST_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    tev.resize(4 * kMaxR + 8);
+    for (auto& e : tev) MST_CUDA_CHECK(cudaEventCreate(&e));
+  }
+
+  void release() {
+    cudaSetDevice(device);
+    cudaStreamSynchronize(stream);
+    for (auto& kv : bufs) cudaFree(kv.second.p);
+    bufs.clear();
+    if (status) cudaFree(status);
+    status = nullptr;
+    status_words = 0;
+  }
+
+  template <class T>
+  T* get(const std::string& name, size_t count) {
+    const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+    Buf& b = bufs[name];
+    if (b.bytes < bytes) {
+      if (b.p) {
+        MST_CUDA_CHECK(cudaStreamSynchronize(stream));
+        MST_CUDA_CHECK(cudaFree(b.p));
+        b.p = nullptr;
+        b.bytes = 0;
+      }
+      MST_CUDA_CHECK(cudaMalloc(&b.p, bytes));
+      b.bytes = bytes;
+    }
+    return static_cast<T*>(b.p);
+  }
+
+  unsigned long long* status_array(size_t tiles) {
+    if (status_words < tiles + 1) {
+      MST_CUDA_CHECK(cudaStreamSynchronize(stream));
+      if (status) MST_CUDA_CHECK(cudaFree(status));
+      status_words = tiles + 1;
+      MST_CUDA_CHECK(cudaMalloc(&status, status_words * sizeof(unsigned long long)));
+      MST_CUDA_CHECK(cudaMemsetAsync(status, 0, status_words * sizeof(unsigned long long), stream));
+      epoch = 1;
+    }
+    return status;
+  }
+
+  uint32_t next_epoch() {
+    if (epoch >= (1u << 30) - 1) {
+      MST_CUDA_CHECK(cudaMemsetAsync(status, 0, status_words * sizeof(unsigned long long), stream));
+      epoch = 1;
+    }
+    return epoch++;
+  }
+};
+
+std::mutex g_ws_mu;
+std::map<std::pair<int, int>, std::unique_ptr<Workspace>> g_ws;
+
+Workspace& workspace(int device, int slot = 0) {
+  std::lock_guard<std::mutex> g(g_ws_mu);
+  auto& p = g_ws[{device, slot}];
+  if (!p) {
+    p = std::make_unique<Workspace>();
+    p->init(device);
+  }
+  return *p;
+}
+
+// ------------------------------- launch helpers -----------------------------
+
+int sm_count(int device) {
+  static std::mutex mu;
+  static std::map<int, int> cache;
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find(device);
+  if (it != cache.end()) return it->second;
+  int sms = 0;
+  MST_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  cache[device] = sms;
+  return sms;
+}
+
+template <class K>
+int blocks_per_sm(K kernel) {
+  static std::mutex mu;
+  static std::map<const void*, int> cache;
+  std::lock_guard<std::mutex> g(mu);
+  const void* key = reinterpret_cast<const void*>(kernel);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int nb = 0;
+  MST_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, kBlock, 0));
+  cache[key] = std::max(nb, 1);
+  return cache[key];
+}
+
+// Persistent grid: min(resident capacity, work tiles), at least 1.
+template <class K>
+unsigned persistent_grid(K kernel, int device, uint64_t tiles) {
+  const uint64_t cap = (uint64_t)sm_count(device) * blocks_per_sm(kernel);
+  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(cap, tiles));
+}
+
+uint64_t tiles_of(uint64_t count) { return (count + kTile - 1) / kTile; }
+
+double ms_between(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0;
+  MST_CUDA_CHECK(cudaEventElapsedTime(&ms, a, b));
+  return ms;
+}
+
+// ------------------------------- run state ----------------------------------
+
+struct RunOut {
+  uint64_t count = 0;
+  uint64_t total_weight = 0;
+  uint32_t rounds = 0;
+  uint32_t final_components = 0;
+  uint32_t err = 0;
+  uint32_t launches = 0;
+  double ms_hot = 0;
+  uint32_t hot_launches = 0;
+  uint64_t hot_bytes = 0;
+  DevCounters ctr{};
+};
+
+void init_counters(Workspace& ws, DevCounters* d_ctr, uint32_t n, uint64_t m) {
+  DevCounters& h = ws.h_snap[kMaxR];
+  std::memset(&h, 0, sizeof(h));
+  h.n[1] = n;
+  h.m[1] = m;
+  h.stop_round = kNoStop;
+  MST_CUDA_CHECK(cudaMemcpyAsync(d_ctr, &h, sizeof(DevCounters), cudaMemcpyHostToDevice, ws.stream));
+}
+
+// Sorted id list (ascending) of `count` distinct ids < m_total, via a bitmap.
+uint32_t sort_ids(Workspace& ws, const uint32_t* d_ids, uint64_t count, uint64_t m_total,
+                  uint32_t* d_sorted, DevCounters* d_ctr) {
+  const uint64_t words = (m_total + 31) / 32;
+  uint32_t* bits = ws.get<uint32_t>("bitmap", words);
+  MST_CUDA_CHECK(cudaMemsetAsync(bits, 0, words * sizeof(uint32_t), ws.stream));
+  uint32_t launches = 0;
+  if (count) {
+    const unsigned g = (unsigned)std::min<uint64_t>((count + 255) / 256, (uint64_t)sm_count(ws.device) * 8);
+    k_mark<<<g, 256, 0, ws.stream>>>(d_ids, (uint32_t)count, bits, m_total);
+    ++launches;
+  }
+  unsigned long long* st = ws.status_array(tiles_of(words));
+  unsigned int* tile_ctr = &d_ctr->tile[0][kSlotSort];
+  MST_CUDA_CHECK(cudaMemsetAsync(tile_ctr, 0, sizeof(unsigned int), ws.stream));
+  k_bitmap_emit<<<persistent_grid(k_bitmap_emit, ws.device, tiles_of(words)), kBlock, 0, ws.stream>>>(
+      bits, words, d_sorted, tile_ctr, st, ws.next_epoch());
+  ++launches;
+  MST_CUDA_CHECK(cudaGetLastError());
+  return launches;
+}
+
+bool warp_prereduce_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MST_WARP_PREREDUCE");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+// ------------------------------- single GPU ---------------------------------
+// Literal keys (w<<32 | index into this round's edge array): the hook reads
+// the winning edge directly. Host loop runs one round ahead of the device;
+// kernels of rounds past the stop early-exit on the device counters.
+template <class InView, bool kPre>
+void run_single_impl(Workspace& ws, InView in, uint32_t n, uint64_t m, RunOut& out, bool time_hot) {
+  cudaStream_t s = ws.stream;
+  auto* d_ctr = ws.get<DevCounters>("ctr", 1);
+  unsigned long long* minb[2] = {ws.get<unsigned long long>("minA", n),
+                                 ws.get<unsigned long long>("minB", n)};
+  uint32_t* parent = ws.get<uint32_t>("parent", n);
+  uint32_t* rootlabel = ws.get<uint32_t>("rootlabel", n);
+  uint32_t* L = ws.get<uint32_t>("label", n);
+  uint32_t* mst = ws.get<uint32_t>("mst", n);
+  uint4* E[2] = {ws.get<uint4>("E0", m), ws.get<uint4>("E1", m)};
+  unsigned long long* st = ws.status_array(std::max(tiles_of(m), tiles_of(n)));
+
+  init_counters(ws, d_ctr, n, m);
+  MST_CUDA_CHECK(cudaMemsetAsync(minb[0], 0xFF, (size_t)n * 8, s));
+  uint32_t launches = 0;
+  int tix = 0;
+  auto tmark = [&]() {
+    if (time_hot) MST_CUDA_CHECK(cudaEventRecord(ws.tev[tix++], s));
+  };
+  std::vector<std::pair<int, int>> hot_pairs;  // (start idx, round)
+
+  {
+    auto kmin = k_min_round1<InView, false, kPre>;
+    const unsigned g = (unsigned)std::max<uint64_t>(
+        1, std::min<uint64_t>((m + kBlock - 1) / kBlock, (uint64_t)sm_count(ws.device) * blocks_per_sm(kmin)));
+    const int t0 = tix;
+    tmark();
+    kmin<<<g, kBlock, 0, s>>>(in, n, m, minb[0], d_ctr);
+    tmark();
+    if (time_hot) hot_pairs.push_back({t0, 0});
+    ++launches;
+  }
+
+  uint64_t n_bound = n, m_bound = m;
+  int r = 1;
+  int stop = 0;
+  while (true) {
+    if (r > MST_MAX_ROUNDS) throw MstError{MST_ERR_STALL, "no convergence within MST_MAX_ROUNDS rounds"};
+    unsigned long long* mcur = minb[(r - 1) & 1];
+    unsigned long long* mnext = minb[r & 1];
+    uint4* Eout = E[(r - 1) & 1];
+    const uint32_t ep_h = ws.next_epoch(), ep_c = ws.next_epoch();
+    if (r == 1) {
+      auto kh = k_hook<InView, false>;
+      kh<<<persistent_grid(kh, ws.device, tiles_of(n_bound)), kBlock, 0, s>>>(
+          in, mcur, parent, rootlabel, mst, n, d_ctr, r, st, ep_h);
+    } else {
+      auto kh = k_hook<PackedView, false>;
+      kh<<<persistent_grid(kh, ws.device, tiles_of(n_bound)), kBlock, 0, s>>>(
+          PackedView{E[r & 1]}, mcur, parent, rootlabel, mst, n, d_ctr, r, st, ep_h);
+    }
+    {
+      const unsigned g = (unsigned)std::max<uint64_t>(
+          1, std::min<uint64_t>((n_bound + kBlock - 1) / kBlock,
+                                (uint64_t)sm_count(ws.device) * blocks_per_sm(k_label)));
+      k_label<<<g, kBlock, 0, s>>>(parent, rootlabel, L, mnext, d_ctr, r);
+    }
+    const int t0 = tix;
+    tmark();
+    if (r == 1) {
+      auto kc = k_compact<InView, false, kPre>;
+      kc<<<persistent_grid(kc, ws.device, tiles_of(m_bound)), kBlock, 0, s>>>(
+          in, Eout, L, mnext, Recover{nullptr, nullptr, nullptr}, n, d_ctr, r, st, ep_c);
+    } else {
+      auto kc = k_compact<PackedView, false, kPre>;
+      kc<<<persistent_grid(kc, ws.device, tiles_of(m_bound)), kBlock, 0, s>>>(
+          PackedView{E[r & 1]}, Eout, L, mnext, Recover{nullptr, nullptr, nullptr}, n, d_ctr, r, st,
+          ep_c);
+    }
+    tmark();
+    if (time_hot) hot_pairs.push_back({t0, r});
+    launches += 3;
+    MST_CUDA_CHECK(cudaGetLastError());
+    MST_CUDA_CHECK(cudaMemcpyAsync(&ws.h_snap[r], d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
+    MST_CUDA_CHECK(cudaEventRecord(ws.ev[r], s));
+    if (r >= 2) {
+      MST_CUDA_CHECK(cudaEventSynchronize(ws.ev[r - 1]));
+      const DevCounters& snap = ws.h_snap[r - 1];
+      if (snap.err) break;
+      if (snap.stop_round != kNoStop && (int)snap.stop_round <= r) {
+        stop = (int)snap.stop_round;
+        break;
+      }
+      n_bound = snap.n[r];
+      m_bound = snap.m[r];
+    }
+    ++r;
+  }
+  MST_CUDA_CHECK(cudaMemcpyAsync(&out.ctr, d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
+  MST_CUDA_CHECK(cudaStreamSynchronize(s));
+  const DevCounters& c = out.ctr;
+  out.err = c.err;
+  out.launches = launches;
+  if (c.err) return;
+  stop = (int)c.stop_round;
+  if (c.stop_round == kNoStop) throw MstError{MST_ERR_STALL, "round loop ended without a stop verdict"};
+  out.rounds = (uint32_t)stop - 1;
+  out.final_components = c.n[stop];
+  out.count = (uint64_t)n - out.final_components;
+  out.total_weight = c.total_weight;
+  if (time_hot) {
+    for (auto& hp : hot_pairs) {
+      const int rr = hp.second;
+      if (rr != 0 && rr + 1 >= stop) continue;  // early-exited launch
+      out.ms_hot += ms_between(ws.tev[hp.first], ws.tev[hp.first + 1]);
+      out.hot_launches += 1;
+      if (rr == 0)
+        out.hot_bytes += 12ull * m;
+      else
+        out.hot_bytes += (rr == 1 ? 12ull : 16ull) * c.m[rr] + 16ull * c.m[rr + 1];
+    }
+  }
+}
+
+uint64_t alg_bytes_from(const DevCounters& c, uint32_t rounds) {
+  // 12 m + 32 sum k_r + 32 sum n_r.
+  uint64_t b = 12ull * c.m[1];
+  for (uint32_t r = 1; r <= rounds; ++r) {
+    b += 32ull * c.n[r];
+    if (r + 1 <= rounds) b += 32ull * c.m[r + 1];
+  }
+  return b;
+}
+
+void fill_stats(mst_stats_t* st, const RunOut& o) {
+  if (!st) return;
+  st->rounds = o.rounds;
+  st->final_components = o.final_components;
+  st->alg_bytes = alg_bytes_from(o.ctr, o.rounds);
+  for (int r = 0; r < MST_MAX_ROUNDS; ++r) {
+    const bool live = (uint32_t)(r + 1) <= o.rounds;
+    st->live_edges[r] = live ? o.ctr.m[r + 1] : 0;
+    st->live_comps[r] = live ? o.ctr.n[r + 1] : 0;
+  }
+  st->kernel_launches = o.launches;
+}
+
+void check_err_bits(uint32_t err) {
+  if (err & kErrRange)
+    throw MstError{MST_ERR_RANGE, "endpoint out of range: an edge touches a vertex outside [0,n)"};
+  if (err & kErrWeight) throw MstError{MST_ERR_WEIGHT, "edge weight does not fit in 32 bits"};
+}
+
+void validate_common(uint32_t n, uint64_t m) {
+  if (n < 1) throw MstError{MST_ERR_INVALID_ARG, "vertex count must be >= 1"};
+  if (m >= 0xFFFFFFFFull) throw MstError{MST_ERR_INVALID_ARG, "edge count must be < 2^32-1"};
+}
+
+int current_device_checked() {
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    throw MstError{MST_ERR_NO_DEVICE, std::string("no CUDA device available: ") +
+                                          (e == cudaSuccess ? "0 devices" : cudaGetErrorString(e))};
+  }
+  int dev = 0;
+  MST_CUDA_CHECK(cudaGetDevice(&dev));
+  return dev;
+}
+
+// Common tail: sort the emitted ids, copy back, timing, stats.
+struct SingleArgs {
+  uint32_t n;
+  uint64_t m;
+  int kind;  // 0 SoA, 1 AoS
+  const uint32_t *src, *dst, *w;
+  const mst_edge_t* aos;
+  int on_device;
+  uint32_t* out_ids;       // host (or device when device_out)
+  bool device_out;
+  cudaStream_t user_stream;
+  bool time_hot;
+};
+
+RunOut run_single(const SingleArgs& a, mst_stats_t* stats) {
+  const auto t_start = Clock::now();
+  const int dev = current_device_checked();
+  Workspace& ws = workspace(dev, 0);
+  std::lock_guard<std::mutex> lock(ws.mu);
+  MST_CUDA_CHECK(cudaSetDevice(dev));
+  cudaStream_t saved = ws.stream;
+  if (a.user_stream) ws.stream = a.user_stream;
+  struct Restore {
+    Workspace& w;
+    cudaStream_t s;
+    ~Restore() { w.stream = s; }
+  } restore{ws, saved};
+  cudaStream_t s = ws.stream;
+
+  cudaEvent_t e0, e1, e2, e3;
+  e0 = ws.tev[ws.tev.size() - 4];
+  e1 = ws.tev[ws.tev.size() - 3];
+  e2 = ws.tev[ws.tev.size() - 2];
+  e3 = ws.tev[ws.tev.size() - 1];
+  MST_CUDA_CHECK(cudaEventRecord(e0, s));
+  const uint32_t* src = a.src;
+  const uint32_t* dst = a.dst;
+  const uint32_t* w = a.w;
+  const mst_edge_t* aos = a.aos;
+  if (!a.on_device && a.m > 0) {
+    if (a.kind == 0) {
+      uint32_t* d_src = ws.get<uint32_t>("in_src", a.m);
+      uint32_t* d_dst = ws.get<uint32_t>("in_dst", a.m);
+      uint32_t* d_w = ws.get<uint32_t>("in_w", a.m);
+      MST_CUDA_CHECK(cudaMemcpyAsync(d_src, a.src, a.m * 4, cudaMemcpyHostToDevice, s));
+      MST_CUDA_CHECK(cudaMemcpyAsync(d_dst, a.dst, a.m * 4, cudaMemcpyHostToDevice, s));
+      MST_CUDA_CHECK(cudaMemcpyAsync(d_w, a.w, a.m * 4, cudaMemcpyHostToDevice, s));
+      src = d_src;
+      dst = d_dst;
+      w = d_w;
+    } else {
+      mst_edge_t* d_e = ws.get<mst_edge_t>("in_aos", a.m);
+      MST_CUDA_CHECK(cudaMemcpyAsync(d_e, a.aos, a.m * sizeof(mst_edge_t), cudaMemcpyHostToDevice, s));
+      aos = d_e;
+    }
+  }
+  MST_CUDA_CHECK(cudaEventRecord(e1, s));
+
+  RunOut o;
+  const bool pre = warp_prereduce_enabled();
+  if (a.kind == 0) {
+    SoaView v{src, dst, w, 0};
+    if (pre)
+      run_single_impl<SoaView, true>(ws, v, a.n, a.m, o, a.time_hot);
+    else
+      run_single_impl<SoaView, false>(ws, v, a.n, a.m, o, a.time_hot);
+  } else {
+    AosView v{reinterpret_cast<const uint4*>(aos), 0};
+    if (pre)
+      run_single_impl<AosView, true>(ws, v, a.n, a.m, o, a.time_hot);
+    else
+      run_single_impl<AosView, false>(ws, v, a.n, a.m, o, a.time_hot);
+  }
+  check_err_bits(o.err);
+  uint32_t* d_mst = ws.get<uint32_t>("mst", a.n);
+  uint32_t* d_sorted = a.device_out ? a.out_ids : ws.get<uint32_t>("sorted", a.n);
+  auto* d_ctr = ws.get<DevCounters>("ctr", 1);
+  o.launches += sort_ids(ws, d_mst, o.count, std::max<uint64_t>(a.m, 1), d_sorted, d_ctr);
+  MST_CUDA_CHECK(cudaEventRecord(e2, s));
+  if (!a.device_out && o.count)
+    MST_CUDA_CHECK(cudaMemcpyAsync(a.out_ids, d_sorted, o.count * 4, cudaMemcpyDeviceToHost, s));
+  MST_CUDA_CHECK(cudaEventRecord(e3, s));
+  MST_CUDA_CHECK(cudaStreamSynchronize(s));
+  if (stats) {
+    fill_stats(stats, o);
+    stats->ms_h2d = ms_between(e0, e1);
+    stats->ms_device = ms_between(e1, e2);
+    stats->ms_d2h = ms_between(e2, e3);
+    stats->ms_total = std::chrono::duration<double, std::milli>(Clock::now() - t_start).count();
+  }
+  return o;
+}
+
+// ------------------------------- sharded (multi-GPU) ------------------------
+// Partner-label keys (w<<32 | partner component): after the min exchange
+// every shard can hook without seeing the winning edge; the shard that owns
+// the edge recovers its global id during its next compaction pass.
+
+struct Shard {
+  Workspace* ws = nullptr;
+  uint64_t m = 0;        // local edges
+  uint32_t base = 0;     // global id of local edge 0
+  SoaView in{};
+  unsigned long long* minb[2]{};
+  uint32_t *parent = nullptr, *rootlabel = nullptr, *L = nullptr, *mstpos = nullptr,
+           *slots = nullptr;
+  uint4* E[2]{};
+  DevCounters* d_ctr = nullptr;
+  unsigned long long* st = nullptr;
+};
+
+struct Exchanger {
+  virtual ~Exchanger() = default;
+  virtual void min_u64(std::vector<Shard>& sh, int which, uint64_t count) = 0;
+  virtual void min_u32_slots(std::vector<Shard>& sh, uint64_t count) = 0;
+};
+
+// All shards on one device, one stream: an element-wise min kernel.
+struct EmulatedExchanger : Exchanger {
+  void min_u64(std::vector<Shard>& sh, int which, uint64_t count) override {
+    if (sh.size() == 1 || count == 0) return;
+    ShardPtrs<unsigned long long, 8> p{};
+    for (size_t i = 0; i < sh.size(); ++i) p.p[i] = sh[i].minb[which];
+    k_shard_min<unsigned long long><<<(unsigned)std::min<uint64_t>((count + 255) / 256, 4096), 256, 0,
+                                      sh[0].ws->stream>>>(p, (int)sh.size(), count);
+    MST_CUDA_CHECK(cudaGetLastError());
+  }
+  void min_u32_slots(std::vector<Shard>& sh, uint64_t count) override {
+    if (sh.size() == 1 || count == 0) return;
+    ShardPtrs<uint32_t, 8> p{};
+    for (size_t i = 0; i < sh.size(); ++i) p.p[i] = sh[i].slots;
+    k_shard_min<uint32_t><<<(unsigned)std::min<uint64_t>((count + 255) / 256, 4096), 256, 0,
+                            sh[0].ws->stream>>>(p, (int)sh.size(), count);
+    MST_CUDA_CHECK(cudaGetLastError());
+  }
+};
+
+// NCCL: one communicator per shard (single process driving several GPUs via
+// ncclCommInitAll, or one rank per process via ncclCommInitRank).
+struct NcclExchanger : Exchanger {
+  std::vector<ncclComm_t> comms;
+  void min_u64(std::vector<Shard>& sh, int which, uint64_t count) override {
+    if (count == 0) return;
+    MST_NCCL_CHECK(nccl().GroupStart());
+    for (size_t i = 0; i < sh.size(); ++i) {
+      MST_CUDA_CHECK(cudaSetDevice(sh[i].ws->device));
+      MST_NCCL_CHECK(nccl().AllReduce(sh[i].minb[which], sh[i].minb[which], count, ncclUint64, ncclMin,
+                                      comms[i], sh[i].ws->stream));
+    }
+    MST_NCCL_CHECK(nccl().GroupEnd());
+  }
+  void min_u32_slots(std::vector<Shard>& sh, uint64_t count) override {
+    if (count == 0) return;
+    MST_NCCL_CHECK(nccl().GroupStart());
+    for (size_t i = 0; i < sh.size(); ++i) {
+      MST_CUDA_CHECK(cudaSetDevice(sh[i].ws->device));
+      MST_NCCL_CHECK(nccl().AllReduce(sh[i].slots, sh[i].slots, count, ncclUint32, ncclMin, comms[i],
+                                      sh[i].ws->stream));
+    }
+    MST_NCCL_CHECK(nccl().GroupEnd());
+  }
+};
+
+template <bool kPre>
+void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, RunOut& out) {
+  const int G = (int)sh.size();
+  uint32_t launches = 0;
+  for (auto& s : sh) {
+    MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
+    init_counters(*s.ws, s.d_ctr, n, s.m);
+    MST_CUDA_CHECK(cudaMemsetAsync(s.minb[0], 0xFF, (size_t)n * 8, s.ws->stream));
+    MST_CUDA_CHECK(cudaMemsetAsync(s.slots, 0xFF, (size_t)n * 4, s.ws->stream));
+    auto kmin = k_min_round1<SoaView, true, kPre>;
+    const unsigned g = (unsigned)std::max<uint64_t>(
+        1, std::min<uint64_t>((s.m + kBlock - 1) / kBlock,
+                              (uint64_t)sm_count(s.ws->device) * blocks_per_sm(kmin)));
+    kmin<<<g, kBlock, 0, s.ws->stream>>>(s.in, n, s.m, s.minb[0], s.d_ctr);
+    ++launches;
+    MST_CUDA_CHECK(cudaGetLastError());
+  }
+  // errors (range) are checked before the first exchange
+  for (auto& s : sh) {
+    MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
+    MST_CUDA_CHECK(cudaMemcpyAsync(&s.ws->h_snap[0], s.d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost,
+                                   s.ws->stream));
+    MST_CUDA_CHECK(cudaStreamSynchronize(s.ws->stream));
+    if (s.ws->h_snap[0].err) {
+      out.err = s.ws->h_snap[0].err;
+      return;
+    }
+  }
+  ex.min_u64(sh, 0, n);
+  uint64_t n_bound = n;
+  int r = 1;
+  int stop = 0;
+  while (true) {
+    if (r > MST_MAX_ROUNDS) throw MstError{MST_ERR_STALL, "no convergence within MST_MAX_ROUNDS rounds"};
+    const int cur = (r - 1) & 1, nxt = r & 1;
+    for (auto& s : sh) {
+      MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
+      Workspace& ws = *s.ws;
+      const uint32_t ep_h = ws.next_epoch(), ep_c = ws.next_epoch();
+      if (r == 1) {
+        auto kh = k_hook<SoaView, true>;
+        kh<<<persistent_grid(kh, ws.device, tiles_of(n_bound)), kBlock, 0, ws.stream>>>(
+            s.in, s.minb[cur], s.parent, s.rootlabel, s.mstpos, n, s.d_ctr, r, s.st, ep_h);
+      } else {
+        auto kh = k_hook<PackedView, true>;
+        kh<<<persistent_grid(kh, ws.device, tiles_of(n_bound)), kBlock, 0, ws.stream>>>(
+            PackedView{s.E[r & 1]}, s.minb[cur], s.parent, s.rootlabel, s.mstpos, n, s.d_ctr, r, s.st, ep_h);
+      }
+      const unsigned gl = (unsigned)std::max<uint64_t>(
+          1, std::min<uint64_t>((n_bound + kBlock - 1) / kBlock,
+                                (uint64_t)sm_count(ws.device) * blocks_per_sm(k_label)));
+      k_label<<<gl, kBlock, 0, ws.stream>>>(s.parent, s.rootlabel, s.L, s.minb[nxt], s.d_ctr, r);
+      MST_CUDA_CHECK(cudaMemcpyAsync(&ws.h_snap[r], s.d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost,
+                                     ws.stream));
+      MST_CUDA_CHECK(cudaEventRecord(ws.ev[r], ws.stream));
+      const uint64_t m_bound = r == 1 ? s.m : ws.h_snap[r - 1].m[r];
+      Recover rec{s.minb[cur], s.mstpos, s.slots};
+      uint4* Eout = s.E[(r - 1) & 1];
+      if (r == 1) {
+        auto kc = k_compact<SoaView, true, kPre>;
+        kc<<<persistent_grid(kc, ws.device, tiles_of(m_bound)), kBlock, 0, ws.stream>>>(
+            s.in, Eout, s.L, s.minb[nxt], rec, n, s.d_ctr, r, s.st, ep_c);
+      } else {
+        auto kc = k_compact<PackedView, true, kPre>;
+        kc<<<persistent_grid(kc, ws.device, tiles_of(m_bound)), kBlock, 0, ws.stream>>>(
+            PackedView{s.E[r & 1]}, Eout, s.L, s.minb[nxt], rec, n, s.d_ctr, r, s.st, ep_c);
+      }
+      launches += 3;
+      MST_CUDA_CHECK(cudaGetLastError());
+    }
+    // verdict after label (identical on every shard: replicated hook)
+    uint32_t verdict = kNoStop;
+    uint32_t n_next = 0;
+    for (int g = 0; g < G; ++g) {
+      MST_CUDA_CHECK(cudaEventSynchronize(sh[g].ws->ev[r]));
+      const DevCounters& snap = sh[g].ws->h_snap[r];
+      if (g == 0) {
+        verdict = snap.stop_round;
+        n_next = snap.n[r + 1];
+      } else if (snap.stop_round != verdict || snap.n[r + 1] != n_next) {
+        throw MstError{MST_ERR_STALL, "replicated hook diverged between shards"};
+      }
+    }
+    if (verdict != kNoStop && (int)verdict <= r + 1) {
+      stop = (int)verdict;
+      break;
+    }
+    // compaction of round r writes min_next; the snapshot after label gave
+    // n_{r+1}, the exchange size
+    for (auto& s : sh) {
+      MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
+      MST_CUDA_CHECK(cudaMemcpyAsync(&s.ws->h_snap[r], s.d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost,
+                                     s.ws->stream));
+    }
+    ex.min_u64(sh, nxt, n_next);
+    n_bound = n_next;
+    for (auto& s : sh) {
+      MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
+      MST_CUDA_CHECK(cudaStreamSynchronize(s.ws->stream));
+      // a compaction can also end the loop (no edges left anywhere is only
+      // visible globally; the next hook sees isolated components and stops)
+    }
+    ++r;
+  }
+  for (auto& s : sh) {
+    MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
+    MST_CUDA_CHECK(cudaStreamSynchronize(s.ws->stream));
+  }
+  DevCounters c;
+  MST_CUDA_CHECK(cudaSetDevice(sh[0].ws->device));
+  MST_CUDA_CHECK(cudaMemcpy(&c, sh[0].d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost));
+  out.ctr = c;
+  // per-shard kept counts differ; report the sum over shards as m_r
+  for (int g = 1; g < G; ++g) {
+    DevCounters cg;
+    MST_CUDA_CHECK(cudaSetDevice(sh[g].ws->device));
+    MST_CUDA_CHECK(cudaMemcpy(&cg, sh[g].d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost));
+    for (int r2 = 1; r2 < kMaxR; ++r2) out.ctr.m[r2] += cg.m[r2];
+    out.err |= cg.err;
+  }
+  out.err |= c.err;
+  out.launches = launches;
+  out.rounds = (uint32_t)stop - 1;
+  out.final_components = c.n[stop];
+  out.count = (uint64_t)n - out.final_components;
+  out.total_weight = c.total_weight;
+}
+
+// Shared driver for emulated / single-process multi-GPU / one-rank-per-process.
+// `parts` gives each local shard's (device, slot, src, dst, w, m, base).
+struct PartSpec {
+  int device, slot;
+  const uint32_t *src, *dst, *w;
+  uint64_t m;
+  uint32_t base;
+  int on_device;
+};
+
+RunOut run_sharded(const std::vector<PartSpec>& parts, Exchanger& ex, uint32_t n, uint64_t m_total,
+                   uint32_t* out_ids, mst_stats_t* stats) {
+  const auto t_start = Clock::now();
+  std::vector<Shard> sh(parts.size());
+  std::vector<std::unique_lock<std::mutex>> locks;
+  for (size_t i = 0; i < parts.size(); ++i) {
+    Workspace& ws = workspace(parts[i].device, parts[i].slot);
+    locks.emplace_back(ws.mu);
+    MST_CUDA_CHECK(cudaSetDevice(ws.device));
+    Shard& s = sh[i];
+    s.ws = &ws;
+    s.m = parts[i].m;
+    s.base = parts[i].base;
+    const uint32_t* src = parts[i].src;
+    const uint32_t* dst = parts[i].dst;
+    const uint32_t* w = parts[i].w;
+    if (!parts[i].on_device && s.m) {
+      uint32_t* d_src = ws.get<uint32_t>("in_src", s.m);
+      uint32_t* d_dst = ws.get<uint32_t>("in_dst", s.m);
+      uint32_t* d_w = ws.get<uint32_t>("in_w", s.m);
+      MST_CUDA_CHECK(cudaMemcpyAsync(d_src, src, s.m * 4, cudaMemcpyHostToDevice, ws.stream));
+      MST_CUDA_CHECK(cudaMemcpyAsync(d_dst, dst, s.m * 4, cudaMemcpyHostToDevice, ws.stream));
+      MST_CUDA_CHECK(cudaMemcpyAsync(d_w, w, s.m * 4, cudaMemcpyHostToDevice, ws.stream));
+      src = d_src;
+      dst = d_dst;
+      w = d_w;
+    }
+    s.in = SoaView{src, dst, w, s.base};
+    s.minb[0] = ws.get<unsigned long long>("minA", n);
+    s.minb[1] = ws.get<unsigned long long>("minB", n);
+    s.parent = ws.get<uint32_t>("parent", n);
+    s.rootlabel = ws.get<uint32_t>("rootlabel", n);
+    s.L = ws.get<uint32_t>("label", n);
+    s.mstpos = ws.get<uint32_t>("mstpos", n);
+    s.slots = ws.get<uint32_t>("mst", n);
+    s.E[0] = ws.get<uint4>("E0", s.m);
+    s.E[1] = ws.get<uint4>("E1", s.m);
+    s.d_ctr = ws.get<DevCounters>("ctr", 1);
+    s.st = ws.status_array(std::max(tiles_of(s.m), tiles_of(n)));
+  }
+  MST_CUDA_CHECK(cudaSetDevice(sh[0].ws->device));
+  cudaEvent_t e1 = sh[0].ws->tev[sh[0].ws->tev.size() - 3];
+  cudaEvent_t e2 = sh[0].ws->tev[sh[0].ws->tev.size() - 2];
+  MST_CUDA_CHECK(cudaEventRecord(e1, sh[0].ws->stream));
+  RunOut o;
+  if (warp_prereduce_enabled())
+    run_sharded_rounds<true>(sh, ex, n, o);
+  else
+    run_sharded_rounds<false>(sh, ex, n, o);
+  check_err_bits(o.err);
+  ex.min_u32_slots(sh, o.count);
+  Workspace& ws0 = *sh[0].ws;
+  MST_CUDA_CHECK(cudaSetDevice(ws0.device));
+  uint32_t* d_sorted = ws0.get<uint32_t>("sorted", n);
+  o.launches += sort_ids(ws0, sh[0].slots, o.count, std::max<uint64_t>(m_total, 1), d_sorted, sh[0].d_ctr);
+  MST_CUDA_CHECK(cudaEventRecord(e2, ws0.stream));
+  if (o.count && out_ids)
+    MST_CUDA_CHECK(cudaMemcpyAsync(out_ids, d_sorted, o.count * 4, cudaMemcpyDeviceToHost, ws0.stream));
+  for (auto& s : sh) {
+    MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
+    MST_CUDA_CHECK(cudaStreamSynchronize(s.ws->stream));
+  }
+  if (stats) {
+    fill_stats(stats, o);
+    stats->ms_device = ms_between(e1, e2);
+    stats->ms_h2d = 0;
+    stats->ms_d2h = 0;
+    stats->ms_total = std::chrono::duration<double, std::milli>(Clock::now() - t_start).count();
+  }
+  return o;
+}
+
+int finish_status(const RunOut& o, uint64_t* out_count, uint64_t* out_total) {
+  if (out_count) *out_count = o.count;
+  if (out_total) *out_total = o.total_weight;
+  if (o.final_components > 1) {
+    set_last_error("disconnected: " + std::to_string(o.final_components) +
+                   " components (a minimum spanning forest was returned)");
+    return MST_ERR_DISCONNECTED;
+  }
+  set_last_error("");
+  return MST_OK;
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    return f();
+  } catch (const MstError& e) {
+    set_last_error(e.msg);
+    return e.code;
+  } catch (const std::exception& e) {
+    set_last_error(std::string("internal error: ") + e.what());
+    return MST_ERR_CUDA;
+  }
+}
+
+}  // namespace
+
+struct CommImpl {
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0, device = 0;
+};
+
+}  // namespace mstgpu
+
+using namespace mstgpu;
+
+struct mst_comm {
+  CommImpl impl;
+};
+
+extern "C" {
+
+const char* mst_gpu_last_error(void) { return t_last_error.c_str(); }
+
+const char* mst_gpu_version(void) { return "paper_2005_06913_b200 0.1 (sm_100a)"; }
+
+int mst_gpu_device_count(void) {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return c;
+}
+
+int mst_gpu_boruvka(const mst_edges_soa_t* edges, int num_gpus, uint32_t* out_ids,
+                    uint64_t* out_count, uint64_t* out_total_weight, mst_stats_t* stats) {
+  return guarded([&]() -> int {
+    if (!edges) throw MstError{MST_ERR_INVALID_ARG, "edges is NULL"};
+    validate_common(edges->n, edges->m);
+    if (num_gpus < 1 || num_gpus > 8) throw MstError{MST_ERR_INVALID_ARG, "num_gpus must be in [1,8]"};
+    if (edges->m && (!edges->src || !edges->dst || !edges->w))
+      throw MstError{MST_ERR_INVALID_ARG, "edge arrays are NULL"};
+    if (edges->n > 1 && !out_ids) throw MstError{MST_ERR_INVALID_ARG, "out_ids is NULL"};
+    if (num_gpus > 1 && edges->on_device)
+      throw MstError{MST_ERR_INVALID_ARG, "device input requires num_gpus == 1"};
+    const int dev = current_device_checked();
+    if (num_gpus == 1) {
+      SingleArgs a{edges->n, edges->m, 0, edges->src, edges->dst, edges->w, nullptr,
+                   edges->on_device, out_ids, false, nullptr, false};
+      RunOut o = run_single(a, stats);
+      return finish_status(o, out_count, out_total_weight);
+    }
+    int count = 0;
+    MST_CUDA_CHECK(cudaGetDeviceCount(&count));
+    if (count < num_gpus)
+      throw MstError{MST_ERR_INVALID_ARG, "num_gpus=" + std::to_string(num_gpus) + " but only " +
+                                              std::to_string(count) + " devices are visible"};
+    (void)dev;
+    NcclExchanger ex;
+    ex.comms.resize(num_gpus);
+    std::vector<int> devs(num_gpus);
+    for (int g = 0; g < num_gpus; ++g) devs[g] = g;
+    MST_NCCL_CHECK(nccl().CommInitAll(ex.comms.data(), num_gpus, devs.data()));
+    struct Destroy {
+      std::vector<ncclComm_t>& c;
+      ~Destroy() {
+        for (auto x : c) nccl().CommDestroy(x);
+      }
+    } destroy{ex.comms};
+    std::vector<PartSpec> parts;
+    for (int g = 0; g < num_gpus; ++g) {
+      const uint64_t lo = edges->m * g / num_gpus, hi = edges->m * (g + 1) / num_gpus;
+      parts.push_back(PartSpec{g, 0, edges->src + lo, edges->dst + lo, edges->w + lo, hi - lo, (uint32_t)lo, 0});
+    }
+    RunOut o = run_sharded(parts, ex, edges->n, edges->m, out_ids, stats);
+    return finish_status(o, out_count, out_total_weight);
+  });
+}
+
+int mst_gpu_boruvka_aos(uint32_t n, uint64_t m, const mst_edge_t* edges, int on_device,
+                        uint32_t* out_ids, uint64_t* out_count, uint64_t* out_total_weight,
+                        mst_stats_t* stats) {
+  return guarded([&]() -> int {
+    validate_common(n, m);
+    if (m && !edges) throw MstError{MST_ERR_INVALID_ARG, "edges is NULL"};
+    if (n > 1 && !out_ids) throw MstError{MST_ERR_INVALID_ARG, "out_ids is NULL"};
+    current_device_checked();
+    SingleArgs a{n, m, 1, nullptr, nullptr, nullptr, edges, on_device, out_ids, false, nullptr, false};
+    RunOut o = run_single(a, stats);
+    return finish_status(o, out_count, out_total_weight);
+  });
+}
+
+int mst_gpu_boruvka_emulated(const mst_edges_soa_t* edges, int num_shards, uint32_t* out_ids,
+                             uint64_t* out_count, uint64_t* out_total_weight, mst_stats_t* stats) {
+  return guarded([&]() -> int {
+    if (!edges) throw MstError{MST_ERR_INVALID_ARG, "edges is NULL"};
+    validate_common(edges->n, edges->m);
+    if (num_shards < 1 || num_shards > 8) throw MstError{MST_ERR_INVALID_ARG, "num_shards must be in [1,8]"};
+    if (edges->m && (!edges->src || !edges->dst || !edges->w))
+      throw MstError{MST_ERR_INVALID_ARG, "edge arrays are NULL"};
+    if (edges->n > 1 && !out_ids) throw MstError{MST_ERR_INVALID_ARG, "out_ids is NULL"};
+    const int dev = current_device_checked();
+    // every emulated shard shares the first shard's stream (serial, one device)
+    Workspace& ws0 = workspace(dev, 1);
+    std::vector<PartSpec> parts;
+    for (int g = 0; g < num_shards; ++g) {
+      const uint64_t lo = edges->m * g / num_shards, hi = edges->m * (g + 1) / num_shards;
+      parts.push_back(PartSpec{dev, 1 + g, edges->src + lo, edges->dst + lo, edges->w + lo, hi - lo,
+                               (uint32_t)lo, edges->on_device});
+      Workspace& wsg = workspace(dev, 1 + g);
+      if (g > 0) {
+        std::lock_guard<std::mutex> lk(wsg.mu);
+        wsg.stream = ws0.stream;
+      }
+    }
+    EmulatedExchanger ex;
+    RunOut o = run_sharded(parts, ex, edges->n, edges->m, out_ids, stats);
+    return finish_status(o, out_count, out_total_weight);
+  });
+}
+
+int mst_comm_unique_id(uint8_t out_id[MST_UNIQUE_ID_BYTES]) {
+  return guarded([&]() -> int {
+    if (!out_id) throw MstError{MST_ERR_INVALID_ARG, "out_id is NULL"};
+    ncclUniqueId id;
+    MST_NCCL_CHECK(nccl().GetUniqueId(&id));
+    std::memcpy(out_id, id.internal, MST_UNIQUE_ID_BYTES);
+    return MST_OK;
+  });
+}
+
+int mst_comm_init(const uint8_t id[MST_UNIQUE_ID_BYTES], int nranks, int rank, int device,
+                  mst_comm_t* out_comm) {
+  return guarded([&]() -> int {
+    if (!id || !out_comm) throw MstError{MST_ERR_INVALID_ARG, "NULL argument"};
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw MstError{MST_ERR_INVALID_ARG, "bad rank/nranks"};
+    current_device_checked();
+    MST_CUDA_CHECK(cudaSetDevice(device));
+    ncclUniqueId uid;
+    std::memcpy(uid.internal, id, MST_UNIQUE_ID_BYTES);
+    auto* c = new mst_comm;
+    c->impl.nranks = nranks;
+    c->impl.rank = rank;
+    c->impl.device = device;
+    ncclResult_t r = nccl().CommInitRank(&c->impl.comm, nranks, uid, rank);
+    if (r != ncclSuccess) {
+      delete c;
+      throw MstError{MST_ERR_NCCL, std::string("ncclCommInitRank failed: ") + nccl().GetErrorString(r)};
+    }
+    *out_comm = c;
+    return MST_OK;
+  });
+}
+
+int mst_comm_destroy(mst_comm_t comm) {
+  return guarded([&]() -> int {
+    if (!comm) return MST_OK;
+    if (comm->impl.comm) nccl().CommDestroy(comm->impl.comm);
+    delete comm;
+    return MST_OK;
+  });
+}
+
+int mst_gpu_boruvka_rank(mst_comm_t comm, uint32_t n, uint64_t m_total, uint64_t shard_base,
+                         uint64_t shard_m, const uint32_t* src, const uint32_t* dst, const uint32_t* w,
+                         int on_device, uint32_t* out_ids, uint64_t* out_count,
+                         uint64_t* out_total_weight, mst_stats_t* stats) {
+  return guarded([&]() -> int {
+    if (!comm) throw MstError{MST_ERR_INVALID_ARG, "comm is NULL"};
+    validate_common(n, m_total);
+    if (shard_base + shard_m > m_total) throw MstError{MST_ERR_INVALID_ARG, "shard outside [0, m_total)"};
+    if (shard_m && (!src || !dst || !w)) throw MstError{MST_ERR_INVALID_ARG, "edge arrays are NULL"};
+    if (n > 1 && !out_ids) throw MstError{MST_ERR_INVALID_ARG, "out_ids is NULL"};
+    current_device_checked();
+    MST_CUDA_CHECK(cudaSetDevice(comm->impl.device));
+    NcclExchanger ex;
+    ex.comms = {comm->impl.comm};
+    std::vector<PartSpec> parts{
+        PartSpec{comm->impl.device, 0, src, dst, w, shard_m, (uint32_t)shard_base, on_device}};
+    RunOut o = run_sharded(parts, ex, n, m_total, out_ids, stats);
+    return finish_status(o, out_count, out_total_weight);
+  });
+}
+
+int mst_gpu_boruvka_device(const mst_edges_soa_t* edges, uint32_t* d_out_ids, void* stream,
+                           uint64_t* out_count, uint64_t* out_total_weight, mst_stats_t* stats,
+                           double* ms_hot, uint32_t* hot_launches) {
+  return guarded([&]() -> int {
+    if (!edges || !d_out_ids) throw MstError{MST_ERR_INVALID_ARG, "NULL argument"};
+    validate_common(edges->n, edges->m);
+    if (!edges->on_device) throw MstError{MST_ERR_INVALID_ARG, "mst_gpu_boruvka_device needs device input"};
+    current_device_checked();
+    SingleArgs a{edges->n, edges->m, 0, edges->src, edges->dst, edges->w, nullptr, 1, d_out_ids, true,
+                 (cudaStream_t)stream, ms_hot != nullptr};
+    RunOut o = run_single(a, stats);
+    if (ms_hot) *ms_hot = o.ms_hot;
+    if (hot_launches) *hot_launches = o.hot_launches;
+    if (stats) stats->alg_bytes = alg_bytes_from(o.ctr, o.rounds);
+    return finish_status(o, out_count, out_total_weight);
+  });
+}
+
+int mst_gpu_round1_min(const mst_edges_soa_t* edges, uint64_t* out_min) {
+  return guarded([&]() -> int {
+    if (!edges || !out_min) throw MstError{MST_ERR_INVALID_ARG, "NULL argument"};
+    validate_common(edges->n, edges->m);
+    if (edges->m && (!edges->src || !edges->dst || !edges->w))
+      throw MstError{MST_ERR_INVALID_ARG, "edge arrays are NULL"};
+    const int dev = current_device_checked();
+    Workspace& ws = workspace(dev, 0);
+    std::lock_guard<std::mutex> lock(ws.mu);
+    MST_CUDA_CHECK(cudaSetDevice(dev));
+    const uint32_t n = edges->n;
+    const uint64_t m = edges->m;
+    const uint32_t *src = edges->src, *dst = edges->dst, *w = edges->w;
+    if (!edges->on_device && m) {
+      uint32_t* d_src = ws.get<uint32_t>("in_src", m);
+      uint32_t* d_dst = ws.get<uint32_t>("in_dst", m);
+      uint32_t* d_w = ws.get<uint32_t>("in_w", m);
+      MST_CUDA_CHECK(cudaMemcpyAsync(d_src, src, m * 4, cudaMemcpyHostToDevice, ws.stream));
+      MST_CUDA_CHECK(cudaMemcpyAsync(d_dst, dst, m * 4, cudaMemcpyHostToDevice, ws.stream));
+      MST_CUDA_CHECK(cudaMemcpyAsync(d_w, w, m * 4, cudaMemcpyHostToDevice, ws.stream));
+      src = d_src;
+      dst = d_dst;
+      w = d_w;
+    }
+    auto* d_ctr = ws.get<DevCounters>("ctr", 1);
+    auto* mn = ws.get<unsigned long long>("minA", n);
+    init_counters(ws, d_ctr, n, m);
+    MST_CUDA_CHECK(cudaMemsetAsync(mn, 0xFF, (size_t)n * 8, ws.stream));
+    auto kmin = warp_prereduce_enabled() ? k_min_round1<SoaView, false, true>
+                                         : k_min_round1<SoaView, false, false>;
+    const unsigned g = (unsigned)std::max<uint64_t>(
+        1, std::min<uint64_t>((m + kBlock - 1) / kBlock, (uint64_t)sm_count(dev) * blocks_per_sm(kmin)));
+    kmin<<<g, kBlock, 0, ws.stream>>>(SoaView{src, dst, w, 0}, n, m, mn, d_ctr);
+    MST_CUDA_CHECK(cudaGetLastError());
+    MST_CUDA_CHECK(cudaMemcpyAsync(out_min, mn, (size_t)n * 8, cudaMemcpyDeviceToHost, ws.stream));
+    MST_CUDA_CHECK(cudaMemcpyAsync(&ws.h_snap[0], d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost,
+                                   ws.stream));
+    MST_CUDA_CHECK(cudaStreamSynchronize(ws.stream));
+    check_err_bits(ws.h_snap[0].err);
+    return MST_OK;
+  });
+}
+
+int mst_gpu_release_workspace(void) {
+  return guarded([&]() -> int {
+    std::lock_guard<std::mutex> g(g_ws_mu);
+    for (auto& kv : g_ws) {
+      std::lock_guard<std::mutex> lk(kv.second->mu);
+      kv.second->release();
+    }
+    return MST_OK;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,103 @@
+"""The N>1 host path on CPU: world_size-2 gloo processes.
+
+* shard planning (dist.shard_range) partitions the edge list,
+* the NCCL unique id made on rank 0 reaches rank 1 byte-identical
+  (dist.exchange_unique_id over torch.distributed),
+* the sharded protocol (oracle/sharded_model.py, the numpy model of the
+  kKeyPartner kernels) with a real allreduce(min) between two processes
+  returns exactly the oracle's MST on every rank.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import GOLDEN, load_npz
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, cases, queue):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    from oracle.sharded_model import sharded_boruvka
+    from paper_2005_06913_b200 import dist as D
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    try:
+        # unique-id plumbing with a deterministic stand-in id maker
+        uid = D.exchange_unique_id(rank, make_id=lambda: bytes(range(128)))
+        out = {"uid_ok": uid == bytes(range(128))}
+
+        def allreduce_min(a):
+            t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.int64))
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            return t.numpy()
+
+        res = []
+        for n, src, dst, w in cases:
+            lo, hi = D.shard_range(len(src), rank, world)
+            ids, total, rounds = sharded_boruvka(n, src[lo:hi], dst[lo:hi], w[lo:hi], lo, allreduce_min)
+            res.append((ids.tolist(), total))
+        out["res"] = res
+        queue.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def _cases():
+    cases = []
+    for name in ["gen_3000_6_2", "gen_1500_4_13", "multi_mid", "gen_100_3_5"]:
+        g = load_npz(GOLDEN / f"{name}.npz")
+        cases.append((int(g["n"]), g["src"], g["dst"], g["w"], g["ids"].tolist(), int(g["total"])))
+    return cases
+
+
+def test_shard_range_partitions():
+    from paper_2005_06913_b200.dist import shard_range
+    for m in (0, 1, 7, 100, 8_384_512):
+        for world in (1, 2, 3, 4, 8):
+            spans = [shard_range(m, r, world) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == m
+            assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+    with pytest.raises(ValueError):
+        shard_range(10, 2, 2)
+
+
+def test_sharded_protocol_world2_gloo():
+    cases = _cases()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    inputs = [(n, s, d, w) for n, s, d, w, _, _ in cases]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, inputs, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = dict(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank in (0, 1):
+        assert outs[rank]["uid_ok"]
+        for (ids, total), case in zip(outs[rank]["res"], cases):
+            assert ids == case[4] and total == case[5]
+
+
+def test_sharded_model_single_rank_matches_oracle(oracle_mod):
+    from oracle.sharded_model import sharded_boruvka
+    for n, src, dst, w, ids, total in _cases():
+        got, tot, _ = sharded_boruvka(n, src, dst, w, 0, lambda a: a)
+        assert got.tolist() == ids and tot == total
+        # 3 shards in one process: allreduce = elementwise min over shards
+        # is exercised by the gloo test; here shards are emulated serially

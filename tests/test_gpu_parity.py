@@ -1,0 +1,249 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle.
+
+Bit-exact: the MST edge-id set and the u64 total weight (integer work, no
+tolerance). Run on a B200 with `pytest -m gpu`.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, golden_gen_files, load_npz, small_cases
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mst():
+    import paper_2005_06913_b200 as P
+    from paper_2005_06913_b200 import _lib as L
+    assert L.lib().mst_gpu_device_count() > 0, "no CUDA device: -m gpu tests need a B200"
+    return P
+
+
+def _check(P, n, src, dst, w, ids, total, shards=(2, 3)):
+    g = P.Graph(n, src, dst, w)
+    r = P.boruvka_gpu(g)
+    assert r.mst_edges.tolist() == list(ids), "single-GPU edge set differs from the oracle"
+    assert r.total_weight == int(total)
+    a = P.boruvka_gpu_aos(n, g.to_aos())
+    assert a.mst_edges.tolist() == list(ids) and a.total_weight == int(total)
+    for s in shards:
+        e = P.boruvka_gpu_emulated(g, s)
+        assert e.mst_edges.tolist() == list(ids), f"{s}-shard edge set differs"
+        assert e.total_weight == int(total)
+
+
+def test_small_golden_graphs(mst):
+    # hand graphs of the reference tests + 200 random graphs checked against
+    # brute force (tests/golden/make_golden.py)
+    for name, n, src, dst, w, ids, total in small_cases():
+        _check(mst, n, src, dst, w, ids, total, shards=(2,))
+
+
+@pytest.mark.parametrize("path", golden_gen_files(), ids=lambda p: p.stem)
+def test_generated_golden_graphs(mst, path):
+    g = load_npz(path)
+    _check(mst, int(g["n"]), g["src"], g["dst"], g["w"], g["ids"].tolist(), int(g["total"]),
+           shards=(2, 3, 8))
+
+
+def test_app_b_100k_presets(mst, oracle_mod):
+    if not oracle_mod.ref_available():
+        pytest.skip("oracle/_ref not built")
+    app_b = {(100_000, 3, 1003): 5_460_175_173, (100_000, 6, 1006): 5_911_779_114,
+             (100_000, 9, 1009): 5_981_724_212}
+    for (n, d, seed), total in app_b.items():
+        src, dst, w = oracle_mod.ref_generate_graph(n, d, seed)
+        k = oracle_mod.kruskal(n, src, dst, w)
+        assert k.total_weight == total
+        _check(mst, n, src, dst, w, k.ids.tolist(), total, shards=(4,))
+
+
+def test_round1_min_table(mst, oracle_mod):
+    rng = np.random.default_rng(1)
+    for n, m, wmax in [(1, 0, 1), (10, 40, 5), (5000, 40000, 2**32 - 1), (100000, 300000, 1000)]:
+        src = rng.integers(0, n, m).astype(np.uint32)
+        dst = rng.integers(0, n, m).astype(np.uint32)
+        w = rng.integers(0, wmax, m, dtype=np.uint64).astype(np.uint32)  # ties -> lower id
+        got = mst.api.round1_min(mst.Graph(n, src, dst, w))
+        assert np.array_equal(got, oracle_mod.min_edges(n, src, dst, w))
+
+
+def _oracle_check(P, O, n, src, dst, w, shards=(2,)):
+    k = O.kruskal(n, src, dst, w)
+    _check(P, n, src, dst, w, k.ids.tolist(), k.total_weight, shards=shards)
+    return k
+
+
+def test_edge_cases(mst, oracle_mod):
+    P, O = mst, oracle_mod
+    # n = 1: empty MST, with and without self-loops
+    r = P.boruvka_gpu(P.Graph(1, [], [], []))
+    assert r.mst_edges.size == 0 and r.total_weight == 0
+    r = P.boruvka_gpu(P.Graph(1, [0, 0], [0, 0], [5, 1]))
+    assert r.mst_edges.size == 0
+    # single edge, zero weight, max weight
+    _oracle_check(P, O, 2, [0], [1], [0])
+    _oracle_check(P, O, 2, [1, 0], [0, 1], [2**32 - 1, 2**32 - 2])
+    # self-loops and parallel edges mixed in
+    _oracle_check(P, O, 4, [0, 0, 1, 1, 2, 3, 3, 0], [0, 1, 0, 2, 2, 2, 0, 3],
+                  [3, 9, 4, 7, 1, 8, 2, 6])
+    # duplicate weights: ties broken by lower edge id (stable Kruskal)
+    rng = np.random.default_rng(2)
+    n, m = 3000, 20000
+    src = np.concatenate([np.arange(1, n), rng.integers(0, n, m - n + 1)]).astype(np.uint32)
+    dst = np.concatenate([rng.integers(0, np.arange(1, n)), rng.integers(0, n, m - n + 1)]).astype(np.uint32)
+    w = rng.integers(0, 50, m).astype(np.uint32)
+    k = O.kruskal(n, src, dst, w)
+    r = P.boruvka_gpu(P.Graph(n, src, dst, w))
+    assert r.mst_edges.tolist() == k.ids.tolist() and r.total_weight == k.total_weight
+    # all weights equal
+    w0 = np.zeros(m, dtype=np.uint32)
+    k = O.kruskal(n, src, dst, w0)
+    assert P.boruvka_gpu(P.Graph(n, src, dst, w0)).mst_edges.tolist() == k.ids.tolist()
+
+
+def test_disconnected_returns_forest(mst, oracle_mod):
+    P, O = mst, oracle_mod
+    src = np.array([0, 1, 0, 3, 4, 3], dtype=np.uint32)
+    dst = np.array([1, 2, 2, 4, 5, 5], dtype=np.uint32)
+    w = np.array([1, 2, 3, 4, 5, 6], dtype=np.uint32)
+    for n in (6, 9):  # 9: three isolated vertices too
+        with pytest.raises(P.GraphError) as ei:
+            P.boruvka_gpu(P.Graph(n, src, dst, w))
+        assert ei.value.kind == "Disconnected"
+        f = ei.value.forest
+        assert f.mst_edges.tolist() == O.kruskal(n, src, dst, w).ids.tolist() == [0, 1, 3, 4]
+        with pytest.raises(P.GraphError):
+            P.boruvka_gpu_emulated(P.Graph(n, src, dst, w), 2)
+    with pytest.raises(P.GraphError) as ei:
+        P.boruvka_gpu(P.Graph(5, [], [], []))
+    assert ei.value.kind == "Disconnected" and ei.value.forest.mst_edges.size == 0
+
+
+def test_input_errors(mst):
+    P = mst
+    with pytest.raises(P.GraphError) as ei:
+        P.boruvka_gpu(P.Graph(3, [0, 3], [1, 2], [1, 2]))
+    assert ei.value.kind == "EndpointOutOfRange"
+    with pytest.raises(P.GraphError) as ei:
+        P.boruvka_gpu_emulated(P.Graph(3, [0, 1], [1, 7], [1, 2]), 2)
+    assert ei.value.kind == "EndpointOutOfRange"
+    aos = P.Graph(3, [0, 1], [1, 2], [1, 2]).to_aos()
+    aos["weight"][1] = 2**32 + 5
+    with pytest.raises(P.GraphError) as ei:
+        P.boruvka_gpu_aos(3, aos)
+    assert ei.value.kind == "WeightOverflow"
+
+
+def test_adversarial_shapes(mst, oracle_mod):
+    P, O = mst, oracle_mod
+    n = 1_000_000
+    # path with increasing weights: the hook forest is one chain of depth n
+    a = np.arange(n - 1, dtype=np.uint32)
+    _oracle_check(P, O, n, a, a + 1, np.arange(n - 1, dtype=np.uint32), shards=(2,))
+    # and decreasing weights
+    _oracle_check(P, O, n, a, a + 1, np.arange(n - 1, 0, -1, dtype=np.uint32), shards=())
+    # star: one hub component absorbs everything in round 1
+    _oracle_check(P, O, n, np.zeros(n - 1, dtype=np.uint32), a + 1,
+                  np.random.default_rng(0).permutation(n - 1).astype(np.uint32), shards=(2,))
+    # dense small graph (complete K_400) with random distinct weights
+    k = 400
+    iu = np.triu_indices(k, 1)
+    ws = np.random.default_rng(1).permutation(iu[0].size).astype(np.uint32)
+    _oracle_check(P, O, k, iu[0], iu[1], ws, shards=(3,))
+
+
+def test_workspace_reuse_across_sizes(mst, oracle_mod):
+    """Big, small, big, repeated: look-back epochs and grown buffers stay valid."""
+    from paper_2005_06913_b200 import configs as C
+    P, O = mst, oracle_mod
+    specs = [C.uniform(200_000, 1_000_000, seed=5), C.grid(3, 4, seed=1),
+             C.rmat(14, 8, seed=3), C.uniform(200_000, 1_000_000, seed=5)]
+    first = None
+    for spec in specs:
+        g = C.generate_host(spec)
+        k = O.kruskal(g.n, g.src, g.dst, g.w)
+        for _ in range(2):
+            r = P.boruvka_gpu(g)
+            assert r.mst_edges.tolist() == k.ids.tolist() and r.total_weight == k.total_weight
+        if first is None:
+            first = r.mst_edges
+    assert np.array_equal(first, r.mst_edges)
+
+
+@pytest.mark.parametrize("cfg", ["c0", "c1", "c2"])
+def test_baseline_configs_full_size(mst, oracle_mod, cfg):
+    from paper_2005_06913_b200 import configs as C
+    P, O = mst, oracle_mod
+    g = C.generate_host(C.CONFIGS[cfg])
+    k = O.kruskal(g.n, g.src, g.dst, g.w)
+    assert k.ids.size == g.n - 1
+    info = P.GpuRunInfo()
+    r = P.boruvka_gpu(g, info=info)
+    assert np.array_equal(r.mst_edges, k.ids.astype(np.int64)) and r.total_weight == k.total_weight
+    assert info.final_components == 1 and info.rounds == r.rounds >= 1
+    e = P.boruvka_gpu_emulated(g, 2)
+    assert np.array_equal(e.mst_edges, r.mst_edges)
+
+
+def test_c3_full_size(mst, oracle_mod):
+    """268 M edges: full oracle Kruskal (slow on CPU) plus structural checks."""
+    from paper_2005_06913_b200 import configs as C
+    P, O = mst, oracle_mod
+    g = C.generate_host(C.CONFIGS["c3"])
+    r = P.boruvka_gpu(g)
+    v = O.verify(g.n, g.src, g.dst, g.w, r.mst_edges.astype(np.uint32))
+    assert v["edge_count_ok"] and v["is_acyclic"] and v["is_spanning"]
+    assert v["total_weight"] == r.total_weight
+    k = O.kruskal(g.n, g.src, g.dst, g.w)
+    assert np.array_equal(r.mst_edges, k.ids.astype(np.int64)) and r.total_weight == k.total_weight
+
+
+@pytest.mark.skipif(os.environ.get("MST_FULL_PARITY") != "1", reason="set MST_FULL_PARITY=1 (c4, ~1.1 B edges)")
+def test_c4_full_size(mst, oracle_mod):
+    from paper_2005_06913_b200 import configs as C
+    P, O = mst, oracle_mod
+    g = C.generate_host(C.CONFIGS["c4"])
+    r = P.boruvka_gpu(g)
+    v = O.verify(g.n, g.src, g.dst, g.w, r.mst_edges.astype(np.uint32))
+    assert v["edge_count_ok"] and v["is_acyclic"] and v["is_spanning"]
+    e = P.boruvka_gpu_emulated(g, 2)
+    assert np.array_equal(e.mst_edges, r.mst_edges) and e.total_weight == r.total_weight
+    k = O.kruskal(g.n, g.src, g.dst, g.w)
+    assert np.array_equal(r.mst_edges, k.ids.astype(np.int64)) and r.total_weight == k.total_weight
+
+
+def test_gpu_generator_matches_host(mst):
+    import torch
+    from paper_2005_06913_b200 import configs as C
+    for spec in [C.uniform(10_000, 50_000, seed=4), C.grid(33, 65, seed=2), C.rmat(13, 16, seed=7),
+                 C.CONFIGS["c1"]]:
+        h = C.generate_host(spec)
+        n, m, s, d, w = C.generate_torch(spec)
+        assert n == h.n and m == h.edge_count()
+        assert np.array_equal(s.cpu().numpy().view(np.uint32), h.src)
+        assert np.array_equal(d.cpu().numpy().view(np.uint32), h.dst)
+        assert np.array_equal(w.cpu().numpy().view(np.uint32), h.w)
+        del s, d, w
+        torch.cuda.empty_cache()
+
+
+def test_device_resident_entry(mst, oracle_mod):
+    import torch
+    from paper_2005_06913_b200 import configs as C
+    P = mst
+    spec = C.uniform(100_000, 400_000, seed=8)
+    n, m, s, d, w = C.generate_torch(spec)
+    out = torch.empty(n, dtype=torch.int32, device="cuda")
+    hot = {}
+    info = P.GpuRunInfo()
+    count, total = P.boruvka_gpu_device(n, m, s.data_ptr(), d.data_ptr(), w.data_ptr(), out.data_ptr(),
+                                        torch.cuda.current_stream().cuda_stream, info=info, hot=hot)
+    h = C.generate_host(spec)
+    k = oracle_mod.kruskal(n, h.src, h.dst, h.w)
+    assert count == n - 1 and total == k.total_weight
+    assert np.array_equal(out[:count].cpu().numpy().view(np.uint32), k.ids)
+    assert hot["launches"] >= 2 and hot["ms"] > 0
+    assert info.alg_bytes > 12 * m
