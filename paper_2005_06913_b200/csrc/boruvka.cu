@@ -237,8 +237,11 @@ void init_counters(Workspace& ws, DevCounters* d_ctr, uint32_t n, uint64_t m) {
   DevCounters& h = ws.h_snap[kMaxR];
   std::memset(&h, 0, sizeof(h));
   h.n[1] = n;
+  h.m[0] = m;
   h.m[1] = m;
   h.stop_round = kNoStop;
+  h.phase_end = kNoStop;
+  h.pivot = 0xFFFFFFFFu;
   MST_CUDA_CHECK(cudaMemcpyAsync(d_ctr, &h, sizeof(DevCounters), cudaMemcpyHostToDevice, ws.stream));
 }
 
@@ -275,10 +278,43 @@ bool warp_prereduce_enabled() {
 
 // ------------------------------- single GPU ---------------------------------
 // Literal keys (w<<32 | index into this round's edge array): the hook reads
-// the winning edge directly. Host loop runs one round ahead of the device;
-// kernels of rounds past the stop early-exit on the device counters.
+// the winning edge directly. The host runs one round ahead of the device;
+// kernels of rounds past a stop early-exit on the device counters.
+//
+// Filter-Boruvka (default when m >= 3n): a sampled weight pivot splits the
+// edges; the round loop first runs on the light edges alone (phase B), then
+// one pass drops every heavy edge inside a light component (cycle property,
+// exact) and the loop continues on the survivors (phase D). Uniform and
+// R-MAT graphs keep most edges alive for many rounds otherwise
+// (sum m_r = 4.5-8.3 m).
+
+enum { kHotMin1 = 0, kHotCompact = 1, kHotSplit = 2, kHotHeavy = 3 };
+struct HotLaunch {
+  int ev;
+  int kind;
+  int r;
+  bool light;
+};
+
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return (e && *e) ? atoi(e) : dflt;
+}
+
+double env_double(const char* name, double dflt) {
+  const char* e = getenv(name);
+  return (e && *e) ? atof(e) : dflt;
+}
+
+bool filter_mode(uint32_t n, uint64_t m) {
+  const int f = env_int("MST_FILTER", -1);
+  if (f >= 0) return f > 0 && m > 0;
+  return m >= (uint64_t)3 * n && m >= (1u << 16);
+}
+
 template <class InView, bool kPre>
-void run_single_impl(Workspace& ws, InView in, uint32_t n, uint64_t m, RunOut& out, bool time_hot) {
+void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t wstride, uint32_t n,
+                     uint64_t m, RunOut& out, bool time_hot, bool filter) {
   cudaStream_t s = ws.stream;
   auto* d_ctr = ws.get<DevCounters>("ctr", 1);
   unsigned long long* minb[2] = {ws.get<unsigned long long>("minA", n),
@@ -289,77 +325,137 @@ void run_single_impl(Workspace& ws, InView in, uint32_t n, uint64_t m, RunOut& o
   uint32_t* mst = ws.get<uint32_t>("mst", n);
   uint4* E[2] = {ws.get<uint4>("E0", m), ws.get<uint4>("E1", m)};
   unsigned long long* st = ws.status_array(std::max(tiles_of(m), tiles_of(n)));
+  const Recover no_rec{nullptr, nullptr, nullptr};
+  const int dev = ws.device;
 
   init_counters(ws, d_ctr, n, m);
   MST_CUDA_CHECK(cudaMemsetAsync(minb[0], 0xFF, (size_t)n * 8, s));
   uint32_t launches = 0;
   int tix = 0;
+  std::vector<HotLaunch> hot;
   auto tmark = [&]() {
     if (time_hot) MST_CUDA_CHECK(cudaEventRecord(ws.tev[tix++], s));
   };
-  std::vector<std::pair<int, int>> hot_pairs;  // (start idx, round)
+  auto hot_begin = [&](int kind, int r, bool light) {
+    if (time_hot) hot.push_back(HotLaunch{tix, kind, r, light});
+    tmark();
+  };
 
-  {
+  if (filter) {
+    uint32_t* hist = ws.get<uint32_t>("hist", 65536);
+    MST_CUDA_CHECK(cudaMemsetAsync(hist, 0, 65536 * sizeof(uint32_t), s));
+    const uint32_t samples = (uint32_t)std::min<uint64_t>(m, 1u << 20);
+    const uint64_t step = std::max<uint64_t>(1, m / samples);
+    k_weight_hist<<<std::max(1u, samples / 1024), 256, 0, s>>>(wbase, wstride, m, step, samples, hist);
+    const double beta = env_double("MST_FILTER_BETA", 2.0);
+    const double frac = std::min(1.0, beta * (double)n / (double)m);
+    const uint32_t target = (uint32_t)std::max(1.0, frac * samples);
+    k_pick_pivot<<<1, 1024, 0, s>>>(hist, target, d_ctr);
+    launches += 2;
+    auto kc = k_compact<InView, false, kPre, kFilterLight>;
+    hot_begin(kHotSplit, 0, true);
+    kc<<<persistent_grid(kc, dev, tiles_of(m)), kBlock, 0, s>>>(in, E[1], nullptr, minb[0], no_rec, n, d_ctr,
+                                                               0, st, ws.next_epoch(), kSlotCompact, 0);
+    tmark();
+    ++launches;
+  } else {
     auto kmin = k_min_round1<InView, false, kPre>;
     const unsigned g = (unsigned)std::max<uint64_t>(
-        1, std::min<uint64_t>((m + kBlock - 1) / kBlock, (uint64_t)sm_count(ws.device) * blocks_per_sm(kmin)));
-    const int t0 = tix;
-    tmark();
+        1, std::min<uint64_t>((m + kBlock - 1) / kBlock, (uint64_t)sm_count(dev) * blocks_per_sm(kmin)));
+    hot_begin(kHotMin1, 0, false);
     kmin<<<g, kBlock, 0, s>>>(in, n, m, minb[0], d_ctr);
     tmark();
-    if (time_hot) hot_pairs.push_back({t0, 0});
     ++launches;
   }
 
+  bool light = filter;
+  std::vector<std::pair<uint32_t*, int>> levels;  // light-phase relabel maps (buffer, round)
   uint64_t n_bound = n, m_bound = m;
-  int r = 1;
-  int stop = 0;
+  int r = 1, loop_start = 1;
+  int phase_end = 0;
+  DevCounters snap_b{};  // counters at the end of the light phase
   while (true) {
     if (r > MST_MAX_ROUNDS) throw MstError{MST_ERR_STALL, "no convergence within MST_MAX_ROUNDS rounds"};
     unsigned long long* mcur = minb[(r - 1) & 1];
     unsigned long long* mnext = minb[r & 1];
-    uint4* Eout = E[(r - 1) & 1];
+    uint4* Eout = E[(r + 1) & 1];
+    const bool original_in = (r == 1 && !filter);
     const uint32_t ep_h = ws.next_epoch(), ep_c = ws.next_epoch();
-    if (r == 1) {
+    if (original_in) {
       auto kh = k_hook<InView, false>;
-      kh<<<persistent_grid(kh, ws.device, tiles_of(n_bound)), kBlock, 0, s>>>(
-          in, mcur, parent, rootlabel, mst, n, d_ctr, r, st, ep_h);
+      kh<<<persistent_grid(kh, dev, tiles_of(n_bound)), kBlock, 0, s>>>(in, mcur, parent, rootlabel, mst, n,
+                                                                        d_ctr, r, st, ep_h, (int)light);
     } else {
       auto kh = k_hook<PackedView, false>;
-      kh<<<persistent_grid(kh, ws.device, tiles_of(n_bound)), kBlock, 0, s>>>(
-          PackedView{E[r & 1]}, mcur, parent, rootlabel, mst, n, d_ctr, r, st, ep_h);
+      kh<<<persistent_grid(kh, dev, tiles_of(n_bound)), kBlock, 0, s>>>(
+          PackedView{E[r & 1]}, mcur, parent, rootlabel, mst, n, d_ctr, r, st, ep_h, (int)light);
+    }
+    uint32_t* Lr = L;
+    if (light) {
+      Lr = ws.get<uint32_t>("Llvl" + std::to_string(r), n_bound);
+      levels.push_back({Lr, r});
     }
     {
       const unsigned g = (unsigned)std::max<uint64_t>(
-          1, std::min<uint64_t>((n_bound + kBlock - 1) / kBlock,
-                                (uint64_t)sm_count(ws.device) * blocks_per_sm(k_label)));
-      k_label<<<g, kBlock, 0, s>>>(parent, rootlabel, L, mnext, d_ctr, r);
+          1, std::min<uint64_t>((n_bound + kBlock - 1) / kBlock, (uint64_t)sm_count(dev) * blocks_per_sm(k_label)));
+      k_label<<<g, kBlock, 0, s>>>(parent, rootlabel, Lr, mnext, d_ctr, r);
     }
-    const int t0 = tix;
-    tmark();
-    if (r == 1) {
-      auto kc = k_compact<InView, false, kPre>;
-      kc<<<persistent_grid(kc, ws.device, tiles_of(m_bound)), kBlock, 0, s>>>(
-          in, Eout, L, mnext, Recover{nullptr, nullptr, nullptr}, n, d_ctr, r, st, ep_c);
+    hot_begin(kHotCompact, r, light);
+    if (original_in) {
+      auto kc = k_compact<InView, false, kPre, kFilterNone>;
+      kc<<<persistent_grid(kc, dev, tiles_of(m_bound)), kBlock, 0, s>>>(in, Eout, Lr, mnext, no_rec, n, d_ctr, r, st,
+                                                                       ep_c, kSlotCompact, (int)light);
     } else {
-      auto kc = k_compact<PackedView, false, kPre>;
-      kc<<<persistent_grid(kc, ws.device, tiles_of(m_bound)), kBlock, 0, s>>>(
-          PackedView{E[r & 1]}, Eout, L, mnext, Recover{nullptr, nullptr, nullptr}, n, d_ctr, r, st,
-          ep_c);
+      auto kc = k_compact<PackedView, false, kPre, kFilterNone>;
+      kc<<<persistent_grid(kc, dev, tiles_of(m_bound)), kBlock, 0, s>>>(
+          PackedView{E[r & 1]}, Eout, Lr, mnext, no_rec, n, d_ctr, r, st, ep_c, kSlotCompact, (int)light);
     }
     tmark();
-    if (time_hot) hot_pairs.push_back({t0, r});
     launches += 3;
     MST_CUDA_CHECK(cudaGetLastError());
     MST_CUDA_CHECK(cudaMemcpyAsync(&ws.h_snap[r], d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
     MST_CUDA_CHECK(cudaEventRecord(ws.ev[r], s));
-    if (r >= 2) {
+    if (r > loop_start) {
       MST_CUDA_CHECK(cudaEventSynchronize(ws.ev[r - 1]));
       const DevCounters& snap = ws.h_snap[r - 1];
       if (snap.err) break;
-      if (snap.stop_round != kNoStop && (int)snap.stop_round <= r) {
-        stop = (int)snap.stop_round;
-        break;
+      if (snap.stop_round != kNoStop && (int)snap.stop_round <= r) break;
+      if (light && snap.phase_end != kNoStop && (int)snap.phase_end <= r) {
+        phase_end = (int)snap.phase_end;
+        snap_b = snap;
+        if (phase_end == 1) {
+          // not a single light non-loop edge: run the plain loop instead
+          MST_CUDA_CHECK(cudaStreamSynchronize(s));
+          RunOut plain;
+          run_single_impl<InView, kPre>(ws, in, wbase, wstride, n, m, plain, time_hot, false);
+          plain.launches += launches;
+          out = plain;
+          return;
+        }
+        while (!levels.empty() && levels.back().second >= phase_end) levels.pop_back();
+        for (int k = (int)levels.size() - 2; k >= 0; --k) {
+          const unsigned g = (unsigned)std::max<uint64_t>(
+              1, std::min<uint64_t>((snap.n[levels[k].second] + 255) / 256, (uint64_t)sm_count(dev) * 8));
+          k_compose<<<g, 256, 0, s>>>(levels[k].first, levels[k + 1].first, d_ctr, levels[k].second);
+          ++launches;
+        }
+        const uint32_t* vlabel = levels.empty() ? nullptr : levels[0].first;
+        MST_CUDA_CHECK(cudaMemsetAsync(&d_ctr->phase_end, 0xFF, sizeof(unsigned int), s));
+        const int R1 = phase_end;
+        auto kc = k_compact<InView, false, kPre, kFilterHeavy>;
+        hot_begin(kHotHeavy, R1, false);
+        kc<<<persistent_grid(kc, dev, tiles_of(m)), kBlock, 0, s>>>(in, E[R1 & 1], vlabel, minb[(R1 - 1) & 1],
+                                                                   no_rec, n, d_ctr, R1, st, ws.next_epoch(),
+                                                                   kSlotFilter, 0);
+        tmark();
+        ++launches;
+        MST_CUDA_CHECK(cudaGetLastError());
+        light = false;
+        r = R1;
+        loop_start = R1;
+        n_bound = snap.n[R1];
+        m_bound = m;
+        continue;
       }
       n_bound = snap.n[r];
       m_bound = snap.m[r];
@@ -372,22 +468,31 @@ void run_single_impl(Workspace& ws, InView in, uint32_t n, uint64_t m, RunOut& o
   out.err = c.err;
   out.launches = launches;
   if (c.err) return;
-  stop = (int)c.stop_round;
+  const int stop = (int)c.stop_round;
   if (c.stop_round == kNoStop) throw MstError{MST_ERR_STALL, "round loop ended without a stop verdict"};
   out.rounds = (uint32_t)stop - 1;
   out.final_components = c.n[stop];
   out.count = (uint64_t)n - out.final_components;
   out.total_weight = c.total_weight;
   if (time_hot) {
-    for (auto& hp : hot_pairs) {
-      const int rr = hp.second;
-      if (rr != 0 && rr + 1 >= stop) continue;  // early-exited launch
-      out.ms_hot += ms_between(ws.tev[hp.first], ws.tev[hp.first + 1]);
+    for (const HotLaunch& h : hot) {
+      uint64_t bytes = 0;
+      if (h.kind == kHotMin1) {
+        bytes = 12ull * m;
+      } else if (h.kind == kHotSplit) {
+        bytes = 12ull * m + 16ull * c.m[1];
+      } else if (h.kind == kHotHeavy) {
+        bytes = 12ull * m + 16ull * c.m[h.r];
+      } else {
+        const bool ran = h.r + 1 < stop && (!h.light || phase_end == 0 || h.r < phase_end);
+        if (!ran) continue;
+        const DevCounters& cc = (h.light && phase_end) ? snap_b : c;
+        const uint64_t in_bytes = (h.r == 1 && !filter) ? 12ull : 16ull;
+        bytes = in_bytes * cc.m[h.r] + 16ull * cc.m[h.r + 1];
+      }
+      out.ms_hot += ms_between(ws.tev[h.ev], ws.tev[h.ev + 1]);
       out.hot_launches += 1;
-      if (rr == 0)
-        out.hot_bytes += 12ull * m;
-      else
-        out.hot_bytes += (rr == 1 ? 12ull : 16ull) * c.m[rr] + 16ull * c.m[rr + 1];
+      out.hot_bytes += bytes;
     }
   }
 }
@@ -501,16 +606,19 @@ RunOut run_single(const SingleArgs& a, mst_stats_t* stats) {
   const bool pre = warp_prereduce_enabled();
   if (a.kind == 0) {
     SoaView v{src, dst, w, 0};
+    const bool filt = filter_mode(a.n, a.m);
     if (pre)
-      run_single_impl<SoaView, true>(ws, v, a.n, a.m, o, a.time_hot);
+      run_single_impl<SoaView, true>(ws, v, w, 1, a.n, a.m, o, a.time_hot, filt);
     else
-      run_single_impl<SoaView, false>(ws, v, a.n, a.m, o, a.time_hot);
+      run_single_impl<SoaView, false>(ws, v, w, 1, a.n, a.m, o, a.time_hot, filt);
   } else {
     AosView v{reinterpret_cast<const uint4*>(aos), 0};
+    const uint32_t* wb = reinterpret_cast<const uint32_t*>(aos) + 2;
+    const bool filt = filter_mode(a.n, a.m);
     if (pre)
-      run_single_impl<AosView, true>(ws, v, a.n, a.m, o, a.time_hot);
+      run_single_impl<AosView, true>(ws, v, wb, 4, a.n, a.m, o, a.time_hot, filt);
     else
-      run_single_impl<AosView, false>(ws, v, a.n, a.m, o, a.time_hot);
+      run_single_impl<AosView, false>(ws, v, wb, 4, a.n, a.m, o, a.time_hot, filt);
   }
   check_err_bits(o.err);
   uint32_t* d_mst = ws.get<uint32_t>("mst", a.n);
@@ -644,11 +752,11 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, RunOu
       if (r == 1) {
         auto kh = k_hook<SoaView, true>;
         kh<<<persistent_grid(kh, ws.device, tiles_of(n_bound)), kBlock, 0, ws.stream>>>(
-            s.in, s.minb[cur], s.parent, s.rootlabel, s.mstpos, n, s.d_ctr, r, s.st, ep_h);
+            s.in, s.minb[cur], s.parent, s.rootlabel, s.mstpos, n, s.d_ctr, r, s.st, ep_h, 0);
       } else {
         auto kh = k_hook<PackedView, true>;
         kh<<<persistent_grid(kh, ws.device, tiles_of(n_bound)), kBlock, 0, ws.stream>>>(
-            PackedView{s.E[r & 1]}, s.minb[cur], s.parent, s.rootlabel, s.mstpos, n, s.d_ctr, r, s.st, ep_h);
+            PackedView{s.E[r & 1]}, s.minb[cur], s.parent, s.rootlabel, s.mstpos, n, s.d_ctr, r, s.st, ep_h, 0);
       }
       const unsigned gl = (unsigned)std::max<uint64_t>(
           1, std::min<uint64_t>((n_bound + kBlock - 1) / kBlock,
@@ -661,13 +769,13 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, RunOu
       Recover rec{s.minb[cur], s.mstpos, s.slots};
       uint4* Eout = s.E[(r - 1) & 1];
       if (r == 1) {
-        auto kc = k_compact<SoaView, true, kPre>;
+        auto kc = k_compact<SoaView, true, kPre, kFilterNone>;
         kc<<<persistent_grid(kc, ws.device, tiles_of(m_bound)), kBlock, 0, ws.stream>>>(
-            s.in, Eout, s.L, s.minb[nxt], rec, n, s.d_ctr, r, s.st, ep_c);
+            s.in, Eout, s.L, s.minb[nxt], rec, n, s.d_ctr, r, s.st, ep_c, kSlotCompact, 0);
       } else {
-        auto kc = k_compact<PackedView, true, kPre>;
+        auto kc = k_compact<PackedView, true, kPre, kFilterNone>;
         kc<<<persistent_grid(kc, ws.device, tiles_of(m_bound)), kBlock, 0, ws.stream>>>(
-            PackedView{s.E[r & 1]}, Eout, s.L, s.minb[nxt], rec, n, s.d_ctr, r, s.st, ep_c);
+            PackedView{s.E[r & 1]}, Eout, s.L, s.minb[nxt], rec, n, s.d_ctr, r, s.st, ep_c, kSlotCompact, 0);
       }
       launches += 3;
       MST_CUDA_CHECK(cudaGetLastError());

@@ -41,7 +41,7 @@ constexpr uint32_t kErrWeight = 2u;
 constexpr uint32_t kNoStop = 0xFFFFFFFFu;
 
 // Tile-counter slots per round.
-enum { kSlotHook = 0, kSlotCompact = 1, kSlotSort = 2, kSlotSpare = 3 };
+enum { kSlotHook = 0, kSlotCompact = 1, kSlotSort = 2, kSlotFilter = 3 };
 
 // Per-call device counters. Round r (1-based) reads n[r], m[r] and writes
 // n[r+1], m[r+1]; nothing is reset between rounds, so the whole round
@@ -52,6 +52,8 @@ struct DevCounters {
   unsigned int tile[kMaxR][4];
   unsigned int err;
   unsigned int stop_round;  // first round whose hook must not run
+  unsigned int phase_end;   // first round past the light phase (Filter-Boruvka)
+  unsigned int pivot;       // light edges: w < pivot
   unsigned long long total_weight;
 };
 
@@ -293,12 +295,13 @@ __global__ void __launch_bounds__(kBlock) k_hook(View E, const unsigned long lon
                                                  uint32_t* __restrict__ rootlabel,
                                                  uint32_t* __restrict__ mst_or_pos, uint32_t n_orig,
                                                  DevCounters* ctr, int r,
-                                                 unsigned long long* status, uint32_t epoch) {
+                                                 unsigned long long* status, uint32_t epoch,
+                                                 int light_phase) {
   __shared__ uint32_t s_scan[32];
   __shared__ uint32_t s_misc[2];
   __shared__ uint32_t s_tile;
   __shared__ unsigned long long s_wsum[kWarps];
-  if ((uint32_t)r >= ctr->stop_round) return;
+  if ((uint32_t)r >= ctr->stop_round || (uint32_t)r >= ctr->phase_end) return;
   const uint32_t n_r = ctr->n[r];
   const uint32_t mst_base = n_orig - n_r;
   const uint32_t ntiles = (uint32_t)(((uint64_t)n_r + kTile - 1) / kTile);
@@ -366,7 +369,16 @@ __global__ void __launch_bounds__(kBlock) k_hook(View E, const unsigned long lon
     if (tile == ntiles - 1 && threadIdx.x == 0) {
       const uint32_t roots = prefix + total;
       ctr->n[r + 1] = roots;
-      if (roots <= 1 || roots == n_r) ctr->stop_round = (uint32_t)r + 1;
+      if (roots <= 1) {
+        ctr->stop_round = (uint32_t)r + 1;
+      } else if (roots == n_r) {
+        // no live edge anywhere: done (a forest if roots > 1), unless this is
+        // the light phase of Filter-Boruvka, which then simply ends
+        if (light_phase)
+          ctr->phase_end = (uint32_t)r;
+        else
+          ctr->stop_round = (uint32_t)r + 1;
+      }
     }
     __syncthreads();
   }
@@ -387,7 +399,7 @@ __global__ void __launch_bounds__(kBlock) k_label(uint32_t* __restrict__ parent,
                                                   uint32_t* __restrict__ L,
                                                   unsigned long long* __restrict__ min_next,
                                                   DevCounters* ctr, int r) {
-  if ((uint32_t)r + 1 >= ctr->stop_round) return;
+  if ((uint32_t)r + 1 >= ctr->stop_round || (uint32_t)r >= ctr->phase_end) return;
   const uint32_t n_r = ctr->n[r];
   const uint32_t n_next = ctr->n[r + 1];
   const uint64_t stride = (uint64_t)gridDim.x * kBlock;
@@ -408,23 +420,36 @@ struct Recover {
   uint32_t* __restrict__ slots;
 };
 
-template <class View, bool kKeyPartner, bool kWarpPre>
+// kFilter selects the edge predicate of the pass:
+//   kFilterNone  : round r of the plain loop: keep a != b after relabelling
+//   kFilterLight : the split pass of Filter-Boruvka (over the caller's list,
+//                  labels = vertex ids): keep the light edges w < pivot
+//   kFilterHeavy : the filter pass (caller's list, labels = the light-phase
+//                  components): keep heavy edges w >= pivot whose endpoints
+//                  lie in different light components. Heavier edges closing
+//                  a cycle of lighter ones are never in the MST (cycle
+//                  property), so dropping them is exact.
+enum { kFilterNone = 0, kFilterLight = 1, kFilterHeavy = 2 };
+
+template <class View, bool kKeyPartner, bool kWarpPre, int kFilter>
 __global__ void __launch_bounds__(kBlock) k_compact(View Ein, uint4* __restrict__ Eout,
                                                     const uint32_t* __restrict__ L,
                                                     unsigned long long* __restrict__ min_next,
                                                     Recover rec, uint32_t n_orig, DevCounters* ctr,
                                                     int r, unsigned long long* status,
-                                                    uint32_t epoch) {
+                                                    uint32_t epoch, int slot, int light_phase) {
   __shared__ uint32_t s_scan[32];
   __shared__ uint32_t s_misc[2];
   __shared__ uint32_t s_tile;
   const uint32_t stop = ctr->stop_round;
+  if ((uint32_t)r >= ctr->phase_end) return;
   const bool full = (uint32_t)r + 1 < stop;
   if (!full && !(kKeyPartner && (uint32_t)r < stop)) return;
-  const uint64_t m_r = ctr->m[r];
+  const uint64_t m_r = kFilter == kFilterHeavy ? ctr->m[0] : ctr->m[r];
+  const uint32_t pivot = ctr->pivot;
   const uint32_t ntiles = (uint32_t)((m_r + kTile - 1) / kTile);
   while (true) {
-    if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->tile[r][kSlotCompact], 1u);
+    if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->tile[r][slot], 1u);
     __syncthreads();
     const uint32_t tile = s_tile;
     if (tile >= ntiles) break;
@@ -442,7 +467,12 @@ __global__ void __launch_bounds__(kBlock) k_compact(View Ein, uint4* __restrict_
       const uint64_t i = (uint64_t)tile * kTile + k * kBlock + threadIdx.x;
       if (i < m_r) {
         bool ok = true;
-        if (View::kOriginal) ok = e[k].a < n_orig && e[k].b < n_orig && e[k].ok;
+        if (View::kOriginal) {
+          ok = e[k].a < n_orig && e[k].b < n_orig && e[k].ok;
+          if (!ok) atomicOr(&ctr->err, (e[k].a < n_orig && e[k].b < n_orig) ? kErrWeight : kErrRange);
+        }
+        if (kFilter == kFilterLight) ok = ok && e[k].w < pivot;
+        if (kFilter == kFilterHeavy) ok = ok && e[k].w >= pivot;
         if (ok) {
           if (kKeyPartner) {
             const unsigned long long hi = (unsigned long long)e[k].w << 32;
@@ -456,8 +486,10 @@ __global__ void __launch_bounds__(kBlock) k_compact(View Ein, uint4* __restrict_
             }
           }
           if (full) {
-            e[k].a = __ldg(L + e[k].a);
-            e[k].b = __ldg(L + e[k].b);
+            if (kFilter == kFilterNone || (kFilter == kFilterHeavy && L != nullptr)) {
+              e[k].a = __ldg(L + e[k].a);
+              e[k].b = __ldg(L + e[k].b);
+            }
             keep[k] = e[k].a != e[k].b;
           }
         }
@@ -482,12 +514,67 @@ __global__ void __launch_bounds__(kBlock) k_compact(View Ein, uint4* __restrict_
     if (tile == ntiles - 1 && threadIdx.x == 0) {
       const uint32_t kept = prefix + total;
       ctr->m[r + 1] = kept;
-      // sharded mode: a shard running dry says nothing about the others;
-      // termination comes from the replicated hook there
-      if (!kKeyPartner && kept == 0 && ctr->stop_round == kNoStop) ctr->stop_round = (uint32_t)r + 1;
+      // A light phase running dry ends the phase (the filter pass follows);
+      // a sharded shard running dry says nothing about the others (the
+      // replicated hook decides there); otherwise no edges left = done.
+      if (kept == 0 && kFilter == kFilterNone) {
+        if (light_phase)
+          ctr->phase_end = (uint32_t)r + 1;
+        else if (!kKeyPartner && ctr->stop_round == kNoStop)
+          ctr->stop_round = (uint32_t)r + 1;
+      }
     }
     __syncthreads();
   }
+}
+
+// Pivot of the split: histogram of the top 16 weight bits over a strided
+// sample, then the smallest bin boundary with >= target sampled weights
+// below it (kept in ctr->pivot; 0xFFFFFFFF means "everything light").
+__global__ void k_weight_hist(const uint32_t* __restrict__ w, uint32_t wstride, uint64_t m,
+                              uint64_t step, uint32_t samples, uint32_t* __restrict__ hist) {
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < samples; k += gridDim.x * blockDim.x) {
+    const uint64_t i = (uint64_t)k * step;
+    if (i < m) atomicAdd(hist + (__ldg(w + i * wstride) >> 16), 1u);
+  }
+}
+
+__global__ void k_pick_pivot(const uint32_t* __restrict__ hist, uint32_t target, DevCounters* ctr) {
+  // one block of 1024 threads: 64 bins per thread, block scan of sums
+  __shared__ uint32_t s_sum[1024];
+  const uint32_t t = threadIdx.x;
+  uint32_t sum = 0;
+  for (int i = 0; i < 64; ++i) sum += hist[t * 64 + i];
+  s_sum[t] = sum;
+  __syncthreads();
+  for (int d = 1; d < 1024; d <<= 1) {
+    const uint32_t v = t >= (uint32_t)d ? s_sum[t - d] : 0u;
+    __syncthreads();
+    s_sum[t] += v;
+    __syncthreads();
+  }
+  const uint32_t before = t ? s_sum[t - 1] : 0u;
+  if (before < target && s_sum[t] >= target) {
+    uint32_t run = before;
+    for (int i = 0; i < 64; ++i) {
+      run += hist[t * 64 + i];
+      if (run >= target) {
+        const uint32_t bin = t * 64 + i;
+        ctr->pivot = bin == 0xFFFFu ? 0xFFFFFFFFu : (bin + 1) << 16;
+        break;
+      }
+    }
+  }
+}
+
+// Top-down composition of the light phase's relabel maps:
+// L_r[c] = L_{r+1}[L_r[c]] for c < n[r] (in place on level r).
+__global__ void k_compose(uint32_t* __restrict__ Lr, const uint32_t* __restrict__ Lnext,
+                          const DevCounters* ctr, int r) {
+  const uint32_t n_r = ctr->n[r];
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n_r; c += stride)
+    Lr[c] = __ldg(Lnext + Lr[c]);
 }
 
 // ------------------------------ result -------------------------------------

@@ -21,13 +21,38 @@ def mst():
     return P
 
 
-def _check(P, n, src, dst, w, ids, total, shards=(2, 3)):
+class _env:
+    """Force a single-GPU mode for one call (MST_FILTER / MST_FILTER_BETA)."""
+
+    def __init__(self, **kv):
+        self.kv = kv
+
+    def __enter__(self):
+        self.old = {k: os.environ.get(k) for k in self.kv}
+        os.environ.update({k: str(v) for k, v in self.kv.items()})
+
+    def __exit__(self, *a):
+        for k, v in self.old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+# plain round loop, and Filter-Boruvka with a small / default / large light set
+MODES = [dict(MST_FILTER=0), dict(MST_FILTER=1, MST_FILTER_BETA=0.3),
+         dict(MST_FILTER=1, MST_FILTER_BETA=2), dict(MST_FILTER=1, MST_FILTER_BETA=50)]
+
+
+def _check(P, n, src, dst, w, ids, total, shards=(2, 3), modes=MODES):
     g = P.Graph(n, src, dst, w)
-    r = P.boruvka_gpu(g)
-    assert r.mst_edges.tolist() == list(ids), "single-GPU edge set differs from the oracle"
-    assert r.total_weight == int(total)
-    a = P.boruvka_gpu_aos(n, g.to_aos())
-    assert a.mst_edges.tolist() == list(ids) and a.total_weight == int(total)
+    for mode in modes:
+        with _env(**mode):
+            r = P.boruvka_gpu(g)
+            assert r.mst_edges.tolist() == list(ids), f"single-GPU edge set differs from the oracle ({mode})"
+            assert r.total_weight == int(total)
+            a = P.boruvka_gpu_aos(n, g.to_aos())
+            assert a.mst_edges.tolist() == list(ids) and a.total_weight == int(total)
     for s in shards:
         e = P.boruvka_gpu_emulated(g, s)
         assert e.mst_edges.tolist() == list(ids), f"{s}-shard edge set differs"
@@ -38,7 +63,7 @@ def test_small_golden_graphs(mst):
     # hand graphs of the reference tests + 200 random graphs checked against
     # brute force (tests/golden/make_golden.py)
     for name, n, src, dst, w, ids, total in small_cases():
-        _check(mst, n, src, dst, w, ids, total, shards=(2,))
+        _check(mst, n, src, dst, w, ids, total, shards=(2,), modes=MODES[:2])
 
 
 @pytest.mark.parametrize("path", golden_gen_files(), ids=lambda p: p.stem)
@@ -96,12 +121,24 @@ def test_edge_cases(mst, oracle_mod):
     dst = np.concatenate([rng.integers(0, np.arange(1, n)), rng.integers(0, n, m - n + 1)]).astype(np.uint32)
     w = rng.integers(0, 50, m).astype(np.uint32)
     k = O.kruskal(n, src, dst, w)
-    r = P.boruvka_gpu(P.Graph(n, src, dst, w))
-    assert r.mst_edges.tolist() == k.ids.tolist() and r.total_weight == k.total_weight
-    # all weights equal
+    for mode in MODES:
+        with _env(**mode):
+            r = P.boruvka_gpu(P.Graph(n, src, dst, w))
+            assert r.mst_edges.tolist() == k.ids.tolist() and r.total_weight == k.total_weight
+    # all weights equal (the filter pivot then splits nothing off)
     w0 = np.zeros(m, dtype=np.uint32)
     k = O.kruskal(n, src, dst, w0)
-    assert P.boruvka_gpu(P.Graph(n, src, dst, w0)).mst_edges.tolist() == k.ids.tolist()
+    for mode in MODES:
+        with _env(**mode):
+            assert P.boruvka_gpu(P.Graph(n, src, dst, w0)).mst_edges.tolist() == k.ids.tolist()
+    # only self-loops are light: the light phase is empty
+    sl = np.concatenate([np.arange(50, dtype=np.uint32), src])
+    dl = np.concatenate([np.arange(50, dtype=np.uint32), dst])
+    wl = np.concatenate([np.zeros(50, dtype=np.uint32), w + 1000])
+    k = O.kruskal(n, sl, dl, wl)
+    for mode in MODES:
+        with _env(**mode):
+            assert P.boruvka_gpu(P.Graph(n, sl, dl, wl)).mst_edges.tolist() == k.ids.tolist()
 
 
 def test_disconnected_returns_forest(mst, oracle_mod):
@@ -110,11 +147,13 @@ def test_disconnected_returns_forest(mst, oracle_mod):
     dst = np.array([1, 2, 2, 4, 5, 5], dtype=np.uint32)
     w = np.array([1, 2, 3, 4, 5, 6], dtype=np.uint32)
     for n in (6, 9):  # 9: three isolated vertices too
-        with pytest.raises(P.GraphError) as ei:
-            P.boruvka_gpu(P.Graph(n, src, dst, w))
-        assert ei.value.kind == "Disconnected"
-        f = ei.value.forest
-        assert f.mst_edges.tolist() == O.kruskal(n, src, dst, w).ids.tolist() == [0, 1, 3, 4]
+        for mode in MODES:
+            with _env(**mode):
+                with pytest.raises(P.GraphError) as ei:
+                    P.boruvka_gpu(P.Graph(n, src, dst, w))
+                assert ei.value.kind == "Disconnected"
+                f = ei.value.forest
+                assert f.mst_edges.tolist() == O.kruskal(n, src, dst, w).ids.tolist() == [0, 1, 3, 4]
         with pytest.raises(P.GraphError):
             P.boruvka_gpu_emulated(P.Graph(n, src, dst, w), 2)
     with pytest.raises(P.GraphError) as ei:
@@ -124,17 +163,21 @@ def test_disconnected_returns_forest(mst, oracle_mod):
 
 def test_input_errors(mst):
     P = mst
-    with pytest.raises(P.GraphError) as ei:
-        P.boruvka_gpu(P.Graph(3, [0, 3], [1, 2], [1, 2]))
-    assert ei.value.kind == "EndpointOutOfRange"
+    for mode in MODES:
+        with _env(**mode):
+            with pytest.raises(P.GraphError) as ei:
+                P.boruvka_gpu(P.Graph(3, [0, 3], [1, 2], [1, 2]))
+            assert ei.value.kind == "EndpointOutOfRange"
     with pytest.raises(P.GraphError) as ei:
         P.boruvka_gpu_emulated(P.Graph(3, [0, 1], [1, 7], [1, 2]), 2)
     assert ei.value.kind == "EndpointOutOfRange"
     aos = P.Graph(3, [0, 1], [1, 2], [1, 2]).to_aos()
     aos["weight"][1] = 2**32 + 5
-    with pytest.raises(P.GraphError) as ei:
-        P.boruvka_gpu_aos(3, aos)
-    assert ei.value.kind == "WeightOverflow"
+    for mode in MODES:
+        with _env(**mode):
+            with pytest.raises(P.GraphError) as ei:
+                P.boruvka_gpu_aos(3, aos)
+            assert ei.value.kind == "WeightOverflow"
 
 
 def test_adversarial_shapes(mst, oracle_mod):
@@ -180,10 +223,12 @@ def test_baseline_configs_full_size(mst, oracle_mod, cfg):
     g = C.generate_host(C.CONFIGS[cfg])
     k = O.kruskal(g.n, g.src, g.dst, g.w)
     assert k.ids.size == g.n - 1
-    info = P.GpuRunInfo()
-    r = P.boruvka_gpu(g, info=info)
-    assert np.array_equal(r.mst_edges, k.ids.astype(np.int64)) and r.total_weight == k.total_weight
-    assert info.final_components == 1 and info.rounds == r.rounds >= 1
+    for mode in (MODES[0], MODES[2]):
+        with _env(**mode):
+            info = P.GpuRunInfo()
+            r = P.boruvka_gpu(g, info=info)
+            assert np.array_equal(r.mst_edges, k.ids.astype(np.int64)) and r.total_weight == k.total_weight
+            assert info.final_components == 1 and info.rounds == r.rounds >= 1
     e = P.boruvka_gpu_emulated(g, 2)
     assert np.array_equal(e.mst_edges, r.mst_edges)
 
@@ -193,7 +238,10 @@ def test_c3_full_size(mst, oracle_mod):
     from paper_2005_06913_b200 import configs as C
     P, O = mst, oracle_mod
     g = C.generate_host(C.CONFIGS["c3"])
+    with _env(MST_FILTER=0):
+        r0 = P.boruvka_gpu(g)
     r = P.boruvka_gpu(g)
+    assert np.array_equal(r.mst_edges, r0.mst_edges) and r.total_weight == r0.total_weight
     v = O.verify(g.n, g.src, g.dst, g.w, r.mst_edges.astype(np.uint32))
     assert v["edge_count_ok"] and v["is_acyclic"] and v["is_spanning"]
     assert v["total_weight"] == r.total_weight
