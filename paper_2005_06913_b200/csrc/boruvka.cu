@@ -444,8 +444,9 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
         const int R1 = phase_end;
         auto kc = k_compact<InView, false, kPre, kFilterHeavy>;
         hot_begin(kHotHeavy, R1, false);
+        // launched as round R1-1's producer: it writes m[R1] and E/min of round R1
         kc<<<persistent_grid(kc, dev, tiles_of(m)), kBlock, 0, s>>>(in, E[R1 & 1], vlabel, minb[(R1 - 1) & 1],
-                                                                   no_rec, n, d_ctr, R1, st, ws.next_epoch(),
+                                                                   no_rec, n, d_ctr, R1 - 1, st, ws.next_epoch(),
                                                                    kSlotFilter, 0);
         tmark();
         ++launches;

@@ -539,7 +539,7 @@ __global__ void k_weight_hist(const uint32_t* __restrict__ w, uint32_t wstride, 
   }
 }
 
-__global__ void k_pick_pivot(const uint32_t* __restrict__ hist, uint32_t target, DevCounters* ctr) {
+__global__ void __launch_bounds__(1024) k_pick_pivot(const uint32_t* __restrict__ hist, uint32_t target, DevCounters* ctr) {
   // one block of 1024 threads: 64 bins per thread, block scan of sums
   __shared__ uint32_t s_sum[1024];
   const uint32_t t = threadIdx.x;
