@@ -211,6 +211,16 @@ unsigned persistent_grid(K kernel, int device, uint64_t tiles) {
 }
 
 uint64_t tiles_of(uint64_t count) { return (count + kTile - 1) / kTile; }
+uint64_t tiles_c(uint64_t count) { return (count + kCTile - 1) / kCTile; }
+
+// Read-before-atomic pays off while the min table stays L2-resident.
+int filt_for(uint64_t table_entries) {
+  static const long long limit = [] {
+    const char* e = getenv("MST_FILTER_TABLE_MB");
+    return (long long)((e && *e) ? atof(e) : 48.0) << 20;
+  }();
+  return table_entries * 8 <= (uint64_t)limit ? 1 : 0;
+}
 
 double ms_between(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0;
@@ -354,8 +364,9 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     launches += 2;
     auto kc = k_compact<InView, false, kPre, kFilterLight>;
     hot_begin(kHotSplit, 0, true);
-    kc<<<persistent_grid(kc, dev, tiles_of(m)), kBlock, 0, s>>>(in, E[1], nullptr, minb[0], no_rec, n, d_ctr,
-                                                               0, st, ws.next_epoch(), kSlotCompact, 0);
+    kc<<<persistent_grid(kc, dev, tiles_c(m)), kBlock, 0, s>>>(in, E[1], nullptr, minb[0], no_rec, n, d_ctr,
+                                                               0, st, ws.next_epoch(), kSlotCompact, 0,
+                                                               filt_for(n));
     tmark();
     ++launches;
   } else {
@@ -363,7 +374,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     const unsigned g = (unsigned)std::max<uint64_t>(
         1, std::min<uint64_t>((m + kBlock - 1) / kBlock, (uint64_t)sm_count(dev) * blocks_per_sm(kmin)));
     hot_begin(kHotMin1, 0, false);
-    kmin<<<g, kBlock, 0, s>>>(in, n, m, minb[0], d_ctr);
+    kmin<<<g, kBlock, 0, s>>>(in, n, m, minb[0], d_ctr, filt_for(n));
     tmark();
     ++launches;
   }
@@ -403,12 +414,14 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     hot_begin(kHotCompact, r, light);
     if (original_in) {
       auto kc = k_compact<InView, false, kPre, kFilterNone>;
-      kc<<<persistent_grid(kc, dev, tiles_of(m_bound)), kBlock, 0, s>>>(in, Eout, Lr, mnext, no_rec, n, d_ctr, r, st,
-                                                                       ep_c, kSlotCompact, (int)light);
+      kc<<<persistent_grid(kc, dev, tiles_c(m_bound)), kBlock, 0, s>>>(in, Eout, Lr, mnext, no_rec, n, d_ctr, r, st,
+                                                                       ep_c, kSlotCompact, (int)light,
+                                                                       filt_for(n_bound));
     } else {
       auto kc = k_compact<PackedView, false, kPre, kFilterNone>;
-      kc<<<persistent_grid(kc, dev, tiles_of(m_bound)), kBlock, 0, s>>>(
-          PackedView{E[r & 1]}, Eout, Lr, mnext, no_rec, n, d_ctr, r, st, ep_c, kSlotCompact, (int)light);
+      kc<<<persistent_grid(kc, dev, tiles_c(m_bound)), kBlock, 0, s>>>(
+          PackedView{E[r & 1]}, Eout, Lr, mnext, no_rec, n, d_ctr, r, st, ep_c, kSlotCompact, (int)light,
+          filt_for(n_bound));
     }
     tmark();
     launches += 3;
@@ -445,9 +458,9 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
         auto kc = k_compact<InView, false, kPre, kFilterHeavy>;
         hot_begin(kHotHeavy, R1, false);
         // launched as round R1-1's producer: it writes m[R1] and E/min of round R1
-        kc<<<persistent_grid(kc, dev, tiles_of(m)), kBlock, 0, s>>>(in, E[R1 & 1], vlabel, minb[(R1 - 1) & 1],
+        kc<<<persistent_grid(kc, dev, tiles_c(m)), kBlock, 0, s>>>(in, E[R1 & 1], vlabel, minb[(R1 - 1) & 1],
                                                                    no_rec, n, d_ctr, R1 - 1, st, ws.next_epoch(),
-                                                                   kSlotFilter, 0);
+                                                                   kSlotFilter, 0, filt_for(snap.n[R1]));
         tmark();
         ++launches;
         MST_CUDA_CHECK(cudaGetLastError());
@@ -724,7 +737,7 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, RunOu
     const unsigned g = (unsigned)std::max<uint64_t>(
         1, std::min<uint64_t>((s.m + kBlock - 1) / kBlock,
                               (uint64_t)sm_count(s.ws->device) * blocks_per_sm(kmin)));
-    kmin<<<g, kBlock, 0, s.ws->stream>>>(s.in, n, s.m, s.minb[0], s.d_ctr);
+    kmin<<<g, kBlock, 0, s.ws->stream>>>(s.in, n, s.m, s.minb[0], s.d_ctr, filt_for(n));
     ++launches;
     MST_CUDA_CHECK(cudaGetLastError());
   }
@@ -771,12 +784,13 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, RunOu
       uint4* Eout = s.E[(r - 1) & 1];
       if (r == 1) {
         auto kc = k_compact<SoaView, true, kPre, kFilterNone>;
-        kc<<<persistent_grid(kc, ws.device, tiles_of(m_bound)), kBlock, 0, ws.stream>>>(
-            s.in, Eout, s.L, s.minb[nxt], rec, n, s.d_ctr, r, s.st, ep_c, kSlotCompact, 0);
+        kc<<<persistent_grid(kc, ws.device, tiles_c(m_bound)), kBlock, 0, ws.stream>>>(
+            s.in, Eout, s.L, s.minb[nxt], rec, n, s.d_ctr, r, s.st, ep_c, kSlotCompact, 0, filt_for(n_bound));
       } else {
         auto kc = k_compact<PackedView, true, kPre, kFilterNone>;
-        kc<<<persistent_grid(kc, ws.device, tiles_of(m_bound)), kBlock, 0, ws.stream>>>(
-            PackedView{s.E[r & 1]}, Eout, s.L, s.minb[nxt], rec, n, s.d_ctr, r, s.st, ep_c, kSlotCompact, 0);
+        kc<<<persistent_grid(kc, ws.device, tiles_c(m_bound)), kBlock, 0, ws.stream>>>(
+            PackedView{s.E[r & 1]}, Eout, s.L, s.minb[nxt], rec, n, s.d_ctr, r, s.st, ep_c, kSlotCompact, 0,
+            filt_for(n_bound));
       }
       launches += 3;
       MST_CUDA_CHECK(cudaGetLastError());
@@ -1177,7 +1191,7 @@ int mst_gpu_round1_min(const mst_edges_soa_t* edges, uint64_t* out_min) {
                                          : k_min_round1<SoaView, false, false>;
     const unsigned g = (unsigned)std::max<uint64_t>(
         1, std::min<uint64_t>((m + kBlock - 1) / kBlock, (uint64_t)sm_count(dev) * blocks_per_sm(kmin)));
-    kmin<<<g, kBlock, 0, ws.stream>>>(SoaView{src, dst, w, 0}, n, m, mn, d_ctr);
+    kmin<<<g, kBlock, 0, ws.stream>>>(SoaView{src, dst, w, 0}, n, m, mn, d_ctr, filt_for(n));
     MST_CUDA_CHECK(cudaGetLastError());
     MST_CUDA_CHECK(cudaMemcpyAsync(out_min, mn, (size_t)n * 8, cudaMemcpyDeviceToHost, ws.stream));
     MST_CUDA_CHECK(cudaMemcpyAsync(&ws.h_snap[0], d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost,

@@ -29,9 +29,10 @@ namespace mstgpu {
 
 constexpr int kBlock = 256;
 constexpr int kWarps = kBlock / 32;
-constexpr int kItems = 4;
-constexpr int kTile = kBlock * kItems;  // elements per tile (striped)
-static_assert(kItems * kWarps == 32, "tile scan assumes 32 (item, warp) slots");
+constexpr int kItems = 4;                // per thread, component tiles (hook)
+constexpr int kTile = kBlock * kItems;   // elements per tile (striped)
+constexpr int kCItems = 8;               // per thread, edge tiles (compaction)
+constexpr int kCTile = kBlock * kCItems;
 
 constexpr int kMaxR = MST_MAX_ROUNDS + 2;
 constexpr uint64_t kNoKey = ~0ull;
@@ -158,19 +159,27 @@ __device__ __forceinline__ uint32_t lookback(unsigned long long* status, uint32_
   if (lane == 0) st_relaxed(status + tile, tag | (1ull << 32) | aggregate);
   uint32_t excl = 0;
   int64_t top = (int64_t)tile - 1;
+  uint32_t backoff = 32;
   while (true) {
+    // One read of a 32-tile window per attempt; predecessors that have not
+    // published yet make the warp back off instead of spinning on L2 (the
+    // window's lines are the hottest in the machine while a scan runs).
     const int64_t idx = top - (int64_t)lane;
     uint32_t flag = 2, val = 0;
     if (idx >= 0) {
-      unsigned long long s;
-      do {
-        s = ld_relaxed(status + idx);
-      } while ((uint32_t)(s >> 34) != epoch || ((s >> 32) & 3ull) == 0);
-      flag = (uint32_t)(s >> 32) & 3u;
+      const unsigned long long s = ld_relaxed(status + idx);
+      flag = (uint32_t)(s >> 34) == epoch ? (uint32_t)(s >> 32) & 3u : 0u;
       val = (uint32_t)s;
     }
     const unsigned pm = __ballot_sync(0xffffffffu, flag == 2);
+    const unsigned nr = __ballot_sync(0xffffffffu, flag == 0);
     const int first = pm ? __ffs(pm) - 1 : 31;
+    const unsigned upto = first == 31 ? 0xffffffffu : ((2u << first) - 1u);
+    if (nr & upto) {
+      __nanosleep(backoff);
+      backoff = backoff < 1024 ? backoff * 2 : 1024;
+      continue;
+    }
     excl += warp_sum<uint32_t>((int)lane <= first ? val : 0u);
     if (pm) break;
     top -= 32;
@@ -179,25 +188,41 @@ __device__ __forceinline__ uint32_t lookback(unsigned long long* status, uint32_
   return excl;
 }
 
-// Ordered ranks of per-item flags over a striped tile, with the tile's
-// global exclusive prefix from the look-back. s_scan: 32 words of smem,
-// s_misc: 2 words (prefix, total).
-__device__ __forceinline__ void tile_flag_scan(const bool (&flag)[kItems], uint32_t (&rank)[kItems],
+// Ordered ranks of per-item flags over a striped tile (item k of thread t
+// is tile element k*kBlock + t), with the tile's global exclusive prefix
+// from the look-back. s_scan: kIt*kWarps words of smem; s_misc: 2 words.
+template <int kIt>
+__device__ __forceinline__ void tile_flag_scan(const bool (&flag)[kIt], uint32_t (&rank)[kIt],
                                                uint32_t* s_scan, uint32_t* s_misc,
                                                unsigned long long* status, uint32_t tile,
                                                uint32_t epoch, uint32_t& prefix, uint32_t& total) {
+  constexpr int kSlots = kIt * kWarps;
+  constexpr int kPer = (kSlots + 31) / 32;  // slots per lane in the warp-0 scan
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-  unsigned bal[kItems];
+  unsigned bal[kIt];
 #pragma unroll
-  for (int k = 0; k < kItems; ++k) {
+  for (int k = 0; k < kIt; ++k) {
     bal[k] = __ballot_sync(0xffffffffu, flag[k]);
     if (lane == 0) s_scan[k * kWarps + warp] = __popc(bal[k]);
   }
   __syncthreads();
   if (warp == 0) {
-    const uint32_t v = s_scan[lane];
-    const uint32_t incl = warp_incl_scan(v);
-    s_scan[lane] = incl - v;
+    uint32_t v[kPer];
+    uint32_t sum = 0;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int idx = lane * kPer + j;
+      v[j] = idx < kSlots ? s_scan[idx] : 0u;
+      sum += v[j];
+    }
+    const uint32_t incl = warp_incl_scan(sum);
+    uint32_t run = incl - sum;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int idx = lane * kPer + j;
+      if (idx < kSlots) s_scan[idx] = run;
+      run += v[j];
+    }
     const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
     const uint32_t ex = lookback(status, tile, tot, epoch);
     if (lane == 0) {
@@ -210,7 +235,7 @@ __device__ __forceinline__ void tile_flag_scan(const bool (&flag)[kItems], uint3
   total = s_misc[1];
   const uint32_t lt = lanemask_lt();
 #pragma unroll
-  for (int k = 0; k < kItems; ++k) rank[k] = s_scan[k * kWarps + warp] + __popc(bal[k] & lt);
+  for (int k = 0; k < kIt; ++k) rank[k] = s_scan[k * kWarps + warp] + __popc(bal[k] & lt);
 }
 
 // Filtered 64-bit min: read first (a stale read is never below the true
@@ -220,7 +245,7 @@ __device__ __forceinline__ void tile_flag_scan(const bool (&flag)[kItems], uint3
 // one atomic per warp instead of up to 32.
 template <bool kWarpPre>
 __device__ __forceinline__ void offer(unsigned long long* table, uint32_t c, uint64_t key,
-                                      bool valid) {
+                                      bool valid, bool filt = true) {
   if (kWarpPre) {
     const unsigned act = __ballot_sync(0xffffffffu, valid);
     if (!valid) return;
@@ -233,8 +258,14 @@ __device__ __forceinline__ void offer(unsigned long long* table, uint32_t c, uin
     }
   }
   if (!valid) return;
-  const unsigned long long cur = __ldcg(table + c);
-  if (key < cur) atomicMin(table + c, (unsigned long long)key);
+  // Large (DRAM-resident) tables: a fire-and-forget RED; the read-first
+  // filter would put a dependent DRAM round trip on the critical path.
+  if (filt) {
+    const unsigned long long cur = __ldcg(table + c);
+    if (key < cur) atomicMin(table + c, (unsigned long long)key);
+  } else {
+    atomicMin(table + c, (unsigned long long)key);
+  }
 }
 
 __device__ __forceinline__ uint32_t find_root(uint32_t* parent, uint32_t c) {
@@ -257,7 +288,7 @@ __device__ __forceinline__ uint32_t find_root(uint32_t* parent, uint32_t c) {
 template <class View, bool kKeyPartner, bool kWarpPre>
 __global__ void __launch_bounds__(kBlock) k_min_round1(View v, uint32_t n, uint64_t m,
                                                        unsigned long long* __restrict__ minimum,
-                                                       DevCounters* ctr) {
+                                                       DevCounters* ctr, int filt) {
   const uint64_t stride = (uint64_t)gridDim.x * kBlock;
   uint32_t err = 0;
   for (uint64_t base = (uint64_t)blockIdx.x * kBlock; base < m; base += stride) {
@@ -279,8 +310,8 @@ __global__ void __launch_bounds__(kBlock) k_min_round1(View v, uint32_t n, uint6
     const uint64_t hi = (uint64_t)e.w << 32;
     const uint64_t ka = kKeyPartner ? (hi | e.b) : (hi | (uint32_t)i);
     const uint64_t kb = kKeyPartner ? (hi | e.a) : (hi | (uint32_t)i);
-    offer<kWarpPre>(minimum, e.a, ka, valid);
-    offer<kWarpPre>(minimum, e.b, kb, valid);
+    offer<kWarpPre>(minimum, e.a, ka, valid, filt);
+    offer<kWarpPre>(minimum, e.b, kb, valid, filt);
   }
   if (err) atomicOr(&ctr->err, err);
 }
@@ -345,7 +376,7 @@ __global__ void __launch_bounds__(kBlock) k_hook(View E, const unsigned long lon
       }
     }
     uint32_t rank[kItems], prefix, total;
-    tile_flag_scan(isroot, rank, s_scan, s_misc, status, tile, epoch, prefix, total);
+    tile_flag_scan<kItems>(isroot, rank, s_scan, s_misc, status, tile, epoch, prefix, total);
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
       const uint64_t c = (uint64_t)tile * kTile + k * kBlock + threadIdx.x;
@@ -437,8 +468,8 @@ __global__ void __launch_bounds__(kBlock) k_compact(View Ein, uint4* __restrict_
                                                     unsigned long long* __restrict__ min_next,
                                                     Recover rec, uint32_t n_orig, DevCounters* ctr,
                                                     int r, unsigned long long* status,
-                                                    uint32_t epoch, int slot, int light_phase) {
-  __shared__ uint32_t s_scan[32];
+                                                    uint32_t epoch, int slot, int light_phase, int filt) {
+  __shared__ uint32_t s_scan[kCItems * kWarps];
   __shared__ uint32_t s_misc[2];
   __shared__ uint32_t s_tile;
   const uint32_t stop = ctr->stop_round;
@@ -447,24 +478,24 @@ __global__ void __launch_bounds__(kBlock) k_compact(View Ein, uint4* __restrict_
   if (!full && !(kKeyPartner && (uint32_t)r < stop)) return;
   const uint64_t m_r = kFilter == kFilterHeavy ? ctr->m[0] : ctr->m[r];
   const uint32_t pivot = ctr->pivot;
-  const uint32_t ntiles = (uint32_t)((m_r + kTile - 1) / kTile);
+  const uint32_t ntiles = (uint32_t)((m_r + kCTile - 1) / kCTile);
   while (true) {
     if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->tile[r][slot], 1u);
     __syncthreads();
     const uint32_t tile = s_tile;
     if (tile >= ntiles) break;
-    EdgeRec e[kItems];
-    bool keep[kItems];
+    EdgeRec e[kCItems];
+    bool keep[kCItems];
 #pragma unroll
-    for (int k = 0; k < kItems; ++k) {
-      const uint64_t i = (uint64_t)tile * kTile + k * kBlock + threadIdx.x;
+    for (int k = 0; k < kCItems; ++k) {
+      const uint64_t i = (uint64_t)tile * kCTile + k * kBlock + threadIdx.x;
       keep[k] = false;
       e[k] = EdgeRec{0, 0, 0, 0, false};
       if (i < m_r) e[k] = Ein.stream(i);
     }
 #pragma unroll
-    for (int k = 0; k < kItems; ++k) {
-      const uint64_t i = (uint64_t)tile * kTile + k * kBlock + threadIdx.x;
+    for (int k = 0; k < kCItems; ++k) {
+      const uint64_t i = (uint64_t)tile * kCTile + k * kBlock + threadIdx.x;
       if (i < m_r) {
         bool ok = true;
         if (View::kOriginal) {
@@ -499,17 +530,17 @@ __global__ void __launch_bounds__(kBlock) k_compact(View Ein, uint4* __restrict_
       __syncthreads();
       continue;  // sharded final round: recovery only
     }
-    uint32_t rank[kItems], prefix, total;
-    tile_flag_scan(keep, rank, s_scan, s_misc, status, tile, epoch, prefix, total);
+    uint32_t rank[kCItems], prefix, total;
+    tile_flag_scan<kCItems>(keep, rank, s_scan, s_misc, status, tile, epoch, prefix, total);
 #pragma unroll
-    for (int k = 0; k < kItems; ++k) {
+    for (int k = 0; k < kCItems; ++k) {
       const uint32_t j = prefix + rank[k];
       if (keep[k]) __stcs(Eout + j, make_uint4(e[k].a, e[k].b, e[k].w, e[k].eid));
       const unsigned long long hi = (unsigned long long)e[k].w << 32;
       const unsigned long long ka = kKeyPartner ? (hi | e[k].b) : (hi | j);
       const unsigned long long kb = kKeyPartner ? (hi | e[k].a) : (hi | j);
-      offer<kWarpPre>(min_next, e[k].a, ka, keep[k]);
-      offer<kWarpPre>(min_next, e[k].b, kb, keep[k]);
+      offer<kWarpPre>(min_next, e[k].a, ka, keep[k], filt);
+      offer<kWarpPre>(min_next, e[k].b, kb, keep[k], filt);
     }
     if (tile == ntiles - 1 && threadIdx.x == 0) {
       const uint32_t kept = prefix + total;
