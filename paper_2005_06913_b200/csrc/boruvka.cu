@@ -298,7 +298,7 @@ bool warp_prereduce_enabled() {
 // R-MAT graphs keep most edges alive for many rounds otherwise
 // (sum m_r = 4.5-8.3 m).
 
-enum { kHotMin1 = 0, kHotCompact = 1, kHotSplit = 2, kHotHeavy = 3 };
+enum { kHotMin1 = 0, kHotCompact = 1, kHotSplit = 2, kHotHeavy = 3, kHotTail = 4 };
 struct HotLaunch {
   int ev;
   int kind;
@@ -322,6 +322,36 @@ bool filter_mode(uint32_t n, uint64_t m) {
   return m >= (uint64_t)3 * n && m >= (1u << 16);
 }
 
+
+struct CompactBufs {
+  uint32_t* counts;
+  uint32_t* masks;
+  unsigned long long* st;
+};
+
+// Ordered compaction as count + emit (kernels.cuh, "two-pass ordered compaction").
+template <class View, int kMode, bool kPre>
+void launch_two_pass(Workspace& ws, const CompactBufs& cb, View in, uint4* relabeled, const uint32_t* L, uint4* out,
+                     unsigned long long* min_next, DevCounters* d_ctr, int r, uint64_t m_bound, uint32_t n_orig,
+                     int slot, int light, int filt) {
+  const int dev = ws.device;
+  const uint64_t tiles = tiles_c(m_bound);
+  auto kcnt = k_count<View, kMode>;
+  const unsigned gc = (unsigned)std::max<uint64_t>(
+      1, std::min<uint64_t>(tiles, (uint64_t)sm_count(dev) * blocks_per_sm(kcnt)));
+  kcnt<<<gc, kBlock, 0, ws.stream>>>(in, relabeled, L, cb.masks, cb.counts, n_orig, d_ctr, r);
+  auto ksc = k_scan_counts<kScanEdges>;
+  const unsigned gs = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((tiles + kScanTile - 1) / kScanTile,
+                                                                          (uint64_t)sm_count(dev)));
+  ksc<<<gs, kScanBlock, 0, ws.stream>>>(cb.counts, tiles, d_ctr, r, cb.st, ws.next_epoch(), light,
+                                        View::kOriginal ? 1 : 0);
+  auto kem = k_emit<View, kMode, kPre>;
+  const unsigned ge = (unsigned)std::max<uint64_t>(
+      1, std::min<uint64_t>(tiles, (uint64_t)sm_count(dev) * blocks_per_sm(kem)));
+  kem<<<ge, kBlock, 0, ws.stream>>>(in, relabeled, L, cb.masks, cb.counts, out, min_next, d_ctr, r, filt);
+  MST_CUDA_CHECK(cudaGetLastError());
+}
+
 template <class InView, bool kPre>
 void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t wstride, uint32_t n,
                      uint64_t m, RunOut& out, bool time_hot, bool filter) {
@@ -337,6 +367,11 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   unsigned long long* st = ws.status_array(std::max(tiles_of(m), tiles_of(n)));
   const Recover no_rec{nullptr, nullptr, nullptr};
   const int dev = ws.device;
+  const CompactBufs cb{ws.get<uint32_t>("tile_counts", tiles_c(m)),
+                       ws.get<uint32_t>("tile_masks", tiles_c(m) * kCItems * kWarps), st};
+  uint32_t* hcounts = ws.get<uint32_t>("hook_counts", tiles_of(n));
+  uint32_t* hmasks = ws.get<uint32_t>("hook_masks", tiles_of(n) * kItems * kWarps);
+  (void)no_rec;
 
   init_counters(ws, d_ctr, n, m);
   MST_CUDA_CHECK(cudaMemsetAsync(minb[0], 0xFF, (size_t)n * 8, s));
@@ -362,17 +397,15 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     const uint32_t target = (uint32_t)std::max(1.0, frac * samples);
     k_pick_pivot<<<1, 1024, 0, s>>>(hist, target, d_ctr);
     launches += 2;
-    auto kc = k_compact<InView, false, kPre, kFilterLight>;
     hot_begin(kHotSplit, 0, true);
-    kc<<<persistent_grid(kc, dev, tiles_c(m)), kBlock, 0, s>>>(in, E[1], nullptr, minb[0], no_rec, n, d_ctr,
-                                                               0, st, ws.next_epoch(), kSlotCompact, 0,
-                                                               filt_for(n));
+    launch_two_pass<InView, kModeLight, kPre>(ws, cb, in, nullptr, nullptr, E[1], minb[0], d_ctr, 0, m, n,
+                                              kSlotCompact, 0, filt_for(n));
     tmark();
-    ++launches;
+    launches += 2;
   } else {
     auto kmin = k_min_round1<InView, false, kPre>;
     const unsigned g = (unsigned)std::max<uint64_t>(
-        1, std::min<uint64_t>((m + kBlock - 1) / kBlock, (uint64_t)sm_count(dev) * blocks_per_sm(kmin)));
+        1, std::min<uint64_t>((m + 4 * kBlock - 1) / (4 * kBlock), (uint64_t)sm_count(dev) * blocks_per_sm(kmin)));
     hot_begin(kHotMin1, 0, false);
     kmin<<<g, kBlock, 0, s>>>(in, n, m, minb[0], d_ctr, filt_for(n));
     tmark();
@@ -385,21 +418,102 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   int r = 1, loop_start = 1;
   int phase_end = 0;
   DevCounters snap_b{};  // counters at the end of the light phase
+  const bool tail_on = env_int("MST_TAIL", 1) != 0;
+  const uint64_t tail_edges = (uint64_t)env_double("MST_TAIL_EDGES", 3.0e6);
+
+  // Light phase over: compose its relabel maps into a vertex -> component map,
+  // run the heavy filter pass, continue with the plain loop (phase D).
+  // Returns false when the run was restarted in plain mode.
+  auto end_light_phase = [&](const DevCounters& snap) -> bool {
+    phase_end = (int)snap.phase_end;
+    snap_b = snap;
+    if (phase_end == 1) {
+      // not a single light non-loop edge: run the plain loop instead
+      MST_CUDA_CHECK(cudaStreamSynchronize(s));
+      RunOut plain;
+      run_single_impl<InView, kPre>(ws, in, wbase, wstride, n, m, plain, time_hot, false);
+      plain.launches += launches;
+      out = plain;
+      return false;
+    }
+    while (!levels.empty() && levels.back().second >= phase_end) levels.pop_back();
+    for (int k = (int)levels.size() - 2; k >= 0; --k) {
+      const unsigned g = (unsigned)std::max<uint64_t>(
+          1, std::min<uint64_t>((snap.n[levels[k].second] + 255) / 256, (uint64_t)sm_count(dev) * 8));
+      k_compose<<<g, 256, 0, s>>>(levels[k].first, levels[k + 1].first, d_ctr, levels[k].second);
+      ++launches;
+    }
+    const uint32_t* vlabel = levels.empty() ? nullptr : levels[0].first;
+    MST_CUDA_CHECK(cudaMemsetAsync(&d_ctr->phase_end, 0xFF, sizeof(unsigned int), s));
+    const int R1 = phase_end;
+    hot_begin(kHotHeavy, R1, false);
+    // launched as round R1-1's producer: it writes m[R1] and E/min of round R1
+    launch_two_pass<InView, kModeHeavy, kPre>(ws, cb, in, nullptr, vlabel, E[R1 & 1], minb[(R1 - 1) & 1], d_ctr,
+                                              R1 - 1, m, n, kSlotFilter, 0, filt_for(snap.n[R1]));
+    tmark();
+    launches += 2;
+    light = false;
+    r = R1;
+    loop_start = R1;
+    n_bound = snap.n[R1];
+    m_bound = m;
+    return true;
+  };
+
   while (true) {
     if (r > MST_MAX_ROUNDS) throw MstError{MST_ERR_STALL, "no convergence within MST_MAX_ROUNDS rounds"};
+    const bool original_in = (r == 1 && !filter);
+    if (tail_on && !original_in && m_bound <= tail_edges) {
+      // ---- all remaining rounds in one cooperative launch
+      uint32_t* M = nullptr;
+      if (light) {
+        M = ws.get<uint32_t>("Ltail", n_bound);
+        k_iota<<<(unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_bound + 255) / 256, 4096)), 256, 0, s>>>(
+            M, n_bound);
+        ++launches;
+      }
+      auto kt = k_tail<kPre>;
+      const int bps = std::min(blocks_per_sm(kt), 4);
+      const unsigned G = (unsigned)(sm_count(dev) * bps);
+      uint32_t* bcount = ws.get<uint32_t>("bcount", G);
+      TailArgs ta{{E[0], E[1]}, {minb[0], minb[1]}, parent, rootlabel, L, mst, bcount, M, d_ctr, n, r, (int)light};
+      void* args[] = {&ta};
+      hot_begin(kHotTail, r, light);
+      MST_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)kt, G, kBlock, args, 0, s));
+      tmark();
+      ++launches;
+      MST_CUDA_CHECK(cudaMemcpyAsync(&ws.h_snap[kMaxR - 1], d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
+      MST_CUDA_CHECK(cudaStreamSynchronize(s));
+      const DevCounters& snap = ws.h_snap[kMaxR - 1];
+      if (snap.err || snap.stop_round != kNoStop) break;
+      if (light && snap.phase_end != kNoStop) {
+        if (M) levels.push_back({M, r});
+        if (!end_light_phase(snap)) return;
+        continue;
+      }
+      throw MstError{MST_ERR_STALL, "tail kernel ended without a verdict"};
+    }
     unsigned long long* mcur = minb[(r - 1) & 1];
     unsigned long long* mnext = minb[r & 1];
     uint4* Eout = E[(r + 1) & 1];
-    const bool original_in = (r == 1 && !filter);
-    const uint32_t ep_h = ws.next_epoch(), ep_c = ws.next_epoch();
-    if (original_in) {
-      auto kh = k_hook<InView, false>;
-      kh<<<persistent_grid(kh, dev, tiles_of(n_bound)), kBlock, 0, s>>>(in, mcur, parent, rootlabel, mst, n,
-                                                                        d_ctr, r, st, ep_h, (int)light);
-    } else {
-      auto kh = k_hook<PackedView, false>;
-      kh<<<persistent_grid(kh, dev, tiles_of(n_bound)), kBlock, 0, s>>>(
-          PackedView{E[r & 1]}, mcur, parent, rootlabel, mst, n, d_ctr, r, st, ep_h, (int)light);
+    {
+      const uint64_t ht = tiles_of(n_bound);
+      if (original_in) {
+        auto kd = k_hook_decide<InView>;
+        kd<<<(unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ht, (uint64_t)sm_count(dev) * blocks_per_sm(kd))),
+             kBlock, 0, s>>>(in, mcur, parent, rootlabel, hmasks, hcounts, d_ctr, r);
+      } else {
+        auto kd = k_hook_decide<PackedView>;
+        kd<<<(unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ht, (uint64_t)sm_count(dev) * blocks_per_sm(kd))),
+             kBlock, 0, s>>>(PackedView{E[r & 1]}, mcur, parent, rootlabel, hmasks, hcounts, d_ctr, r);
+      }
+      k_scan_counts<kScanRoots><<<(unsigned)std::max<uint64_t>(1, std::min<uint64_t>((ht + kScanTile - 1) / kScanTile,
+                                                                                     (uint64_t)sm_count(dev))),
+                                  kScanBlock, 0, s>>>(hcounts, ht, d_ctr, r, st, ws.next_epoch(), (int)light, 0);
+      k_hook_emit<<<(unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ht, (uint64_t)sm_count(dev) *
+                                                                              blocks_per_sm(k_hook_emit))),
+                    kBlock, 0, s>>>(parent, rootlabel, hmasks, hcounts, mst, n, d_ctr, r);
+      launches += 2;
     }
     uint32_t* Lr = L;
     if (light) {
@@ -413,18 +527,15 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     }
     hot_begin(kHotCompact, r, light);
     if (original_in) {
-      auto kc = k_compact<InView, false, kPre, kFilterNone>;
-      kc<<<persistent_grid(kc, dev, tiles_c(m_bound)), kBlock, 0, s>>>(in, Eout, Lr, mnext, no_rec, n, d_ctr, r, st,
-                                                                       ep_c, kSlotCompact, (int)light,
-                                                                       filt_for(n_bound));
+      // plain round 1: relabelled copy of the caller's list in E[1], compacted into E[0]
+      launch_two_pass<InView, kModeRelabel, kPre>(ws, cb, in, E[1], Lr, Eout, mnext, d_ctr, r, m_bound, n,
+                                                  kSlotCompact, (int)light, filt_for(n_bound));
     } else {
-      auto kc = k_compact<PackedView, false, kPre, kFilterNone>;
-      kc<<<persistent_grid(kc, dev, tiles_c(m_bound)), kBlock, 0, s>>>(
-          PackedView{E[r & 1]}, Eout, Lr, mnext, no_rec, n, d_ctr, r, st, ep_c, kSlotCompact, (int)light,
-          filt_for(n_bound));
+      launch_two_pass<PackedView, kModeRelabel, kPre>(ws, cb, PackedView{E[r & 1]}, E[r & 1], Lr, Eout, mnext, d_ctr,
+                                                      r, m_bound, n, kSlotCompact, (int)light, filt_for(n_bound));
     }
     tmark();
-    launches += 3;
+    launches += 5;
     MST_CUDA_CHECK(cudaGetLastError());
     MST_CUDA_CHECK(cudaMemcpyAsync(&ws.h_snap[r], d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
     MST_CUDA_CHECK(cudaEventRecord(ws.ev[r], s));
@@ -434,41 +545,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       if (snap.err) break;
       if (snap.stop_round != kNoStop && (int)snap.stop_round <= r) break;
       if (light && snap.phase_end != kNoStop && (int)snap.phase_end <= r) {
-        phase_end = (int)snap.phase_end;
-        snap_b = snap;
-        if (phase_end == 1) {
-          // not a single light non-loop edge: run the plain loop instead
-          MST_CUDA_CHECK(cudaStreamSynchronize(s));
-          RunOut plain;
-          run_single_impl<InView, kPre>(ws, in, wbase, wstride, n, m, plain, time_hot, false);
-          plain.launches += launches;
-          out = plain;
-          return;
-        }
-        while (!levels.empty() && levels.back().second >= phase_end) levels.pop_back();
-        for (int k = (int)levels.size() - 2; k >= 0; --k) {
-          const unsigned g = (unsigned)std::max<uint64_t>(
-              1, std::min<uint64_t>((snap.n[levels[k].second] + 255) / 256, (uint64_t)sm_count(dev) * 8));
-          k_compose<<<g, 256, 0, s>>>(levels[k].first, levels[k + 1].first, d_ctr, levels[k].second);
-          ++launches;
-        }
-        const uint32_t* vlabel = levels.empty() ? nullptr : levels[0].first;
-        MST_CUDA_CHECK(cudaMemsetAsync(&d_ctr->phase_end, 0xFF, sizeof(unsigned int), s));
-        const int R1 = phase_end;
-        auto kc = k_compact<InView, false, kPre, kFilterHeavy>;
-        hot_begin(kHotHeavy, R1, false);
-        // launched as round R1-1's producer: it writes m[R1] and E/min of round R1
-        kc<<<persistent_grid(kc, dev, tiles_c(m)), kBlock, 0, s>>>(in, E[R1 & 1], vlabel, minb[(R1 - 1) & 1],
-                                                                   no_rec, n, d_ctr, R1 - 1, st, ws.next_epoch(),
-                                                                   kSlotFilter, 0, filt_for(snap.n[R1]));
-        tmark();
-        ++launches;
-        MST_CUDA_CHECK(cudaGetLastError());
-        light = false;
-        r = R1;
-        loop_start = R1;
-        n_bound = snap.n[R1];
-        m_bound = m;
+        if (!end_light_phase(snap)) return;
         continue;
       }
       n_bound = snap.n[r];
@@ -497,6 +574,11 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
         bytes = 12ull * m + 16ull * c.m[1];
       } else if (h.kind == kHotHeavy) {
         bytes = 12ull * m + 16ull * c.m[h.r];
+      } else if (h.kind == kHotTail) {
+        // per round: relabel pass (16 B read + 8 B write) + compaction (16 B read + 16 B per kept)
+        const int last = (h.light && phase_end) ? phase_end : stop;
+        const DevCounters& cc = (h.light && phase_end) ? snap_b : c;
+        for (int rr = h.r; rr + 1 < last && rr < kMaxR - 1; ++rr) bytes += 40ull * cc.m[rr] + 16ull * cc.m[rr + 1];
       } else {
         const bool ran = h.r + 1 < stop && (!h.light || phase_end == 0 || h.r < phase_end);
         if (!ran) continue;
@@ -1190,7 +1272,7 @@ int mst_gpu_round1_min(const mst_edges_soa_t* edges, uint64_t* out_min) {
     auto kmin = warp_prereduce_enabled() ? k_min_round1<SoaView, false, true>
                                          : k_min_round1<SoaView, false, false>;
     const unsigned g = (unsigned)std::max<uint64_t>(
-        1, std::min<uint64_t>((m + kBlock - 1) / kBlock, (uint64_t)sm_count(dev) * blocks_per_sm(kmin)));
+        1, std::min<uint64_t>((m + 4 * kBlock - 1) / (4 * kBlock), (uint64_t)sm_count(dev) * blocks_per_sm(kmin)));
     kmin<<<g, kBlock, 0, ws.stream>>>(SoaView{src, dst, w, 0}, n, m, mn, d_ctr, filt_for(n));
     MST_CUDA_CHECK(cudaGetLastError());
     MST_CUDA_CHECK(cudaMemcpyAsync(out_min, mn, (size_t)n * 8, cudaMemcpyDeviceToHost, ws.stream));

@@ -22,6 +22,7 @@
 // Round 1 reads the caller's edge list directly (k_min_round1 + k_compact).
 #pragma once
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -268,6 +269,47 @@ __device__ __forceinline__ void offer(unsigned long long* table, uint32_t c, uin
   }
 }
 
+// kU independent root walks interleaved step by step (path halving), so each
+// thread keeps kU dependent-load chains in flight instead of one.
+template <int kU>
+__device__ __forceinline__ void find_roots(uint32_t* parent, const uint32_t (&c)[kU], const bool (&valid)[kU],
+                                           uint32_t (&root)[kU]) {
+  uint32_t x[kU], px[kU];
+  bool live[kU];
+#pragma unroll
+  for (int k = 0; k < kU; ++k) {
+    x[k] = c[k];
+    live[k] = valid[k];
+    root[k] = c[k];
+    px[k] = live[k] ? __ldcg(parent + x[k]) : x[k];
+  }
+  while (true) {
+    uint32_t gp[kU];
+#pragma unroll
+    for (int k = 0; k < kU; ++k) gp[k] = (live[k] && px[k] != x[k]) ? __ldcg(parent + px[k]) : px[k];
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < kU; ++k) {
+      if (!live[k]) continue;
+      if (px[k] == x[k]) {
+        root[k] = x[k];
+        live[k] = false;
+      } else if (gp[k] == px[k]) {
+        root[k] = px[k];
+        live[k] = false;
+      } else {
+        parent[x[k]] = gp[k];  // path halving: every value ever stored is an ancestor
+        x[k] = gp[k];
+        any = true;
+      }
+    }
+    if (!any) break;
+#pragma unroll
+    for (int k = 0; k < kU; ++k)
+      if (live[k]) px[k] = __ldcg(parent + x[k]);
+  }
+}
+
 __device__ __forceinline__ uint32_t find_root(uint32_t* parent, uint32_t c) {
   uint32_t p = __ldcg(parent + c);
   while (p != c) {
@@ -289,29 +331,38 @@ template <class View, bool kKeyPartner, bool kWarpPre>
 __global__ void __launch_bounds__(kBlock) k_min_round1(View v, uint32_t n, uint64_t m,
                                                        unsigned long long* __restrict__ minimum,
                                                        DevCounters* ctr, int filt) {
-  const uint64_t stride = (uint64_t)gridDim.x * kBlock;
+  constexpr int kU = 4;
+  const uint64_t stride = (uint64_t)gridDim.x * kBlock * kU;
   uint32_t err = 0;
-  for (uint64_t base = (uint64_t)blockIdx.x * kBlock; base < m; base += stride) {
-    const uint64_t i = base + threadIdx.x;
-    bool valid = i < m;
-    EdgeRec e{0, 0, 0, 0, true};
-    if (valid) {
-      e = v.stream(i);
-      if (e.a >= n || e.b >= n) {
-        err |= kErrRange;
-        valid = false;
-      } else if (!e.ok) {
-        err |= kErrWeight;
-        valid = false;
-      } else if (e.a == e.b) {
-        valid = false;  // self-loop: never in an MST
-      }
+  for (uint64_t base = (uint64_t)blockIdx.x * kBlock * kU; base < m; base += stride) {
+    EdgeRec e[kU];
+#pragma unroll
+    for (int k = 0; k < kU; ++k) {
+      const uint64_t i = base + k * kBlock + threadIdx.x;
+      e[k] = EdgeRec{0, 0, 0, 0, false};
+      if (i < m) e[k] = v.stream(i);
     }
-    const uint64_t hi = (uint64_t)e.w << 32;
-    const uint64_t ka = kKeyPartner ? (hi | e.b) : (hi | (uint32_t)i);
-    const uint64_t kb = kKeyPartner ? (hi | e.a) : (hi | (uint32_t)i);
-    offer<kWarpPre>(minimum, e.a, ka, valid, filt);
-    offer<kWarpPre>(minimum, e.b, kb, valid, filt);
+#pragma unroll
+    for (int k = 0; k < kU; ++k) {
+      const uint64_t i = base + k * kBlock + threadIdx.x;
+      bool valid = i < m;
+      if (valid) {
+        if (e[k].a >= n || e[k].b >= n) {
+          err |= kErrRange;
+          valid = false;
+        } else if (!e[k].ok) {
+          err |= kErrWeight;
+          valid = false;
+        } else if (e[k].a == e[k].b) {
+          valid = false;  // self-loop: never in an MST
+        }
+      }
+      const uint64_t hi = (uint64_t)e[k].w << 32;
+      const uint64_t ka = kKeyPartner ? (hi | e[k].b) : (hi | (uint32_t)i);
+      const uint64_t kb = kKeyPartner ? (hi | e[k].a) : (hi | (uint32_t)i);
+      offer<kWarpPre>(minimum, e[k].a, ka, valid, filt);
+      offer<kWarpPre>(minimum, e[k].b, kb, valid, filt);
+    }
   }
   if (err) atomicOr(&ctr->err, err);
 }
@@ -433,11 +484,23 @@ __global__ void __launch_bounds__(kBlock) k_label(uint32_t* __restrict__ parent,
   if ((uint32_t)r + 1 >= ctr->stop_round || (uint32_t)r >= ctr->phase_end) return;
   const uint32_t n_r = ctr->n[r];
   const uint32_t n_next = ctr->n[r + 1];
-  const uint64_t stride = (uint64_t)gridDim.x * kBlock;
-  for (uint64_t c = (uint64_t)blockIdx.x * kBlock + threadIdx.x; c < n_r; c += stride) {
-    const uint32_t root = find_root(parent, (uint32_t)c);
-    L[c] = __ldcg(rootlabel + root);
-    if (c < n_next) min_next[c] = kNoKey;
+  constexpr int kU = 4;
+  const uint64_t stride = (uint64_t)gridDim.x * kBlock * kU;
+  for (uint64_t base = (uint64_t)blockIdx.x * kBlock * kU; base < n_r; base += stride) {
+    uint32_t c[kU], root[kU];
+    bool v[kU];
+#pragma unroll
+    for (int k = 0; k < kU; ++k) {
+      c[k] = (uint32_t)(base + k * kBlock + threadIdx.x);
+      v[k] = base + k * kBlock + threadIdx.x < n_r;
+    }
+    find_roots<kU>(parent, c, v, root);
+#pragma unroll
+    for (int k = 0; k < kU; ++k) {
+      if (!v[k]) continue;
+      L[c[k]] = __ldcg(rootlabel + root[k]);
+      if (c[k] < n_next) min_next[c[k]] = kNoKey;
+    }
   }
 }
 
@@ -606,6 +669,670 @@ __global__ void k_compose(uint32_t* __restrict__ Lr, const uint32_t* __restrict_
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n_r; c += stride)
     Lr[c] = __ldg(Lnext + Lr[c]);
+}
+
+// ------------------------------ two-pass ordered compaction ----------------
+// The single-pass look-back above leaves each tile ~10 us in flight (its
+// aggregate needs the tile's loads + gathers first), which caps a pass at
+// ~1/3 of HBM bandwidth (tools/lookback_bench.cu). Here the work is split:
+//   k_count : per-tile keep counts, no inter-tile dependency (streams at
+//             near copy speed); round compactions relabel in place, the
+//             filter passes record the keep flags as a bitmask (one ballot
+//             word per 32 consecutive edges);
+//   k_emit  : ordered write + fused offers; a tile's aggregate is just
+//             counts[tile], so it is published the moment the tile is taken
+//             and the look-back overlaps the tile's own loads.
+enum { kModeRelabel = 0, kModeLight = 1, kModeHeavy = 2 };
+
+template <class View, int kMode>
+__global__ void __launch_bounds__(kBlock) k_count(View in, uint4* __restrict__ relabeled,
+                                                  const uint32_t* __restrict__ L,
+                                                  uint32_t* __restrict__ masks, uint32_t* __restrict__ counts,
+                                                  uint32_t n_orig, DevCounters* ctr, int r) {
+  __shared__ uint32_t s_cnt[kWarps];
+  const uint32_t stop = ctr->stop_round;
+  if ((uint32_t)r >= ctr->phase_end || (uint32_t)r + 1 >= stop) return;
+  const uint64_t m_r = kMode == kModeRelabel && !View::kOriginal ? ctr->m[r] : ctr->m[0];
+  const uint32_t pivot = ctr->pivot;
+  const uint32_t ntiles = (uint32_t)((m_r + kCTile - 1) / kCTile);
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    EdgeRec e[kCItems];
+#pragma unroll
+    for (int k = 0; k < kCItems; ++k) {
+      const uint64_t i = (uint64_t)tile * kCTile + k * kBlock + threadIdx.x;
+      e[k] = EdgeRec{0, 0, 0, 0, false};
+      if (i < m_r) e[k] = in.stream(i);
+    }
+    uint32_t err = 0, cnt = 0;
+#pragma unroll
+    for (int k = 0; k < kCItems; ++k) {
+      const uint64_t i = (uint64_t)tile * kCTile + k * kBlock + threadIdx.x;
+      bool keep = false;
+      if (i < m_r) {
+        bool ok = true;
+        if (View::kOriginal) {
+          // every input edge is range/weight checked in the first pass over
+          // the caller's list (the light pass may be the only one)
+          ok = e[k].a < n_orig && e[k].b < n_orig && e[k].ok;
+          if (!ok) err |= (e[k].a < n_orig && e[k].b < n_orig) ? kErrWeight : kErrRange;
+        }
+        if (kMode == kModeLight) {
+          keep = ok && e[k].w < pivot && e[k].a != e[k].b;
+        } else if (kMode == kModeHeavy) {
+          if (ok && e[k].w >= pivot) {
+            const uint32_t x = L ? __ldg(L + e[k].a) : e[k].a;
+            const uint32_t y = L ? __ldg(L + e[k].b) : e[k].b;
+            keep = x != y;
+          }
+        } else if (ok) {
+          const uint32_t x = __ldg(L + e[k].a), y = __ldg(L + e[k].b);
+          keep = x != y;
+          if (View::kOriginal)
+            __stcs(relabeled + i, make_uint4(x, y, e[k].w, e[k].eid));
+          else
+            __stcs(reinterpret_cast<uint2*>(relabeled + i), make_uint2(x, y));
+        } else if (View::kOriginal) {
+          __stcs(relabeled + i, make_uint4(0, 0, 0, 0));  // rejected input edge: a self-loop placeholder
+        }
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      if (kMode != kModeRelabel && lane == 0) masks[(uint64_t)tile * (kCItems * kWarps) + k * kWarps + warp] = bal;
+      cnt += __popc(bal);
+    }
+    if (err) atomicOr(&ctr->err, err);
+    if (lane == 0) s_cnt[warp] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t t = 0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) t += s_cnt[w];
+      counts[tile] = t;
+    }
+    __syncthreads();
+  }
+}
+
+template <class View, int kMode, bool kWarpPre>
+__global__ void __launch_bounds__(kBlock) k_emit(View in, const uint4* __restrict__ relabeled,
+                                                 const uint32_t* __restrict__ L,
+                                                 const uint32_t* __restrict__ masks,
+                                                 const uint32_t* __restrict__ offsets, uint4* __restrict__ out,
+                                                 unsigned long long* __restrict__ min_next, DevCounters* ctr,
+                                                 int r, int filt) {
+  __shared__ uint32_t s_scan[kCItems * kWarps];
+  const uint32_t stop = ctr->stop_round;
+  if ((uint32_t)r >= ctr->phase_end || (uint32_t)r + 1 >= stop) return;
+  const uint64_t m_r = kMode == kModeRelabel && !View::kOriginal ? ctr->m[r] : ctr->m[0];
+  const uint32_t ntiles = (uint32_t)((m_r + kCTile - 1) / kCTile);
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    uint4 e[kCItems];
+    unsigned bal[kCItems];
+    bool keep[kCItems];
+#pragma unroll
+    for (int k = 0; k < kCItems; ++k) {
+      const uint64_t i = (uint64_t)tile * kCTile + k * kBlock + threadIdx.x;
+      e[k] = make_uint4(0, 0, 0, 0);
+      if (kMode == kModeRelabel) {
+        if (i < m_r) e[k] = __ldcs(relabeled + i);
+      } else {
+        bal[k] = __ldg(masks + (uint64_t)tile * (kCItems * kWarps) + k * kWarps + warp);
+        if ((bal[k] >> lane) & 1u) {
+          const EdgeRec x = in.gather(i);
+          e[k] = make_uint4(x.a, x.b, x.w, x.eid);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kCItems; ++k) {
+      if (kMode == kModeRelabel) {
+        const uint64_t i = (uint64_t)tile * kCTile + k * kBlock + threadIdx.x;
+        keep[k] = i < m_r && e[k].x != e[k].y;
+        bal[k] = __ballot_sync(0xffffffffu, keep[k]);
+      } else {
+        keep[k] = (bal[k] >> lane) & 1u;
+        if (kMode == kModeHeavy && keep[k] && L) {
+          e[k].x = __ldg(L + e[k].x);
+          e[k].y = __ldg(L + e[k].y);
+        }
+      }
+      if (lane == 0) s_scan[k * kWarps + warp] = __popc(bal[k]);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      constexpr int kSlots = kCItems * kWarps, kPer = (kSlots + 31) / 32;
+      uint32_t v[kPer], sum = 0;
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        const int idx = lane * kPer + j;
+        v[j] = idx < kSlots ? s_scan[idx] : 0u;
+        sum += v[j];
+      }
+      const uint32_t incl = warp_incl_scan(sum);
+      uint32_t run = incl - sum;
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        const int idx = lane * kPer + j;
+        if (idx < kSlots) s_scan[idx] = run;
+        run += v[j];
+      }
+    }
+    __syncthreads();
+    const uint32_t prefix = __ldg(offsets + tile);
+    const uint32_t lt = lanemask_lt();
+#pragma unroll
+    for (int k = 0; k < kCItems; ++k) {
+      const uint32_t j = prefix + s_scan[k * kWarps + warp] + __popc(bal[k] & lt);
+      if (keep[k]) __stcs(out + j, e[k]);
+      const unsigned long long key = ((unsigned long long)e[k].z << 32) | j;
+      offer<kWarpPre>(min_next, e[k].x, key, keep[k], filt);
+      offer<kWarpPre>(min_next, e[k].y, key, keep[k], filt);
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------ tile-count scan ----------------------------
+// Exclusive scan of per-tile counts in place (8192 counts per block, chained
+// with the look-back across <= a few hundred blocks), so the emit passes need
+// no inter-tile communication at all. The last block also publishes the
+// total and the round verdict:
+//   kScanEdges : m[r+1] = kept; none kept -> stop (or light-phase end)
+//   kScanRoots : n[r+1] = roots; <= 1 -> stop; == n[r] -> stop (or light end)
+enum { kScanEdges = 0, kScanRoots = 1, kScanPlain = 2 };
+constexpr int kScanItems = 8;
+constexpr int kScanBlock = 1024;
+constexpr int kScanTile = kScanBlock * kScanItems;
+
+template <int kKind>
+__global__ void __launch_bounds__(kScanBlock) k_scan_counts(uint32_t* __restrict__ counts, uint64_t ntiles_max,
+                                                             DevCounters* ctr, int r, unsigned long long* status,
+                                                             uint32_t epoch, int light_phase, int count_src) {
+  __shared__ uint32_t s_warp[kScanBlock / 32];
+  __shared__ uint32_t s_misc[2];
+  if (kKind != kScanPlain) {
+    if ((uint32_t)r >= ctr->phase_end) return;
+    if (kKind == kScanEdges && (uint32_t)r + 1 >= ctr->stop_round) return;
+    if (kKind == kScanRoots && (uint32_t)r >= ctr->stop_round) return;
+  }
+  // number of tiles actually in use this round
+  uint64_t n_items;
+  if (kKind == kScanRoots)
+    n_items = (ctr->n[r] + (uint64_t)kTile - 1) / kTile;
+  else if (kKind == kScanEdges)
+    n_items = ((count_src ? ctr->m[0] : ctr->m[r]) + (uint64_t)kCTile - 1) / kCTile;
+  else
+    n_items = ntiles_max;
+  const uint32_t nblocks = (uint32_t)((n_items + kScanTile - 1) / kScanTile);
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  for (uint32_t blk = blockIdx.x; blk < max(nblocks, 1u); blk += gridDim.x) {
+    const uint64_t base = (uint64_t)blk * kScanTile + (uint64_t)threadIdx.x * kScanItems;
+    uint32_t v[kScanItems], sum = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      v[k] = base + k < n_items ? counts[base + k] : 0u;
+      sum += v[k];
+    }
+    const uint32_t incl = warp_incl_scan(sum);
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t wv = s_warp[lane];
+      const uint32_t wi = warp_incl_scan(wv);
+      s_warp[lane] = wi - wv;
+      const uint32_t tot = __shfl_sync(0xffffffffu, wi, 31);
+      const uint32_t ex = lookback(status, blk, tot, epoch);
+      if (lane == 0) {
+        s_misc[0] = ex;
+        s_misc[1] = tot;
+      }
+    }
+    __syncthreads();
+    uint32_t run = s_misc[0] + s_warp[warp] + incl - sum;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      if (base + k < n_items) counts[base + k] = run;
+      run += v[k];
+    }
+    if (blk == max(nblocks, 1u) - 1 && threadIdx.x == 0) {
+      const uint32_t total = s_misc[0] + s_misc[1];
+      if (kKind == kScanEdges) {
+        ctr->m[r + 1] = total;
+        if (total == 0) {
+          if (light_phase)
+            ctr->phase_end = (uint32_t)r + 1;
+          else if (ctr->stop_round == kNoStop)
+            ctr->stop_round = (uint32_t)r + 1;
+        }
+      } else if (kKind == kScanRoots) {
+        ctr->n[r + 1] = total;
+        if (total <= 1) {
+          ctr->stop_round = (uint32_t)r + 1;
+        } else if (total == ctr->n[r]) {
+          if (light_phase)
+            ctr->phase_end = (uint32_t)r;
+          else
+            ctr->stop_round = (uint32_t)r + 1;
+        }
+      } else {
+        ctr->m[kMaxR - 1] = total;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------ two-pass hook ------------------------------
+// k_hook_decide: per component, the partner along its lightest edge, the
+// mutual-pair root rule, parent[], the MST edge id stashed in rootlabel[],
+// a root bitmask and per-tile root counts; k_hook_emit turns the scanned
+// counts into dense root labels and MST slots. Same results as k_hook.
+template <class View>
+__global__ void __launch_bounds__(kBlock) k_hook_decide(View E, const unsigned long long* __restrict__ minimum,
+                                                        uint32_t* __restrict__ parent, uint32_t* __restrict__ rootlabel,
+                                                        uint32_t* __restrict__ masks, uint32_t* __restrict__ counts,
+                                                        DevCounters* ctr, int r) {
+  __shared__ uint32_t s_cnt[kWarps];
+  __shared__ unsigned long long s_wsum[kWarps];
+  if ((uint32_t)r >= ctr->stop_round || (uint32_t)r >= ctr->phase_end) return;
+  const uint32_t n_r = ctr->n[r];
+  const uint32_t ntiles = (uint32_t)(((uint64_t)n_r + kTile - 1) / kTile);
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  unsigned long long wsum = 0;
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    unsigned long long key[kItems], okey[kItems];
+    EdgeRec e[kItems];
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      const uint64_t c = (uint64_t)tile * kTile + k * kBlock + threadIdx.x;
+      key[k] = c < n_r ? __ldcs(minimum + c) : kNoKey;
+    }
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      e[k] = EdgeRec{0, 0, 0, 0, true};
+      if (key[k] != kNoKey) e[k] = E.gather((uint32_t)key[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      const uint32_t c = (uint32_t)((uint64_t)tile * kTile + k * kBlock + threadIdx.x);
+      const uint32_t o = (e[k].a == c) ? e[k].b : e[k].a;
+      okey[k] = key[k] != kNoKey ? __ldg(minimum + o) : kNoKey;
+    }
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      const uint64_t c = (uint64_t)tile * kTile + k * kBlock + threadIdx.x;
+      bool isroot = false;
+      if (c < n_r) {
+        if (key[k] == kNoKey) {
+          isroot = true;
+          parent[c] = (uint32_t)c;
+        } else {
+          const uint32_t o = (e[k].a == (uint32_t)c) ? e[k].b : e[k].a;
+          isroot = okey[k] == key[k] && (uint32_t)c < o;
+          parent[c] = isroot ? (uint32_t)c : o;
+          if (!isroot) {
+            rootlabel[c] = e[k].eid;  // stash the MST edge id until its slot is known
+            wsum += (uint32_t)(key[k] >> 32);
+          }
+        }
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, isroot);
+      if (lane == 0) masks[(uint64_t)tile * (kItems * kWarps) + k * kWarps + warp] = bal;
+      cnt += __popc(bal);
+    }
+    if (lane == 0) s_cnt[warp] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t t = 0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) t += s_cnt[w];
+      counts[tile] = t;
+    }
+    __syncthreads();
+  }
+  wsum = warp_sum<unsigned long long>(wsum);
+  if (lane == 0) s_wsum[warp] = wsum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int i = 0; i < kWarps; ++i) t += s_wsum[i];
+    if (t) atomicAdd(&ctr->total_weight, t);
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) k_hook_emit(const uint32_t* __restrict__ parent,
+                                                      uint32_t* __restrict__ rootlabel,
+                                                      const uint32_t* __restrict__ masks,
+                                                      const uint32_t* __restrict__ offsets, uint32_t* __restrict__ mst,
+                                                      uint32_t n_orig, DevCounters* ctr, int r) {
+  __shared__ uint32_t s_scan[kItems * kWarps];
+  if ((uint32_t)r >= ctr->phase_end) return;
+  // runs even when this round stops (the last hook's MST slots are needed)
+  if ((uint32_t)r >= ctr->stop_round && ctr->stop_round != (uint32_t)r + 1) return;
+  const uint32_t n_r = ctr->n[r];
+  const uint32_t mst_base = n_orig - n_r;
+  const uint32_t ntiles = (uint32_t)(((uint64_t)n_r + kTile - 1) / kTile);
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    // exclusive prefix of the (item, warp) root counts inside the tile
+    if (threadIdx.x < 32) {
+      const uint32_t v = __popc(__ldg(masks + (uint64_t)tile * (kItems * kWarps) + lane));
+      const uint32_t incl = warp_incl_scan(v);
+      s_scan[lane] = incl - v;
+    }
+    __syncthreads();
+    const uint32_t base = __ldg(offsets + tile);
+    const uint32_t lt = lanemask_lt();
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      const uint64_t c = (uint64_t)tile * kTile + k * kBlock + threadIdx.x;
+      const unsigned bal = __ldg(masks + (uint64_t)tile * (kItems * kWarps) + k * kWarps + warp);
+      if (c < n_r) {
+        const uint32_t before = base + s_scan[k * kWarps + warp] + __popc(bal & lt);
+        if ((bal >> lane) & 1u)
+          rootlabel[c] = before;
+        else
+          mst[mst_base + ((uint32_t)c - before)] = rootlabel[c];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------ tail megakernel ----------------------------
+
+// Once a round has few live edges, per-round kernel launches, ramp-up/tail
+// effects and look-back latency dominate. k_tail runs all remaining rounds
+// in ONE cooperative launch: every phase of a round (hook decide, hook emit,
+// label, relabel+count, compact+offer) is a grid-wide step separated by
+// grid.sync(), and ordered compaction uses per-block chunk counts instead of
+// a look-back (all blocks are co-resident). Semantics match k_hook /
+// k_label / k_compact exactly (same counters, same literal keys).
+struct TailArgs {
+  uint4* E[2];
+  unsigned long long* minb[2];
+  uint32_t* parent;
+  uint32_t* rootlabel;
+  uint32_t* L;
+  uint32_t* mst;
+  uint32_t* bcount;  // [gridDim.x]
+  uint32_t* M;       // light phase: entry-label -> current-label map (n[r0] entries)
+  DevCounters* ctr;
+  uint32_t n_orig;
+  int r0;
+  int light;
+};
+
+// Ordered ranks of kItems striped flags per thread; returns the total.
+__device__ __forceinline__ uint32_t block_ranks(const bool (&f)[kItems], uint32_t (&rank)[kItems],
+                                                uint32_t* s_cnt) {
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  unsigned bal[kItems];
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) {
+    bal[k] = __ballot_sync(0xffffffffu, f[k]);
+    if (lane == 0) s_cnt[k * kWarps + warp] = __popc(bal[k]);
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t v = s_cnt[lane];
+    const uint32_t incl = warp_incl_scan(v);
+    s_cnt[lane] = incl - v;
+    if (lane == 31) s_cnt[32] = incl;
+  }
+  __syncthreads();
+  const uint32_t lt = lanemask_lt();
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) rank[k] = s_cnt[k * kWarps + warp] + __popc(bal[k] & lt);
+  const uint32_t total = s_cnt[32];
+  __syncthreads();
+  return total;
+}
+
+// Sum of bcount[0..b) (exclusive block prefix), computed by warp 0, broadcast.
+__device__ __forceinline__ uint32_t block_prefix(const uint32_t* bcount, uint32_t b, uint32_t* s_out) {
+  if (threadIdx.x < 32) {
+    uint32_t s = 0;
+    for (uint32_t i = threadIdx.x; i < b; i += 32) s += __ldcg(bcount + i);
+    s = warp_sum<uint32_t>(s);
+    if (threadIdx.x == 0) *s_out = s;
+  }
+  __syncthreads();
+  const uint32_t v = *s_out;
+  __syncthreads();
+  return v;
+}
+
+template <bool kWarpPre>
+__global__ void __launch_bounds__(kBlock) k_tail(TailArgs a) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ uint32_t s_cnt[kItems * kWarps + 1];
+  __shared__ uint32_t s_misc[2];
+  __shared__ unsigned long long s_wsum[kWarps];
+  const uint32_t G = gridDim.x, b = blockIdx.x;
+  volatile DevCounters* vc = a.ctr;
+  const uint32_t n_entry = vc->n[a.r0];
+  for (int r = a.r0; r < kMaxR - 1; ++r) {
+    if ((uint32_t)r >= vc->stop_round || (uint32_t)r >= vc->phase_end) break;
+    const uint32_t n_r = vc->n[r];
+    const uint64_t m_r = vc->m[r];
+    const uint32_t mst_base = a.n_orig - n_r;
+    const unsigned long long* mcur = a.minb[(r - 1) & 1];
+    unsigned long long* mnext = a.minb[r & 1];
+    uint4* Ecur = a.E[r & 1];
+    uint4* Enext = a.E[(r + 1) & 1];
+    // ---- H1: hook decisions over this block's component chunk
+    const uint32_t cs = (n_r + G - 1) / G;
+    const uint32_t clo = min(b * cs, n_r), chi = min(clo + cs, n_r);
+    {
+      uint32_t roots = 0;
+      unsigned long long wsum = 0;
+      for (uint32_t base = clo; base < chi; base += kBlock * kItems) {
+        unsigned long long key[kItems];
+        uint4 e[kItems];
+        bool act[kItems];
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          const uint32_t c = base + k * kBlock + threadIdx.x;
+          act[k] = c < chi;
+          key[k] = act[k] ? mcur[c] : kNoKey;
+        }
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) e[k] = key[k] != kNoKey ? Ecur[(uint32_t)key[k]] : make_uint4(0, 0, 0, 0);
+        unsigned long long okey[kItems];
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          const uint32_t c = base + k * kBlock + threadIdx.x;
+          const uint32_t o = (e[k].x == c) ? e[k].y : e[k].x;
+          okey[k] = key[k] != kNoKey ? __ldcg(mcur + o) : kNoKey;
+        }
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          const uint32_t c = base + k * kBlock + threadIdx.x;
+          bool isroot = false;
+          if (act[k]) {
+            if (key[k] == kNoKey) {
+              isroot = true;
+              a.parent[c] = c;
+            } else {
+              const uint32_t o = (e[k].x == c) ? e[k].y : e[k].x;
+              isroot = okey[k] == key[k] && c < o;
+              a.parent[c] = isroot ? c : o;
+              if (!isroot) {
+                a.rootlabel[c] = e[k].w;  // stash the MST edge id until its slot is known
+                wsum += (uint32_t)(key[k] >> 32);
+              }
+            }
+          }
+          roots += __popc(__ballot_sync(0xffffffffu, isroot));
+        }
+      }
+      wsum = warp_sum<unsigned long long>(wsum);
+      if (lane_id() == 0) {
+        s_wsum[threadIdx.x >> 5] = wsum;
+        s_cnt[threadIdx.x >> 5] = roots;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        uint32_t rc = 0;
+        for (int i = 0; i < kWarps; ++i) {
+          t += s_wsum[i];
+          rc += s_cnt[i];
+        }
+        if (t) atomicAdd(&a.ctr->total_weight, t);
+        a.bcount[b] = rc;
+      }
+      __syncthreads();
+    }
+    grid.sync();
+    // ---- H2: dense root labels and MST slots, in component order
+    {
+      uint32_t running = block_prefix(a.bcount, b, s_misc);
+      const uint32_t start_prefix = running;
+      for (uint32_t base = clo; base < chi; base += kBlock * kItems) {
+        bool f[kItems];
+        uint32_t rank[kItems];
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          const uint32_t c = base + k * kBlock + threadIdx.x;
+          f[k] = c < chi && __ldcg(a.parent + c) == c;
+        }
+        const uint32_t tot = block_ranks(f, rank, s_cnt);
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          const uint32_t c = base + k * kBlock + threadIdx.x;
+          if (c < chi) {
+            const uint32_t before = running + rank[k];
+            if (f[k])
+              a.rootlabel[c] = before;
+            else
+              a.mst[mst_base + (c - before)] = a.rootlabel[c];
+          }
+        }
+        running += tot;
+      }
+      if (b == G - 1 && threadIdx.x == 0) {
+        (void)start_prefix;
+        const uint32_t roots = running;
+        a.ctr->n[r + 1] = roots;
+        if (roots <= 1) {
+          a.ctr->stop_round = (uint32_t)r + 1;
+        } else if (roots == n_r) {
+          if (a.light)
+            a.ctr->phase_end = (uint32_t)r;
+          else
+            a.ctr->stop_round = (uint32_t)r + 1;
+        }
+      }
+    }
+    grid.sync();
+    if ((uint32_t)r + 1 >= vc->stop_round || (uint32_t)r >= vc->phase_end) break;
+    const uint32_t n_next = vc->n[r + 1];
+    // ---- L: labels via root finding, clear the next min table
+    for (uint32_t base = b * kBlock * kItems; base < n_r; base += G * kBlock * kItems) {
+      uint32_t c[kItems], root[kItems];
+      bool v[kItems];
+#pragma unroll
+      for (int k = 0; k < kItems; ++k) {
+        c[k] = base + k * kBlock + threadIdx.x;
+        v[k] = c[k] < n_r;
+      }
+      find_roots<kItems>(a.parent, c, v, root);
+#pragma unroll
+      for (int k = 0; k < kItems; ++k) {
+        if (!v[k]) continue;
+        a.L[c[k]] = __ldcg(a.rootlabel + root[k]);
+        if (c[k] < n_next) mnext[c[k]] = kNoKey;
+      }
+    }
+    grid.sync();
+    // ---- C1: relabel in place, count kept per block (+ light-phase map update)
+    if (a.light) {
+      for (uint32_t x = b * kBlock + threadIdx.x; x < n_entry; x += G * kBlock) a.M[x] = __ldcg(a.L + a.M[x]);
+    }
+    const uint64_t es = (m_r + G - 1) / G;
+    const uint64_t elo = min((uint64_t)b * es, m_r), ehi = min(elo + es, m_r);
+    {
+      uint32_t kept = 0;
+      for (uint64_t base = elo; base < ehi; base += kBlock * kItems) {
+        uint2 e[kItems];
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          const uint64_t i = base + k * kBlock + threadIdx.x;
+          e[k] = i < ehi ? __ldcg(reinterpret_cast<const uint2*>(Ecur + i)) : make_uint2(0, 0);
+        }
+        uint32_t x[kItems], y[kItems];
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          const uint64_t i = base + k * kBlock + threadIdx.x;
+          x[k] = i < ehi ? __ldcg(a.L + e[k].x) : 0u;
+          y[k] = i < ehi ? __ldcg(a.L + e[k].y) : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          const uint64_t i = base + k * kBlock + threadIdx.x;
+          if (i < ehi) {
+            *reinterpret_cast<uint2*>(Ecur + i) = make_uint2(x[k], y[k]);
+            kept += (x[k] != y[k]);
+          }
+        }
+      }
+      kept = warp_sum<uint32_t>(kept);
+      if (lane_id() == 0) s_cnt[threadIdx.x >> 5] = kept;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int i = 0; i < kWarps; ++i) t += s_cnt[i];
+        a.bcount[b] = t;
+      }
+      __syncthreads();
+    }
+    grid.sync();
+    // ---- C2: ordered compaction + offers for round r+1
+    {
+      uint32_t running = block_prefix(a.bcount, b, s_misc);
+      for (uint64_t base = elo; base < ehi; base += kBlock * kItems) {
+        bool f[kItems];
+        uint32_t rank[kItems];
+        uint4 e[kItems];
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          const uint64_t i = base + k * kBlock + threadIdx.x;
+          e[k] = i < ehi ? __ldcg(Ecur + i) : make_uint4(0, 0, 0, 0);
+          f[k] = i < ehi && e[k].x != e[k].y;
+        }
+        const uint32_t tot = block_ranks(f, rank, s_cnt);
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          const uint32_t j = running + rank[k];
+          if (f[k]) Enext[j] = e[k];
+          const unsigned long long key = ((unsigned long long)e[k].z << 32) | j;
+          offer<kWarpPre>(mnext, e[k].x, key, f[k], true);
+          offer<kWarpPre>(mnext, e[k].y, key, f[k], true);
+        }
+        running += tot;
+      }
+      if (b == G - 1 && threadIdx.x == 0) {
+        a.ctr->m[r + 1] = running;
+        if (running == 0) {
+          if (a.light)
+            a.ctr->phase_end = (uint32_t)r + 1;
+          else if (a.ctr->stop_round == kNoStop)
+            a.ctr->stop_round = (uint32_t)r + 1;
+        }
+      }
+    }
+    grid.sync();
+  }
+}
+
+__global__ void k_iota(uint32_t* __restrict__ x, uint64_t count) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x)
+    x[i] = (uint32_t)i;
 }
 
 // ------------------------------ result -------------------------------------

@@ -31,6 +31,8 @@ def main():
     torch.cuda.synchronize()
     print(f"{a.config}: {e0.elapsed_time(e1) / a.reps:.3f} ms/MST rounds={info.rounds} "
           f"launches/MST={info.kernel_launches}")
+    print("  live_edges", info.live_edges)
+    print("  live_comps", info.live_comps)
 
 
 if __name__ == "__main__":
