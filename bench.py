@@ -113,17 +113,6 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def hot_bytes(m: int, live_edges: list) -> int:
-    """Algorithmic bytes of the edge-pass kernels of one MST."""
-    b = 12 * m  # k_min_round1 reads (src, dst, w)
-    R = len(live_edges)
-    for r in range(1, R):  # k_compact(r) runs fully for r < rounds
-        m_r = live_edges[r - 1]
-        k_r = live_edges[r]
-        b += (12 if r == 1 else 16) * m_r + 16 * k_r
-    return b
-
-
 def reference_cpu(g, threads: int, runs: int):
     """The unchanged reference boruvka_cas (oracle/_ref) on the host cores."""
     from oracle import oracle as O
@@ -215,7 +204,7 @@ def run_ours(args):
     for _ in range(max(args.warmup, 3)):
         one_step(info)
     barrier()
-    step_ms, hot_ms, hot_launch, launches = [], 0.0, 0, 0
+    step_ms, hot_ms, hot_launch, hot_b, launches = [], 0.0, 0, 0, 0
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     with ClockSampler(local) as clk:
@@ -229,6 +218,7 @@ def run_ours(args):
             if hot:
                 hot_ms += hot["ms"]
                 hot_launch += hot["launches"]
+                hot_b += hot["bytes"]
             launches += info.kernel_launches
         barrier()
     step_ms = [a.elapsed_time(b) for a, b in ev]
@@ -276,11 +266,12 @@ def run_ours(args):
     peak, peak_src = peaks()
     roofline = None
     if hot_launch:
-        per_mst = hot_bytes(m, info.live_edges)
-        achieved = per_mst * args.steps / (hot_ms / 1e3) / 1e9
+        per_mst = hot_b // args.steps
+        achieved = hot_b / (hot_ms / 1e3) / 1e9
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak, "traffic": None,
-                    "kernel": "edge pass (k_min_round1 + k_compact), summed over rounds",
+                    "kernel": "edge passes (round-1 min / split / round compactions / heavy filter / tail), "
+                              "summed over one MST; bytes = SURVEY 8(d) per-unit figures",
                     "bytes_per_mst": per_mst, "launches_per_mst": hot_launch / args.steps,
                     "kernel_ms_per_mst": hot_ms / args.steps, "peak_source": peak_src,
                     "whole_mst_alg_bytes": info.alg_bytes,

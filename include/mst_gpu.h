@@ -89,6 +89,8 @@ typedef struct mst_stats {
   uint64_t live_edges[MST_MAX_ROUNDS]; /* m_r: live edges entering round r */
   uint64_t live_comps[MST_MAX_ROUNDS]; /* n_r: live components in round r */
   uint32_t kernel_launches;   /* kernels launched by this call */
+  uint64_t hot_bytes;         /* algorithmic bytes of the timed edge passes
+                                 (mst_gpu_boruvka_device with ms_hot only) */
 } mst_stats_t;
 
 /* Single-GPU (num_gpus == 1) or single-process multi-GPU (num_gpus in 2..8,

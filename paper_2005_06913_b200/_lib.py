@@ -62,6 +62,7 @@ class MstStats(ctypes.Structure):
         ("live_edges", ctypes.c_uint64 * MST_MAX_ROUNDS),
         ("live_comps", ctypes.c_uint64 * MST_MAX_ROUNDS),
         ("kernel_launches", ctypes.c_uint32),
+        ("hot_bytes", ctypes.c_uint64),
     ]
 
 

@@ -166,8 +166,9 @@ def _raise_for(rc: int, result: MstResult | None = None) -> None:
 def _finish(rc, ids, count, total, stats, info):
     res = None
     if rc in (L.MST_OK, L.MST_ERR_DISCONNECTED):
-        res = MstResult(ids[: count.value].astype(np.int64), int(total.value), int(stats.rounds),
-                        float(stats.ms_total))
+        # uint32 ids (m < 2^32 - 1 is a boundary check); the C++ wrapper widens
+        # to the reference's int64 EdgeId
+        res = MstResult(ids[: count.value], int(total.value), int(stats.rounds), float(stats.ms_total))
     _info_from(stats, info)
     _raise_for(rc, res)
     return res
@@ -247,5 +248,6 @@ def boruvka_gpu_device(n: int, m: int, src_ptr: int, dst_ptr: int, w_ptr: int, o
     if hot is not None:
         hot["ms"] = ms_hot.value
         hot["launches"] = hot_n.value
+        hot["bytes"] = int(stats.hot_bytes)
     _raise_for(rc)
     return int(count.value), int(total.value)

@@ -55,7 +55,7 @@ def build_oracle(verbose: bool = True) -> None:
     """oracle/liboracle.so always; oracle/_ref when /root/reference exists."""
     targets = ["all"]
     if Path("/root/reference/proj/src/graph.cpp").exists():
-        targets.append("ref")
+        targets += ["ref", "dropin"]  # dropin links libmstgpu.so: build_library() first
     subprocess.run(["make", "-s", "-C", str(ROOT / "oracle"), *targets], check=True,
                    stdout=None if verbose else subprocess.DEVNULL)
 

@@ -277,13 +277,13 @@ uint32_t sort_ids(Workspace& ws, const uint32_t* d_ids, uint64_t count, uint64_t
   return launches;
 }
 
+// Warp pre-reduction (__match_any_sync + redux) before the filtered atomicMin
+// costs more than it saves on the BASELINE graphs once the read-first filter
+// is on (c1: 1.25 -> 0.96 ms without it); kept selectable for hub-heavy
+// inputs: MST_WARP_PREREDUCE=1.
 bool warp_prereduce_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("MST_WARP_PREREDUCE");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
+  const char* e = getenv("MST_WARP_PREREDUCE");
+  return e && e[0] == '1';
 }
 
 // ------------------------------- single GPU ---------------------------------
@@ -472,11 +472,17 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
             M, n_bound);
         ++launches;
       }
-      auto kt = k_tail<kPre>;
-      const int bps = std::min(blocks_per_sm(kt), 4);
+      auto kt = getenv("MST_TAIL_PREREDUCE") && getenv("MST_TAIL_PREREDUCE")[0] == '1' ? k_tail<true> : k_tail<false>;
+      const int bps = std::max(1, std::min(blocks_per_sm(kt), env_int("MST_TAIL_BPS", 4)));
       const unsigned G = (unsigned)(sm_count(dev) * bps);
       uint32_t* bcount = ws.get<uint32_t>("bcount", G);
-      TailArgs ta{{E[0], E[1]}, {minb[0], minb[1]}, parent, rootlabel, L, mst, bcount, M, d_ctr, n, r, (int)light};
+      unsigned long long* trace = nullptr;
+      if (env_int("MST_TAIL_TRACE", 0)) {
+        trace = ws.get<unsigned long long>("tail_trace", 512);
+        MST_CUDA_CHECK(cudaMemsetAsync(trace, 0, 512 * 8, s));
+      }
+      TailArgs ta{{E[0], E[1]}, {minb[0], minb[1]}, parent, rootlabel, L, mst, bcount, M, trace, d_ctr, n, r,
+                  (int)light};
       void* args[] = {&ta};
       hot_begin(kHotTail, r, light);
       MST_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)kt, G, kBlock, args, 0, s));
@@ -485,6 +491,13 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       MST_CUDA_CHECK(cudaMemcpyAsync(&ws.h_snap[kMaxR - 1], d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
       MST_CUDA_CHECK(cudaStreamSynchronize(s));
       const DevCounters& snap = ws.h_snap[kMaxR - 1];
+      if (trace) {
+        std::vector<unsigned long long> tt(512);
+        MST_CUDA_CHECK(cudaMemcpy(tt.data(), trace, 512 * 8, cudaMemcpyDeviceToHost));
+        fprintf(stderr, "tail r0=%d G=%u:", r, G);
+        for (int i = 1; i < 512 && tt[i]; ++i) fprintf(stderr, " %.1f", (tt[i] - tt[i - 1]) * 1e-3);
+        fprintf(stderr, " (us per phase: H1 H2 L C1 C2 per round)\n");
+      }
       if (snap.err || snap.stop_round != kNoStop) break;
       if (light && snap.phase_end != kNoStop) {
         if (M) levels.push_back({M, r});
@@ -575,10 +588,10 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       } else if (h.kind == kHotHeavy) {
         bytes = 12ull * m + 16ull * c.m[h.r];
       } else if (h.kind == kHotTail) {
-        // per round: relabel pass (16 B read + 8 B write) + compaction (16 B read + 16 B per kept)
+        // algorithmic: one 16 B read per live edge, one 16 B write per kept edge
         const int last = (h.light && phase_end) ? phase_end : stop;
         const DevCounters& cc = (h.light && phase_end) ? snap_b : c;
-        for (int rr = h.r; rr + 1 < last && rr < kMaxR - 1; ++rr) bytes += 40ull * cc.m[rr] + 16ull * cc.m[rr + 1];
+        for (int rr = h.r; rr + 1 < last && rr < kMaxR - 1; ++rr) bytes += 16ull * cc.m[rr] + 16ull * cc.m[rr + 1];
       } else {
         const bool ran = h.r + 1 < stop && (!h.light || phase_end == 0 || h.r < phase_end);
         if (!ran) continue;
@@ -1236,6 +1249,7 @@ int mst_gpu_boruvka_device(const mst_edges_soa_t* edges, uint32_t* d_out_ids, vo
     RunOut o = run_single(a, stats);
     if (ms_hot) *ms_hot = o.ms_hot;
     if (hot_launches) *hot_launches = o.hot_launches;
+    if (stats) stats->hot_bytes = o.hot_bytes;
     if (stats) stats->alg_bytes = alg_bytes_from(o.ctr, o.rounds);
     return finish_status(o, out_count, out_total_weight);
   });

@@ -1059,6 +1059,7 @@ struct TailArgs {
   uint32_t* mst;
   uint32_t* bcount;  // [gridDim.x]
   uint32_t* M;       // light phase: entry-label -> current-label map (n[r0] entries)
+  unsigned long long* trace;  // optional: globaltimer stamps at phase boundaries (block 0)
   DevCounters* ctr;
   uint32_t n_orig;
   int r0;
@@ -1105,10 +1106,21 @@ __device__ __forceinline__ uint32_t block_prefix(const uint32_t* bcount, uint32_
   return v;
 }
 
+__device__ __forceinline__ void tail_stamp(const TailArgs& a, int& slot) {
+  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && slot < 512) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[slot] = t;
+  }
+  ++slot;
+}
+
 template <bool kWarpPre>
 __global__ void __launch_bounds__(kBlock) k_tail(TailArgs a) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
+  int slot = 0;
+  tail_stamp(a, slot);
   __shared__ uint32_t s_cnt[kItems * kWarps + 1];
   __shared__ uint32_t s_misc[2];
   __shared__ unsigned long long s_wsum[kWarps];
@@ -1189,6 +1201,7 @@ __global__ void __launch_bounds__(kBlock) k_tail(TailArgs a) {
       __syncthreads();
     }
     grid.sync();
+    tail_stamp(a, slot);
     // ---- H2: dense root labels and MST slots, in component order
     {
       uint32_t running = block_prefix(a.bcount, b, s_misc);
@@ -1230,6 +1243,7 @@ __global__ void __launch_bounds__(kBlock) k_tail(TailArgs a) {
       }
     }
     grid.sync();
+    tail_stamp(a, slot);
     if ((uint32_t)r + 1 >= vc->stop_round || (uint32_t)r >= vc->phase_end) break;
     const uint32_t n_next = vc->n[r + 1];
     // ---- L: labels via root finding, clear the next min table
@@ -1250,6 +1264,7 @@ __global__ void __launch_bounds__(kBlock) k_tail(TailArgs a) {
       }
     }
     grid.sync();
+    tail_stamp(a, slot);
     // ---- C1: relabel in place, count kept per block (+ light-phase map update)
     if (a.light) {
       for (uint32_t x = b * kBlock + threadIdx.x; x < n_entry; x += G * kBlock) a.M[x] = __ldcg(a.L + a.M[x]);
@@ -1292,6 +1307,7 @@ __global__ void __launch_bounds__(kBlock) k_tail(TailArgs a) {
       __syncthreads();
     }
     grid.sync();
+    tail_stamp(a, slot);
     // ---- C2: ordered compaction + offers for round r+1
     {
       uint32_t running = block_prefix(a.bcount, b, s_misc);
@@ -1327,6 +1343,7 @@ __global__ void __launch_bounds__(kBlock) k_tail(TailArgs a) {
       }
     }
     grid.sync();
+    tail_stamp(a, slot);
   }
 }
 
