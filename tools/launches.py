@@ -12,7 +12,8 @@ for r in rows:
         continue
     if hdr and len(r) == len(hdr):
         d = dict(zip(hdr, r))
-        out.append((d['Kernel Name'].split('(')[0].replace('void ', '')[:60], float(d['Metric Value'])))
+        nm = d['Kernel Name'].split('(')[0].replace('void ', '').replace('mstgpu::', '').replace('<unnamed>::', '')
+        out.append((nm[:60], float(d['Metric Value'])))
 ends = [i for i, (k, _) in enumerate(out) if k.startswith('k_bitmap_emit')]
 start = ends[-2] + 1 if len(ends) >= 2 else 0
 last = out[start:ends[-1] + 1]
