@@ -267,12 +267,22 @@ uint32_t sort_ids(Workspace& ws, const uint32_t* d_ids, uint64_t count, uint64_t
     k_mark<<<g, 256, 0, ws.stream>>>(d_ids, (uint32_t)count, bits, m_total);
     ++launches;
   }
-  unsigned long long* st = ws.status_array(tiles_of(words));
-  unsigned int* tile_ctr = &d_ctr->tile[0][kSlotSort];
-  MST_CUDA_CHECK(cudaMemsetAsync(tile_ctr, 0, sizeof(unsigned int), ws.stream));
-  k_bitmap_emit<<<persistent_grid(k_bitmap_emit, ws.device, tiles_of(words)), kBlock, 0, ws.stream>>>(
-      bits, words, d_sorted, tile_ctr, st, ws.next_epoch());
-  ++launches;
+  const uint64_t tiles = tiles_of(words);
+  uint32_t* counts = ws.get<uint32_t>("sort_counts", tiles);
+  const int fused = tiles <= kFusedScanMaxTiles ? 1 : 0;
+  MST_CUDA_CHECK(cudaMemsetAsync(&d_ctr->done[0][kSlotSort], 0, sizeof(unsigned int), ws.stream));
+  const unsigned g = (unsigned)std::max<uint64_t>(
+      1, std::min<uint64_t>(tiles, (uint64_t)sm_count(ws.device) * blocks_per_sm(k_bitmap_count)));
+  k_bitmap_count<<<g, kBlock, 0, ws.stream>>>(bits, words, counts, d_ctr, fused);
+  if (!fused) {
+    unsigned long long* st = ws.status_array(tiles_of(words));
+    k_scan_counts<kScanPlain><<<(unsigned)std::max<uint64_t>(
+                                    1, std::min<uint64_t>((tiles + kScanTile - 1) / kScanTile, (uint64_t)sm_count(ws.device))),
+                                kScanBlock, 0, ws.stream>>>(counts, tiles, d_ctr, 0, st, ws.next_epoch(), 0, 0);
+    ++launches;
+  }
+  k_bitmap_emit<<<g, kBlock, 0, ws.stream>>>(bits, words, counts, d_sorted);
+  launches += 2;
   MST_CUDA_CHECK(cudaGetLastError());
   return launches;
 }
@@ -339,12 +349,15 @@ void launch_two_pass(Workspace& ws, const CompactBufs& cb, View in, uint4* relab
   auto kcnt = k_count<View, kMode>;
   const unsigned gc = (unsigned)std::max<uint64_t>(
       1, std::min<uint64_t>(tiles, (uint64_t)sm_count(dev) * blocks_per_sm(kcnt)));
-  kcnt<<<gc, kBlock, 0, ws.stream>>>(in, relabeled, L, cb.masks, cb.counts, n_orig, d_ctr, r);
-  auto ksc = k_scan_counts<kScanEdges>;
-  const unsigned gs = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((tiles + kScanTile - 1) / kScanTile,
-                                                                          (uint64_t)sm_count(dev)));
-  ksc<<<gs, kScanBlock, 0, ws.stream>>>(cb.counts, tiles, d_ctr, r, cb.st, ws.next_epoch(), light,
-                                        View::kOriginal ? 1 : 0);
+  const int fused = tiles <= kFusedScanMaxTiles ? 1 : 0;  // small: the last count block scans
+  kcnt<<<gc, kBlock, 0, ws.stream>>>(in, relabeled, L, cb.masks, cb.counts, n_orig, d_ctr, r, fused, slot, light);
+  if (!fused) {
+    auto ksc = k_scan_counts<kScanEdges>;
+    const unsigned gs = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((tiles + kScanTile - 1) / kScanTile,
+                                                                            (uint64_t)sm_count(dev)));
+    ksc<<<gs, kScanBlock, 0, ws.stream>>>(cb.counts, tiles, d_ctr, r, cb.st, ws.next_epoch(), light,
+                                          View::kOriginal ? 1 : 0);
+  }
   auto kem = k_emit<View, kMode, kPre>;
   const unsigned ge = (unsigned)std::max<uint64_t>(
       1, std::min<uint64_t>(tiles, (uint64_t)sm_count(dev) * blocks_per_sm(kem)));
@@ -511,18 +524,21 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     uint4* Eout = E[(r + 1) & 1];
     {
       const uint64_t ht = tiles_of(n_bound);
+      const int hfused = ht <= kFusedScanMaxTiles ? 1 : 0;
       if (original_in) {
         auto kd = k_hook_decide<InView>;
         kd<<<(unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ht, (uint64_t)sm_count(dev) * blocks_per_sm(kd))),
-             kBlock, 0, s>>>(in, mcur, parent, rootlabel, hmasks, hcounts, d_ctr, r);
+             kBlock, 0, s>>>(in, mcur, parent, rootlabel, hmasks, hcounts, d_ctr, r, hfused, (int)light);
       } else {
         auto kd = k_hook_decide<PackedView>;
         kd<<<(unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ht, (uint64_t)sm_count(dev) * blocks_per_sm(kd))),
-             kBlock, 0, s>>>(PackedView{E[r & 1]}, mcur, parent, rootlabel, hmasks, hcounts, d_ctr, r);
+             kBlock, 0, s>>>(PackedView{E[r & 1]}, mcur, parent, rootlabel, hmasks, hcounts, d_ctr, r, hfused,
+                             (int)light);
       }
-      k_scan_counts<kScanRoots><<<(unsigned)std::max<uint64_t>(1, std::min<uint64_t>((ht + kScanTile - 1) / kScanTile,
-                                                                                     (uint64_t)sm_count(dev))),
-                                  kScanBlock, 0, s>>>(hcounts, ht, d_ctr, r, st, ws.next_epoch(), (int)light, 0);
+      if (!hfused)
+        k_scan_counts<kScanRoots><<<(unsigned)std::max<uint64_t>(
+                                        1, std::min<uint64_t>((ht + kScanTile - 1) / kScanTile, (uint64_t)sm_count(dev))),
+                                    kScanBlock, 0, s>>>(hcounts, ht, d_ctr, r, st, ws.next_epoch(), (int)light, 0);
       k_hook_emit<<<(unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ht, (uint64_t)sm_count(dev) *
                                                                               blocks_per_sm(k_hook_emit))),
                     kBlock, 0, s>>>(parent, rootlabel, hmasks, hcounts, mst, n, d_ctr, r);

@@ -52,6 +52,7 @@ struct DevCounters {
   unsigned long long m[kMaxR];
   unsigned int n[kMaxR];
   unsigned int tile[kMaxR][4];
+  unsigned int done[kMaxR][4];  // last-block-done check-ins (fused scans)
   unsigned int err;
   unsigned int stop_round;  // first round whose hook must not run
   unsigned int phase_end;   // first round past the light phase (Filter-Boruvka)
@@ -671,6 +672,90 @@ __global__ void k_compose(uint32_t* __restrict__ Lr, const uint32_t* __restrict_
     Lr[c] = __ldg(Lnext + Lr[c]);
 }
 
+// ------------------------------ scan helpers -------------------------------
+//   kScanEdges : m[r+1] = kept; none kept -> stop (or light-phase end)
+//   kScanRoots : n[r+1] = roots; <= 1 -> stop; == n[r] -> stop (or light end)
+enum { kScanEdges = 0, kScanRoots = 1, kScanPlain = 2 };
+constexpr uint32_t kFusedScanMaxTiles = 16384;  // one block scans <= this many counts
+
+template <int kKind>
+__device__ __forceinline__ void scan_verdict(DevCounters* ctr, int r, uint32_t total, int light_phase) {
+  if (kKind == kScanEdges) {
+    ctr->m[r + 1] = total;
+    if (total == 0) {
+      if (light_phase)
+        ctr->phase_end = (uint32_t)r + 1;
+      else if (ctr->stop_round == kNoStop)
+        ctr->stop_round = (uint32_t)r + 1;
+    }
+  } else if (kKind == kScanRoots) {
+    ctr->n[r + 1] = total;
+    if (total <= 1) {
+      ctr->stop_round = (uint32_t)r + 1;
+    } else if (total == ctr->n[r]) {
+      // no live edge anywhere: done (a forest if total > 1), unless this is
+      // the light phase of Filter-Boruvka, which then simply ends
+      if (light_phase)
+        ctr->phase_end = (uint32_t)r;
+      else
+        ctr->stop_round = (uint32_t)r + 1;
+    }
+  } else {
+    ctr->m[kMaxR - 1] = total;
+  }
+}
+
+// Exclusive in-place scan of counts[0..T) by ONE block of kBlock threads
+// (chunks of kBlock*8 with a running offset). Returns the total.
+__device__ __forceinline__ uint32_t block_scan_counts(uint32_t* counts, uint32_t T, uint32_t* s_warp) {
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  uint32_t running = 0;
+  for (uint32_t base = 0; base < T; base += kBlock * 8) {
+    const uint32_t i0 = base + threadIdx.x * 8;
+    uint32_t v[8], sum = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      v[k] = i0 + k < T ? __ldcg(counts + i0 + k) : 0u;
+      sum += v[k];
+    }
+    const uint32_t incl = warp_incl_scan(sum);
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t wv = lane < kWarps ? s_warp[lane] : 0u;
+      const uint32_t wi = warp_incl_scan(wv);
+      if (lane < kWarps) s_warp[lane] = wi - wv;
+      if (lane == 31) s_warp[kWarps] = wi;
+    }
+    __syncthreads();
+    uint32_t run = running + s_warp[warp] + incl - sum;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (i0 + k < T) counts[i0 + k] = run;
+      run += v[k];
+    }
+    running += s_warp[kWarps];
+    __syncthreads();
+  }
+  return running;
+}
+
+// Last-block-done: every block fences its count writes and checks in; the
+// block that checks in last scans all T counts and publishes the verdict.
+template <int kKind>
+__device__ __forceinline__ void fused_scan_if_last(uint32_t* counts, uint32_t T, DevCounters* ctr, int r, int slot,
+                                                   int light_phase, uint32_t* s_warp, uint32_t* s_flag) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) *s_flag = atomicAdd(&ctr->done[r][slot], 1u) == gridDim.x - 1 ? 1u : 0u;
+  __syncthreads();
+  if (*s_flag) {
+    __threadfence();
+    const uint32_t total = block_scan_counts(counts, T, s_warp);
+    if (threadIdx.x == 0) scan_verdict<kKind>(ctr, r, total, light_phase);
+  }
+}
+
 // ------------------------------ two-pass ordered compaction ----------------
 // The single-pass look-back above leaves each tile ~10 us in flight (its
 // aggregate needs the tile's loads + gathers first), which caps a pass at
@@ -688,7 +773,8 @@ template <class View, int kMode>
 __global__ void __launch_bounds__(kBlock) k_count(View in, uint4* __restrict__ relabeled,
                                                   const uint32_t* __restrict__ L,
                                                   uint32_t* __restrict__ masks, uint32_t* __restrict__ counts,
-                                                  uint32_t n_orig, DevCounters* ctr, int r) {
+                                                  uint32_t n_orig, DevCounters* ctr, int r, int fused, int slot,
+                                                  int light_phase) {
   __shared__ uint32_t s_cnt[kWarps];
   const uint32_t stop = ctr->stop_round;
   if ((uint32_t)r >= ctr->phase_end || (uint32_t)r + 1 >= stop) return;
@@ -750,6 +836,10 @@ __global__ void __launch_bounds__(kBlock) k_count(View in, uint4* __restrict__ r
       counts[tile] = t;
     }
     __syncthreads();
+  }
+  if (fused) {
+    __shared__ uint32_t s_warp[kWarps + 1], s_flag;
+    fused_scan_if_last<kScanEdges>(counts, ntiles, ctr, r, slot, light_phase, s_warp, &s_flag);
   }
 }
 
@@ -837,10 +927,8 @@ __global__ void __launch_bounds__(kBlock) k_emit(View in, const uint4* __restric
 // Exclusive scan of per-tile counts in place (8192 counts per block, chained
 // with the look-back across <= a few hundred blocks), so the emit passes need
 // no inter-tile communication at all. The last block also publishes the
-// total and the round verdict:
-//   kScanEdges : m[r+1] = kept; none kept -> stop (or light-phase end)
-//   kScanRoots : n[r+1] = roots; <= 1 -> stop; == n[r] -> stop (or light end)
-enum { kScanEdges = 0, kScanRoots = 1, kScanPlain = 2 };
+// total and the round verdict (scan_verdict). Small scans are instead fused
+// into the counting kernel (fused_scan_if_last) and cost no launch.
 constexpr int kScanItems = 8;
 constexpr int kScanBlock = 1024;
 constexpr int kScanTile = kScanBlock * kScanItems;
@@ -895,30 +983,7 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_counts(uint32_t* __restrict
       if (base + k < n_items) counts[base + k] = run;
       run += v[k];
     }
-    if (blk == max(nblocks, 1u) - 1 && threadIdx.x == 0) {
-      const uint32_t total = s_misc[0] + s_misc[1];
-      if (kKind == kScanEdges) {
-        ctr->m[r + 1] = total;
-        if (total == 0) {
-          if (light_phase)
-            ctr->phase_end = (uint32_t)r + 1;
-          else if (ctr->stop_round == kNoStop)
-            ctr->stop_round = (uint32_t)r + 1;
-        }
-      } else if (kKind == kScanRoots) {
-        ctr->n[r + 1] = total;
-        if (total <= 1) {
-          ctr->stop_round = (uint32_t)r + 1;
-        } else if (total == ctr->n[r]) {
-          if (light_phase)
-            ctr->phase_end = (uint32_t)r;
-          else
-            ctr->stop_round = (uint32_t)r + 1;
-        }
-      } else {
-        ctr->m[kMaxR - 1] = total;
-      }
-    }
+    if (blk == max(nblocks, 1u) - 1 && threadIdx.x == 0) scan_verdict<kKind>(ctr, r, s_misc[0] + s_misc[1], light_phase);
     __syncthreads();
   }
 }
@@ -932,7 +997,7 @@ template <class View>
 __global__ void __launch_bounds__(kBlock) k_hook_decide(View E, const unsigned long long* __restrict__ minimum,
                                                         uint32_t* __restrict__ parent, uint32_t* __restrict__ rootlabel,
                                                         uint32_t* __restrict__ masks, uint32_t* __restrict__ counts,
-                                                        DevCounters* ctr, int r) {
+                                                        DevCounters* ctr, int r, int fused, int light_phase) {
   __shared__ uint32_t s_cnt[kWarps];
   __shared__ unsigned long long s_wsum[kWarps];
   if ((uint32_t)r >= ctr->stop_round || (uint32_t)r >= ctr->phase_end) return;
@@ -1000,6 +1065,10 @@ __global__ void __launch_bounds__(kBlock) k_hook_decide(View E, const unsigned l
     for (int i = 0; i < kWarps; ++i) t += s_wsum[i];
     if (t) atomicAdd(&ctr->total_weight, t);
   }
+  if (fused) {
+    __shared__ uint32_t s_warp[kWarps + 1], s_flag;
+    fused_scan_if_last<kScanRoots>(counts, ntiles, ctr, r, 0, light_phase, s_warp, &s_flag);
+  }
 }
 
 __global__ void __launch_bounds__(kBlock) k_hook_emit(const uint32_t* __restrict__ parent,
@@ -1066,6 +1135,8 @@ struct TailArgs {
   int light;
 };
 
+constexpr uint32_t kTailSmemMin = 4096;  // block-local min table entries (32 KB)
+
 // Ordered ranks of kItems striped flags per thread; returns the total.
 __device__ __forceinline__ uint32_t block_ranks(const bool (&f)[kItems], uint32_t (&rank)[kItems],
                                                 uint32_t* s_cnt) {
@@ -1124,6 +1195,7 @@ __global__ void __launch_bounds__(kBlock) k_tail(TailArgs a) {
   __shared__ uint32_t s_cnt[kItems * kWarps + 1];
   __shared__ uint32_t s_misc[2];
   __shared__ unsigned long long s_wsum[kWarps];
+  __shared__ unsigned long long s_min[kTailSmemMin];
   const uint32_t G = gridDim.x, b = blockIdx.x;
   volatile DevCounters* vc = a.ctr;
   const uint32_t n_entry = vc->n[a.r0];
@@ -1310,6 +1382,13 @@ __global__ void __launch_bounds__(kBlock) k_tail(TailArgs a) {
     tail_stamp(a, slot);
     // ---- C2: ordered compaction + offers for round r+1
     {
+      // Few components left: offers hammer a handful of lines. Aggregate them
+      // in a block-local shared-memory table and flush once per block.
+      const bool local = n_next <= kTailSmemMin;
+      if (local) {
+        for (uint32_t c = threadIdx.x; c < n_next; c += kBlock) s_min[c] = kNoKey;
+        __syncthreads();
+      }
       uint32_t running = block_prefix(a.bcount, b, s_misc);
       for (uint64_t base = elo; base < ehi; base += kBlock * kItems) {
         bool f[kItems];
@@ -1327,10 +1406,24 @@ __global__ void __launch_bounds__(kBlock) k_tail(TailArgs a) {
           const uint32_t j = running + rank[k];
           if (f[k]) Enext[j] = e[k];
           const unsigned long long key = ((unsigned long long)e[k].z << 32) | j;
-          offer<kWarpPre>(mnext, e[k].x, key, f[k], true);
-          offer<kWarpPre>(mnext, e[k].y, key, f[k], true);
+          if (local) {
+            if (f[k]) {
+              atomicMin(s_min + e[k].x, key);
+              atomicMin(s_min + e[k].y, key);
+            }
+          } else {
+            offer<kWarpPre>(mnext, e[k].x, key, f[k], true);
+            offer<kWarpPre>(mnext, e[k].y, key, f[k], true);
+          }
         }
         running += tot;
+      }
+      if (local) {
+        __syncthreads();
+        for (uint32_t c = threadIdx.x; c < n_next; c += kBlock) {
+          const unsigned long long v = s_min[c];
+          if (v != kNoKey && v < __ldcg(mnext + c)) atomicMin(mnext + c, v);
+        }
       }
       if (b == G - 1 && threadIdx.x == 0) {
         a.ctr->m[r + 1] = running;
@@ -1385,20 +1478,45 @@ __global__ void k_mark(const uint32_t* __restrict__ ids, uint32_t count, uint32_
 
 // Sorted id list from the bitmap: popc per word, ordered scan with look-back,
 // then each word writes its set bits in ascending order.
-__global__ void __launch_bounds__(kBlock) k_bitmap_emit(const uint32_t* __restrict__ bits,
-                                                        uint64_t words, uint32_t* __restrict__ out,
-                                                        unsigned int* tile_ctr,
-                                                        unsigned long long* status, uint32_t epoch) {
-  __shared__ uint32_t s_scan[32];
-  __shared__ uint32_t s_misc[2];
-  __shared__ uint32_t s_tile;
+// Sorted output, two passes like the compactions: popcount per tile of
+// bitmap words (+ fused or separate scan), then each word writes its set
+// bits at their final positions in ascending order.
+__global__ void __launch_bounds__(kBlock) k_bitmap_count(const uint32_t* __restrict__ bits, uint64_t words,
+                                                         uint32_t* __restrict__ counts, DevCounters* ctr,
+                                                         int fused) {
+  __shared__ uint32_t s_cnt[kWarps];
   const uint32_t ntiles = (uint32_t)((words + kTile - 1) / kTile);
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-  while (true) {
-    if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      const uint64_t i = (uint64_t)tile * kTile + k * kBlock + threadIdx.x;
+      c += i < words ? __popc(__ldcs(bits + i)) : 0u;
+    }
+    c = warp_sum<uint32_t>(c);
+    if (lane == 0) s_cnt[warp] = c;
     __syncthreads();
-    const uint32_t tile = s_tile;
-    if (tile >= ntiles) break;
+    if (threadIdx.x == 0) {
+      uint32_t t = 0;
+      for (int w = 0; w < kWarps; ++w) t += s_cnt[w];
+      counts[tile] = t;
+    }
+    __syncthreads();
+  }
+  if (fused) {
+    __shared__ uint32_t s_warp[kWarps + 1], s_flag;
+    fused_scan_if_last<kScanPlain>(counts, ntiles, ctr, 0, kSlotSort, 0, s_warp, &s_flag);
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) k_bitmap_emit(const uint32_t* __restrict__ bits, uint64_t words,
+                                                        const uint32_t* __restrict__ offsets,
+                                                        uint32_t* __restrict__ out) {
+  __shared__ uint32_t s_scan[32];
+  const uint32_t ntiles = (uint32_t)((words + kTile - 1) / kTile);
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     uint32_t wv[kItems], cnt[kItems], incl[kItems];
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
@@ -1413,21 +1531,18 @@ __global__ void __launch_bounds__(kBlock) k_bitmap_emit(const uint32_t* __restri
       const uint32_t v = s_scan[lane];
       const uint32_t in = warp_incl_scan(v);
       s_scan[lane] = in - v;
-      const uint32_t tot = __shfl_sync(0xffffffffu, in, 31);
-      const uint32_t ex = lookback(status, tile, tot, epoch);
-      if (lane == 0) s_misc[0] = ex;
     }
     __syncthreads();
-    const uint32_t prefix = s_misc[0];
+    const uint32_t prefix = __ldg(offsets + tile);
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
       const uint64_t i = (uint64_t)tile * kTile + k * kBlock + threadIdx.x;
       uint32_t pos = prefix + s_scan[k * kWarps + warp] + incl[k] - cnt[k];
       uint32_t x = wv[k];
       while (x) {
-        const int b = __ffs(x) - 1;
+        const int bit = __ffs(x) - 1;
         x &= x - 1;
-        out[pos++] = (uint32_t)(i * 32 + b);
+        out[pos++] = (uint32_t)(i * 32 + bit);
       }
     }
     __syncthreads();
