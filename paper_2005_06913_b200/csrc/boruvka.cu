@@ -212,6 +212,11 @@ unsigned persistent_grid(K kernel, int device, uint64_t tiles) {
 
 uint64_t tiles_of(uint64_t count) { return (count + kTile - 1) / kTile; }
 uint64_t tiles_c(uint64_t count) { return (count + kCTile - 1) / kCTile; }
+unsigned long long next_pow2(unsigned long long x) {
+  unsigned long long p = 1024;
+  while (p < x) p <<= 1;
+  return p;
+}
 
 // Read-before-atomic pays off while the min table stays L2-resident.
 int filt_for(uint64_t table_entries) {
@@ -337,20 +342,32 @@ struct CompactBufs {
   uint32_t* counts;
   uint32_t* masks;
   unsigned long long* st;
+  uint4* stage;  // survivors of the sparse modes, compacted per tile
 };
 
 // Ordered compaction as count + emit (kernels.cuh, "two-pass ordered compaction").
 template <class View, int kMode, bool kPre>
 void launch_two_pass(Workspace& ws, const CompactBufs& cb, View in, uint4* relabeled, const uint32_t* L, uint4* out,
                      unsigned long long* min_next, DevCounters* d_ctr, int r, uint64_t m_bound, uint32_t n_orig,
-                     int slot, int light, int filt) {
+                     int slot, int light, int filt, PairTable pt = PairTable{nullptr, nullptr, 0}) {
   const int dev = ws.device;
   const uint64_t tiles = tiles_c(m_bound);
+  const int fused = tiles <= kFusedScanMaxTiles ? 1 : 0;  // small: the last count block scans
+  const bool armed = kMode == kModeRelabel && !View::kOriginal && pt.pairs != nullptr;
   auto kcnt = k_count<View, kMode>;
   const unsigned gc = (unsigned)std::max<uint64_t>(
       1, std::min<uint64_t>(tiles, (uint64_t)sm_count(dev) * blocks_per_sm(kcnt)));
-  const int fused = tiles <= kFusedScanMaxTiles ? 1 : 0;  // small: the last count block scans
-  kcnt<<<gc, kBlock, 0, ws.stream>>>(in, relabeled, L, cb.masks, cb.counts, n_orig, d_ctr, r, fused, slot, light);
+  // armed: this launch relabels + inserts pairs if the device chose dedup
+  // (decided and table cleared by k_label), the kModeDedup pass counts
+  kcnt<<<gc, kBlock, 0, ws.stream>>>(in, kMode == kModeRelabel ? relabeled : cb.stage, L, cb.masks, cb.counts, n_orig,
+                                     d_ctr, r, fused, slot, light, pt);
+  if constexpr (!View::kOriginal) {
+    if (armed) {
+      auto kdc = k_count<View, kModeDedup>;
+      kdc<<<gc, kBlock, 0, ws.stream>>>(PackedView{relabeled}, cb.stage, L, cb.masks, cb.counts, n_orig, d_ctr, r,
+                                        fused, slot, light, pt);
+    }
+  }
   if (!fused) {
     auto ksc = k_scan_counts<kScanEdges>;
     const unsigned gs = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((tiles + kScanTile - 1) / kScanTile,
@@ -358,10 +375,19 @@ void launch_two_pass(Workspace& ws, const CompactBufs& cb, View in, uint4* relab
     ksc<<<gs, kScanBlock, 0, ws.stream>>>(cb.counts, tiles, d_ctr, r, cb.st, ws.next_epoch(), light,
                                           View::kOriginal ? 1 : 0);
   }
-  auto kem = k_emit<View, kMode, kPre>;
-  const unsigned ge = (unsigned)std::max<uint64_t>(
-      1, std::min<uint64_t>(tiles, (uint64_t)sm_count(dev) * blocks_per_sm(kem)));
-  kem<<<ge, kBlock, 0, ws.stream>>>(in, relabeled, L, cb.masks, cb.counts, out, min_next, d_ctr, r, filt);
+  const unsigned ge = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)sm_count(dev) * 8));
+  if (armed) {
+    auto kde = k_emit_staged<kModeDedup, kPre>;
+    kde<<<ge, kBlock, 0, ws.stream>>>(cb.stage, cb.counts, out, min_next, d_ctr, r, filt);
+  }
+  if (kMode == kModeRelabel) {
+    auto kem = k_emit<View, kMode, kPre>;
+    kem<<<ge, kBlock, 0, ws.stream>>>(in, relabeled, L, cb.masks, cb.counts, out, min_next, d_ctr, r, filt,
+                                      armed ? 1 : 0);
+  } else {
+    auto kes = k_emit_staged<kMode, kPre>;
+    kes<<<ge, kBlock, 0, ws.stream>>>(cb.stage, cb.counts, out, min_next, d_ctr, r, filt);
+  }
   MST_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -381,7 +407,8 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   const Recover no_rec{nullptr, nullptr, nullptr};
   const int dev = ws.device;
   const CompactBufs cb{ws.get<uint32_t>("tile_counts", tiles_c(m)),
-                       ws.get<uint32_t>("tile_masks", tiles_c(m) * kCItems * kWarps), st};
+                       ws.get<uint32_t>("tile_masks", tiles_c(m) * kCItems * kWarps), st,
+                       ws.get<uint4>("stage", tiles_c(m) * kCTile)};
   uint32_t* hcounts = ws.get<uint32_t>("hook_counts", tiles_of(n));
   uint32_t* hmasks = ws.get<uint32_t>("hook_masks", tiles_of(n) * kItems * kWarps);
   (void)no_rec;
@@ -432,6 +459,8 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   int phase_end = 0;
   DevCounters snap_b{};  // counters at the end of the light phase
   const bool tail_on = env_int("MST_TAIL", 1) != 0;
+  const bool dedup_on = env_int("MST_DEDUP", 1) != 0;
+  const uint64_t dedup_min_edges = (uint64_t)env_double("MST_DEDUP_MIN_EDGES", 2.0e6);
   const uint64_t tail_edges = (uint64_t)env_double("MST_TAIL_EDGES", 3.0e6);
 
   // Light phase over: compose its relabel maps into a vertex -> component map,
@@ -549,10 +578,18 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       Lr = ws.get<uint32_t>("Llvl" + std::to_string(r), n_bound);
       levels.push_back({Lr, r});
     }
+    // pair dedup is armed for big rounds; k_label decides on the device
+    PairTable pt{nullptr, nullptr, 0};
+    if (!original_in && dedup_on && m_bound >= dedup_min_edges) {
+      const unsigned long long cap = std::min<unsigned long long>(1ull << 25, next_pow2(m_bound / 2));
+      unsigned long long* tab = ws.get<unsigned long long>("pair_table", 2 * cap);
+      pt = PairTable{tab, nullptr, cap};
+      launches += 2;
+    }
     {
       const unsigned g = (unsigned)std::max<uint64_t>(
           1, std::min<uint64_t>((n_bound + kBlock - 1) / kBlock, (uint64_t)sm_count(dev) * blocks_per_sm(k_label)));
-      k_label<<<g, kBlock, 0, s>>>(parent, rootlabel, Lr, mnext, d_ctr, r);
+      k_label<<<g, kBlock, 0, s>>>(parent, rootlabel, Lr, mnext, d_ctr, r, pt.pairs, pt.mins, pt.cap);
     }
     hot_begin(kHotCompact, r, light);
     if (original_in) {
@@ -561,7 +598,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
                                                   kSlotCompact, (int)light, filt_for(n_bound));
     } else {
       launch_two_pass<PackedView, kModeRelabel, kPre>(ws, cb, PackedView{E[r & 1]}, E[r & 1], Lr, Eout, mnext, d_ctr,
-                                                      r, m_bound, n, kSlotCompact, (int)light, filt_for(n_bound));
+                                                      r, m_bound, n, kSlotCompact, (int)light, filt_for(n_bound), pt);
     }
     tmark();
     launches += 5;
@@ -594,6 +631,11 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   out.final_components = c.n[stop];
   out.count = (uint64_t)n - out.final_components;
   out.total_weight = c.total_weight;
+  if (env_int("MST_DEBUG_ROUNDS", 0)) {
+    for (int rr = 1; rr < stop && rr < kMaxR; ++rr)
+      fprintf(stderr, "round %2d: n=%u m=%llu active=%u dedup=%u%s\n", rr, c.n[rr], (unsigned long long)c.m[rr],
+              c.active[rr], c.dedup[rr], (phase_end && rr == phase_end) ? "  <- heavy survivors" : "");
+  }
   if (time_hot) {
     for (const HotLaunch& h : hot) {
       uint64_t bytes = 0;
@@ -886,7 +928,7 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, RunOu
       const unsigned gl = (unsigned)std::max<uint64_t>(
           1, std::min<uint64_t>((n_bound + kBlock - 1) / kBlock,
                                 (uint64_t)sm_count(ws.device) * blocks_per_sm(k_label)));
-      k_label<<<gl, kBlock, 0, ws.stream>>>(s.parent, s.rootlabel, s.L, s.minb[nxt], s.d_ctr, r);
+      k_label<<<gl, kBlock, 0, ws.stream>>>(s.parent, s.rootlabel, s.L, s.minb[nxt], s.d_ctr, r, nullptr, nullptr, 0);
       MST_CUDA_CHECK(cudaMemcpyAsync(&ws.h_snap[r], s.d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost,
                                      ws.stream));
       MST_CUDA_CHECK(cudaEventRecord(ws.ev[r], ws.stream));

@@ -58,6 +58,11 @@ struct DevCounters {
   unsigned int phase_end;   // first round past the light phase (Filter-Boruvka)
   unsigned int pivot;       // light edges: w < pivot
   unsigned long long total_weight;
+  unsigned int active[kMaxR];     // components with a live edge at round r (hook)
+  unsigned int dedup[kMaxR];      // round r's compaction keeps one edge per component pair
+  unsigned long long pair_mask[kMaxR];
+  unsigned int pair_count[kMaxR];  // distinct pairs inserted
+  unsigned int pair_abort[kMaxR];  // table overflowed: keep every edge this round
 };
 
 // ------------------------------ edge views ---------------------------------
@@ -481,10 +486,33 @@ __global__ void __launch_bounds__(kBlock) k_label(uint32_t* __restrict__ parent,
                                                   const uint32_t* __restrict__ rootlabel,
                                                   uint32_t* __restrict__ L,
                                                   unsigned long long* __restrict__ min_next,
-                                                  DevCounters* ctr, int r) {
+                                                  DevCounters* ctr, int r, unsigned long long* pair_keys,
+                                                  unsigned long long* pair_mins, unsigned long long pair_cap) {
   if ((uint32_t)r + 1 >= ctr->stop_round || (uint32_t)r >= ctr->phase_end) return;
   const uint32_t n_r = ctr->n[r];
   const uint32_t n_next = ctr->n[r + 1];
+  if (pair_keys) {
+    // Pair dedup (see "pair dedup" below): decide for this round's compaction
+    // and clear the table. Tried when few active components carry many edges
+    // each; the table takes m_r/8 distinct pairs at half load, more aborts
+    // the attempt (the round then compacts like a plain one).
+    const unsigned long long K = ctr->active[r];
+    const unsigned long long m_r = ctr->m[r];
+    const bool use = K <= 262144ull && m_r >= 8 * K && m_r >= 4096;
+    unsigned long long P = 1024;
+    while (P < m_r / 4 && P < pair_cap) P <<= 1;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      ctr->dedup[r] = use ? 1u : 0u;
+      ctr->pair_mask[r] = P - 1;
+      ctr->pair_count[r] = 0;
+      ctr->pair_abort[r] = 0;
+    }
+    if (use)
+      for (unsigned long long i = (unsigned long long)blockIdx.x * kBlock + threadIdx.x; i < P;
+           i += (unsigned long long)gridDim.x * kBlock) {
+        reinterpret_cast<ulonglong2*>(pair_keys)[i] = make_ulonglong2(~0ull, ~0ull);
+      }
+  }
   constexpr int kU = 4;
   const uint64_t stride = (uint64_t)gridDim.x * kBlock * kU;
   for (uint64_t base = (uint64_t)blockIdx.x * kBlock * kU; base < n_r; base += stride) {
@@ -767,18 +795,112 @@ __device__ __forceinline__ void fused_scan_if_last(uint32_t* counts, uint32_t T,
 //   k_emit  : ordered write + fused offers; a tile's aggregate is just
 //             counts[tile], so it is published the moment the tile is taken
 //             and the look-back overlaps the tile's own loads.
-enum { kModeRelabel = 0, kModeLight = 1, kModeHeavy = 2 };
+enum { kModeRelabel = 0, kModeLight = 1, kModeHeavy = 2, kModeDedup = 3 };
+
+// ------------------------------ pair dedup ---------------------------------
+// When few components carry many edges (a "dense core": R-MAT hubs, the
+// giant component of a light phase), Boruvka keeps every parallel edge
+// between the same two components alive for several rounds. Only the
+// lightest edge of a component pair can be in the MST (cycle property), so a
+// round may keep just that one: relabel + insert (pair -> lightest key) into
+// an open-addressing table, then keep an edge iff it is its pair's minimum.
+// Decided on the device per round from the active-component count:
+// components with a live edge at round r+1 <= active[r]/2, so pairs <=
+// (active[r]/2)^2/2; dedup when that is < m_r/4.
+struct PairTable {
+  unsigned long long* pairs;  // slot i = {pair, min key} at pairs[2i], pairs[2i+1]: one sector
+  unsigned long long* mins;   // unused (layout kept for the launch signature)
+  unsigned long long cap;  // power of two, allocated slots
+};
+constexpr unsigned long long kNoPair = ~0ull;
+constexpr int kPairProbes = 64;
+constexpr unsigned long long kDedupActive = 262144;
+
+__device__ __forceinline__ unsigned long long pair_hash(unsigned long long p) {
+  p ^= p >> 33;
+  p *= 0xff51afd7ed558ccdull;
+  p ^= p >> 33;
+  return p;
+}
+
+// Relabel in place and record each pair's lightest (w<<32 | index) key
+// (the first pass of a dedup round, run by k_count<kModeRelabel>).
+__device__ __forceinline__ void dedup_insert(uint4* __restrict__ E, const uint32_t* __restrict__ L, PairTable t,
+                                             DevCounters* ctr, int r) {
+  const uint64_t m_r = ctr->m[r];
+  const unsigned long long mask = ctr->pair_mask[r];
+  const unsigned int limit = (unsigned int)((mask + 1) / 2);  // half load
+  volatile unsigned int* abort_flag = &ctr->pair_abort[r];
+  constexpr int kU = 4;
+  for (uint64_t base = (uint64_t)blockIdx.x * kBlock * kU; base < m_r; base += (uint64_t)gridDim.x * kBlock * kU) {
+    uint4 e[kU];
+#pragma unroll
+    for (int k = 0; k < kU; ++k) {
+      const uint64_t i = base + k * kBlock + threadIdx.x;
+      e[k] = i < m_r ? __ldcs(E + i) : make_uint4(0, 0, 0, 0);
+    }
+    const bool aborted = *abort_flag != 0;
+    uint32_t fresh = 0;
+#pragma unroll
+    for (int k = 0; k < kU; ++k) {
+      const uint64_t i = base + k * kBlock + threadIdx.x;
+      if (i >= m_r) continue;
+      const uint32_t x = __ldg(L + e[k].x), y = __ldg(L + e[k].y);
+      *reinterpret_cast<uint2*>(E + i) = make_uint2(x, y);
+      if (x == y || aborted) continue;
+      const unsigned long long pair = ((unsigned long long)min(x, y) << 32) | max(x, y);
+      const unsigned long long key = ((unsigned long long)e[k].z << 32) | (uint32_t)i;
+      unsigned long long h = pair_hash(pair) & mask;
+      for (int probe = 0; probe < kPairProbes; ++probe) {
+        const unsigned long long cur = __ldcg(t.pairs + 2 * h);
+        const unsigned long long got = cur == pair ? pair : atomicCAS(t.pairs + 2 * h, kNoPair, pair);
+        if (got == kNoPair || got == pair) {
+          fresh += got == kNoPair;
+          if (key < __ldcg(t.pairs + 2 * h + 1)) atomicMin(t.pairs + 2 * h + 1, key);
+          break;
+        }
+        h = (h + 1) & mask;  // a failed insert keeps the edge (see pair_keep)
+      }
+    }
+    fresh = warp_sum<uint32_t>(fresh);
+    if (lane_id() == 0 && fresh && atomicAdd(&ctr->pair_count[r], fresh) + fresh > limit) *abort_flag = 1;
+  }
+}
+
+__device__ __forceinline__ bool pair_keep(const PairTable& t, unsigned long long mask, uint32_t x, uint32_t y,
+                                          unsigned long long key) {
+  const unsigned long long pair = ((unsigned long long)min(x, y) << 32) | max(x, y);
+  unsigned long long h = pair_hash(pair) & mask;
+  for (int probe = 0; probe < kPairProbes; ++probe) {
+    const ulonglong2 slot = __ldcg(reinterpret_cast<const ulonglong2*>(t.pairs) + h);
+    const unsigned long long cur = slot.x;
+    if (cur == pair) return key <= slot.y;
+    if (cur == kNoPair) return true;
+    h = (h + 1) & mask;
+  }
+  return true;
+}
 
 template <class View, int kMode>
 __global__ void __launch_bounds__(kBlock) k_count(View in, uint4* __restrict__ relabeled,
                                                   const uint32_t* __restrict__ L,
                                                   uint32_t* __restrict__ masks, uint32_t* __restrict__ counts,
                                                   uint32_t n_orig, DevCounters* ctr, int r, int fused, int slot,
-                                                  int light_phase) {
+                                                  int light_phase, PairTable pt) {
   __shared__ uint32_t s_cnt[kWarps];
+  __shared__ uint32_t s_slot[kCItems * kWarps];
   const uint32_t stop = ctr->stop_round;
   if ((uint32_t)r >= ctr->phase_end || (uint32_t)r + 1 >= stop) return;
-  const uint64_t m_r = kMode == kModeRelabel && !View::kOriginal ? ctr->m[r] : ctr->m[0];
+  // A dedup round: this pass relabels + inserts pairs, the kModeDedup pass
+  // counts (and stages survivors unless the attempt aborted).
+  if (kMode == kModeRelabel && !View::kOriginal && pt.pairs && ctr->dedup[r]) {
+    dedup_insert(reinterpret_cast<uint4*>(relabeled), L, pt, ctr, r);
+    return;
+  }
+  if (kMode == kModeDedup && !ctr->dedup[r]) return;
+  const uint64_t m_r = (kMode == kModeRelabel || kMode == kModeDedup) && !View::kOriginal ? ctr->m[r] : ctr->m[0];
+  const unsigned long long pmask = kMode == kModeDedup ? ctr->pair_mask[r] : 0ull;
+  const bool pabort = kMode == kModeDedup && ctr->pair_abort[r] != 0;
   const uint32_t pivot = ctr->pivot;
   const uint32_t ntiles = (uint32_t)((m_r + kCTile - 1) / kCTile);
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
@@ -791,10 +913,12 @@ __global__ void __launch_bounds__(kBlock) k_count(View in, uint4* __restrict__ r
       if (i < m_r) e[k] = in.stream(i);
     }
     uint32_t err = 0, cnt = 0;
+    bool keep[kCItems];
+    unsigned bal[kCItems];
 #pragma unroll
     for (int k = 0; k < kCItems; ++k) {
       const uint64_t i = (uint64_t)tile * kCTile + k * kBlock + threadIdx.x;
-      bool keep = false;
+      keep[k] = false;
       if (i < m_r) {
         bool ok = true;
         if (View::kOriginal) {
@@ -804,16 +928,21 @@ __global__ void __launch_bounds__(kBlock) k_count(View in, uint4* __restrict__ r
           if (!ok) err |= (e[k].a < n_orig && e[k].b < n_orig) ? kErrWeight : kErrRange;
         }
         if (kMode == kModeLight) {
-          keep = ok && e[k].w < pivot && e[k].a != e[k].b;
+          keep[k] = ok && e[k].w < pivot && e[k].a != e[k].b;
+        } else if (kMode == kModeDedup) {
+          keep[k] = e[k].a != e[k].b &&
+                    (pabort || pair_keep(pt, pmask, e[k].a, e[k].b, ((unsigned long long)e[k].w << 32) | (uint32_t)i));
         } else if (kMode == kModeHeavy) {
           if (ok && e[k].w >= pivot) {
-            const uint32_t x = L ? __ldg(L + e[k].a) : e[k].a;
-            const uint32_t y = L ? __ldg(L + e[k].b) : e[k].b;
-            keep = x != y;
+            if (L) {
+              e[k].a = __ldg(L + e[k].a);
+              e[k].b = __ldg(L + e[k].b);
+            }
+            keep[k] = e[k].a != e[k].b;
           }
         } else if (ok) {
           const uint32_t x = __ldg(L + e[k].a), y = __ldg(L + e[k].b);
-          keep = x != y;
+          keep[k] = x != y;
           if (View::kOriginal)
             __stcs(relabeled + i, make_uint4(x, y, e[k].w, e[k].eid));
           else
@@ -822,13 +951,42 @@ __global__ void __launch_bounds__(kBlock) k_count(View in, uint4* __restrict__ r
           __stcs(relabeled + i, make_uint4(0, 0, 0, 0));  // rejected input edge: a self-loop placeholder
         }
       }
-      const unsigned bal = __ballot_sync(0xffffffffu, keep);
-      if (kMode != kModeRelabel && lane == 0) masks[(uint64_t)tile * (kCItems * kWarps) + k * kWarps + warp] = bal;
-      cnt += __popc(bal);
+      bal[k] = __ballot_sync(0xffffffffu, keep[k]);
+      if (lane == 0) s_slot[k * kWarps + warp] = __popc(bal[k]);
+      cnt += __popc(bal[k]);
     }
     if (err) atomicOr(&ctr->err, err);
     if (lane == 0) s_cnt[warp] = cnt;
     __syncthreads();
+    if (kMode != kModeRelabel && !pabort) {
+      // sparse survivors: stage them compacted inside the tile's own slice,
+      // so the emit pass touches survivors only
+      if (warp == 0) {
+        constexpr int kSlots = kCItems * kWarps, kPer = (kSlots + 31) / 32;
+        uint32_t v[kPer], sum = 0;
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+          const int idx = lane * kPer + j;
+          v[j] = idx < kSlots ? s_slot[idx] : 0u;
+          sum += v[j];
+        }
+        const uint32_t incl = warp_incl_scan(sum);
+        uint32_t run = incl - sum;
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+          const int idx = lane * kPer + j;
+          if (idx < kSlots) s_slot[idx] = run;
+          run += v[j];
+        }
+      }
+      __syncthreads();
+      const uint32_t lt = lanemask_lt();
+#pragma unroll
+      for (int k = 0; k < kCItems; ++k)
+        if (keep[k])
+          __stcs(relabeled + (uint64_t)tile * kCTile + s_slot[k * kWarps + warp] + __popc(bal[k] & lt),
+                 make_uint4(e[k].a, e[k].b, e[k].w, e[k].eid));
+    }
     if (threadIdx.x == 0) {
       uint32_t t = 0;
 #pragma unroll
@@ -849,11 +1007,13 @@ __global__ void __launch_bounds__(kBlock) k_emit(View in, const uint4* __restric
                                                  const uint32_t* __restrict__ masks,
                                                  const uint32_t* __restrict__ offsets, uint4* __restrict__ out,
                                                  unsigned long long* __restrict__ min_next, DevCounters* ctr,
-                                                 int r, int filt) {
+                                                 int r, int filt, int dedup_armed) {
   __shared__ uint32_t s_scan[kCItems * kWarps];
   const uint32_t stop = ctr->stop_round;
   if ((uint32_t)r >= ctr->phase_end || (uint32_t)r + 1 >= stop) return;
-  const uint64_t m_r = kMode == kModeRelabel && !View::kOriginal ? ctr->m[r] : ctr->m[0];
+  if (kMode == kModeRelabel && !View::kOriginal && dedup_armed && ctr->dedup[r] && !ctr->pair_abort[r]) return;
+  if (kMode == kModeDedup && !ctr->dedup[r]) return;
+  const uint64_t m_r = (kMode == kModeRelabel || kMode == kModeDedup) && !View::kOriginal ? ctr->m[r] : ctr->m[0];
   const uint32_t ntiles = (uint32_t)((m_r + kCTile - 1) / kCTile);
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -920,6 +1080,35 @@ __global__ void __launch_bounds__(kBlock) k_emit(View in, const uint4* __restric
       offer<kWarpPre>(min_next, e[k].y, key, keep[k], filt);
     }
     __syncthreads();
+  }
+}
+
+// Emit of the staged modes: tile t's survivors sit at stage[t*kCTile ..
+// t*kCTile + count); copy them to their final slots and make the offers.
+template <int kMode, bool kWarpPre>
+__global__ void __launch_bounds__(kBlock) k_emit_staged(const uint4* __restrict__ stage,
+                                                        const uint32_t* __restrict__ offsets, uint4* __restrict__ out,
+                                                        unsigned long long* __restrict__ min_next, DevCounters* ctr,
+                                                        int r, int filt) {
+  const uint32_t stop = ctr->stop_round;
+  if ((uint32_t)r >= ctr->phase_end || (uint32_t)r + 1 >= stop) return;
+  if (kMode == kModeDedup && (!ctr->dedup[r] || ctr->pair_abort[r])) return;
+  const uint64_t m_src = kMode == kModeDedup ? ctr->m[r] : ctr->m[0];
+  const uint32_t total = (uint32_t)ctr->m[r + 1];
+  const uint32_t ntiles = (uint32_t)((m_src + kCTile - 1) / kCTile);
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint32_t off = __ldg(offsets + tile);
+    const uint32_t end = tile + 1 < ntiles ? __ldg(offsets + tile + 1) : total;
+    const uint32_t cnt = end - off;
+    for (uint32_t base = 0; base < cnt; base += kBlock) {
+      const uint32_t j = base + threadIdx.x;
+      const bool v = j < cnt;
+      const uint4 e = v ? __ldcs(stage + (uint64_t)tile * kCTile + j) : make_uint4(0, 0, 0, 0);
+      if (v) __stcs(out + off + j, e);
+      const unsigned long long key = ((unsigned long long)e.z << 32) | (off + j);
+      offer<kWarpPre>(min_next, e.x, key, v, filt);
+      offer<kWarpPre>(min_next, e.y, key, v, filt);
+    }
   }
 }
 
@@ -1005,6 +1194,7 @@ __global__ void __launch_bounds__(kBlock) k_hook_decide(View E, const unsigned l
   const uint32_t ntiles = (uint32_t)(((uint64_t)n_r + kTile - 1) / kTile);
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   unsigned long long wsum = 0;
+  uint32_t active = 0;
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     unsigned long long key[kItems], okey[kItems];
     EdgeRec e[kItems];
@@ -1037,6 +1227,7 @@ __global__ void __launch_bounds__(kBlock) k_hook_decide(View E, const unsigned l
           const uint32_t o = (e[k].a == (uint32_t)c) ? e[k].b : e[k].a;
           isroot = okey[k] == key[k] && (uint32_t)c < o;
           parent[c] = isroot ? (uint32_t)c : o;
+          ++active;
           if (!isroot) {
             rootlabel[c] = e[k].eid;  // stash the MST edge id until its slot is known
             wsum += (uint32_t)(key[k] >> 32);
@@ -1058,12 +1249,21 @@ __global__ void __launch_bounds__(kBlock) k_hook_decide(View E, const unsigned l
     __syncthreads();
   }
   wsum = warp_sum<unsigned long long>(wsum);
-  if (lane == 0) s_wsum[warp] = wsum;
+  active = warp_sum<uint32_t>(active);
+  if (lane == 0) {
+    s_wsum[warp] = wsum;
+    s_cnt[warp] = active;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned long long t = 0;
-    for (int i = 0; i < kWarps; ++i) t += s_wsum[i];
+    uint32_t a = 0;
+    for (int i = 0; i < kWarps; ++i) {
+      t += s_wsum[i];
+      a += s_cnt[i];
+    }
     if (t) atomicAdd(&ctr->total_weight, t);
+    if (a) atomicAdd(&ctr->active[r], a);
   }
   if (fused) {
     __shared__ uint32_t s_warp[kWarps + 1], s_flag;

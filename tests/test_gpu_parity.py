@@ -41,7 +41,10 @@ class _env:
 
 # plain round loop, and Filter-Boruvka with a small / default / large light set
 MODES = [dict(MST_FILTER=0), dict(MST_FILTER=1, MST_FILTER_BETA=0.3),
-         dict(MST_FILTER=1, MST_FILTER_BETA=2), dict(MST_FILTER=1, MST_FILTER_BETA=50)]
+         dict(MST_FILTER=1, MST_FILTER_BETA=2), dict(MST_FILTER=1, MST_FILTER_BETA=50),
+         # every round through the separate kernels with the pair-dedup variant armed
+         dict(MST_FILTER=0, MST_TAIL=0, MST_DEDUP_MIN_EDGES=0),
+         dict(MST_FILTER=1, MST_TAIL=0, MST_DEDUP_MIN_EDGES=0)]
 
 
 def _check(P, n, src, dst, w, ids, total, shards=(2, 3), modes=MODES):
@@ -223,7 +226,7 @@ def test_baseline_configs_full_size(mst, oracle_mod, cfg):
     g = C.generate_host(C.CONFIGS[cfg])
     k = O.kruskal(g.n, g.src, g.dst, g.w)
     assert k.ids.size == g.n - 1
-    for mode in (MODES[0], MODES[2]):
+    for mode in (MODES[0], MODES[2], MODES[5]):
         with _env(**mode):
             info = P.GpuRunInfo()
             r = P.boruvka_gpu(g, info=info)
