@@ -260,6 +260,28 @@ void init_counters(Workspace& ws, DevCounters* d_ctr, uint32_t n, uint64_t m) {
   MST_CUDA_CHECK(cudaMemcpyAsync(d_ctr, &h, sizeof(DevCounters), cudaMemcpyHostToDevice, ws.stream));
 }
 
+// Sorted id list from the per-edge flags the hook kernels set.
+uint32_t sort_from_flags(Workspace& ws, const uint8_t* flags, uint64_t m, uint32_t* d_sorted, DevCounters* d_ctr) {
+  const uint64_t tiles = (m + kFlagTile - 1) / kFlagTile;
+  uint32_t* counts = ws.get<uint32_t>("sort_counts", std::max<uint64_t>(tiles, 1));
+  const int fused = tiles <= kFusedScanMaxTiles ? 1 : 0;
+  MST_CUDA_CHECK(cudaMemsetAsync(&d_ctr->done[0][kSlotSort], 0, sizeof(unsigned int), ws.stream));
+  const unsigned g = (unsigned)std::max<uint64_t>(
+      1, std::min<uint64_t>(tiles, (uint64_t)sm_count(ws.device) * blocks_per_sm(k_flags_count)));
+  k_flags_count<<<g, kBlock, 0, ws.stream>>>(flags, m, counts, d_ctr, fused);
+  uint32_t launches = 2;
+  if (!fused) {
+    unsigned long long* st = ws.status_array(tiles);
+    k_scan_counts<kScanPlain><<<(unsigned)std::max<uint64_t>(
+                                    1, std::min<uint64_t>((tiles + kScanTile - 1) / kScanTile, (uint64_t)sm_count(ws.device))),
+                                kScanBlock, 0, ws.stream>>>(counts, tiles, d_ctr, 0, st, ws.next_epoch(), 0, 0);
+    ++launches;
+  }
+  k_flags_emit<<<g, kBlock, 0, ws.stream>>>(flags, m, counts, d_sorted);
+  MST_CUDA_CHECK(cudaGetLastError());
+  return launches;
+}
+
 // Sorted id list (ascending) of `count` distinct ids < m_total, via a bitmap.
 uint32_t sort_ids(Workspace& ws, const uint32_t* d_ids, uint64_t count, uint64_t m_total,
                   uint32_t* d_sorted, DevCounters* d_ctr) {
@@ -415,6 +437,8 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
 
   init_counters(ws, d_ctr, n, m);
   MST_CUDA_CHECK(cudaMemsetAsync(minb[0], 0xFF, (size_t)n * 8, s));
+  uint8_t* flags = ws.get<uint8_t>("mst_flags", m + 16);
+  MST_CUDA_CHECK(cudaMemsetAsync(flags, 0, m + 16, s));
   uint32_t launches = 0;
   int tix = 0;
   std::vector<HotLaunch> hot;
@@ -458,7 +482,9 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   int r = 1, loop_start = 1;
   int phase_end = 0;
   DevCounters snap_b{};  // counters at the end of the light phase
-  const bool tail_on = env_int("MST_TAIL", 1) != 0;
+  const int tail_mode = env_int("MST_TAIL", 1);  // 0 off, 1 compacting tail, 2 sparse-label tail
+  const bool tail_on = tail_mode != 0;
+  const bool tail_v2 = tail_mode == 2;
   const bool dedup_on = env_int("MST_DEDUP", 1) != 0;
   const uint64_t dedup_min_edges = (uint64_t)env_double("MST_DEDUP_MIN_EDGES", 2.0e6);
   const uint64_t tail_edges = (uint64_t)env_double("MST_TAIL_EDGES", 3.0e6);
@@ -514,7 +540,9 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
             M, n_bound);
         ++launches;
       }
-      auto kt = getenv("MST_TAIL_PREREDUCE") && getenv("MST_TAIL_PREREDUCE")[0] == '1' ? k_tail<true> : k_tail<false>;
+      auto kt = tail_v2 ? k_tail2
+                        : (getenv("MST_TAIL_PREREDUCE") && getenv("MST_TAIL_PREREDUCE")[0] == '1' ? k_tail<true>
+                                                                                                  : k_tail<false>);
       const int bps = std::max(1, std::min(blocks_per_sm(kt), env_int("MST_TAIL_BPS", 4)));
       const unsigned G = (unsigned)(sm_count(dev) * bps);
       uint32_t* bcount = ws.get<uint32_t>("bcount", G);
@@ -523,7 +551,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
         trace = ws.get<unsigned long long>("tail_trace", 512);
         MST_CUDA_CHECK(cudaMemsetAsync(trace, 0, 512 * 8, s));
       }
-      TailArgs ta{{E[0], E[1]}, {minb[0], minb[1]}, parent, rootlabel, L, mst, bcount, M, trace, d_ctr, n, r,
+      TailArgs ta{{E[0], E[1]}, {minb[0], minb[1]}, parent, rootlabel, L, mst, bcount, M, flags, trace, d_ctr, n, r,
                   (int)light};
       void* args[] = {&ta};
       hot_begin(kHotTail, r, light);
@@ -570,7 +598,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
                                     kScanBlock, 0, s>>>(hcounts, ht, d_ctr, r, st, ws.next_epoch(), (int)light, 0);
       k_hook_emit<<<(unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ht, (uint64_t)sm_count(dev) *
                                                                               blocks_per_sm(k_hook_emit))),
-                    kBlock, 0, s>>>(parent, rootlabel, hmasks, hcounts, mst, n, d_ctr, r);
+                    kBlock, 0, s>>>(parent, rootlabel, hmasks, hcounts, mst, n, d_ctr, r, flags);
       launches += 2;
     }
     uint32_t* Lr = L;
@@ -791,7 +819,9 @@ RunOut run_single(const SingleArgs& a, mst_stats_t* stats) {
   uint32_t* d_mst = ws.get<uint32_t>("mst", a.n);
   uint32_t* d_sorted = a.device_out ? a.out_ids : ws.get<uint32_t>("sorted", a.n);
   auto* d_ctr = ws.get<DevCounters>("ctr", 1);
-  o.launches += sort_ids(ws, d_mst, o.count, std::max<uint64_t>(a.m, 1), d_sorted, d_ctr);
+  (void)d_mst;
+  o.launches += sort_from_flags(ws, ws.get<uint8_t>("mst_flags", a.m + 16), std::max<uint64_t>(a.m, 1), d_sorted,
+                                d_ctr);
   MST_CUDA_CHECK(cudaEventRecord(e2, s));
   if (!a.device_out && o.count)
     MST_CUDA_CHECK(cudaMemcpyAsync(a.out_ids, d_sorted, o.count * 4, cudaMemcpyDeviceToHost, s));

@@ -62,6 +62,9 @@ struct DevCounters {
   unsigned int dedup[kMaxR];      // round r's compaction keeps one edge per component pair
   unsigned long long pair_mask[kMaxR];
   unsigned int pair_count[kMaxR];  // distinct pairs inserted
+  unsigned int hooks[kMaxR];       // tail v2: hooks per round
+  unsigned int live[kMaxR];        // tail v2: live edges entering round r
+  unsigned int mst_fill;           // tail v2: next free MST slot
   unsigned int pair_abort[kMaxR];  // table overflowed: keep every edge this round
 };
 
@@ -1275,7 +1278,8 @@ __global__ void __launch_bounds__(kBlock) k_hook_emit(const uint32_t* __restrict
                                                       uint32_t* __restrict__ rootlabel,
                                                       const uint32_t* __restrict__ masks,
                                                       const uint32_t* __restrict__ offsets, uint32_t* __restrict__ mst,
-                                                      uint32_t n_orig, DevCounters* ctr, int r) {
+                                                      uint32_t n_orig, DevCounters* ctr, int r,
+                                                      uint8_t* __restrict__ flags) {
   __shared__ uint32_t s_scan[kItems * kWarps];
   if ((uint32_t)r >= ctr->phase_end) return;
   // runs even when this round stops (the last hook's MST slots are needed)
@@ -1303,7 +1307,11 @@ __global__ void __launch_bounds__(kBlock) k_hook_emit(const uint32_t* __restrict
         if ((bal >> lane) & 1u)
           rootlabel[c] = before;
         else
-          mst[mst_base + ((uint32_t)c - before)] = rootlabel[c];
+        {
+          const uint32_t eid = rootlabel[c];
+          mst[mst_base + ((uint32_t)c - before)] = eid;
+          if (flags) flags[eid] = 1;  // sorted output is read off these flags
+        }
       }
     }
     __syncthreads();
@@ -1328,6 +1336,7 @@ struct TailArgs {
   uint32_t* mst;
   uint32_t* bcount;  // [gridDim.x]
   uint32_t* M;       // light phase: entry-label -> current-label map (n[r0] entries)
+  uint8_t* flags;    // MST edge flags (sorted output)
   unsigned long long* trace;  // optional: globaltimer stamps at phase boundaries (block 0)
   DevCounters* ctr;
   uint32_t n_orig;
@@ -1404,10 +1413,11 @@ __global__ void __launch_bounds__(kBlock) k_tail(TailArgs a) {
     const uint32_t n_r = vc->n[r];
     const uint64_t m_r = vc->m[r];
     const uint32_t mst_base = a.n_orig - n_r;
-    const unsigned long long* mcur = a.minb[(r - 1) & 1];
-    unsigned long long* mnext = a.minb[r & 1];
-    uint4* Ecur = a.E[r & 1];
-    uint4* Enext = a.E[(r + 1) & 1];
+    // ternaries, not a dynamic index: keeps TailArgs out of local memory
+    const unsigned long long* mcur = (r & 1) ? a.minb[0] : a.minb[1];
+    unsigned long long* mnext = (r & 1) ? a.minb[1] : a.minb[0];
+    uint4* Ecur = (r & 1) ? a.E[1] : a.E[0];
+    uint4* Enext = (r & 1) ? a.E[0] : a.E[1];
     // ---- H1: hook decisions over this block's component chunk
     const uint32_t cs = (n_r + G - 1) / G;
     const uint32_t clo = min(b * cs, n_r), chi = min(clo + cs, n_r);
@@ -1495,7 +1505,11 @@ __global__ void __launch_bounds__(kBlock) k_tail(TailArgs a) {
             if (f[k])
               a.rootlabel[c] = before;
             else
-              a.mst[mst_base + (c - before)] = a.rootlabel[c];
+            {
+              const uint32_t eid = a.rootlabel[c];
+              a.mst[mst_base + (c - before)] = eid;
+              if (a.flags) a.flags[eid] = 1;
+            }
           }
         }
         running += tot;
@@ -1640,6 +1654,261 @@ __global__ void __launch_bounds__(kBlock) k_tail(TailArgs a) {
   }
 }
 
+// Tail v2: sparse labels, no compaction, two grid-wide steps per round.
+// Components keep their tail-entry label (a root id in [0, n0)); a round is
+//   H: every live root reads its key, the winning edge (whose endpoints were
+//      rewritten to current roots by the previous C step) and the partner's
+//      key, hooks (parent[c] = partner) unless it is the lower end of a
+//      mutual pair, and appends its MST edge at an atomically taken slot
+//      (the output is sorted by the bitmap pass anyway); clears the next
+//      min table;
+//   C: every live edge rewrites its endpoints to their current roots (path
+//      halving finds), drops out once both agree, and offers
+//      (w<<32 | entry index) to both roots (block-local smem table when the
+//      id space is small).
+// Entry: dense labels [0, n0) and the round-r0 min table, exactly as the
+// round kernels leave them. On exit in the light phase the roots are
+// densified (one prefix) so the filter pass and phase D see dense labels.
+__global__ void __launch_bounds__(kBlock) k_tail2(TailArgs a) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ unsigned long long s_min[kTailSmemMin];
+  __shared__ uint32_t s_red[kWarps];
+  __shared__ unsigned long long s_wred[kWarps];
+  __shared__ uint32_t s_misc[2];
+  const uint32_t G = gridDim.x, b = blockIdx.x;
+  const uint64_t T = (uint64_t)G * kBlock;
+  const uint64_t tid = (uint64_t)b * kBlock + threadIdx.x;
+  volatile DevCounters* vc = a.ctr;
+  const int r0 = a.r0;
+  int slot = 0;
+  tail_stamp(a, slot);
+  if ((uint32_t)r0 >= vc->stop_round || (uint32_t)r0 >= vc->phase_end) return;  // uniform
+  const uint32_t n0 = vc->n[r0];
+  const uint64_t m0 = vc->m[r0];
+  uint4* E = (r0 & 1) ? a.E[1] : a.E[0];
+  for (uint64_t c = tid; c < n0; c += T) a.parent[c] = (uint32_t)c;
+  if (tid == 0) a.ctr->mst_fill = a.n_orig - n0;
+  grid.sync();
+  int r = r0;
+  bool densify = false;
+  for (; r < kMaxR - 2; ++r) {
+    const unsigned long long* mcur = (r & 1) ? a.minb[0] : a.minb[1];
+    unsigned long long* mnext = (r & 1) ? a.minb[1] : a.minb[0];
+    // ---- H: hooks
+    uint32_t hooks = 0;
+    unsigned long long wsum = 0;
+    for (uint64_t base = (uint64_t)b * kBlock * kItems; base < n0; base += T * kItems) {
+      uint32_t c[kItems];
+      unsigned long long key[kItems], okey[kItems];
+      uint4 e[kItems];
+      bool live[kItems];
+#pragma unroll
+      for (int k = 0; k < kItems; ++k) {
+        c[k] = (uint32_t)(base + k * kBlock + threadIdx.x);
+        live[k] = c[k] < n0 && __ldcg(a.parent + c[k]) == c[k];
+        if (c[k] < n0) mnext[c[k]] = kNoKey;
+        key[k] = live[k] ? __ldcg(mcur + c[k]) : kNoKey;
+      }
+#pragma unroll
+      for (int k = 0; k < kItems; ++k) e[k] = key[k] != kNoKey ? __ldcg(E + (uint32_t)key[k]) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int k = 0; k < kItems; ++k) {
+        const uint32_t o = e[k].x == c[k] ? e[k].y : e[k].x;
+        okey[k] = key[k] != kNoKey ? __ldcg(mcur + o) : kNoKey;
+      }
+#pragma unroll
+      for (int k = 0; k < kItems; ++k) {
+        bool hook = false;
+        uint32_t o = 0;
+        if (key[k] != kNoKey) {
+          o = e[k].x == c[k] ? e[k].y : e[k].x;
+          hook = !(okey[k] == key[k] && c[k] < o);
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, hook);
+        if (bal) {
+          const uint32_t lane = lane_id();
+          uint32_t basepos = 0;
+          if (lane == __ffs(bal) - 1) basepos = atomicAdd(&a.ctr->mst_fill, (uint32_t)__popc(bal));
+          basepos = __shfl_sync(0xffffffffu, basepos, __ffs(bal) - 1);
+          if (hook) {
+            a.parent[c[k]] = o;
+            a.mst[basepos + __popc(bal & lanemask_lt())] = e[k].w;
+            if (a.flags) a.flags[e[k].w] = 1;
+            wsum += (uint32_t)(key[k] >> 32);
+          }
+          hooks += __popc(bal) * (lane == 0);
+        }
+      }
+    }
+    hooks = warp_sum<uint32_t>(hooks);
+    wsum = warp_sum<unsigned long long>(wsum);
+    if (lane_id() == 0) {
+      s_red[threadIdx.x >> 5] = hooks;
+      s_wred[threadIdx.x >> 5] = wsum;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t h = 0;
+      unsigned long long ws = 0;
+      for (int i = 0; i < kWarps; ++i) {
+        h += s_red[i];
+        ws += s_wred[i];
+      }
+      if (h) atomicAdd(&a.ctr->hooks[r], h);
+      if (ws) atomicAdd(&a.ctr->total_weight, ws);
+    }
+    grid.sync();
+    tail_stamp(a, slot);
+    const uint32_t n_r = vc->n[r];
+    const uint32_t n_next = n_r - vc->hooks[r];
+    if (tid == 0) {
+      a.ctr->n[r + 1] = n_next;
+      if (n_next <= 1) {
+        a.ctr->stop_round = (uint32_t)r + 1;
+      } else if (n_next == n_r) {
+        if (a.light)
+          a.ctr->phase_end = (uint32_t)r;
+        else
+          a.ctr->stop_round = (uint32_t)r + 1;
+      }
+    }
+    if (n_next <= 1 || (n_next == n_r && !a.light)) break;
+    if (n_next == n_r) {  // light phase with nothing left to hook: densify below
+      densify = true;
+      break;
+    }
+    // ---- C: relabel live edges to current roots, offer for round r+1
+    const bool local = n0 <= kTailSmemMin;
+    if (local) {
+      for (uint32_t c = threadIdx.x; c < n0; c += kBlock) s_min[c] = kNoKey;
+      __syncthreads();
+    }
+    uint32_t live = 0;
+    for (uint64_t base = (uint64_t)b * kBlock * kItems; base < m0; base += T * kItems) {
+      uint4 e[kItems];
+      bool v[kItems];
+#pragma unroll
+      for (int k = 0; k < kItems; ++k) {
+        const uint64_t i = base + k * kBlock + threadIdx.x;
+        e[k] = i < m0 ? __ldcg(E + i) : make_uint4(0, 0, 0, 0);
+        v[k] = i < m0 && e[k].x != e[k].y;
+      }
+      uint32_t xs[kItems], ys[kItems], rx[kItems], ry[kItems];
+#pragma unroll
+      for (int k = 0; k < kItems; ++k) {
+        xs[k] = e[k].x;
+        ys[k] = e[k].y;
+      }
+      find_roots<kItems>(a.parent, xs, v, rx);
+      find_roots<kItems>(a.parent, ys, v, ry);
+#pragma unroll
+      for (int k = 0; k < kItems; ++k) {
+        if (!v[k]) continue;
+        const uint64_t i = base + k * kBlock + threadIdx.x;
+        if (rx[k] != e[k].x || ry[k] != e[k].y) *reinterpret_cast<uint2*>(E + i) = make_uint2(rx[k], ry[k]);
+        if (rx[k] == ry[k]) continue;
+        ++live;
+        const unsigned long long key = ((unsigned long long)e[k].z << 32) | (uint32_t)i;
+        if (local) {
+          atomicMin(s_min + rx[k], key);
+          atomicMin(s_min + ry[k], key);
+        } else {
+          if (key < __ldcg(mnext + rx[k])) atomicMin(mnext + rx[k], key);
+          if (key < __ldcg(mnext + ry[k])) atomicMin(mnext + ry[k], key);
+        }
+      }
+    }
+    if (local) {
+      __syncthreads();
+      for (uint32_t c = threadIdx.x; c < n0; c += kBlock) {
+        const unsigned long long v = s_min[c];
+        if (v != kNoKey && v < __ldcg(mnext + c)) atomicMin(mnext + c, v);
+      }
+    }
+    live = warp_sum<uint32_t>(live);
+    if (lane_id() == 0) s_red[threadIdx.x >> 5] = live;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t t = 0;
+      for (int i = 0; i < kWarps; ++i) t += s_red[i];
+      if (t) atomicAdd(&a.ctr->live[r + 1], t);
+    }
+    grid.sync();
+    tail_stamp(a, slot);
+    const uint32_t lv = vc->live[r + 1];
+    if (tid == 0) {
+      a.ctr->m[r + 1] = lv;
+      if (lv == 0) {
+        if (a.light)
+          a.ctr->phase_end = (uint32_t)r + 1;
+        else if (a.ctr->stop_round == kNoStop)
+          a.ctr->stop_round = (uint32_t)r + 1;
+      }
+    }
+    if (lv == 0) {
+      densify = a.light != 0;
+      break;
+    }
+  }
+  if (!densify) return;
+  // ---- light-phase exit: dense labels for the roots, entry-label map M,
+  // clear the min table of the round the filter pass feeds
+  const int R1 = (int)vc->phase_end;
+  const uint32_t cs = (n0 + G - 1) / G;
+  const uint32_t clo = min(b * cs, n0), chi = min(clo + cs, n0);
+  {
+    uint32_t roots = 0;
+    for (uint32_t c = clo + threadIdx.x; c < chi; c += kBlock) roots += __ldcg(a.parent + c) == c;
+    roots = warp_sum<uint32_t>(roots);
+    if (lane_id() == 0) s_red[threadIdx.x >> 5] = roots;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t t = 0;
+      for (int i = 0; i < kWarps; ++i) t += s_red[i];
+      a.bcount[b] = t;
+    }
+  }
+  grid.sync();
+  {
+    uint32_t running = block_prefix(a.bcount, b, s_misc);
+    for (uint32_t base = clo; base < chi; base += kBlock) {
+      const uint32_t c = base + threadIdx.x;
+      const bool f = c < chi && __ldcg(a.parent + c) == c;
+      const unsigned bal = __ballot_sync(0xffffffffu, f);
+      if (lane_id() == 0) s_red[threadIdx.x >> 5] = __popc(bal);
+      __syncthreads();
+      uint32_t before = running, tot = 0;
+      for (int i = 0; i < kWarps; ++i) {
+        before += i < (int)(threadIdx.x >> 5) ? s_red[i] : 0u;
+        tot += s_red[i];
+      }
+      if (f) a.rootlabel[c] = before + __popc(bal & lanemask_lt());
+      running += tot;
+      __syncthreads();
+    }
+  }
+  grid.sync();
+  const uint32_t n_final = vc->n[R1];
+  unsigned long long* mR1 = (R1 & 1) ? a.minb[0] : a.minb[1];
+  for (uint64_t base = (uint64_t)b * kBlock * kItems; base < n0; base += T * kItems) {
+    uint32_t c[kItems], root[kItems];
+    bool v[kItems];
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      c[k] = (uint32_t)(base + k * kBlock + threadIdx.x);
+      v[k] = c[k] < n0;
+    }
+    find_roots<kItems>(a.parent, c, v, root);
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      if (!v[k]) continue;
+      a.M[c[k]] = __ldcg(a.rootlabel + root[k]);
+      if (c[k] < n_final) mR1[c[k]] = kNoKey;
+    }
+  }
+}
+
 __global__ void k_iota(uint32_t* __restrict__ x, uint64_t count) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x)
     x[i] = (uint32_t)i;
@@ -1743,6 +2012,91 @@ __global__ void __launch_bounds__(kBlock) k_bitmap_emit(const uint32_t* __restri
         const int bit = __ffs(x) - 1;
         x &= x - 1;
         out[pos++] = (uint32_t)(i * 32 + bit);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Sorted output from per-edge flags set by the hook kernels (no atomics):
+// count set flags per tile of kTile x 16 bytes, scan, emit ids ascending.
+constexpr int kFlagTile = kTile * 16;
+
+__global__ void __launch_bounds__(kBlock) k_flags_count(const uint8_t* __restrict__ flags, uint64_t m,
+                                                        uint32_t* __restrict__ counts, DevCounters* ctr, int fused) {
+  __shared__ uint32_t s_cnt[kWarps];
+  const uint32_t ntiles = (uint32_t)((m + kFlagTile - 1) / kFlagTile);
+  const uint64_t nvec = (m + 15) / 16;
+  const uint4* v4 = reinterpret_cast<const uint4*>(flags);
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      const uint64_t i = (uint64_t)tile * kTile + k * kBlock + threadIdx.x;
+      if (i < nvec) {
+        const uint4 v = __ldcs(v4 + i);
+        c += ((v.x * 0x01010101u) >> 24) + ((v.y * 0x01010101u) >> 24) + ((v.z * 0x01010101u) >> 24) +
+             ((v.w * 0x01010101u) >> 24);
+      }
+    }
+    c = warp_sum<uint32_t>(c);
+    if (lane_id() == 0) s_cnt[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t t = 0;
+      for (int w = 0; w < kWarps; ++w) t += s_cnt[w];
+      counts[tile] = t;
+    }
+    __syncthreads();
+  }
+  if (fused) {
+    __shared__ uint32_t s_warp[kWarps + 1], s_flag;
+    fused_scan_if_last<kScanPlain>(counts, ntiles, ctr, 0, kSlotSort, 0, s_warp, &s_flag);
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) k_flags_emit(const uint8_t* __restrict__ flags, uint64_t m,
+                                                       const uint32_t* __restrict__ offsets,
+                                                       uint32_t* __restrict__ out) {
+  __shared__ uint32_t s_scan[32];
+  const uint32_t ntiles = (uint32_t)((m + kFlagTile - 1) / kFlagTile);
+  const uint64_t nvec = (m + 15) / 16;
+  const uint4* v4 = reinterpret_cast<const uint4*>(flags);
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    uint4 v[kItems];
+    uint32_t cnt[kItems], incl[kItems];
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      const uint64_t i = (uint64_t)tile * kTile + k * kBlock + threadIdx.x;
+      v[k] = i < nvec ? __ldcs(v4 + i) : make_uint4(0, 0, 0, 0);
+      cnt[k] = ((v[k].x * 0x01010101u) >> 24) + ((v[k].y * 0x01010101u) >> 24) + ((v[k].z * 0x01010101u) >> 24) +
+               ((v[k].w * 0x01010101u) >> 24);
+      incl[k] = warp_incl_scan(cnt[k]);
+      if (lane == 31) s_scan[k * kWarps + warp] = incl[k];
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t x = s_scan[lane];
+      const uint32_t in = warp_incl_scan(x);
+      s_scan[lane] = in - x;
+    }
+    __syncthreads();
+    const uint32_t prefix = __ldg(offsets + tile);
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      if (!cnt[k]) continue;
+      const uint64_t i = (uint64_t)tile * kTile + k * kBlock + threadIdx.x;
+      uint32_t pos = prefix + s_scan[k * kWarps + warp] + incl[k] - cnt[k];
+      const uint32_t words[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t wd = words[q];
+        while (wd) {
+          const int byte = (__ffs(wd) - 1) >> 3;
+          wd &= ~(0xFFu << (byte * 8));
+          out[pos++] = (uint32_t)(i * 16 + q * 4 + byte);
+        }
       }
     }
     __syncthreads();
