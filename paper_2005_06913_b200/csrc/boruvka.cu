@@ -260,6 +260,32 @@ void init_counters(Workspace& ws, DevCounters* d_ctr, uint32_t n, uint64_t m) {
   MST_CUDA_CHECK(cudaMemcpyAsync(d_ctr, &h, sizeof(DevCounters), cudaMemcpyHostToDevice, ws.stream));
 }
 
+
+// Kernel launch with programmatic dependent launch (kernels.cuh pdl_prologue):
+// the next kernel's launch overlaps this one's tail. MST_PDL=0 disables it.
+bool pdl_enabled() {
+  static const int v = [] {
+    const char* e = getenv("MST_PDL");
+    return (e && *e) ? atoi(e) : 1;
+  }();
+  return v != 0;
+}
+
+template <typename... KArgs, typename... Args>
+void launch_k(void (*kernel)(KArgs...), unsigned grid, unsigned block, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr{};
+  attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr.val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  MST_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+}
+
 // Sorted id list from the per-edge flags the hook kernels set.
 uint32_t sort_from_flags(Workspace& ws, const uint8_t* flags, uint64_t m, uint32_t* d_sorted, DevCounters* d_ctr) {
   const uint64_t tiles = (m + kFlagTile - 1) / kFlagTile;
@@ -268,16 +294,15 @@ uint32_t sort_from_flags(Workspace& ws, const uint8_t* flags, uint64_t m, uint32
   MST_CUDA_CHECK(cudaMemsetAsync(&d_ctr->done[0][kSlotSort], 0, sizeof(unsigned int), ws.stream));
   const unsigned g = (unsigned)std::max<uint64_t>(
       1, std::min<uint64_t>(tiles, (uint64_t)sm_count(ws.device) * blocks_per_sm(k_flags_count)));
-  k_flags_count<<<g, kBlock, 0, ws.stream>>>(flags, m, counts, d_ctr, fused);
+  launch_k(k_flags_count, g, kBlock, ws.stream, flags, m, counts, d_ctr, fused);
   uint32_t launches = 2;
   if (!fused) {
     unsigned long long* st = ws.status_array(tiles);
-    k_scan_counts<kScanPlain><<<(unsigned)std::max<uint64_t>(
-                                    1, std::min<uint64_t>((tiles + kScanTile - 1) / kScanTile, (uint64_t)sm_count(ws.device))),
-                                kScanBlock, 0, ws.stream>>>(counts, tiles, d_ctr, 0, st, ws.next_epoch(), 0, 0);
+    launch_k(k_scan_counts<kScanPlain>, (unsigned)std::max<uint64_t>(
+                                    1, std::min<uint64_t>((tiles + kScanTile - 1) / kScanTile, (uint64_t)sm_count(ws.device))), kScanBlock, ws.stream, counts, tiles, d_ctr, 0, st, ws.next_epoch(), 0, 0);
     ++launches;
   }
-  k_flags_emit<<<g, kBlock, 0, ws.stream>>>(flags, m, counts, d_sorted);
+  launch_k(k_flags_emit, g, kBlock, ws.stream, flags, m, counts, d_sorted);
   MST_CUDA_CHECK(cudaGetLastError());
   return launches;
 }
@@ -291,7 +316,7 @@ uint32_t sort_ids(Workspace& ws, const uint32_t* d_ids, uint64_t count, uint64_t
   uint32_t launches = 0;
   if (count) {
     const unsigned g = (unsigned)std::min<uint64_t>((count + 255) / 256, (uint64_t)sm_count(ws.device) * 8);
-    k_mark<<<g, 256, 0, ws.stream>>>(d_ids, (uint32_t)count, bits, m_total);
+    launch_k(k_mark, g, 256, ws.stream, d_ids, (uint32_t)count, bits, m_total);
     ++launches;
   }
   const uint64_t tiles = tiles_of(words);
@@ -300,15 +325,14 @@ uint32_t sort_ids(Workspace& ws, const uint32_t* d_ids, uint64_t count, uint64_t
   MST_CUDA_CHECK(cudaMemsetAsync(&d_ctr->done[0][kSlotSort], 0, sizeof(unsigned int), ws.stream));
   const unsigned g = (unsigned)std::max<uint64_t>(
       1, std::min<uint64_t>(tiles, (uint64_t)sm_count(ws.device) * blocks_per_sm(k_bitmap_count)));
-  k_bitmap_count<<<g, kBlock, 0, ws.stream>>>(bits, words, counts, d_ctr, fused);
+  launch_k(k_bitmap_count, g, kBlock, ws.stream, bits, words, counts, d_ctr, fused);
   if (!fused) {
     unsigned long long* st = ws.status_array(tiles_of(words));
-    k_scan_counts<kScanPlain><<<(unsigned)std::max<uint64_t>(
-                                    1, std::min<uint64_t>((tiles + kScanTile - 1) / kScanTile, (uint64_t)sm_count(ws.device))),
-                                kScanBlock, 0, ws.stream>>>(counts, tiles, d_ctr, 0, st, ws.next_epoch(), 0, 0);
+    launch_k(k_scan_counts<kScanPlain>, (unsigned)std::max<uint64_t>(
+                                    1, std::min<uint64_t>((tiles + kScanTile - 1) / kScanTile, (uint64_t)sm_count(ws.device))), kScanBlock, ws.stream, counts, tiles, d_ctr, 0, st, ws.next_epoch(), 0, 0);
     ++launches;
   }
-  k_bitmap_emit<<<g, kBlock, 0, ws.stream>>>(bits, words, counts, d_sorted);
+  launch_k(k_bitmap_emit, g, kBlock, ws.stream, bits, words, counts, d_sorted);
   launches += 2;
   MST_CUDA_CHECK(cudaGetLastError());
   return launches;
@@ -381,12 +405,12 @@ void launch_two_pass(Workspace& ws, const CompactBufs& cb, View in, uint4* relab
       1, std::min<uint64_t>(tiles, (uint64_t)sm_count(dev) * blocks_per_sm(kcnt)));
   // armed: this launch relabels + inserts pairs if the device chose dedup
   // (decided and table cleared by k_label), the kModeDedup pass counts
-  kcnt<<<gc, kBlock, 0, ws.stream>>>(in, kMode == kModeRelabel ? relabeled : cb.stage, L, cb.masks, cb.counts, n_orig,
+  launch_k(kcnt, gc, kBlock, ws.stream, in, kMode == kModeRelabel ? relabeled : cb.stage, L, cb.masks, cb.counts, n_orig,
                                      d_ctr, r, fused, slot, light, pt);
   if constexpr (!View::kOriginal) {
     if (armed) {
       auto kdc = k_count<View, kModeDedup>;
-      kdc<<<gc, kBlock, 0, ws.stream>>>(PackedView{relabeled}, cb.stage, L, cb.masks, cb.counts, n_orig, d_ctr, r,
+      launch_k(kdc, gc, kBlock, ws.stream, PackedView{relabeled}, cb.stage, L, cb.masks, cb.counts, n_orig, d_ctr, r,
                                         fused, slot, light, pt);
     }
   }
@@ -394,21 +418,21 @@ void launch_two_pass(Workspace& ws, const CompactBufs& cb, View in, uint4* relab
     auto ksc = k_scan_counts<kScanEdges>;
     const unsigned gs = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((tiles + kScanTile - 1) / kScanTile,
                                                                             (uint64_t)sm_count(dev)));
-    ksc<<<gs, kScanBlock, 0, ws.stream>>>(cb.counts, tiles, d_ctr, r, cb.st, ws.next_epoch(), light,
+    launch_k(ksc, gs, kScanBlock, ws.stream, cb.counts, tiles, d_ctr, r, cb.st, ws.next_epoch(), light,
                                           View::kOriginal ? 1 : 0);
   }
   const unsigned ge = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)sm_count(dev) * 8));
   if (armed) {
     auto kde = k_emit_staged<kModeDedup, kPre>;
-    kde<<<ge, kBlock, 0, ws.stream>>>(cb.stage, cb.counts, out, min_next, d_ctr, r, filt);
+    launch_k(kde, ge, kBlock, ws.stream, cb.stage, cb.counts, out, min_next, d_ctr, r, filt);
   }
   if (kMode == kModeRelabel) {
     auto kem = k_emit<View, kMode, kPre>;
-    kem<<<ge, kBlock, 0, ws.stream>>>(in, relabeled, L, cb.masks, cb.counts, out, min_next, d_ctr, r, filt,
-                                      armed ? 1 : 0);
+    launch_k(kem, ge, kBlock, ws.stream, in, relabeled, L, cb.masks, cb.counts, out, min_next, d_ctr, r, filt,
+                                      armed ? 1 : 0, n_orig);
   } else {
     auto kes = k_emit_staged<kMode, kPre>;
-    kes<<<ge, kBlock, 0, ws.stream>>>(cb.stage, cb.counts, out, min_next, d_ctr, r, filt);
+    launch_k(kes, ge, kBlock, ws.stream, cb.stage, cb.counts, out, min_next, d_ctr, r, filt);
   }
   MST_CUDA_CHECK(cudaGetLastError());
 }
@@ -455,11 +479,11 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     MST_CUDA_CHECK(cudaMemsetAsync(hist, 0, 65536 * sizeof(uint32_t), s));
     const uint32_t samples = (uint32_t)std::min<uint64_t>(m, 1u << 20);
     const uint64_t step = std::max<uint64_t>(1, m / samples);
-    k_weight_hist<<<std::max(1u, samples / 1024), 256, 0, s>>>(wbase, wstride, m, step, samples, hist);
+    launch_k(k_weight_hist, std::max(1u, samples / 1024), 256, s, wbase, wstride, m, step, samples, hist);
     const double beta = env_double("MST_FILTER_BETA", 2.0);
     const double frac = std::min(1.0, beta * (double)n / (double)m);
     const uint32_t target = (uint32_t)std::max(1.0, frac * samples);
-    k_pick_pivot<<<1, 1024, 0, s>>>(hist, target, d_ctr);
+    launch_k(k_pick_pivot, 1, 1024, s, hist, target, d_ctr);
     launches += 2;
     hot_begin(kHotSplit, 0, true);
     launch_two_pass<InView, kModeLight, kPre>(ws, cb, in, nullptr, nullptr, E[1], minb[0], d_ctr, 0, m, n,
@@ -471,7 +495,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     const unsigned g = (unsigned)std::max<uint64_t>(
         1, std::min<uint64_t>((m + 4 * kBlock - 1) / (4 * kBlock), (uint64_t)sm_count(dev) * blocks_per_sm(kmin)));
     hot_begin(kHotMin1, 0, false);
-    kmin<<<g, kBlock, 0, s>>>(in, n, m, minb[0], d_ctr, filt_for(n));
+    launch_k(kmin, g, kBlock, s, in, n, m, minb[0], d_ctr, filt_for(n));
     tmark();
     ++launches;
   }
@@ -487,7 +511,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   const bool tail_v2 = tail_mode == 2;
   const bool dedup_on = env_int("MST_DEDUP", 1) != 0;
   const uint64_t dedup_min_edges = (uint64_t)env_double("MST_DEDUP_MIN_EDGES", 2.0e6);
-  const uint64_t tail_edges = (uint64_t)env_double("MST_TAIL_EDGES", 3.0e6);
+  const uint64_t tail_edges = (uint64_t)env_double("MST_TAIL_EDGES", 6.0e6);
 
   // Light phase over: compose its relabel maps into a vertex -> component map,
   // run the heavy filter pass, continue with the plain loop (phase D).
@@ -508,7 +532,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     for (int k = (int)levels.size() - 2; k >= 0; --k) {
       const unsigned g = (unsigned)std::max<uint64_t>(
           1, std::min<uint64_t>((snap.n[levels[k].second] + 255) / 256, (uint64_t)sm_count(dev) * 8));
-      k_compose<<<g, 256, 0, s>>>(levels[k].first, levels[k + 1].first, d_ctr, levels[k].second);
+      launch_k(k_compose, g, 256, s, levels[k].first, levels[k + 1].first, d_ctr, levels[k].second);
       ++launches;
     }
     const uint32_t* vlabel = levels.empty() ? nullptr : levels[0].first;
@@ -536,14 +560,14 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       uint32_t* M = nullptr;
       if (light) {
         M = ws.get<uint32_t>("Ltail", n_bound);
-        k_iota<<<(unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_bound + 255) / 256, 4096)), 256, 0, s>>>(
+        launch_k(k_iota, (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_bound + 255) / 256, 4096)), 256, s, 
             M, n_bound);
         ++launches;
       }
       auto kt = tail_v2 ? k_tail2
                         : (getenv("MST_TAIL_PREREDUCE") && getenv("MST_TAIL_PREREDUCE")[0] == '1' ? k_tail<true>
                                                                                                   : k_tail<false>);
-      const int bps = std::max(1, std::min(blocks_per_sm(kt), env_int("MST_TAIL_BPS", 4)));
+      const int bps = std::max(1, std::min(blocks_per_sm(kt), env_int("MST_TAIL_BPS", 2)));
       const unsigned G = (unsigned)(sm_count(dev) * bps);
       uint32_t* bcount = ws.get<uint32_t>("bcount", G);
       unsigned long long* trace = nullptr;
@@ -584,21 +608,17 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       const int hfused = ht <= kFusedScanMaxTiles ? 1 : 0;
       if (original_in) {
         auto kd = k_hook_decide<InView>;
-        kd<<<(unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ht, (uint64_t)sm_count(dev) * blocks_per_sm(kd))),
-             kBlock, 0, s>>>(in, mcur, parent, rootlabel, hmasks, hcounts, d_ctr, r, hfused, (int)light);
+        launch_k(kd, (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ht, (uint64_t)sm_count(dev) * blocks_per_sm(kd))), kBlock, s, in, mcur, parent, rootlabel, hmasks, hcounts, d_ctr, r, hfused, (int)light);
       } else {
         auto kd = k_hook_decide<PackedView>;
-        kd<<<(unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ht, (uint64_t)sm_count(dev) * blocks_per_sm(kd))),
-             kBlock, 0, s>>>(PackedView{E[r & 1]}, mcur, parent, rootlabel, hmasks, hcounts, d_ctr, r, hfused,
+        launch_k(kd, (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ht, (uint64_t)sm_count(dev) * blocks_per_sm(kd))), kBlock, s, PackedView{E[r & 1]}, mcur, parent, rootlabel, hmasks, hcounts, d_ctr, r, hfused,
                              (int)light);
       }
       if (!hfused)
-        k_scan_counts<kScanRoots><<<(unsigned)std::max<uint64_t>(
-                                        1, std::min<uint64_t>((ht + kScanTile - 1) / kScanTile, (uint64_t)sm_count(dev))),
-                                    kScanBlock, 0, s>>>(hcounts, ht, d_ctr, r, st, ws.next_epoch(), (int)light, 0);
-      k_hook_emit<<<(unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ht, (uint64_t)sm_count(dev) *
-                                                                              blocks_per_sm(k_hook_emit))),
-                    kBlock, 0, s>>>(parent, rootlabel, hmasks, hcounts, mst, n, d_ctr, r, flags);
+        launch_k(k_scan_counts<kScanRoots>, (unsigned)std::max<uint64_t>(
+                                        1, std::min<uint64_t>((ht + kScanTile - 1) / kScanTile, (uint64_t)sm_count(dev))), kScanBlock, s, hcounts, ht, d_ctr, r, st, ws.next_epoch(), (int)light, 0);
+      launch_k(k_hook_emit, (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ht, (uint64_t)sm_count(dev) *
+                                                                              blocks_per_sm(k_hook_emit))), kBlock, s, parent, rootlabel, hmasks, hcounts, mst, n, d_ctr, r, flags);
       launches += 2;
     }
     uint32_t* Lr = L;
@@ -617,7 +637,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     {
       const unsigned g = (unsigned)std::max<uint64_t>(
           1, std::min<uint64_t>((n_bound + kBlock - 1) / kBlock, (uint64_t)sm_count(dev) * blocks_per_sm(k_label)));
-      k_label<<<g, kBlock, 0, s>>>(parent, rootlabel, Lr, mnext, d_ctr, r, pt.pairs, pt.mins, pt.cap);
+      launch_k(k_label, g, kBlock, s, parent, rootlabel, Lr, mnext, d_ctr, r, pt.pairs, pt.mins, pt.cap);
     }
     hot_begin(kHotCompact, r, light);
     if (original_in) {

@@ -68,6 +68,16 @@ struct DevCounters {
   unsigned int pair_abort[kMaxR];  // table overflowed: keep every edge this round
 };
 
+
+// Programmatic dependent launch: every kernel first waits for its stream
+// predecessor to complete (and its memory to be visible), then lets its own
+// successor start launching, so launch latency and block ramp-up overlap the
+// predecessor's tail. Without a PDL launch both are no-ops.
+__device__ __forceinline__ void pdl_prologue() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ------------------------------ edge views ---------------------------------
 
 struct EdgeRec {
@@ -340,6 +350,7 @@ template <class View, bool kKeyPartner, bool kWarpPre>
 __global__ void __launch_bounds__(kBlock) k_min_round1(View v, uint32_t n, uint64_t m,
                                                        unsigned long long* __restrict__ minimum,
                                                        DevCounters* ctr, int filt) {
+  pdl_prologue();
   constexpr int kU = 4;
   const uint64_t stride = (uint64_t)gridDim.x * kBlock * kU;
   uint32_t err = 0;
@@ -388,6 +399,7 @@ __global__ void __launch_bounds__(kBlock) k_hook(View E, const unsigned long lon
                                                  DevCounters* ctr, int r,
                                                  unsigned long long* status, uint32_t epoch,
                                                  int light_phase) {
+  pdl_prologue();
   __shared__ uint32_t s_scan[32];
   __shared__ uint32_t s_misc[2];
   __shared__ uint32_t s_tile;
@@ -491,6 +503,7 @@ __global__ void __launch_bounds__(kBlock) k_label(uint32_t* __restrict__ parent,
                                                   unsigned long long* __restrict__ min_next,
                                                   DevCounters* ctr, int r, unsigned long long* pair_keys,
                                                   unsigned long long* pair_mins, unsigned long long pair_cap) {
+  pdl_prologue();
   if ((uint32_t)r + 1 >= ctr->stop_round || (uint32_t)r >= ctr->phase_end) return;
   const uint32_t n_r = ctr->n[r];
   const uint32_t n_next = ctr->n[r + 1];
@@ -564,6 +577,7 @@ __global__ void __launch_bounds__(kBlock) k_compact(View Ein, uint4* __restrict_
                                                     Recover rec, uint32_t n_orig, DevCounters* ctr,
                                                     int r, unsigned long long* status,
                                                     uint32_t epoch, int slot, int light_phase, int filt) {
+  pdl_prologue();
   __shared__ uint32_t s_scan[kCItems * kWarps];
   __shared__ uint32_t s_misc[2];
   __shared__ uint32_t s_tile;
@@ -659,6 +673,7 @@ __global__ void __launch_bounds__(kBlock) k_compact(View Ein, uint4* __restrict_
 // below it (kept in ctr->pivot; 0xFFFFFFFF means "everything light").
 __global__ void k_weight_hist(const uint32_t* __restrict__ w, uint32_t wstride, uint64_t m,
                               uint64_t step, uint32_t samples, uint32_t* __restrict__ hist) {
+  pdl_prologue();
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < samples; k += gridDim.x * blockDim.x) {
     const uint64_t i = (uint64_t)k * step;
     if (i < m) atomicAdd(hist + (__ldg(w + i * wstride) >> 16), 1u);
@@ -666,6 +681,7 @@ __global__ void k_weight_hist(const uint32_t* __restrict__ w, uint32_t wstride, 
 }
 
 __global__ void __launch_bounds__(1024) k_pick_pivot(const uint32_t* __restrict__ hist, uint32_t target, DevCounters* ctr) {
+  pdl_prologue();
   // one block of 1024 threads: 64 bins per thread, block scan of sums
   __shared__ uint32_t s_sum[1024];
   const uint32_t t = threadIdx.x;
@@ -697,6 +713,7 @@ __global__ void __launch_bounds__(1024) k_pick_pivot(const uint32_t* __restrict_
 // L_r[c] = L_{r+1}[L_r[c]] for c < n[r] (in place on level r).
 __global__ void k_compose(uint32_t* __restrict__ Lr, const uint32_t* __restrict__ Lnext,
                           const DevCounters* ctr, int r) {
+  pdl_prologue();
   const uint32_t n_r = ctr->n[r];
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n_r; c += stride)
@@ -890,6 +907,7 @@ __global__ void __launch_bounds__(kBlock) k_count(View in, uint4* __restrict__ r
                                                   uint32_t* __restrict__ masks, uint32_t* __restrict__ counts,
                                                   uint32_t n_orig, DevCounters* ctr, int r, int fused, int slot,
                                                   int light_phase, PairTable pt) {
+  pdl_prologue();
   __shared__ uint32_t s_cnt[kWarps];
   __shared__ uint32_t s_slot[kCItems * kWarps];
   const uint32_t stop = ctr->stop_round;
@@ -946,12 +964,7 @@ __global__ void __launch_bounds__(kBlock) k_count(View in, uint4* __restrict__ r
         } else if (ok) {
           const uint32_t x = __ldg(L + e[k].a), y = __ldg(L + e[k].b);
           keep[k] = x != y;
-          if (View::kOriginal)
-            __stcs(relabeled + i, make_uint4(x, y, e[k].w, e[k].eid));
-          else
-            __stcs(reinterpret_cast<uint2*>(relabeled + i), make_uint2(x, y));
-        } else if (View::kOriginal) {
-          __stcs(relabeled + i, make_uint4(0, 0, 0, 0));  // rejected input edge: a self-loop placeholder
+          if (!View::kOriginal) __stcs(reinterpret_cast<uint2*>(relabeled + i), make_uint2(x, y));
         }
       }
       bal[k] = __ballot_sync(0xffffffffu, keep[k]);
@@ -1010,7 +1023,8 @@ __global__ void __launch_bounds__(kBlock) k_emit(View in, const uint4* __restric
                                                  const uint32_t* __restrict__ masks,
                                                  const uint32_t* __restrict__ offsets, uint4* __restrict__ out,
                                                  unsigned long long* __restrict__ min_next, DevCounters* ctr,
-                                                 int r, int filt, int dedup_armed) {
+                                                 int r, int filt, int dedup_armed, uint32_t n_orig) {
+  pdl_prologue();
   __shared__ uint32_t s_scan[kCItems * kWarps];
   const uint32_t stop = ctr->stop_round;
   if ((uint32_t)r >= ctr->phase_end || (uint32_t)r + 1 >= stop) return;
@@ -1027,7 +1041,15 @@ __global__ void __launch_bounds__(kBlock) k_emit(View in, const uint4* __restric
     for (int k = 0; k < kCItems; ++k) {
       const uint64_t i = (uint64_t)tile * kCTile + k * kBlock + threadIdx.x;
       e[k] = make_uint4(0, 0, 0, 0);
-      if (kMode == kModeRelabel) {
+      if (kMode == kModeRelabel && View::kOriginal) {
+        // plain round 1: re-read the caller's list and re-gather the labels
+        // (cheaper than writing + reading a relabelled 16 B copy)
+        if (i < m_r) {
+          const EdgeRec x = in.stream(i);
+          const bool ok = x.a < n_orig && x.b < n_orig && x.ok;
+          e[k] = ok ? make_uint4(__ldg(L + x.a), __ldg(L + x.b), x.w, x.eid) : make_uint4(0, 0, 0, 0);
+        }
+      } else if (kMode == kModeRelabel) {
         if (i < m_r) e[k] = __ldcs(relabeled + i);
       } else {
         bal[k] = __ldg(masks + (uint64_t)tile * (kCItems * kWarps) + k * kWarps + warp);
@@ -1093,6 +1115,7 @@ __global__ void __launch_bounds__(kBlock) k_emit_staged(const uint4* __restrict_
                                                         const uint32_t* __restrict__ offsets, uint4* __restrict__ out,
                                                         unsigned long long* __restrict__ min_next, DevCounters* ctr,
                                                         int r, int filt) {
+  pdl_prologue();
   const uint32_t stop = ctr->stop_round;
   if ((uint32_t)r >= ctr->phase_end || (uint32_t)r + 1 >= stop) return;
   if (kMode == kModeDedup && (!ctr->dedup[r] || ctr->pair_abort[r])) return;
@@ -1129,6 +1152,7 @@ template <int kKind>
 __global__ void __launch_bounds__(kScanBlock) k_scan_counts(uint32_t* __restrict__ counts, uint64_t ntiles_max,
                                                              DevCounters* ctr, int r, unsigned long long* status,
                                                              uint32_t epoch, int light_phase, int count_src) {
+  pdl_prologue();
   __shared__ uint32_t s_warp[kScanBlock / 32];
   __shared__ uint32_t s_misc[2];
   if (kKind != kScanPlain) {
@@ -1190,6 +1214,7 @@ __global__ void __launch_bounds__(kBlock) k_hook_decide(View E, const unsigned l
                                                         uint32_t* __restrict__ parent, uint32_t* __restrict__ rootlabel,
                                                         uint32_t* __restrict__ masks, uint32_t* __restrict__ counts,
                                                         DevCounters* ctr, int r, int fused, int light_phase) {
+  pdl_prologue();
   __shared__ uint32_t s_cnt[kWarps];
   __shared__ unsigned long long s_wsum[kWarps];
   if ((uint32_t)r >= ctr->stop_round || (uint32_t)r >= ctr->phase_end) return;
@@ -1280,6 +1305,7 @@ __global__ void __launch_bounds__(kBlock) k_hook_emit(const uint32_t* __restrict
                                                       const uint32_t* __restrict__ offsets, uint32_t* __restrict__ mst,
                                                       uint32_t n_orig, DevCounters* ctr, int r,
                                                       uint8_t* __restrict__ flags) {
+  pdl_prologue();
   __shared__ uint32_t s_scan[kItems * kWarps];
   if ((uint32_t)r >= ctr->phase_end) return;
   // runs even when this round stops (the last hook's MST slots are needed)
@@ -1397,6 +1423,7 @@ __device__ __forceinline__ void tail_stamp(const TailArgs& a, int& slot) {
 
 template <bool kWarpPre>
 __global__ void __launch_bounds__(kBlock) k_tail(TailArgs a) {
+  pdl_prologue();
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   int slot = 0;
@@ -1670,6 +1697,7 @@ __global__ void __launch_bounds__(kBlock) k_tail(TailArgs a) {
 // round kernels leave them. On exit in the light phase the roots are
 // densified (one prefix) so the filter pass and phase D see dense labels.
 __global__ void __launch_bounds__(kBlock) k_tail2(TailArgs a) {
+  pdl_prologue();
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   __shared__ unsigned long long s_min[kTailSmemMin];
@@ -1910,6 +1938,7 @@ __global__ void __launch_bounds__(kBlock) k_tail2(TailArgs a) {
 }
 
 __global__ void k_iota(uint32_t* __restrict__ x, uint64_t count) {
+  pdl_prologue();
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x)
     x[i] = (uint32_t)i;
 }
@@ -1925,6 +1954,7 @@ struct ShardPtrs {
 
 template <class T>
 __global__ void k_shard_min(ShardPtrs<T, 8> bufs, int shards, uint64_t count) {
+  pdl_prologue();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
     T v = bufs.p[0][i];
@@ -1938,6 +1968,7 @@ __global__ void k_shard_min(ShardPtrs<T, 8> bufs, int shards, uint64_t count) {
 
 __global__ void k_mark(const uint32_t* __restrict__ ids, uint32_t count, uint32_t* __restrict__ bits,
                        uint64_t m) {
+  pdl_prologue();
   const uint32_t stride = gridDim.x * blockDim.x;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
     const uint32_t e = ids[i];
@@ -1953,6 +1984,7 @@ __global__ void k_mark(const uint32_t* __restrict__ ids, uint32_t count, uint32_
 __global__ void __launch_bounds__(kBlock) k_bitmap_count(const uint32_t* __restrict__ bits, uint64_t words,
                                                          uint32_t* __restrict__ counts, DevCounters* ctr,
                                                          int fused) {
+  pdl_prologue();
   __shared__ uint32_t s_cnt[kWarps];
   const uint32_t ntiles = (uint32_t)((words + kTile - 1) / kTile);
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
@@ -1982,6 +2014,7 @@ __global__ void __launch_bounds__(kBlock) k_bitmap_count(const uint32_t* __restr
 __global__ void __launch_bounds__(kBlock) k_bitmap_emit(const uint32_t* __restrict__ bits, uint64_t words,
                                                         const uint32_t* __restrict__ offsets,
                                                         uint32_t* __restrict__ out) {
+  pdl_prologue();
   __shared__ uint32_t s_scan[32];
   const uint32_t ntiles = (uint32_t)((words + kTile - 1) / kTile);
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
@@ -2024,6 +2057,7 @@ constexpr int kFlagTile = kTile * 16;
 
 __global__ void __launch_bounds__(kBlock) k_flags_count(const uint8_t* __restrict__ flags, uint64_t m,
                                                         uint32_t* __restrict__ counts, DevCounters* ctr, int fused) {
+  pdl_prologue();
   __shared__ uint32_t s_cnt[kWarps];
   const uint32_t ntiles = (uint32_t)((m + kFlagTile - 1) / kFlagTile);
   const uint64_t nvec = (m + 15) / 16;
@@ -2058,6 +2092,7 @@ __global__ void __launch_bounds__(kBlock) k_flags_count(const uint8_t* __restric
 __global__ void __launch_bounds__(kBlock) k_flags_emit(const uint8_t* __restrict__ flags, uint64_t m,
                                                        const uint32_t* __restrict__ offsets,
                                                        uint32_t* __restrict__ out) {
+  pdl_prologue();
   __shared__ uint32_t s_scan[32];
   const uint32_t ntiles = (uint32_t)((m + kFlagTile - 1) / kFlagTile);
   const uint64_t nvec = (m + 15) / 16;
