@@ -483,7 +483,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     const uint32_t samples = (uint32_t)std::min<uint64_t>(m, 1u << 20);
     const uint64_t step = std::max<uint64_t>(1, m / samples);
     launch_k(k_weight_hist, std::max(1u, samples / 1024), 256, s, wbase, wstride, m, step, samples, hist);
-    const double beta = env_double("MST_FILTER_BETA", 2.0);
+    const double beta = env_double("MST_FILTER_BETA", 1.5);
     const double frac = std::min(1.0, beta * (double)n / (double)m);
     const uint32_t target = (uint32_t)std::max(1.0, frac * samples);
     launch_k(k_pick_pivot, 1, 1024, s, hist, target, d_ctr);
