@@ -514,6 +514,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   const bool tail_v2 = tail_mode == 2;
   const bool dedup_on = env_int("MST_DEDUP", 1) != 0;
   const uint64_t dedup_min_edges = (uint64_t)env_double("MST_DEDUP_MIN_EDGES", 2.0e6);
+  const unsigned int dedup_active = (unsigned int)env_double("MST_DEDUP_ACTIVE", 262144);
   const uint64_t tail_edges = (uint64_t)env_double("MST_TAIL_EDGES", 6.0e6);
 
   // Light phase over: compose its relabel maps into a vertex -> component map,
@@ -640,7 +641,8 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     {
       const unsigned g = (unsigned)std::max<uint64_t>(
           1, std::min<uint64_t>((n_bound + kBlock - 1) / kBlock, (uint64_t)sm_count(dev) * blocks_per_sm(k_label)));
-      launch_k(k_label, g, kBlock, s, parent, rootlabel, Lr, mnext, d_ctr, r, pt.pairs, pt.mins, pt.cap);
+      launch_k(k_label, g, kBlock, s, parent, rootlabel, Lr, mnext, d_ctr, r, pt.pairs, pt.mins, pt.cap,
+               dedup_active);
     }
     hot_begin(kHotCompact, r, light);
     if (original_in) {
@@ -981,7 +983,8 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, RunOu
       const unsigned gl = (unsigned)std::max<uint64_t>(
           1, std::min<uint64_t>((n_bound + kBlock - 1) / kBlock,
                                 (uint64_t)sm_count(ws.device) * blocks_per_sm(k_label)));
-      k_label<<<gl, kBlock, 0, ws.stream>>>(s.parent, s.rootlabel, s.L, s.minb[nxt], s.d_ctr, r, nullptr, nullptr, 0);
+      k_label<<<gl, kBlock, 0, ws.stream>>>(s.parent, s.rootlabel, s.L, s.minb[nxt], s.d_ctr, r, nullptr, nullptr, 0,
+                                            0u);
       MST_CUDA_CHECK(cudaMemcpyAsync(&ws.h_snap[r], s.d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost,
                                      ws.stream));
       MST_CUDA_CHECK(cudaEventRecord(ws.ev[r], ws.stream));

@@ -502,7 +502,8 @@ __global__ void __launch_bounds__(kBlock) k_label(uint32_t* __restrict__ parent,
                                                   uint32_t* __restrict__ L,
                                                   unsigned long long* __restrict__ min_next,
                                                   DevCounters* ctr, int r, unsigned long long* pair_keys,
-                                                  unsigned long long* pair_mins, unsigned long long pair_cap) {
+                                                  unsigned long long* pair_mins, unsigned long long pair_cap,
+                                                  unsigned int dedup_active) {
   pdl_prologue();
   if ((uint32_t)r + 1 >= ctr->stop_round || (uint32_t)r >= ctr->phase_end) return;
   const uint32_t n_r = ctr->n[r];
@@ -514,7 +515,7 @@ __global__ void __launch_bounds__(kBlock) k_label(uint32_t* __restrict__ parent,
     // the attempt (the round then compacts like a plain one).
     const unsigned long long K = ctr->active[r];
     const unsigned long long m_r = ctr->m[r];
-    const bool use = K <= 262144ull && m_r >= 8 * K && m_r >= 4096;
+    const bool use = K <= dedup_active && m_r >= 8 * K && m_r >= 4096;
     unsigned long long P = 1024;
     while (P < m_r / 4 && P < pair_cap) P <<= 1;
     if (blockIdx.x == 0 && threadIdx.x == 0) {

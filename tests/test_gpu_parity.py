@@ -298,3 +298,22 @@ def test_device_resident_entry(mst, oracle_mod):
     assert np.array_equal(out[:count].cpu().numpy().view(np.uint32), k.ids)
     assert hot["launches"] >= 2 and hot["ms"] > 0
     assert info.alg_bytes > 12 * m
+
+
+def test_nccl_rank_path_single_rank(mst, oracle_mod):
+    """The one-process-per-GPU entry (mst_comm_* + mst_gpu_boruvka_rank) with a
+    real NCCL communicator of one rank: exercises dlopen(libnccl), comm init,
+    the per-round ncclAllReduce(min, u64) and the final slot allreduce."""
+    from paper_2005_06913_b200 import configs as C
+    from paper_2005_06913_b200 import dist as D
+    P, O = mst, oracle_mod
+    uid = D.new_unique_id()
+    comm = D.RankComm(uid, 1, 0, 0)
+    try:
+        for spec in (C.uniform(50_000, 200_000, seed=3), C.grid(100, 100, seed=2), C.rmat(13, 8, seed=5)):
+            g = C.generate_host(spec)
+            k = O.kruskal(g.n, g.src, g.dst, g.w)
+            r = comm.boruvka(g.n, g.edge_count(), 0, g.src, g.dst, g.w)
+            assert r.mst_edges.tolist() == k.ids.tolist() and r.total_weight == k.total_weight
+    finally:
+        comm.close()
