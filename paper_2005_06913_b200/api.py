@@ -26,6 +26,7 @@ to the CPU.
 from __future__ import annotations
 
 import ctypes
+import sys
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -132,6 +133,21 @@ def _ptr(a: np.ndarray) -> int:
     return a.ctypes.data if a.size else 0
 
 
+def _host_out(count: int) -> np.ndarray:
+    """uint32 output buffer. When torch is already loaded, take it from torch's
+    caching pinned-host allocator so the device->host copy runs at full link
+    speed (16 MB: 0.3 ms pinned vs 1.1 ms pageable on the B200 host); otherwise
+    plain numpy (the library stages pageable copies itself)."""
+    torch = sys.modules.get("torch")
+    if torch is not None:
+        try:
+            if torch.cuda.is_available():
+                return torch.empty(count, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+        except Exception:
+            pass
+    return np.empty(count, dtype=np.uint32)
+
+
 def _info_from(stats: L.MstStats, info: GpuRunInfo | None) -> None:
     if info is None:
         return
@@ -184,7 +200,7 @@ def boruvka_gpu(g: Graph, num_gpus: int = 1, info: GpuRunInfo | None = None) -> 
         raise ValueError("boruvka: need num_gpus >= 1")
     lib = L.lib()
     e = L.MstEdgesSoa(g.n, g.edge_count(), _ptr(g.src), _ptr(g.dst), _ptr(g.w), 0)
-    ids = np.empty(max(g.n - 1, 1), dtype=np.uint32)
+    ids = _host_out(max(g.n - 1, 1))
     count, total = ctypes.c_uint64(0), ctypes.c_uint64(0)
     stats = L.MstStats()
     rc = lib.mst_gpu_boruvka(ctypes.byref(e), num_gpus, ids.ctypes.data, ctypes.byref(count),
@@ -196,7 +212,7 @@ def boruvka_gpu_aos(n: int, edges: np.ndarray, info: GpuRunInfo | None = None) -
     """Same, fed the reference's AoS ``Edge`` array unchanged (EDGE_DTYPE)."""
     edges = np.ascontiguousarray(edges, dtype=EDGE_DTYPE)
     lib = L.lib()
-    ids = np.empty(max(n - 1, 1), dtype=np.uint32)
+    ids = _host_out(max(n - 1, 1))
     count, total = ctypes.c_uint64(0), ctypes.c_uint64(0)
     stats = L.MstStats()
     rc = lib.mst_gpu_boruvka_aos(n, edges.shape[0], _ptr(edges), 0, ids.ctypes.data,

@@ -22,7 +22,7 @@ DEPS = SOURCES + ["kernels.cuh", "common.cuh"]
 NVCC_FLAGS = [
     "-std=c++17", "-O3", "-lineinfo",
     "-gencode", "arch=compute_100a,code=sm_100a",
-    "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
+    "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", "-Xcompiler", "-fopenmp",
     "-shared",
 ]
 
@@ -44,7 +44,7 @@ def _stale(target: Path, deps) -> bool:
 def build_library(force: bool = False, verbose: bool = True) -> Path:
     deps = [CSRC / d for d in DEPS] + [ROOT / "include" / "mst_gpu.h"]
     if force or _stale(LIB, deps):
-        cmd = [_nvcc(), *NVCC_FLAGS, *[str(CSRC / s) for s in SOURCES], "-o", str(LIB), "-ldl"]
+        cmd = [_nvcc(), *NVCC_FLAGS, *[str(CSRC / s) for s in SOURCES], "-o", str(LIB), "-ldl", "-lgomp"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True, cwd=str(CSRC))
