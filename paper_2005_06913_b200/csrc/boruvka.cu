@@ -542,6 +542,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
                        ws.get<uint4>("stage", tiles_c(m) * kCTile)};
   uint32_t* hcounts = ws.get<uint32_t>("hook_counts", tiles_of(n));
   uint32_t* hmasks = ws.get<uint32_t>("hook_masks", tiles_of(n) * kItems * kWarps);
+  uint32_t* hslot = ws.get<uint32_t>("hook_slotpref", tiles_of(n) * kItems * kWarps);
   (void)no_rec;
 
   init_counters(ws, d_ctr, n, m);
@@ -694,18 +695,19 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       const int hfused = ht <= kFusedScanMaxTiles ? 1 : 0;
       if (original_in) {
         auto kd = k_hook_decide<InView>;
-        launch_k(kd, (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ht, (uint64_t)sm_count(dev) * blocks_per_sm(kd))), kBlock, s, in, mcur, parent, rootlabel, hmasks, hcounts, d_ctr, r, hfused, (int)light);
+        launch_k(kd, (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ht, (uint64_t)sm_count(dev) * blocks_per_sm(kd))),
+                 kBlock, s, in, mcur, parent, rootlabel, hmasks, hcounts, d_ctr, r, hfused, (int)light, hslot);
       } else {
         auto kd = k_hook_decide<PackedView>;
-        launch_k(kd, (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ht, (uint64_t)sm_count(dev) * blocks_per_sm(kd))), kBlock, s, PackedView{E[r & 1]}, mcur, parent, rootlabel, hmasks, hcounts, d_ctr, r, hfused,
-                             (int)light);
+        launch_k(kd, (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ht, (uint64_t)sm_count(dev) * blocks_per_sm(kd))),
+                 kBlock, s, PackedView{E[r & 1]}, mcur, parent, rootlabel, hmasks, hcounts, d_ctr, r, hfused,
+                 (int)light, hslot);
       }
       if (!hfused)
-        launch_k(k_scan_counts<kScanRoots>, (unsigned)std::max<uint64_t>(
-                                        1, std::min<uint64_t>((ht + kScanTile - 1) / kScanTile, (uint64_t)sm_count(dev))), kScanBlock, s, hcounts, ht, d_ctr, r, st, ws.next_epoch(), (int)light, 0);
-      launch_k(k_hook_emit, (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ht, (uint64_t)sm_count(dev) *
-                                                                              blocks_per_sm(k_hook_emit))), kBlock, s, parent, rootlabel, hmasks, hcounts, mst, n, d_ctr, r, flags);
-      launches += 2;
+        launch_k(k_scan_counts<kScanRoots>,
+                 (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((ht + kScanTile - 1) / kScanTile, (uint64_t)sm_count(dev))),
+                 kScanBlock, s, hcounts, ht, d_ctr, r, st, ws.next_epoch(), (int)light, 0);
+      launches += 1;
     }
     uint32_t* Lr = L;
     if (light) {
@@ -722,9 +724,9 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     }
     {
       const unsigned g = (unsigned)std::max<uint64_t>(
-          1, std::min<uint64_t>((n_bound + kBlock - 1) / kBlock, (uint64_t)sm_count(dev) * blocks_per_sm(k_label)));
-      launch_k(k_label, g, kBlock, s, parent, rootlabel, Lr, mnext, d_ctr, r, pt.pairs, pt.mins, pt.cap,
-               dedup_active);
+          1, std::min<uint64_t>(tiles_of(n_bound), (uint64_t)sm_count(dev) * blocks_per_sm(k_label2)));
+      launch_k(k_label2, g, kBlock, s, parent, rootlabel, hmasks, hslot, hcounts, Lr, mnext, mst, flags, n, d_ctr, r,
+               pt.pairs, pt.cap, dedup_active);
     }
     hot_begin(kHotCompact, r, light);
     if (original_in) {

@@ -1214,9 +1214,11 @@ template <class View>
 __global__ void __launch_bounds__(kBlock) k_hook_decide(View E, const unsigned long long* __restrict__ minimum,
                                                         uint32_t* __restrict__ parent, uint32_t* __restrict__ rootlabel,
                                                         uint32_t* __restrict__ masks, uint32_t* __restrict__ counts,
-                                                        DevCounters* ctr, int r, int fused, int light_phase) {
+                                                        DevCounters* ctr, int r, int fused, int light_phase,
+                                                        uint32_t* __restrict__ slotpref) {
   pdl_prologue();
   __shared__ uint32_t s_cnt[kWarps];
+  __shared__ uint32_t s_slot[kItems * kWarps];
   __shared__ unsigned long long s_wsum[kWarps];
   if ((uint32_t)r >= ctr->stop_round || (uint32_t)r >= ctr->phase_end) return;
   const uint32_t n_r = ctr->n[r];
@@ -1264,11 +1266,20 @@ __global__ void __launch_bounds__(kBlock) k_hook_decide(View E, const unsigned l
         }
       }
       const unsigned bal = __ballot_sync(0xffffffffu, isroot);
-      if (lane == 0) masks[(uint64_t)tile * (kItems * kWarps) + k * kWarps + warp] = bal;
+      if (lane == 0) {
+        masks[(uint64_t)tile * (kItems * kWarps) + k * kWarps + warp] = bal;
+        s_slot[k * kWarps + warp] = __popc(bal);
+      }
       cnt += __popc(bal);
     }
     if (lane == 0) s_cnt[warp] = cnt;
     __syncthreads();
+    if (slotpref && warp == 0) {
+      // in-tile exclusive root prefix per (item, warp) slot, for k_label2
+      const uint32_t v = s_slot[lane];
+      const uint32_t incl = warp_incl_scan(v);
+      slotpref[(uint64_t)tile * 32 + lane] = incl - v;
+    }
     if (threadIdx.x == 0) {
       uint32_t t = 0;
 #pragma unroll
@@ -1342,6 +1353,93 @@ __global__ void __launch_bounds__(kBlock) k_hook_emit(const uint32_t* __restrict
       }
     }
     __syncthreads();
+  }
+}
+
+// ------------------------------ hook emit + label, fused -------------------
+// The dense label of a root is the number of roots before it; with the
+// hook's root masks, per-tile offsets (scanned counts) and in-tile slot
+// prefixes it is three small loads, so no separate kernel has to write
+// rootlabel[] first: k_label2 does k_hook_emit's MST slots and k_label's
+// relabel in one pass. Same outputs as k_hook_emit + k_label.
+__device__ __forceinline__ uint32_t roots_before(uint32_t x, const uint32_t* __restrict__ masks,
+                                                 const uint32_t* __restrict__ slotpref,
+                                                 const uint32_t* __restrict__ offsets) {
+  const uint32_t t = x / kTile, rem = x % kTile;
+  const uint32_t k = rem / kBlock, within = rem % kBlock;
+  const uint32_t slot = k * kWarps + (within >> 5), lane = within & 31;
+  const uint32_t m = __ldg(masks + (uint64_t)t * 32 + slot);
+  return __ldg(offsets + t) + __ldg(slotpref + (uint64_t)t * 32 + slot) + __popc(m & ((1u << lane) - 1u));
+}
+
+__global__ void __launch_bounds__(kBlock) k_label2(uint32_t* __restrict__ parent, const uint32_t* __restrict__ stash,
+                                                   const uint32_t* __restrict__ masks,
+                                                   const uint32_t* __restrict__ slotpref,
+                                                   const uint32_t* __restrict__ offsets, uint32_t* __restrict__ L,
+                                                   unsigned long long* __restrict__ min_next,
+                                                   uint32_t* __restrict__ mst, uint8_t* __restrict__ flags,
+                                                   uint32_t n_orig, DevCounters* ctr, int r,
+                                                   unsigned long long* pair_keys, unsigned long long pair_cap,
+                                                   unsigned int dedup_active) {
+  pdl_prologue();
+  if ((uint32_t)r >= ctr->stop_round || (uint32_t)r >= ctr->phase_end) return;
+  const bool labels = (uint32_t)r + 1 < ctr->stop_round;  // the last hook round only emits MST slots
+  const uint32_t n_r = ctr->n[r];
+  const uint32_t n_next = ctr->n[r + 1];
+  const uint32_t mst_base = n_orig - n_r;
+  if (labels && pair_keys) {
+    // pair dedup decision for this round's compaction + table clear (see
+    // "pair dedup"); tried when few active components carry many edges each
+    const unsigned long long K = ctr->active[r];
+    const unsigned long long m_r = ctr->m[r];
+    const bool use = K <= dedup_active && m_r >= 8 * K && m_r >= 4096;
+    unsigned long long P = 1024;
+    while (P < m_r / 4 && P < pair_cap) P <<= 1;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      ctr->dedup[r] = use ? 1u : 0u;
+      ctr->pair_mask[r] = P - 1;
+      ctr->pair_count[r] = 0;
+      ctr->pair_abort[r] = 0;
+    }
+    if (use)
+      for (unsigned long long i = (unsigned long long)blockIdx.x * kBlock + threadIdx.x; i < P;
+           i += (unsigned long long)gridDim.x * kBlock)
+        reinterpret_cast<ulonglong2*>(pair_keys)[i] = make_ulonglong2(~0ull, ~0ull);
+  }
+  const uint32_t ntiles = (uint32_t)(((uint64_t)n_r + kTile - 1) / kTile);
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint32_t lt = lanemask_lt();
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint32_t toff = __ldg(offsets + tile);
+    uint32_t c[kItems], root[kItems], own[kItems];
+    bool v[kItems], isroot[kItems];
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      c[k] = tile * kTile + k * kBlock + threadIdx.x;
+      v[k] = c[k] < n_r;
+      const uint32_t slot = k * kWarps + warp;
+      const uint32_t m = __ldg(masks + (uint64_t)tile * 32 + slot);
+      isroot[k] = (m >> lane) & 1u;
+      own[k] = toff + __ldg(slotpref + (uint64_t)tile * 32 + slot) + __popc(m & lt);
+    }
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      if (!v[k] || isroot[k]) continue;
+      const uint32_t eid = __ldg(stash + c[k]);
+      mst[mst_base + (c[k] - own[k])] = eid;
+      if (flags) flags[eid] = 1;
+    }
+    if (!labels) continue;
+    bool walk[kItems];
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) walk[k] = v[k] && !isroot[k];
+    find_roots<kItems>(parent, c, walk, root);
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      if (!v[k]) continue;
+      L[c[k]] = isroot[k] ? own[k] : roots_before(root[k], masks, slotpref, offsets);
+      if (c[k] < n_next) min_next[c[k]] = kNoKey;
+    }
   }
 }
 
