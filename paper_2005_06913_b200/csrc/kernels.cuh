@@ -98,6 +98,7 @@ struct SoaView {
   __device__ __forceinline__ EdgeRec gather(uint64_t i) const {
     return EdgeRec{__ldg(src + i), __ldg(dst + i), __ldg(w + i), base + (uint32_t)i, true};
   }
+  __device__ __forceinline__ uint32_t weight(uint64_t i) const { return __ldcs(w + i); }
 };
 
 // The reference's AoS Edge {u32 src, u32 dest, u64 weight} (graph.hpp:41-45).
@@ -113,6 +114,9 @@ struct AosView {
     const uint4 v = __ldg(e + i);
     return EdgeRec{v.x, v.y, v.z, base + (uint32_t)i, v.w == 0};
   }
+  __device__ __forceinline__ uint32_t weight(uint64_t i) const {
+    return __ldcs(reinterpret_cast<const uint32_t*>(e + i) + 2);
+  }
 };
 
 // Compacted edges of round >= 2: {a, b, w, eid} (16 B/edge, one LDG.128).
@@ -127,6 +131,10 @@ struct PackedView {
     const uint4 v = __ldg(e + i);
     return EdgeRec{v.x, v.y, v.z, v.w, true};
   }
+  __device__ __forceinline__ uint32_t weight(uint64_t i) const {
+    return __ldcs(reinterpret_cast<const uint32_t*>(e + i) + 2);
+  }
+  static constexpr uint32_t base = 0;
 };
 
 // ------------------------------ primitives ---------------------------------
@@ -965,7 +973,12 @@ __global__ void __launch_bounds__(kBlock) k_count(View in, uint4* __restrict__ r
         } else if (ok) {
           const uint32_t x = __ldg(L + e[k].a), y = __ldg(L + e[k].b);
           keep[k] = x != y;
-          if (!View::kOriginal) __stcs(reinterpret_cast<uint2*>(relabeled + i), make_uint2(x, y));
+          if (View::kOriginal)
+            __stcs(reinterpret_cast<uint2*>(relabeled) + i, make_uint2(x, y));
+          else
+            __stcs(reinterpret_cast<uint2*>(relabeled + i), make_uint2(x, y));
+        } else if (View::kOriginal && kMode == kModeRelabel) {
+          __stcs(reinterpret_cast<uint2*>(relabeled) + i, make_uint2(0, 0));  // rejected edge: a self-loop
         }
       }
       bal[k] = __ballot_sync(0xffffffffu, keep[k]);
@@ -1043,12 +1056,11 @@ __global__ void __launch_bounds__(kBlock) k_emit(View in, const uint4* __restric
       const uint64_t i = (uint64_t)tile * kCTile + k * kBlock + threadIdx.x;
       e[k] = make_uint4(0, 0, 0, 0);
       if (kMode == kModeRelabel && View::kOriginal) {
-        // plain round 1: re-read the caller's list and re-gather the labels
-        // (cheaper than writing + reading a relabelled 16 B copy)
+        // plain round 1: the count pass left the new endpoint labels as an
+        // 8 B pair per edge; weight from the caller's list, id = position
         if (i < m_r) {
-          const EdgeRec x = in.stream(i);
-          const bool ok = x.a < n_orig && x.b < n_orig && x.ok;
-          e[k] = ok ? make_uint4(__ldg(L + x.a), __ldg(L + x.b), x.w, x.eid) : make_uint4(0, 0, 0, 0);
+          const uint2 xy = __ldcs(reinterpret_cast<const uint2*>(relabeled) + i);
+          e[k] = make_uint4(xy.x, xy.y, in.weight(i), in.base + (uint32_t)i);
         }
       } else if (kMode == kModeRelabel) {
         if (i < m_r) e[k] = __ldcs(relabeled + i);
