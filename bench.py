@@ -12,7 +12,7 @@ m / MST wall time (BASELINE.json), whole job over all ranks.
   (a 512 MiB write) between timed steps; max over ranks.
 * e2e: the same MST through the public API with HOST (pinned) edge arrays:
   H2D of src/dst/w and D2H of the sorted ids inside the timed region.
-* roofline: the edge-pass kernels (k_min_round1 + k_compact), algorithmic
+* roofline: the edge-pass kernels (k_min_round1, k_count, k_emit), algorithmic
   bytes per SURVEY.md §8(d) (12 B/edge round 1, 16 B/live edge later,
   +16 B/kept edge) over their CUDA-event time, against MEASURED_PEAKS.json.
 * cpu_baseline: the unchanged reference boruvka_cas (oracle/_ref) on the

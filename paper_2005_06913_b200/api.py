@@ -221,7 +221,7 @@ def boruvka_gpu_aos(n: int, edges: np.ndarray, info: GpuRunInfo | None = None) -
 
 
 def boruvka_gpu_emulated(g: Graph, shards: int, info: GpuRunInfo | None = None) -> MstResult:
-    """The multi-GPU (sharded, partner-label key) algorithm with `shards` edge
+    """The multi-GPU (sharded, exchanged-key) algorithm with `shards` edge
     shards emulated on the current GPU; used to test the sharded protocol."""
     lib = L.lib()
     e = L.MstEdgesSoa(g.n, g.edge_count(), _ptr(g.src), _ptr(g.dst), _ptr(g.w), 0)
@@ -248,7 +248,7 @@ def boruvka_gpu_device(n: int, m: int, src_ptr: int, dst_ptr: int, w_ptr: int, o
 
     Returns (count, total_weight). With ``hot`` a dict, fills
     ``hot['ms']``/``hot['launches']`` with the summed CUDA-event time and
-    launch count of the edge-pass kernels (k_min_round1 + k_compact).
+    launch count of the edge-pass kernels (k_min_round1, k_count, k_emit).
     """
     lib = L.lib()
     e = L.MstEdgesSoa(n, m, src_ptr, dst_ptr, w_ptr, 1)

@@ -489,7 +489,7 @@ void launch_two_pass(Workspace& ws, const CompactBufs& cb, View in, uint4* relab
   const unsigned gc = (unsigned)std::max<uint64_t>(
       1, std::min<uint64_t>(tiles, (uint64_t)sm_count(dev) * blocks_per_sm(kcnt)));
   // armed: this launch relabels + inserts pairs if the device chose dedup
-  // (decided and table cleared by k_label), the kModeDedup pass counts
+  // (decided and table cleared by k_label2), the kModeDedup pass counts
   launch_k(kcnt, gc, kBlock, ws.stream, in, kMode == kModeRelabel ? relabeled : cb.stage, L, cb.masks, cb.counts, n_orig,
                                      d_ctr, r, fused, slot, light, pt);
   if constexpr (!View::kOriginal) {
@@ -535,7 +535,6 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   uint32_t* mst = ws.get<uint32_t>("mst", n);
   uint4* E[2] = {ws.get<uint4>("E0", m), ws.get<uint4>("E1", m)};
   unsigned long long* st = ws.status_array(std::max(tiles_of(m), tiles_of(n)));
-  const Recover no_rec{nullptr, nullptr, nullptr};
   const int dev = ws.device;
   const CompactBufs cb{ws.get<uint32_t>("tile_counts", tiles_c(m)),
                        ws.get<uint32_t>("tile_masks", tiles_c(m) * kCItems * kWarps), st,
@@ -543,7 +542,6 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   uint32_t* hcounts = ws.get<uint32_t>("hook_counts", tiles_of(n));
   uint32_t* hmasks = ws.get<uint32_t>("hook_masks", tiles_of(n) * kItems * kWarps);
   uint32_t* hslot = ws.get<uint32_t>("hook_slotpref", tiles_of(n) * kItems * kWarps);
-  (void)no_rec;
 
   init_counters(ws, d_ctr, n, m);
   MST_CUDA_CHECK(cudaMemsetAsync(minb[0], 0xFF, (size_t)n * 8, s));
@@ -577,7 +575,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     tmark();
     launches += 2;
   } else {
-    auto kmin = k_min_round1<InView, false, kPre>;
+    auto kmin = k_min_round1<InView, kPre>;
     const unsigned g = (unsigned)std::max<uint64_t>(
         1, std::min<uint64_t>((m + 4 * kBlock - 1) / (4 * kBlock), (uint64_t)sm_count(dev) * blocks_per_sm(kmin)));
     hot_begin(kHotMin1, 0, false);
@@ -714,7 +712,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       Lr = ws.get<uint32_t>("Llvl" + std::to_string(r), n_bound);
       levels.push_back({Lr, r});
     }
-    // pair dedup is armed for big rounds; k_label decides on the device
+    // pair dedup is armed for big rounds; k_label2 decides on the device
     PairTable pt{nullptr, nullptr, 0};
     if (!original_in && dedup_on && m_bound >= dedup_min_edges) {
       const unsigned long long cap = std::min<unsigned long long>(1ull << 25, next_pow2(m_bound / 2));
@@ -947,9 +945,10 @@ RunOut run_single(const SingleArgs& a, mst_stats_t* stats) {
 }
 
 // ------------------------------- sharded (multi-GPU) ------------------------
-// Partner-label keys (w<<32 | partner component): after the min exchange
-// every shard can hook without seeing the winning edge; the shard that owns
-// the edge recovers its global id during its next compaction pass.
+// Edge-sharded, component state replicated (kernels.cuh, "sharded exchange"):
+// every shard runs the same hook/label on the all-reduced (w, global id) keys
+// and partner labels, so the MST ids, labels and verdicts agree everywhere and
+// only the local edge lists differ.
 
 struct Shard {
   Workspace* ws = nullptr;
@@ -957,8 +956,8 @@ struct Shard {
   uint32_t base = 0;     // global id of local edge 0
   SoaView in{};
   unsigned long long* minb[2]{};
-  uint32_t *parent = nullptr, *rootlabel = nullptr, *L = nullptr, *mstpos = nullptr,
-           *slots = nullptr;
+  unsigned long long *xch = nullptr, *own = nullptr;
+  uint32_t *parent = nullptr, *rootlabel = nullptr, *L = nullptr, *partner = nullptr, *mst = nullptr;
   uint4* E[2]{};
   DevCounters* d_ctr = nullptr;
   unsigned long long* st = nullptr;
@@ -966,53 +965,47 @@ struct Shard {
 
 struct Exchanger {
   virtual ~Exchanger() = default;
-  virtual void min_u64(std::vector<Shard>& sh, int which, uint64_t count) = 0;
-  virtual void min_u32_slots(std::vector<Shard>& sh, uint64_t count) = 0;
+  virtual void min_u64(std::vector<Shard>& sh, unsigned long long* Shard::*buf, uint64_t count) = 0;
+  virtual void min_u32(std::vector<Shard>& sh, uint32_t* Shard::*buf, uint64_t count) = 0;
 };
 
 // All shards on one device, one stream: an element-wise min kernel.
 struct EmulatedExchanger : Exchanger {
-  void min_u64(std::vector<Shard>& sh, int which, uint64_t count) override {
+  template <class T>
+  static void run(std::vector<Shard>& sh, T* Shard::*buf, uint64_t count) {
     if (sh.size() == 1 || count == 0) return;
-    ShardPtrs<unsigned long long, 8> p{};
-    for (size_t i = 0; i < sh.size(); ++i) p.p[i] = sh[i].minb[which];
-    k_shard_min<unsigned long long><<<(unsigned)std::min<uint64_t>((count + 255) / 256, 4096), 256, 0,
-                                      sh[0].ws->stream>>>(p, (int)sh.size(), count);
+    ShardPtrs<T, 8> p{};
+    for (size_t i = 0; i < sh.size(); ++i) p.p[i] = sh[i].*buf;
+    k_shard_min<T><<<(unsigned)std::min<uint64_t>((count + 255) / 256, 4096), 256, 0, sh[0].ws->stream>>>(
+        p, (int)sh.size(), count);
     MST_CUDA_CHECK(cudaGetLastError());
   }
-  void min_u32_slots(std::vector<Shard>& sh, uint64_t count) override {
-    if (sh.size() == 1 || count == 0) return;
-    ShardPtrs<uint32_t, 8> p{};
-    for (size_t i = 0; i < sh.size(); ++i) p.p[i] = sh[i].slots;
-    k_shard_min<uint32_t><<<(unsigned)std::min<uint64_t>((count + 255) / 256, 4096), 256, 0,
-                            sh[0].ws->stream>>>(p, (int)sh.size(), count);
-    MST_CUDA_CHECK(cudaGetLastError());
+  void min_u64(std::vector<Shard>& sh, unsigned long long* Shard::*buf, uint64_t count) override {
+    run(sh, buf, count);
   }
+  void min_u32(std::vector<Shard>& sh, uint32_t* Shard::*buf, uint64_t count) override { run(sh, buf, count); }
 };
 
 // NCCL: one communicator per shard (single process driving several GPUs via
 // ncclCommInitAll, or one rank per process via ncclCommInitRank).
 struct NcclExchanger : Exchanger {
   std::vector<ncclComm_t> comms;
-  void min_u64(std::vector<Shard>& sh, int which, uint64_t count) override {
+  template <class T>
+  void run(std::vector<Shard>& sh, T* Shard::*buf, uint64_t count, ncclDataType_t type) {
     if (count == 0) return;
     MST_NCCL_CHECK(nccl().GroupStart());
     for (size_t i = 0; i < sh.size(); ++i) {
       MST_CUDA_CHECK(cudaSetDevice(sh[i].ws->device));
-      MST_NCCL_CHECK(nccl().AllReduce(sh[i].minb[which], sh[i].minb[which], count, ncclUint64, ncclMin,
-                                      comms[i], sh[i].ws->stream));
+      T* p = sh[i].*buf;
+      MST_NCCL_CHECK(nccl().AllReduce(p, p, count, type, ncclMin, comms[i], sh[i].ws->stream));
     }
     MST_NCCL_CHECK(nccl().GroupEnd());
   }
-  void min_u32_slots(std::vector<Shard>& sh, uint64_t count) override {
-    if (count == 0) return;
-    MST_NCCL_CHECK(nccl().GroupStart());
-    for (size_t i = 0; i < sh.size(); ++i) {
-      MST_CUDA_CHECK(cudaSetDevice(sh[i].ws->device));
-      MST_NCCL_CHECK(nccl().AllReduce(sh[i].slots, sh[i].slots, count, ncclUint32, ncclMin, comms[i],
-                                      sh[i].ws->stream));
-    }
-    MST_NCCL_CHECK(nccl().GroupEnd());
+  void min_u64(std::vector<Shard>& sh, unsigned long long* Shard::*buf, uint64_t count) override {
+    run(sh, buf, count, ncclUint64);
+  }
+  void min_u32(std::vector<Shard>& sh, uint32_t* Shard::*buf, uint64_t count) override {
+    run(sh, buf, count, ncclUint32);
   }
 };
 
@@ -1024,14 +1017,10 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, RunOu
     MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
     init_counters(*s.ws, s.d_ctr, n, s.m);
     MST_CUDA_CHECK(cudaMemsetAsync(s.minb[0], 0xFF, (size_t)n * 8, s.ws->stream));
-    MST_CUDA_CHECK(cudaMemsetAsync(s.slots, 0xFF, (size_t)n * 4, s.ws->stream));
-    auto kmin = k_min_round1<SoaView, true, kPre>;
-    const unsigned g = (unsigned)std::max<uint64_t>(
-        1, std::min<uint64_t>((s.m + kBlock - 1) / kBlock,
-                              (uint64_t)sm_count(s.ws->device) * blocks_per_sm(kmin)));
-    kmin<<<g, kBlock, 0, s.ws->stream>>>(s.in, n, s.m, s.minb[0], s.d_ctr, filt_for(n));
+    auto kmin = k_min_round1<SoaView, kPre>;
+    launch_k(kmin, persistent_grid(kmin, s.ws->device, (s.m + kBlock - 1) / kBlock), kBlock, s.ws->stream, s.in, n, s.m,
+             s.minb[0], s.d_ctr, filt_for(n));
     ++launches;
-    MST_CUDA_CHECK(cudaGetLastError());
   }
   // errors (range) are checked before the first exchange
   for (auto& s : sh) {
@@ -1044,48 +1033,68 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, RunOu
       return;
     }
   }
-  ex.min_u64(sh, 0, n);
   uint64_t n_bound = n;
   int r = 1;
   int stop = 0;
   while (true) {
-    if (r > MST_MAX_ROUNDS) throw MstError{MST_ERR_STALL, "no convergence within MST_MAX_ROUNDS rounds"};
-    const int cur = (r - 1) & 1, nxt = r & 1;
+    if (r >= MST_MAX_ROUNDS) throw MstError{MST_ERR_STALL, "no convergence within MST_MAX_ROUNDS rounds"};
+    // 1. local literal keys -> (w, global id) keys + owned partners; exchange
+    for (auto& s : sh) {
+      MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
+      const uint64_t t = (n_bound + kBlock - 1) / kBlock;
+      if (r == 1) {
+        auto kk = k_shard_keys<SoaView>;
+        launch_k(kk, persistent_grid(kk, s.ws->device, t), kBlock, s.ws->stream, s.in, s.minb[0], s.xch, s.own, s.d_ctr, r);
+      } else {
+        auto kk = k_shard_keys<PackedView>;
+        launch_k(kk, persistent_grid(kk, s.ws->device, t), kBlock, s.ws->stream, PackedView{s.E[r & 1]},
+                 s.minb[(r - 1) & 1], s.xch, s.own, s.d_ctr, r);
+      }
+    }
+    ex.min_u64(sh, &Shard::xch, n_bound);
+    for (auto& s : sh) {
+      MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
+      launch_k(k_shard_partner, persistent_grid(k_shard_partner, s.ws->device, (n_bound + kBlock - 1) / kBlock), kBlock,
+               s.ws->stream, s.xch, s.own, s.partner, s.d_ctr, r);
+    }
+    ex.min_u32(sh, &Shard::partner, n_bound);
+    launches += 2;
+    // 2. replicated hook + label, local compaction (as the single-device loop)
     for (auto& s : sh) {
       MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
       Workspace& ws = *s.ws;
-      const uint32_t ep_h = ws.next_epoch(), ep_c = ws.next_epoch();
-      if (r == 1) {
-        auto kh = k_hook<SoaView, true>;
-        kh<<<persistent_grid(kh, ws.device, tiles_of(n_bound)), kBlock, 0, ws.stream>>>(
-            s.in, s.minb[cur], s.parent, s.rootlabel, s.mstpos, n, s.d_ctr, r, s.st, ep_h, 0);
-      } else {
-        auto kh = k_hook<PackedView, true>;
-        kh<<<persistent_grid(kh, ws.device, tiles_of(n_bound)), kBlock, 0, ws.stream>>>(
-            PackedView{s.E[r & 1]}, s.minb[cur], s.parent, s.rootlabel, s.mstpos, n, s.d_ctr, r, s.st, ep_h, 0);
-      }
-      const unsigned gl = (unsigned)std::max<uint64_t>(
-          1, std::min<uint64_t>((n_bound + kBlock - 1) / kBlock,
-                                (uint64_t)sm_count(ws.device) * blocks_per_sm(k_label)));
-      k_label<<<gl, kBlock, 0, ws.stream>>>(s.parent, s.rootlabel, s.L, s.minb[nxt], s.d_ctr, r, nullptr, nullptr, 0,
-                                            0u);
-      MST_CUDA_CHECK(cudaMemcpyAsync(&ws.h_snap[r], s.d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost,
-                                     ws.stream));
-      MST_CUDA_CHECK(cudaEventRecord(ws.ev[r], ws.stream));
+      const int dev = ws.device;
+      cudaStream_t st = ws.stream;
+      const uint64_t ht = tiles_of(n_bound);
+      const int hfused = ht <= kFusedScanMaxTiles ? 1 : 0;
+      uint32_t* hcounts = ws.get<uint32_t>("hook_counts", tiles_of(n));
+      uint32_t* hmasks = ws.get<uint32_t>("hook_masks", tiles_of(n) * kItems * kWarps);
+      uint32_t* hslot = ws.get<uint32_t>("hook_slotpref", tiles_of(n) * kItems * kWarps);
+      auto kd = k_hook_decide<PartnerView, true>;
+      launch_k(kd, persistent_grid(kd, dev, ht), kBlock, st, PartnerView{s.partner}, s.xch, s.parent, s.rootlabel, hmasks,
+               hcounts, s.d_ctr, r, hfused, (int)kPhasePlain, hslot);
+      if (!hfused)
+        launch_k(k_scan_counts<kScanRoots>,
+                 (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((ht + kScanTile - 1) / kScanTile, (uint64_t)sm_count(dev))),
+                 kScanBlock, st, hcounts, ht, s.d_ctr, r, s.st, ws.next_epoch(), (int)kPhasePlain, 0);
+      unsigned long long* mnext = s.minb[r & 1];
+      launch_k(k_label2, persistent_grid(k_label2, dev, ht), kBlock, st, s.parent, s.rootlabel, hmasks, hslot, hcounts, s.L,
+               mnext, s.mst, (uint8_t*)nullptr, n, s.d_ctr, r, (unsigned long long*)nullptr, 0ull, 0u);
+      MST_CUDA_CHECK(cudaMemcpyAsync(&ws.h_snap[r], s.d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, st));
+      MST_CUDA_CHECK(cudaEventRecord(ws.ev[r], st));
       const uint64_t m_bound = r == 1 ? s.m : ws.h_snap[r - 1].m[r];
-      Recover rec{s.minb[cur], s.mstpos, s.slots};
-      uint4* Eout = s.E[(r - 1) & 1];
-      if (r == 1) {
-        auto kc = k_compact<SoaView, true, kPre, kFilterNone>;
-        kc<<<persistent_grid(kc, ws.device, tiles_c(m_bound)), kBlock, 0, ws.stream>>>(
-            s.in, Eout, s.L, s.minb[nxt], rec, n, s.d_ctr, r, s.st, ep_c, kSlotCompact, 0, filt_for(n_bound));
-      } else {
-        auto kc = k_compact<PackedView, true, kPre, kFilterNone>;
-        kc<<<persistent_grid(kc, ws.device, tiles_c(m_bound)), kBlock, 0, ws.stream>>>(
-            PackedView{s.E[r & 1]}, Eout, s.L, s.minb[nxt], rec, n, s.d_ctr, r, s.st, ep_c, kSlotCompact, 0,
-            filt_for(n_bound));
-      }
-      launches += 3;
+      const CompactBufs cb{ws.get<uint32_t>("tile_counts", tiles_c(s.m)),
+                           ws.get<uint32_t>("tile_masks", tiles_c(s.m) * kCItems * kWarps), s.st,
+                           ws.get<uint4>("stage", kCTile)};
+      uint4* Eout = s.E[(r + 1) & 1];
+      if (r == 1)
+        launch_two_pass<SoaView, kModeRelabel, kPre>(ws, cb, s.in, s.E[1], s.L, Eout, mnext, s.d_ctr, r, m_bound, n,
+                                                     kSlotCompact, (int)kPhaseSharded, filt_for(n_bound));
+      else
+        launch_two_pass<PackedView, kModeRelabel, kPre>(ws, cb, PackedView{s.E[r & 1]}, s.E[r & 1], s.L, Eout, mnext,
+                                                        s.d_ctr, r, m_bound, n, kSlotCompact, (int)kPhaseSharded,
+                                                        filt_for(n_bound));
+      launches += 5;
       MST_CUDA_CHECK(cudaGetLastError());
     }
     // verdict after label (identical on every shard: replicated hook)
@@ -1105,21 +1114,14 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, RunOu
       stop = (int)verdict;
       break;
     }
-    // compaction of round r writes min_next; the snapshot after label gave
-    // n_{r+1}, the exchange size
+    // the compaction's kept count m[r+1] sizes the next round's passes
     for (auto& s : sh) {
       MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
       MST_CUDA_CHECK(cudaMemcpyAsync(&s.ws->h_snap[r], s.d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost,
                                      s.ws->stream));
-    }
-    ex.min_u64(sh, nxt, n_next);
-    n_bound = n_next;
-    for (auto& s : sh) {
-      MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
       MST_CUDA_CHECK(cudaStreamSynchronize(s.ws->stream));
-      // a compaction can also end the loop (no edges left anywhere is only
-      // visible globally; the next hook sees isolated components and stops)
     }
+    n_bound = n_next;
     ++r;
   }
   for (auto& s : sh) {
@@ -1186,11 +1188,13 @@ RunOut run_sharded(const std::vector<PartSpec>& parts, Exchanger& ex, uint32_t n
     s.in = SoaView{src, dst, w, s.base};
     s.minb[0] = ws.get<unsigned long long>("minA", n);
     s.minb[1] = ws.get<unsigned long long>("minB", n);
+    s.xch = ws.get<unsigned long long>("xch", n);
+    s.own = ws.get<unsigned long long>("own", n);
     s.parent = ws.get<uint32_t>("parent", n);
     s.rootlabel = ws.get<uint32_t>("rootlabel", n);
     s.L = ws.get<uint32_t>("label", n);
-    s.mstpos = ws.get<uint32_t>("mstpos", n);
-    s.slots = ws.get<uint32_t>("mst", n);
+    s.partner = ws.get<uint32_t>("partner", n);
+    s.mst = ws.get<uint32_t>("mst", n);
     s.E[0] = ws.get<uint4>("E0", s.m);
     s.E[1] = ws.get<uint4>("E1", s.m);
     s.d_ctr = ws.get<DevCounters>("ctr", 1);
@@ -1206,11 +1210,10 @@ RunOut run_sharded(const std::vector<PartSpec>& parts, Exchanger& ex, uint32_t n
   else
     run_sharded_rounds<false>(sh, ex, n, o);
   check_err_bits(o.err);
-  ex.min_u32_slots(sh, o.count);
   Workspace& ws0 = *sh[0].ws;
   MST_CUDA_CHECK(cudaSetDevice(ws0.device));
   uint32_t* d_sorted = ws0.get<uint32_t>("sorted", n);
-  o.launches += sort_ids(ws0, sh[0].slots, o.count, std::max<uint64_t>(m_total, 1), d_sorted, sh[0].d_ctr);
+  o.launches += sort_ids(ws0, sh[0].mst, o.count, std::max<uint64_t>(m_total, 1), d_sorted, sh[0].d_ctr);
   MST_CUDA_CHECK(cudaEventRecord(e2, ws0.stream));
   if (o.count && out_ids)
     copy_d2h(ws0, out_ids, d_sorted, o.count * 4);
@@ -1481,8 +1484,8 @@ int mst_gpu_round1_min(const mst_edges_soa_t* edges, uint64_t* out_min) {
     auto* mn = ws.get<unsigned long long>("minA", n);
     init_counters(ws, d_ctr, n, m);
     MST_CUDA_CHECK(cudaMemsetAsync(mn, 0xFF, (size_t)n * 8, ws.stream));
-    auto kmin = warp_prereduce_enabled() ? k_min_round1<SoaView, false, true>
-                                         : k_min_round1<SoaView, false, false>;
+    auto kmin = warp_prereduce_enabled() ? k_min_round1<SoaView, true>
+                                         : k_min_round1<SoaView, false>;
     const unsigned g = (unsigned)std::max<uint64_t>(
         1, std::min<uint64_t>((m + 4 * kBlock - 1) / (4 * kBlock), (uint64_t)sm_count(dev) * blocks_per_sm(kmin)));
     kmin<<<g, kBlock, 0, ws.stream>>>(SoaView{src, dst, w, 0}, n, m, mn, d_ctr, filt_for(n));

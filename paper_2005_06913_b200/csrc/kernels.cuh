@@ -1,25 +1,29 @@
 // Device kernels of the B200 parallel Boruvka (arXiv 2005.06913, CAS variant
 // re-designed for the GPU). One round r with n_r live components (dense
-// labels 0..n_r-1) and m_r live edges runs three kernels:
+// labels 0..n_r-1) and m_r live edges:
 //
-//   k_hook    (n_r)  every component reads its lightest edge key, picks the
-//                    partner, breaks mutual 2-cycles by lower label, emits its
-//                    MST edge and flags roots; a decoupled look-back scan over
-//                    the root flags assigns the next round's dense labels.
-//                    Replaces the merge phase + try_union_cas
-//                    (boruvka_parallel.cpp:176-227, union_find.cpp:75-92).
-//   k_label  (n_r)   root finding with concurrent path halving over the hook
-//                    forest (the reference's find walk, union_find.cpp:28-35)
-//                    and the dense relabel; clears the next min table.
-//   k_compact (m_r)  relabels both endpoints, drops intra-component edges
-//                    (the covered flags, graph.hpp:62-67), writes the kept
-//                    edges in order (ballot + block scan + decoupled
-//                    look-back) and, fused, offers every kept edge to both
-//                    endpoint components of round r+1 with a filtered 64-bit
-//                    atomicMin (the edge scan + offer,
-//                    boruvka_parallel.cpp:150-167).
+//   k_hook_decide (n_r)  every component reads its lightest edge key, picks
+//                        the partner, breaks mutual 2-cycles by lower label,
+//                        flags roots and counts them per tile. Replaces the
+//                        merge phase + try_union_cas (boruvka_parallel.cpp:
+//                        176-227, union_find.cpp:75-92).
+//   k_label2      (n_r)  MST slot n - n_r + c - roots_before(c) for every
+//                        hooked component, root finding with concurrent path
+//                        halving over the hook forest (the reference's find
+//                        walk, union_find.cpp:28-35), dense relabel, clears
+//                        the next min table.
+//   k_count       (m_r)  relabels both endpoints, drops intra-component
+//                        edges (the covered flags, graph.hpp:62-67), counts
+//                        the kept edges per tile.
+//   k_emit        (m_r)  writes the kept edges in order and offers each to
+//                        both endpoint components of round r+1 with a
+//                        filtered 64-bit atomicMin (the edge scan + offer,
+//                        boruvka_parallel.cpp:150-167).
 //
-// Round 1 reads the caller's edge list directly (k_min_round1 + k_compact).
+// Round 1 reads the caller's edge list directly (k_min_round1 + the two
+// passes over the original view). Filter-Boruvka, pair dedup, the tail
+// megakernel, the sorted output and the sharded exchange are described at
+// their kernels below.
 #pragma once
 
 #include <cooperative_groups.h>
@@ -216,56 +220,6 @@ __device__ __forceinline__ uint32_t lookback(unsigned long long* status, uint32_
   return excl;
 }
 
-// Ordered ranks of per-item flags over a striped tile (item k of thread t
-// is tile element k*kBlock + t), with the tile's global exclusive prefix
-// from the look-back. s_scan: kIt*kWarps words of smem; s_misc: 2 words.
-template <int kIt>
-__device__ __forceinline__ void tile_flag_scan(const bool (&flag)[kIt], uint32_t (&rank)[kIt],
-                                               uint32_t* s_scan, uint32_t* s_misc,
-                                               unsigned long long* status, uint32_t tile,
-                                               uint32_t epoch, uint32_t& prefix, uint32_t& total) {
-  constexpr int kSlots = kIt * kWarps;
-  constexpr int kPer = (kSlots + 31) / 32;  // slots per lane in the warp-0 scan
-  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-  unsigned bal[kIt];
-#pragma unroll
-  for (int k = 0; k < kIt; ++k) {
-    bal[k] = __ballot_sync(0xffffffffu, flag[k]);
-    if (lane == 0) s_scan[k * kWarps + warp] = __popc(bal[k]);
-  }
-  __syncthreads();
-  if (warp == 0) {
-    uint32_t v[kPer];
-    uint32_t sum = 0;
-#pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-      const int idx = lane * kPer + j;
-      v[j] = idx < kSlots ? s_scan[idx] : 0u;
-      sum += v[j];
-    }
-    const uint32_t incl = warp_incl_scan(sum);
-    uint32_t run = incl - sum;
-#pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-      const int idx = lane * kPer + j;
-      if (idx < kSlots) s_scan[idx] = run;
-      run += v[j];
-    }
-    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-    const uint32_t ex = lookback(status, tile, tot, epoch);
-    if (lane == 0) {
-      s_misc[0] = ex;
-      s_misc[1] = tot;
-    }
-  }
-  __syncthreads();
-  prefix = s_misc[0];
-  total = s_misc[1];
-  const uint32_t lt = lanemask_lt();
-#pragma unroll
-  for (int k = 0; k < kIt; ++k) rank[k] = s_scan[k * kWarps + warp] + __popc(bal[k] & lt);
-}
-
 // Filtered 64-bit min: read first (a stale read is never below the true
 // value, so skipping is always safe), atomic only when it can win. With
 // kWarpPre, lanes of a warp that target the same component first reduce
@@ -351,10 +305,9 @@ __device__ __forceinline__ uint32_t find_root(uint32_t* parent, uint32_t c) {
 
 // ------------------------------ round 1 ------------------------------------
 
-// Lightest incident edge per vertex over the caller's list. kKeyPartner
-// selects the sharded key (w<<32 | partner vertex) instead of the literal
-// (w<<32 | local index); both are decided by the weight (distinct weights).
-template <class View, bool kKeyPartner, bool kWarpPre>
+// Lightest incident edge per vertex over the caller's list, literal keys
+// (w<<32 | index in the list).
+template <class View, bool kWarpPre>
 __global__ void __launch_bounds__(kBlock) k_min_round1(View v, uint32_t n, uint64_t m,
                                                        unsigned long long* __restrict__ minimum,
                                                        DevCounters* ctr, int filt) {
@@ -385,297 +338,15 @@ __global__ void __launch_bounds__(kBlock) k_min_round1(View v, uint32_t n, uint6
           valid = false;  // self-loop: never in an MST
         }
       }
-      const uint64_t hi = (uint64_t)e[k].w << 32;
-      const uint64_t ka = kKeyPartner ? (hi | e[k].b) : (hi | (uint32_t)i);
-      const uint64_t kb = kKeyPartner ? (hi | e[k].a) : (hi | (uint32_t)i);
-      offer<kWarpPre>(minimum, e[k].a, ka, valid, filt);
-      offer<kWarpPre>(minimum, e[k].b, kb, valid, filt);
+      const uint64_t key = ((uint64_t)e[k].w << 32) | (uint32_t)i;
+      offer<kWarpPre>(minimum, e[k].a, key, valid, filt);
+      offer<kWarpPre>(minimum, e[k].b, key, valid, filt);
     }
   }
   if (err) atomicOr(&ctr->err, err);
 }
 
-// ------------------------------ hook ---------------------------------------
-
-// kKeyPartner = false: key low word indexes the round's edge array (E).
-// kKeyPartner = true:  key low word is the partner label (sharded mode).
-template <class View, bool kKeyPartner>
-__global__ void __launch_bounds__(kBlock) k_hook(View E, const unsigned long long* __restrict__ minimum,
-                                                 uint32_t* __restrict__ parent,
-                                                 uint32_t* __restrict__ rootlabel,
-                                                 uint32_t* __restrict__ mst_or_pos, uint32_t n_orig,
-                                                 DevCounters* ctr, int r,
-                                                 unsigned long long* status, uint32_t epoch,
-                                                 int light_phase) {
-  pdl_prologue();
-  __shared__ uint32_t s_scan[32];
-  __shared__ uint32_t s_misc[2];
-  __shared__ uint32_t s_tile;
-  __shared__ unsigned long long s_wsum[kWarps];
-  if ((uint32_t)r >= ctr->stop_round || (uint32_t)r >= ctr->phase_end) return;
-  const uint32_t n_r = ctr->n[r];
-  const uint32_t mst_base = n_orig - n_r;
-  const uint32_t ntiles = (uint32_t)(((uint64_t)n_r + kTile - 1) / kTile);
-  unsigned long long wsum = 0;
-  while (true) {
-    if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->tile[r][kSlotHook], 1u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
-    if (tile >= ntiles) break;
-    bool isroot[kItems];
-    uint32_t part[kItems], eidv[kItems], wv[kItems];
-#pragma unroll
-    for (int k = 0; k < kItems; ++k) {
-      const uint64_t c = (uint64_t)tile * kTile + k * kBlock + threadIdx.x;
-      isroot[k] = false;
-      part[k] = kNone;
-      eidv[k] = 0;
-      wv[k] = 0;
-      if (c < n_r) {
-        const unsigned long long key = minimum[c];
-        if (key == kNoKey) {
-          isroot[k] = true;  // no live edge: isolated component
-        } else {
-          const uint32_t w = (uint32_t)(key >> 32);
-          uint32_t o;
-          unsigned long long mutual_key;
-          if (kKeyPartner) {
-            o = (uint32_t)key;
-            mutual_key = ((unsigned long long)w << 32) | (uint32_t)c;
-          } else {
-            const EdgeRec e = E.gather((uint32_t)key);
-            o = (e.a == (uint32_t)c) ? e.b : e.a;
-            mutual_key = key;
-            eidv[k] = e.eid;
-          }
-          const bool mutual = __ldg(minimum + o) == mutual_key;
-          isroot[k] = mutual && (uint32_t)c < o;
-          part[k] = o;
-          wv[k] = w;
-        }
-      }
-    }
-    uint32_t rank[kItems], prefix, total;
-    tile_flag_scan<kItems>(isroot, rank, s_scan, s_misc, status, tile, epoch, prefix, total);
-#pragma unroll
-    for (int k = 0; k < kItems; ++k) {
-      const uint64_t c = (uint64_t)tile * kTile + k * kBlock + threadIdx.x;
-      if (c < n_r) {
-        const uint32_t roots_before = prefix + rank[k];
-        if (isroot[k]) {
-          parent[c] = (uint32_t)c;
-          rootlabel[c] = roots_before;
-          if (kKeyPartner) mst_or_pos[c] = kNone;
-        } else {
-          parent[c] = part[k];
-          const uint32_t pos = mst_base + ((uint32_t)c - roots_before);
-          if (kKeyPartner)
-            mst_or_pos[c] = pos;
-          else
-            mst_or_pos[pos] = eidv[k];
-          wsum += wv[k];
-        }
-      }
-    }
-    if (tile == ntiles - 1 && threadIdx.x == 0) {
-      const uint32_t roots = prefix + total;
-      ctr->n[r + 1] = roots;
-      if (roots <= 1) {
-        ctr->stop_round = (uint32_t)r + 1;
-      } else if (roots == n_r) {
-        // no live edge anywhere: done (a forest if roots > 1), unless this is
-        // the light phase of Filter-Boruvka, which then simply ends
-        if (light_phase)
-          ctr->phase_end = (uint32_t)r;
-        else
-          ctr->stop_round = (uint32_t)r + 1;
-      }
-    }
-    __syncthreads();
-  }
-  wsum = warp_sum<unsigned long long>(wsum);
-  if (lane_id() == 0) s_wsum[threadIdx.x >> 5] = wsum;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long t = 0;
-    for (int i = 0; i < kWarps; ++i) t += s_wsum[i];
-    if (t) atomicAdd(&ctr->total_weight, t);
-  }
-}
-
-// ------------------------------ label --------------------------------------
-
-__global__ void __launch_bounds__(kBlock) k_label(uint32_t* __restrict__ parent,
-                                                  const uint32_t* __restrict__ rootlabel,
-                                                  uint32_t* __restrict__ L,
-                                                  unsigned long long* __restrict__ min_next,
-                                                  DevCounters* ctr, int r, unsigned long long* pair_keys,
-                                                  unsigned long long* pair_mins, unsigned long long pair_cap,
-                                                  unsigned int dedup_active) {
-  pdl_prologue();
-  if ((uint32_t)r + 1 >= ctr->stop_round || (uint32_t)r >= ctr->phase_end) return;
-  const uint32_t n_r = ctr->n[r];
-  const uint32_t n_next = ctr->n[r + 1];
-  if (pair_keys) {
-    // Pair dedup (see "pair dedup" below): decide for this round's compaction
-    // and clear the table. Tried when few active components carry many edges
-    // each; the table takes m_r/8 distinct pairs at half load, more aborts
-    // the attempt (the round then compacts like a plain one).
-    const unsigned long long K = ctr->active[r];
-    const unsigned long long m_r = ctr->m[r];
-    const bool use = K <= dedup_active && m_r >= 8 * K && m_r >= 4096;
-    unsigned long long P = 1024;
-    while (P < m_r / 4 && P < pair_cap) P <<= 1;
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      ctr->dedup[r] = use ? 1u : 0u;
-      ctr->pair_mask[r] = P - 1;
-      ctr->pair_count[r] = 0;
-      ctr->pair_abort[r] = 0;
-    }
-    if (use)
-      for (unsigned long long i = (unsigned long long)blockIdx.x * kBlock + threadIdx.x; i < P;
-           i += (unsigned long long)gridDim.x * kBlock) {
-        reinterpret_cast<ulonglong2*>(pair_keys)[i] = make_ulonglong2(~0ull, ~0ull);
-      }
-  }
-  constexpr int kU = 4;
-  const uint64_t stride = (uint64_t)gridDim.x * kBlock * kU;
-  for (uint64_t base = (uint64_t)blockIdx.x * kBlock * kU; base < n_r; base += stride) {
-    uint32_t c[kU], root[kU];
-    bool v[kU];
-#pragma unroll
-    for (int k = 0; k < kU; ++k) {
-      c[k] = (uint32_t)(base + k * kBlock + threadIdx.x);
-      v[k] = base + k * kBlock + threadIdx.x < n_r;
-    }
-    find_roots<kU>(parent, c, v, root);
-#pragma unroll
-    for (int k = 0; k < kU; ++k) {
-      if (!v[k]) continue;
-      L[c[k]] = __ldcg(rootlabel + root[k]);
-      if (c[k] < n_next) min_next[c[k]] = kNoKey;
-    }
-  }
-}
-
-// ------------------------------ compact + next-round min -------------------
-
-// Sharded-mode extra work (kKeyPartner): recover the global id of every edge
-// some component hooked along in round r, into its MST slot.
-struct Recover {
-  const unsigned long long* __restrict__ min_cur;
-  const uint32_t* __restrict__ mstpos;
-  uint32_t* __restrict__ slots;
-};
-
-// kFilter selects the edge predicate of the pass:
-//   kFilterNone  : round r of the plain loop: keep a != b after relabelling
-//   kFilterLight : the split pass of Filter-Boruvka (over the caller's list,
-//                  labels = vertex ids): keep the light edges w < pivot
-//   kFilterHeavy : the filter pass (caller's list, labels = the light-phase
-//                  components): keep heavy edges w >= pivot whose endpoints
-//                  lie in different light components. Heavier edges closing
-//                  a cycle of lighter ones are never in the MST (cycle
-//                  property), so dropping them is exact.
-enum { kFilterNone = 0, kFilterLight = 1, kFilterHeavy = 2 };
-
-template <class View, bool kKeyPartner, bool kWarpPre, int kFilter>
-__global__ void __launch_bounds__(kBlock) k_compact(View Ein, uint4* __restrict__ Eout,
-                                                    const uint32_t* __restrict__ L,
-                                                    unsigned long long* __restrict__ min_next,
-                                                    Recover rec, uint32_t n_orig, DevCounters* ctr,
-                                                    int r, unsigned long long* status,
-                                                    uint32_t epoch, int slot, int light_phase, int filt) {
-  pdl_prologue();
-  __shared__ uint32_t s_scan[kCItems * kWarps];
-  __shared__ uint32_t s_misc[2];
-  __shared__ uint32_t s_tile;
-  const uint32_t stop = ctr->stop_round;
-  if ((uint32_t)r >= ctr->phase_end) return;
-  const bool full = (uint32_t)r + 1 < stop;
-  if (!full && !(kKeyPartner && (uint32_t)r < stop)) return;
-  const uint64_t m_r = kFilter == kFilterHeavy ? ctr->m[0] : ctr->m[r];
-  const uint32_t pivot = ctr->pivot;
-  const uint32_t ntiles = (uint32_t)((m_r + kCTile - 1) / kCTile);
-  while (true) {
-    if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->tile[r][slot], 1u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
-    if (tile >= ntiles) break;
-    EdgeRec e[kCItems];
-    bool keep[kCItems];
-#pragma unroll
-    for (int k = 0; k < kCItems; ++k) {
-      const uint64_t i = (uint64_t)tile * kCTile + k * kBlock + threadIdx.x;
-      keep[k] = false;
-      e[k] = EdgeRec{0, 0, 0, 0, false};
-      if (i < m_r) e[k] = Ein.stream(i);
-    }
-#pragma unroll
-    for (int k = 0; k < kCItems; ++k) {
-      const uint64_t i = (uint64_t)tile * kCTile + k * kBlock + threadIdx.x;
-      if (i < m_r) {
-        bool ok = true;
-        if (View::kOriginal) {
-          ok = e[k].a < n_orig && e[k].b < n_orig && e[k].ok;
-          if (!ok) atomicOr(&ctr->err, (e[k].a < n_orig && e[k].b < n_orig) ? kErrWeight : kErrRange);
-        }
-        if (kFilter == kFilterLight) ok = ok && e[k].w < pivot;
-        if (kFilter == kFilterHeavy) ok = ok && e[k].w >= pivot;
-        if (ok) {
-          if (kKeyPartner) {
-            const unsigned long long hi = (unsigned long long)e[k].w << 32;
-            if (__ldcg(rec.min_cur + e[k].a) == (hi | e[k].b)) {
-              const uint32_t p = __ldg(rec.mstpos + e[k].a);
-              if (p != kNone) rec.slots[p] = e[k].eid;
-            }
-            if (__ldcg(rec.min_cur + e[k].b) == (hi | e[k].a)) {
-              const uint32_t p = __ldg(rec.mstpos + e[k].b);
-              if (p != kNone) rec.slots[p] = e[k].eid;
-            }
-          }
-          if (full) {
-            if (kFilter == kFilterNone || (kFilter == kFilterHeavy && L != nullptr)) {
-              e[k].a = __ldg(L + e[k].a);
-              e[k].b = __ldg(L + e[k].b);
-            }
-            keep[k] = e[k].a != e[k].b;
-          }
-        }
-      }
-    }
-    if (!full) {
-      __syncthreads();
-      continue;  // sharded final round: recovery only
-    }
-    uint32_t rank[kCItems], prefix, total;
-    tile_flag_scan<kCItems>(keep, rank, s_scan, s_misc, status, tile, epoch, prefix, total);
-#pragma unroll
-    for (int k = 0; k < kCItems; ++k) {
-      const uint32_t j = prefix + rank[k];
-      if (keep[k]) __stcs(Eout + j, make_uint4(e[k].a, e[k].b, e[k].w, e[k].eid));
-      const unsigned long long hi = (unsigned long long)e[k].w << 32;
-      const unsigned long long ka = kKeyPartner ? (hi | e[k].b) : (hi | j);
-      const unsigned long long kb = kKeyPartner ? (hi | e[k].a) : (hi | j);
-      offer<kWarpPre>(min_next, e[k].a, ka, keep[k], filt);
-      offer<kWarpPre>(min_next, e[k].b, kb, keep[k], filt);
-    }
-    if (tile == ntiles - 1 && threadIdx.x == 0) {
-      const uint32_t kept = prefix + total;
-      ctr->m[r + 1] = kept;
-      // A light phase running dry ends the phase (the filter pass follows);
-      // a sharded shard running dry says nothing about the others (the
-      // replicated hook decides there); otherwise no edges left = done.
-      if (kept == 0 && kFilter == kFilterNone) {
-        if (light_phase)
-          ctr->phase_end = (uint32_t)r + 1;
-        else if (!kKeyPartner && ctr->stop_round == kNoStop)
-          ctr->stop_round = (uint32_t)r + 1;
-      }
-    }
-    __syncthreads();
-  }
-}
+// ------------------------------ Filter-Boruvka helpers --------------------
 
 // Pivot of the split: histogram of the top 16 weight bits over a strided
 // sample, then the smallest bin boundary with >= target sampled weights
@@ -733,16 +404,20 @@ __global__ void k_compose(uint32_t* __restrict__ Lr, const uint32_t* __restrict_
 //   kScanEdges : m[r+1] = kept; none kept -> stop (or light-phase end)
 //   kScanRoots : n[r+1] = roots; <= 1 -> stop; == n[r] -> stop (or light end)
 enum { kScanEdges = 0, kScanRoots = 1, kScanPlain = 2 };
+// the `light_phase` argument of the scans: which loop the round belongs to
+enum { kPhasePlain = 0, kPhaseLight = 1, kPhaseSharded = 2 };
 constexpr uint32_t kFusedScanMaxTiles = 16384;  // one block scans <= this many counts
 
 template <int kKind>
 __device__ __forceinline__ void scan_verdict(DevCounters* ctr, int r, uint32_t total, int light_phase) {
   if (kKind == kScanEdges) {
     ctr->m[r + 1] = total;
+    // a shard holding no edge says nothing about the others: the sharded
+    // loop stops on the replicated hook verdict only
     if (total == 0) {
-      if (light_phase)
+      if (light_phase == kPhaseLight)
         ctr->phase_end = (uint32_t)r + 1;
-      else if (ctr->stop_round == kNoStop)
+      else if (light_phase == kPhasePlain && ctr->stop_round == kNoStop)
         ctr->stop_round = (uint32_t)r + 1;
     }
   } else if (kKind == kScanRoots) {
@@ -752,7 +427,7 @@ __device__ __forceinline__ void scan_verdict(DevCounters* ctr, int r, uint32_t t
     } else if (total == ctr->n[r]) {
       // no live edge anywhere: done (a forest if total > 1), unless this is
       // the light phase of Filter-Boruvka, which then simply ends
-      if (light_phase)
+      if (light_phase == kPhaseLight)
         ctr->phase_end = (uint32_t)r;
       else
         ctr->stop_round = (uint32_t)r + 1;
@@ -1217,12 +892,67 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_counts(uint32_t* __restrict
   }
 }
 
-// ------------------------------ two-pass hook ------------------------------
+// ------------------------------ sharded exchange ---------------------------
+// Each shard holds a contiguous slice of the caller's edge list (global id =
+// base + local index) and runs the same rounds with replicated component
+// state. A shard's local table has literal keys (w << 32 | position in the
+// shard's current list); since compaction keeps list order, the position
+// order is the global id order, so the local minimum is also the minimum of
+// (w, global id). Per round:
+//   k_shard_keys    : xch[c] = (w << 32 | global id), own[c] = (id, partner)
+//   allreduce(min, u64) of xch        -> the global lightest edge per component
+//   k_shard_partner : partner[c] = own partner if this shard owns xch[c], else ~0
+//   allreduce(min, u32) of partner    -> the other endpoint's label
+// and k_hook_decide<_, kExchanged> then hooks exactly like the single-device
+// loop (same keys, same tie order, MST ids straight from the keys).
+struct PartnerView {
+  static constexpr bool kOriginal = false;
+  const uint32_t* partner;
+};
+
+template <class View>
+__global__ void __launch_bounds__(kBlock) k_shard_keys(View E, const unsigned long long* __restrict__ minimum,
+                                                       unsigned long long* __restrict__ xch,
+                                                       unsigned long long* __restrict__ own, DevCounters* ctr, int r) {
+  pdl_prologue();
+  if ((uint32_t)r >= ctr->stop_round) return;
+  const uint32_t n_r = ctr->n[r];
+  for (uint64_t c = (uint64_t)blockIdx.x * kBlock + threadIdx.x; c < n_r; c += (uint64_t)gridDim.x * kBlock) {
+    const unsigned long long key = __ldcs(minimum + c);
+    unsigned long long x = kNoKey, o = kNoKey;
+    if (key != kNoKey) {
+      const EdgeRec e = E.gather((uint32_t)key);
+      const uint32_t partner = e.a == (uint32_t)c ? e.b : e.a;
+      x = (key & 0xFFFFFFFF00000000ull) | e.eid;
+      o = ((unsigned long long)e.eid << 32) | partner;
+    }
+    xch[c] = x;
+    own[c] = o;
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) k_shard_partner(const unsigned long long* __restrict__ xch,
+                                                          const unsigned long long* __restrict__ own,
+                                                          uint32_t* __restrict__ partner, DevCounters* ctr, int r) {
+  pdl_prologue();
+  if ((uint32_t)r >= ctr->stop_round) return;
+  const uint32_t n_r = ctr->n[r];
+  for (uint64_t c = (uint64_t)blockIdx.x * kBlock + threadIdx.x; c < n_r; c += (uint64_t)gridDim.x * kBlock) {
+    const unsigned long long x = __ldcs(xch + c), o = __ldcs(own + c);
+    // ids are unique across shards: exactly one shard owns the winner
+    partner[c] = (x != kNoKey && o != kNoKey && (uint32_t)x == (uint32_t)(o >> 32)) ? (uint32_t)o : kNone;
+  }
+}
+
+// ------------------------------ hook ---------------------------------------
 // k_hook_decide: per component, the partner along its lightest edge, the
 // mutual-pair root rule, parent[], the MST edge id stashed in rootlabel[],
-// a root bitmask and per-tile root counts; k_hook_emit turns the scanned
-// counts into dense root labels and MST slots. Same results as k_hook.
-template <class View>
+// a root bitmask, in-tile root prefixes and per-tile root counts; k_label2
+// turns the scanned counts into dense root labels and MST slots.
+// kExchanged: the sharded loop. minimum[c] holds the all-reduced global
+// key (w << 32 | global edge id) and E.partner[c] the other endpoint's label
+// of that edge (all-reduced too), so nothing is gathered from an edge list.
+template <class View, bool kExchanged = false>
 __global__ void __launch_bounds__(kBlock) k_hook_decide(View E, const unsigned long long* __restrict__ minimum,
                                                         uint32_t* __restrict__ parent, uint32_t* __restrict__ rootlabel,
                                                         uint32_t* __restrict__ masks, uint32_t* __restrict__ counts,
@@ -1249,7 +979,12 @@ __global__ void __launch_bounds__(kBlock) k_hook_decide(View E, const unsigned l
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
       e[k] = EdgeRec{0, 0, 0, 0, true};
-      if (key[k] != kNoKey) e[k] = E.gather((uint32_t)key[k]);
+      if constexpr (kExchanged) {
+        const uint32_t c = (uint32_t)((uint64_t)tile * kTile + k * kBlock + threadIdx.x);
+        if (key[k] != kNoKey) e[k] = EdgeRec{c, __ldg(E.partner + c), (uint32_t)(key[k] >> 32), (uint32_t)key[k], true};
+      } else {
+        if (key[k] != kNoKey) e[k] = E.gather((uint32_t)key[k]);
+      }
     }
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
@@ -1323,57 +1058,12 @@ __global__ void __launch_bounds__(kBlock) k_hook_decide(View E, const unsigned l
   }
 }
 
-__global__ void __launch_bounds__(kBlock) k_hook_emit(const uint32_t* __restrict__ parent,
-                                                      uint32_t* __restrict__ rootlabel,
-                                                      const uint32_t* __restrict__ masks,
-                                                      const uint32_t* __restrict__ offsets, uint32_t* __restrict__ mst,
-                                                      uint32_t n_orig, DevCounters* ctr, int r,
-                                                      uint8_t* __restrict__ flags) {
-  pdl_prologue();
-  __shared__ uint32_t s_scan[kItems * kWarps];
-  if ((uint32_t)r >= ctr->phase_end) return;
-  // runs even when this round stops (the last hook's MST slots are needed)
-  if ((uint32_t)r >= ctr->stop_round && ctr->stop_round != (uint32_t)r + 1) return;
-  const uint32_t n_r = ctr->n[r];
-  const uint32_t mst_base = n_orig - n_r;
-  const uint32_t ntiles = (uint32_t)(((uint64_t)n_r + kTile - 1) / kTile);
-  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    // exclusive prefix of the (item, warp) root counts inside the tile
-    if (threadIdx.x < 32) {
-      const uint32_t v = __popc(__ldg(masks + (uint64_t)tile * (kItems * kWarps) + lane));
-      const uint32_t incl = warp_incl_scan(v);
-      s_scan[lane] = incl - v;
-    }
-    __syncthreads();
-    const uint32_t base = __ldg(offsets + tile);
-    const uint32_t lt = lanemask_lt();
-#pragma unroll
-    for (int k = 0; k < kItems; ++k) {
-      const uint64_t c = (uint64_t)tile * kTile + k * kBlock + threadIdx.x;
-      const unsigned bal = __ldg(masks + (uint64_t)tile * (kItems * kWarps) + k * kWarps + warp);
-      if (c < n_r) {
-        const uint32_t before = base + s_scan[k * kWarps + warp] + __popc(bal & lt);
-        if ((bal >> lane) & 1u)
-          rootlabel[c] = before;
-        else
-        {
-          const uint32_t eid = rootlabel[c];
-          mst[mst_base + ((uint32_t)c - before)] = eid;
-          if (flags) flags[eid] = 1;  // sorted output is read off these flags
-        }
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// ------------------------------ hook emit + label, fused -------------------
+// ------------------------------ label (fused with the MST slots) -------------------
 // The dense label of a root is the number of roots before it; with the
 // hook's root masks, per-tile offsets (scanned counts) and in-tile slot
 // prefixes it is three small loads, so no separate kernel has to write
-// rootlabel[] first: k_label2 does k_hook_emit's MST slots and k_label's
-// relabel in one pass. Same outputs as k_hook_emit + k_label.
+// rootlabel[] first: k_label2 writes the MST slots and the relabel in one
+// pass.
 __device__ __forceinline__ uint32_t roots_before(uint32_t x, const uint32_t* __restrict__ masks,
                                                  const uint32_t* __restrict__ slotpref,
                                                  const uint32_t* __restrict__ offsets) {
@@ -1462,8 +1152,8 @@ __global__ void __launch_bounds__(kBlock) k_label2(uint32_t* __restrict__ parent
 // in ONE cooperative launch: every phase of a round (hook decide, hook emit,
 // label, relabel+count, compact+offer) is a grid-wide step separated by
 // grid.sync(), and ordered compaction uses per-block chunk counts instead of
-// a look-back (all blocks are co-resident). Semantics match k_hook /
-// k_label / k_compact exactly (same counters, same literal keys).
+// a look-back (all blocks are co-resident). Semantics match k_hook_decide /
+// k_label2 / k_count + k_emit exactly (same counters, same literal keys).
 struct TailArgs {
   uint4* E[2];
   unsigned long long* minb[2];

@@ -4,7 +4,7 @@
 * the NCCL unique id made on rank 0 reaches rank 1 byte-identical
   (dist.exchange_unique_id over torch.distributed),
 * the sharded protocol (oracle/sharded_model.py, the numpy model of the
-  kKeyPartner kernels) with a real allreduce(min) between two processes
+  "sharded exchange" kernels) with a real allreduce(min) between two processes
   returns exactly the oracle's MST on every rank.
 """
 import os
@@ -56,11 +56,25 @@ def _worker(rank, world, port, cases, queue):
         dist.destroy_process_group()
 
 
-def _cases():
+def _tie_case(oracle_mod):
+    # heavy weight ties (16 distinct values): the edge set must still be the
+    # stable-Kruskal one (ties -> lower global id)
+    rng = np.random.default_rng(7)
+    n, m = 2000, 12000
+    src = np.concatenate([np.arange(1, n), rng.integers(0, n, m - n + 1)]).astype(np.uint32)
+    dst = np.concatenate([rng.integers(0, np.arange(1, n)), rng.integers(0, n, m - n + 1)]).astype(np.uint32)
+    w = rng.integers(0, 16, m).astype(np.uint32)
+    k = oracle_mod.kruskal(n, src, dst, w)
+    return (n, src, dst, w, k.ids.tolist(), int(k.total_weight))
+
+
+def _cases(oracle_mod=None):
     cases = []
     for name in ["gen_3000_6_2", "gen_1500_4_13", "multi_mid", "gen_100_3_5"]:
         g = load_npz(GOLDEN / f"{name}.npz")
         cases.append((int(g["n"]), g["src"], g["dst"], g["w"], g["ids"].tolist(), int(g["total"])))
+    if oracle_mod is not None:
+        cases.append(_tie_case(oracle_mod))
     return cases
 
 
@@ -75,8 +89,8 @@ def test_shard_range_partitions():
         shard_range(10, 2, 2)
 
 
-def test_sharded_protocol_world2_gloo():
-    cases = _cases()
+def test_sharded_protocol_world2_gloo(oracle_mod):
+    cases = _cases(oracle_mod)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -96,7 +110,7 @@ def test_sharded_protocol_world2_gloo():
 
 def test_sharded_model_single_rank_matches_oracle(oracle_mod):
     from oracle.sharded_model import sharded_boruvka
-    for n, src, dst, w, ids, total in _cases():
+    for n, src, dst, w, ids, total in _cases(oracle_mod):
         got, tot, _ = sharded_boruvka(n, src, dst, w, 0, lambda a: a)
         assert got.tolist() == ids and tot == total
         # 3 shards in one process: allreduce = elementwise min over shards

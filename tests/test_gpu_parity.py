@@ -128,12 +128,18 @@ def test_edge_cases(mst, oracle_mod):
         with _env(**mode):
             r = P.boruvka_gpu(P.Graph(n, src, dst, w))
             assert r.mst_edges.tolist() == k.ids.tolist() and r.total_weight == k.total_weight
+    # the sharded exchange breaks ties by global id too
+    for s in (2, 3, 8):
+        e = P.boruvka_gpu_emulated(P.Graph(n, src, dst, w), s)
+        assert e.mst_edges.tolist() == k.ids.tolist() and e.total_weight == k.total_weight
     # all weights equal (the filter pivot then splits nothing off)
     w0 = np.zeros(m, dtype=np.uint32)
     k = O.kruskal(n, src, dst, w0)
     for mode in MODES:
         with _env(**mode):
             assert P.boruvka_gpu(P.Graph(n, src, dst, w0)).mst_edges.tolist() == k.ids.tolist()
+    for s in (2, 5):
+        assert P.boruvka_gpu_emulated(P.Graph(n, src, dst, w0), s).mst_edges.tolist() == k.ids.tolist()
     # only self-loops are light: the light phase is empty
     sl = np.concatenate([np.arange(50, dtype=np.uint32), src])
     dl = np.concatenate([np.arange(50, dtype=np.uint32), dst])
