@@ -32,6 +32,7 @@
 #include "mst/boruvka_parallel.hpp"
 #include "mst/graph.hpp"
 #include "mst/mst_result.hpp"
+#include "mst/verify.hpp"
 #include "mst_gpu.h"
 
 namespace mst {
@@ -118,6 +119,76 @@ inline MstResult boruvka_gpu(Graph& g, int num_gpus = 1, GpuRunInfo* info = null
     rc = mst_gpu_boruvka(&soa, num_gpus, ids.data(), &count, &total, &st);
   }
   return gpu_detail::finish(rc, ids, count, total, st, info);
+}
+
+/// verify_mst(g, result, oracle) (verify.hpp:31, verify.cpp:15-57) on the
+/// GPU: the same five flags and details line; the oracle result is the
+/// caller's (computed once per graph). An id outside [0, m) throws
+/// std::out_of_range as the reference does.
+inline VerifyReport verify_mst_gpu(const Graph& g, const MstResult& result, const MstResult& oracle) {
+  const VertexId n = g.vertex_count();
+  const std::uint64_t m = static_cast<std::uint64_t>(g.edge_count());
+  auto narrow = [m](const std::vector<EdgeId>& v) {
+    std::vector<std::uint32_t> out(v.size());
+    for (std::size_t i = 0; i < v.size(); ++i) {
+      if (v[i] < 0 || static_cast<std::uint64_t>(v[i]) >= m)
+        throw std::out_of_range("verify_mst: edge id " + std::to_string(v[i]) + " outside [0," + std::to_string(m) +
+                                ")");
+      out[i] = static_cast<std::uint32_t>(v[i]);
+    }
+    return out;
+  };
+  const std::vector<std::uint32_t> ids = narrow(result.mst_edges);
+  const std::vector<std::uint32_t> oids = narrow(oracle.mst_edges);
+  mst_verify_t v{};
+  const int rc = mst_gpu_verify_aos(n, m, reinterpret_cast<const mst_edge_t*>(g.edges().data()), 0, ids.data(),
+                                    ids.size(), oids.data(), oids.size(), oracle.total_weight, &v);
+  if (rc != MST_OK) gpu_detail::raise(rc);
+  VerifyReport rep;
+  rep.is_spanning = v.is_spanning != 0;
+  rep.is_acyclic = v.is_acyclic != 0;
+  rep.edge_count_ok = v.edge_count_ok != 0;
+  rep.weight_matches_oracle = v.weight_matches_oracle == 1;
+  rep.edge_set_matches_oracle = v.edge_set_matches_oracle == 1;
+  rep.details = "edges=" + std::to_string(result.mst_edges.size()) + " (expected " + std::to_string(n - 1) +
+                "), weight=" + std::to_string(v.weight) + " (oracle " + std::to_string(oracle.total_weight) +
+                "), components=" + std::to_string(v.components) + ", acyclic=" + (rep.is_acyclic ? "yes" : "no") +
+                ", edge_set=" + (rep.edge_set_matches_oracle ? "match" : "MISMATCH");
+  if (v.weight != result.total_weight)
+    rep.details += "; WARNING: result.total_weight=" + std::to_string(result.total_weight) +
+                   " disagrees with its own edge list";
+  return rep;
+}
+
+/// Binary SoA edge file (mst_gpu.h "edge-list files"): the fast companion of
+/// the reference's text load_graph / save_graph (graph.cpp:228-295). The
+/// loaded list goes through the reference's build_graph, so a loaded Graph
+/// meets the same contract as one from load_graph.
+inline void save_graph_soa(const Graph& g, const std::string& path) {
+  const std::uint64_t m = static_cast<std::uint64_t>(g.edge_count());
+  std::vector<std::uint32_t> src(m), dst(m), w(m);
+  for (std::uint64_t i = 0; i < m; ++i) {
+    const Edge& e = g.edge(static_cast<EdgeId>(i));
+    if (e.weight > 0xFFFFFFFFull) throw std::invalid_argument("save_graph_soa: weight does not fit 32 bits");
+    src[i] = e.src;
+    dst[i] = e.dest;
+    w[i] = static_cast<std::uint32_t>(e.weight);
+  }
+  if (mst_io_save_soa(path.c_str(), g.vertex_count(), m, src.data(), dst.data(), w.data()) != MST_OK)
+    throw std::runtime_error("save_graph_soa: " + std::string(mst_gpu_last_error()));
+}
+
+inline Graph load_graph_soa(const std::string& path) {
+  std::uint32_t n = 0;
+  std::uint64_t m = 0;
+  int rc = mst_io_soa_header(path.c_str(), &n, &m);
+  std::vector<std::uint32_t> src(m), dst(m), w(m);
+  if (rc == MST_OK) rc = mst_io_load_soa(path.c_str(), n, m, src.data(), dst.data(), w.data(), 0);
+  if (rc == MST_ERR_PARSE) throw GraphError(GraphErrorKind::ParseError, std::string("parse error: ") + mst_gpu_last_error());
+  if (rc != MST_OK) throw std::runtime_error("load_graph_soa: " + std::string(mst_gpu_last_error()));
+  std::vector<Edge> edges(m);
+  for (std::uint64_t i = 0; i < m; ++i) edges[i] = Edge{src[i], dst[i], w[i]};
+  return build_graph(n, edges);
 }
 
 }  // namespace mst

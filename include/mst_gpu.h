@@ -54,7 +54,9 @@ enum {
   MST_ERR_NCCL = 6,
   MST_ERR_NO_DEVICE = 7,
   MST_ERR_OOM = 8,
-  MST_ERR_STALL = 9
+  MST_ERR_STALL = 9,
+  MST_ERR_PARSE = 10, /* ~ GraphError{ParseError} (graph.cpp:229-281) */
+  MST_ERR_IO = 11
 };
 
 #define MST_MAX_ROUNDS 48
@@ -145,6 +147,56 @@ int mst_gpu_boruvka_rank(mst_comm_t comm, uint32_t n, uint64_t m_total, uint64_t
 int mst_gpu_boruvka_device(const mst_edges_soa_t* edges, uint32_t* d_out_ids, void* stream,
                            uint64_t* out_count, uint64_t* out_total_weight,
                            mst_stats_t* stats, double* ms_hot, uint32_t* hot_launches);
+
+/* ---- GPU verifier ----
+ * The checks of the reference's verify_mst (proj/src/verify.cpp:15-57,
+ * VerifyReport in proj/include/mst/verify.hpp:11-24) on the device, with the
+ * oracle's result supplied by the caller (the reference's second overload,
+ * verify.hpp:31, "computed once and reused"): ids in range (else
+ * MST_ERR_RANGE ~ std::out_of_range, verify.cpp:19-22), |ids| == n-1,
+ * acyclic and spanning through a private union-find over the result edges,
+ * weight sum, and weight / edge-set equality with the oracle. `ids` (and
+ * `oracle_ids`) live where the edges live (edges->on_device). Pass
+ * oracle_total = MST_VERIFY_NO_ORACLE to run the structural checks only;
+ * the two oracle flags are then -1. */
+#define MST_VERIFY_NO_ORACLE (~(uint64_t)0)
+typedef struct mst_verify {
+  int is_spanning;
+  int is_acyclic;
+  int edge_count_ok;
+  int weight_matches_oracle;   /* -1: no oracle given */
+  int edge_set_matches_oracle; /* -1: no oracle given */
+  uint64_t components;         /* after uniting the result edges */
+  uint64_t weight;             /* sum of the result edges' weights */
+} mst_verify_t;
+int mst_gpu_verify(const mst_edges_soa_t* edges, const uint32_t* ids, uint64_t count,
+                   const uint32_t* oracle_ids, uint64_t oracle_count, uint64_t oracle_total,
+                   mst_verify_t* report);
+/* Same over the reference's 16-byte Edge array (full 64-bit weights). */
+int mst_gpu_verify_aos(uint32_t n, uint64_t m, const mst_edge_t* edges, int on_device,
+                       const uint32_t* ids, uint64_t count, const uint32_t* oracle_ids,
+                       uint64_t oracle_count, uint64_t oracle_total, mst_verify_t* report);
+
+/* ---- edge-list files ----
+ * Text: the reference's format, "<n> <m>\n" + m lines "<src> <dest> <weight>\n"
+ * (load_graph / save_graph, graph.cpp:228-295), parsed and formatted in
+ * parallel with load_graph's strict rules and messages (MST_ERR_PARSE);
+ * weights must fit 32 bits (MST_ERR_WEIGHT). build_graph's structural
+ * checks are not applied (see the widenings above).
+ * Binary SoA ("MSTSOA01"): 4 KiB header, then u32 src / dst / w arrays on
+ * 4 KiB boundaries; mst_io_load_soa(on_device = 1) streams the file into
+ * device arrays through pinned chunks (read of chunk k+1 overlaps the copy
+ * of chunk k). The *_header calls give n and m for sizing the arrays. */
+int mst_io_text_header(const char* path, uint32_t* out_n, uint64_t* out_m);
+int mst_io_load_text(const char* path, uint32_t n, uint64_t m, uint32_t* src, uint32_t* dst,
+                     uint32_t* w);
+int mst_io_save_text(const char* path, uint32_t n, uint64_t m, const uint32_t* src,
+                     const uint32_t* dst, const uint32_t* w);
+int mst_io_soa_header(const char* path, uint32_t* out_n, uint64_t* out_m);
+int mst_io_load_soa(const char* path, uint32_t n, uint64_t m, uint32_t* src, uint32_t* dst,
+                    uint32_t* w, int on_device);
+int mst_io_save_soa(const char* path, uint32_t n, uint64_t m, const uint32_t* src,
+                    const uint32_t* dst, const uint32_t* w);
 
 /* Frees the cached device workspaces of the calling thread's devices. */
 int mst_gpu_release_workspace(void);

@@ -70,6 +70,8 @@ def _load_ref():
         lib.ref_generate_graph.argtypes = [_u32, ctypes.c_int, _u64, _vp, _vp, _vp, _u64p]
         lib.ref_solve.argtypes = [ctypes.c_int, ctypes.c_int, _u32, _u64, _vp, _vp, _vp, _vp,
                                   _u64p, _u64p, ctypes.POINTER(ctypes.c_double), _u32p, _u64p]
+        lib.ref_save_generated.argtypes = [_u32, ctypes.c_int, _u64, ctypes.c_char_p]
+        lib.ref_load_graph.argtypes = [ctypes.c_char_p, _u32p, _u64p, _vp, _vp, _vp, _u64]
         _ref = lib
     return _ref
 
@@ -141,6 +143,25 @@ def ref_generate_graph(n: int, avg_degree: int, seed: int):
     if rc:
         raise ValueError(lib.ref_last_error().decode())
     return src, dst, w
+
+
+def ref_save_generated(n: int, avg_degree: int, seed: int, path) -> None:
+    """The reference's save_graph(generate_graph(n, deg, seed), path)."""
+    lib = _load_ref()
+    if lib.ref_save_generated(n, avg_degree, seed, str(path).encode()):
+        raise OSError(lib.ref_last_error().decode())
+
+
+def ref_load_graph(path, cap: int = 1 << 22):
+    """The reference's load_graph(path): (status, message, n, src, dst, w);
+    status 0 ok, 1 ParseError, 2 other GraphError, 3 other exception."""
+    lib = _load_ref()
+    n, m = ctypes.c_uint32(0), ctypes.c_uint64(0)
+    src, dst = np.zeros(cap, np.uint32), np.zeros(cap, np.uint32)
+    w = np.zeros(cap, np.uint64)
+    rc = lib.ref_load_graph(str(path).encode(), ctypes.byref(n), ctypes.byref(m), _p(src), _p(dst), _p(w), cap)
+    k = min(int(m.value), cap)
+    return rc, lib.ref_last_error().decode(), int(n.value), src[:k], dst[:k], w[:k]
 
 
 def ref_solve(n: int, src, dst, w, algo: int = ALGO_KRUSKAL, threads: int = 1) -> OracleResult:

@@ -68,6 +68,40 @@ int ref_generate_graph(uint32_t n, int avg_degree, uint64_t seed, uint32_t* src,
   }
 }
 
+// mst::save_graph (graph.cpp:283-295) of generate_graph(n, deg, seed): the
+// reference's own writer, for the text-format parity tests.
+int ref_save_generated(uint32_t n, int avg_degree, uint64_t seed, const char* path) {
+  try {
+    mst::save_graph(mst::generate_graph(n, avg_degree, seed), path);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(1, e.what());
+  }
+}
+
+// mst::load_graph (graph.cpp:228-281): 0 ok (n, m and up to cap edges
+// returned), 1 GraphError{ParseError}, 2 another GraphError (build_graph's
+// structural checks), 3 any other exception; the message via ref_last_error.
+int ref_load_graph(const char* path, uint32_t* out_n, uint64_t* out_m, uint32_t* src, uint32_t* dst,
+                   uint64_t* w, uint64_t cap) {
+  try {
+    mst::Graph g = mst::load_graph(path);
+    const auto es = g.edges();
+    *out_n = g.vertex_count();
+    *out_m = es.size();
+    for (size_t i = 0; i < es.size() && i < cap; ++i) {
+      src[i] = es[i].src;
+      dst[i] = es[i].dest;
+      w[i] = es[i].weight;
+    }
+    return 0;
+  } catch (const mst::GraphError& e) {
+    return fail(e.kind() == mst::GraphErrorKind::ParseError ? 1 : 2, e.what());
+  } catch (const std::exception& e) {
+    return fail(3, e.what());
+  }
+}
+
 // algo: 0 kruskal_oracle, 1 boruvka_seq, 2 boruvka_seq_opt, 3 boruvka_cas(T),
 //       4 boruvka_lock(T). out_ids holds n-1 entries (ascending on return).
 // out_ms is the reference's own MstResult::elapsed_ms (computation only,

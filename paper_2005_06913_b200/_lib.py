@@ -26,6 +26,8 @@ MST_ERR_NCCL = 6
 MST_ERR_NO_DEVICE = 7
 MST_ERR_OOM = 8
 MST_ERR_STALL = 9
+MST_ERR_PARSE = 10
+MST_ERR_IO = 11
 MST_MAX_ROUNDS = 48
 MST_UNIQUE_ID_BYTES = 128
 
@@ -82,6 +84,20 @@ class MstGenSpec(ctypes.Structure):
     ]
 
 
+class MstVerify(ctypes.Structure):
+    _fields_ = [
+        ("is_spanning", ctypes.c_int),
+        ("is_acyclic", ctypes.c_int),
+        ("edge_count_ok", ctypes.c_int),
+        ("weight_matches_oracle", ctypes.c_int),
+        ("edge_set_matches_oracle", ctypes.c_int),
+        ("components", ctypes.c_uint64),
+        ("weight", ctypes.c_uint64),
+    ]
+
+
+MST_VERIFY_NO_ORACLE = (1 << 64) - 1
+
 _SIGNATURES = {
     "mst_gpu_boruvka": (ctypes.c_int, [ctypes.POINTER(MstEdgesSoa), ctypes.c_int, ctypes.c_void_p,
                                        u64p, u64p, ctypes.POINTER(MstStats)]),
@@ -105,6 +121,22 @@ _SIGNATURES = {
                                               ctypes.POINTER(MstStats),
                                               ctypes.POINTER(ctypes.c_double), u32p]),
     "mst_gpu_round1_min": (ctypes.c_int, [ctypes.POINTER(MstEdgesSoa), ctypes.c_void_p]),
+    "mst_gpu_verify": (ctypes.c_int, [ctypes.POINTER(MstEdgesSoa), ctypes.c_void_p, ctypes.c_uint64,
+                                      ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
+                                      ctypes.POINTER(MstVerify)]),
+    "mst_gpu_verify_aos": (ctypes.c_int, [ctypes.c_uint32, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_int,
+                                          ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p,
+                                          ctypes.c_uint64, ctypes.c_uint64, ctypes.POINTER(MstVerify)]),
+    "mst_io_text_header": (ctypes.c_int, [ctypes.c_char_p, u32p, u64p]),
+    "mst_io_load_text": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_void_p,
+                                        ctypes.c_void_p, ctypes.c_void_p]),
+    "mst_io_save_text": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_void_p,
+                                        ctypes.c_void_p, ctypes.c_void_p]),
+    "mst_io_soa_header": (ctypes.c_int, [ctypes.c_char_p, u32p, u64p]),
+    "mst_io_load_soa": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_void_p,
+                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
+    "mst_io_save_soa": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_void_p,
+                                       ctypes.c_void_p, ctypes.c_void_p]),
     "mst_gpu_release_workspace": (ctypes.c_int, []),
     "mst_gpu_last_error": (ctypes.c_char_p, []),
     "mst_gpu_version": (ctypes.c_char_p, []),

@@ -36,6 +36,7 @@ from . import _lib as L
 __all__ = [
     "Graph", "MstResult", "GpuRunInfo", "GraphError", "WorkerPanic", "build_graph",
     "boruvka_gpu", "boruvka_gpu_aos", "boruvka_gpu_emulated", "boruvka_gpu_device",
+    "VerifyReport", "verify_mst", "verify_mst_aos", "load_graph", "save_graph", "load_graph_device",
     "EDGE_DTYPE",
 ]
 
@@ -176,6 +177,10 @@ def _raise_for(rc: int, result: MstResult | None = None) -> None:
         raise GraphError("WeightOverflow", msg)
     if rc == L.MST_ERR_DISCONNECTED:
         raise GraphError("Disconnected", msg, forest=result)
+    if rc == L.MST_ERR_PARSE:
+        raise GraphError("ParseError", msg)
+    if rc == L.MST_ERR_IO:
+        raise OSError(msg)
     raise WorkerPanic(f"[status {rc}] {msg}")
 
 
@@ -231,6 +236,139 @@ def boruvka_gpu_emulated(g: Graph, shards: int, info: GpuRunInfo | None = None) 
     rc = lib.mst_gpu_boruvka_emulated(ctypes.byref(e), shards, ids.ctypes.data, ctypes.byref(count),
                                       ctypes.byref(total), ctypes.byref(stats))
     return _finish(rc, ids, count, total, stats, info)
+
+
+@dataclass
+class VerifyReport:
+    """mst::VerifyReport (verify.hpp:11-24); the oracle flags are None when
+    no oracle result was given (structural checks only)."""
+
+    is_spanning: bool
+    is_acyclic: bool
+    edge_count_ok: bool
+    weight_matches_oracle: bool | None
+    edge_set_matches_oracle: bool | None
+    components: int
+    weight: int
+    details: str = ""
+
+    def all_ok(self) -> bool:
+        oracle = [f for f in (self.weight_matches_oracle, self.edge_set_matches_oracle) if f is not None]
+        return self.is_spanning and self.is_acyclic and self.edge_count_ok and all(oracle)
+
+
+def _verify_args(ids, oracle):
+    ids = np.ascontiguousarray(ids, dtype=np.int64)
+    if ids.size and (ids.min() < 0 or ids.max() >= 2**32 - 1):
+        raise IndexError("verify_mst: edge id outside [0, m)")
+    ids = ids.astype(np.uint32)
+    if oracle is None:
+        return ids, np.zeros(1, dtype=np.uint32), 0, L.MST_VERIFY_NO_ORACLE
+    oids = np.ascontiguousarray(oracle.mst_edges, dtype=np.int64).astype(np.uint32)
+    return ids, oids, oids.size, int(oracle.total_weight)
+
+
+def _report(rc, rep: "L.MstVerify", n: int, count: int, oracle, own_total) -> VerifyReport:
+    if rc == L.MST_ERR_RANGE:
+        raise IndexError(L.last_error())  # std::out_of_range (verify.cpp:19-22)
+    _raise_for(rc)
+    flag = (lambda v: None if v < 0 else bool(v))
+    r = VerifyReport(bool(rep.is_spanning), bool(rep.is_acyclic), bool(rep.edge_count_ok),
+                     flag(rep.weight_matches_oracle), flag(rep.edge_set_matches_oracle),
+                     int(rep.components), int(rep.weight))
+    # the reference's details line (verify.cpp:45-53)
+    d = f"edges={count} (expected {n - 1}), weight={r.weight}"
+    if oracle is not None:
+        d += f" (oracle {int(oracle.total_weight)})"
+    d += f", components={r.components}, acyclic={'yes' if r.is_acyclic else 'no'}"
+    if r.edge_set_matches_oracle is not None:
+        d += f", edge_set={'match' if r.edge_set_matches_oracle else 'MISMATCH'}"
+    if own_total is not None and own_total != r.weight:
+        d += f"; WARNING: result.total_weight={own_total} disagrees with its own edge list"
+    r.details = d
+    return r
+
+
+def verify_mst(g: Graph, result: MstResult, oracle: MstResult | None = None) -> VerifyReport:
+    """verify_mst(g, result, oracle) (verify.hpp:27-31) on the GPU.
+
+    The oracle result is supplied by the caller (computed once per graph, as
+    the reference's second overload does); without it only the structural
+    checks run. An id outside [0, m) raises IndexError (std::out_of_range).
+    """
+    lib = L.lib()
+    ids, oids, ocount, ototal = _verify_args(result.mst_edges, oracle)
+    e = L.MstEdgesSoa(g.n, g.edge_count(), _ptr(g.src), _ptr(g.dst), _ptr(g.w), 0)
+    rep = L.MstVerify()
+    rc = lib.mst_gpu_verify(ctypes.byref(e), _ptr(ids), ids.size, _ptr(oids), ocount, ototal, ctypes.byref(rep))
+    return _report(rc, rep, g.n, ids.size, oracle, int(result.total_weight))
+
+
+def verify_mst_aos(n: int, edges: np.ndarray, result: MstResult, oracle: MstResult | None = None) -> VerifyReport:
+    """Same over the reference's AoS ``Edge`` array (64-bit weights)."""
+    edges = np.ascontiguousarray(edges, dtype=EDGE_DTYPE)
+    lib = L.lib()
+    ids, oids, ocount, ototal = _verify_args(result.mst_edges, oracle)
+    rep = L.MstVerify()
+    rc = lib.mst_gpu_verify_aos(n, edges.shape[0], _ptr(edges), 0, _ptr(ids), ids.size, _ptr(oids), ocount,
+                                ototal, ctypes.byref(rep))
+    return _report(rc, rep, n, ids.size, oracle, int(result.total_weight))
+
+
+_SOA_MAGIC = b"MSTSOA01"
+
+
+def _is_soa(path) -> bool:
+    with open(path, "rb") as f:
+        return f.read(8) == _SOA_MAGIC
+
+
+def _header(path, fn) -> tuple[int, int]:
+    n, m = ctypes.c_uint32(0), ctypes.c_uint64(0)
+    _raise_for(fn(str(path).encode(), ctypes.byref(n), ctypes.byref(m)))
+    return int(n.value), int(m.value)
+
+
+def load_graph(path) -> Graph:
+    """load_graph(path) (graph.cpp:228-281): the reference's text format, or
+    the binary SoA format (detected by its magic). Parse errors raise
+    GraphError("ParseError") with load_graph's messages."""
+    lib = L.lib()
+    soa = _is_soa(path)
+    n, m = _header(path, lib.mst_io_soa_header if soa else lib.mst_io_text_header)
+    src, dst, w = (np.empty(m, dtype=np.uint32) for _ in range(3))
+    p = str(path).encode()
+    if soa:
+        rc = lib.mst_io_load_soa(p, n, m, _ptr(src), _ptr(dst), _ptr(w), 0)
+    else:
+        rc = lib.mst_io_load_text(p, n, m, _ptr(src), _ptr(dst), _ptr(w))
+    _raise_for(rc)
+    return Graph(n, src, dst, w)
+
+
+def save_graph(g: Graph, path, binary: bool = False) -> None:
+    """save_graph(g, path) (graph.cpp:283-295) in the reference's text format,
+    or (binary=True) the SoA format that load_graph_device streams to HBM."""
+    lib = L.lib()
+    fn = lib.mst_io_save_soa if binary else lib.mst_io_save_text
+    _raise_for(fn(str(path).encode(), g.n, g.edge_count(), _ptr(g.src), _ptr(g.dst), _ptr(g.w)))
+
+
+def load_graph_device(path, device: int | None = None):
+    """Binary SoA file -> device arrays (torch uint32-as-int32 tensors on the
+    current CUDA device): returns (n, m, src, dst, w), ready for
+    boruvka_gpu_device. The file is streamed through pinned chunks."""
+    import torch
+    lib = L.lib()
+    if not _is_soa(path):
+        raise GraphError("ParseError", f"{path}: not an MSTSOA01 file (use save_graph(..., binary=True))")
+    n, m = _header(path, lib.mst_io_soa_header)
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    src, dst, w = (torch.empty(max(m, 1), dtype=torch.int32, device=dev) for _ in range(3))
+    with torch.cuda.device(dev):
+        torch.cuda.synchronize()
+        _raise_for(lib.mst_io_load_soa(str(path).encode(), n, m, src.data_ptr(), dst.data_ptr(), w.data_ptr(), 1))
+    return n, m, src[:m], dst[:m], w[:m]
 
 
 def round1_min(g: Graph) -> np.ndarray:

@@ -16,8 +16,8 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libmstgpu.so"
-SOURCES = ["boruvka.cu", "gen.cu"]
-DEPS = SOURCES + ["kernels.cuh", "common.cuh"]
+SOURCES = ["boruvka.cu", "gen.cu", "io.cu"]
+DEPS = SOURCES + ["kernels.cuh", "common.cuh", "verify.cuh"]
 
 NVCC_FLAGS = [
     "-std=c++17", "-O3", "-lineinfo",

@@ -19,6 +19,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "verify.cuh"
 
 namespace mstgpu {
 
@@ -1271,6 +1272,68 @@ struct mst_comm {
   CommImpl impl;
 };
 
+namespace mstgpu {
+namespace {
+
+// verify.cuh: range, count, acyclic/spanning by a private concurrent
+// union-find, weight sum, and (with an oracle) weight + edge-set equality.
+template <class V>
+void run_verify(V g, uint32_t n, uint64_t m, int on_device, const uint32_t* ids, uint64_t count,
+                const uint32_t* oracle_ids, uint64_t oracle_count, uint64_t oracle_total, mst_verify_t* out) {
+  const int dev = current_device_checked();
+  Workspace& ws = workspace(dev, 0);
+  std::lock_guard<std::mutex> lock(ws.mu);
+  MST_CUDA_CHECK(cudaSetDevice(dev));
+  cudaStream_t s = ws.stream;
+  if (!on_device) {
+    if (count) {
+      uint32_t* d = ws.get<uint32_t>("v_ids", count);
+      copy_h2d(ws, d, ids, count * 4);
+      ids = d;
+    }
+    if (oracle_ids && oracle_count) {
+      uint32_t* d = ws.get<uint32_t>("v_oracle", oracle_count);
+      copy_h2d(ws, d, oracle_ids, oracle_count * 4);
+      oracle_ids = d;
+    }
+  }
+  const bool with_oracle = oracle_total != MST_VERIFY_NO_ORACLE;
+  const uint64_t words4 = (m + 127) / 128;
+  uint32_t* parent = ws.get<uint32_t>("v_parent", n);
+  auto* ctr = ws.get<VerifyCounters>("v_ctr", 1);
+  uint32_t* bits_got = with_oracle ? reinterpret_cast<uint32_t*>(ws.get<uint4>("v_bits_got", std::max<uint64_t>(words4, 1))) : nullptr;
+  uint32_t* bits_ora = with_oracle ? reinterpret_cast<uint32_t*>(ws.get<uint4>("v_bits_ora", std::max<uint64_t>(words4, 1))) : nullptr;
+  MST_CUDA_CHECK(cudaMemsetAsync(ctr, 0, sizeof(VerifyCounters), s));
+  if (with_oracle) {
+    MST_CUDA_CHECK(cudaMemsetAsync(bits_got, 0, std::max<uint64_t>(words4, 1) * 16, s));
+    MST_CUDA_CHECK(cudaMemsetAsync(bits_ora, 0, std::max<uint64_t>(words4, 1) * 16, s));
+  }
+  const unsigned grid = (unsigned)sm_count(dev) * 8;
+  kv_iota<<<grid, 256, 0, s>>>(parent, n);
+  if (count) kv_unite<V><<<grid, 256, 0, s>>>(g, m, ids, count, parent, bits_got, ctr);
+  if (with_oracle) {
+    if (oracle_count) kv_mark<<<grid, 256, 0, s>>>(oracle_ids, oracle_count, m, bits_ora, ctr);
+    if (words4)
+      kv_compare<<<grid, 256, 0, s>>>(reinterpret_cast<const uint4*>(bits_got), reinterpret_cast<const uint4*>(bits_ora),
+                                      words4, ctr);
+  }
+  MST_CUDA_CHECK(cudaGetLastError());
+  VerifyCounters h{};
+  MST_CUDA_CHECK(cudaMemcpyAsync(&h, ctr, sizeof(h), cudaMemcpyDeviceToHost, s));
+  MST_CUDA_CHECK(cudaStreamSynchronize(s));
+  if (h.range_err) throw MstError{MST_ERR_RANGE, "verify: an edge id lies outside [0, m)"};
+  out->edge_count_ok = count == (uint64_t)n - 1;
+  out->components = (uint64_t)n - h.unions;
+  out->is_acyclic = h.unions == count;
+  out->is_spanning = out->components == 1;
+  out->weight = h.weight;
+  out->weight_matches_oracle = with_oracle ? (h.weight == oracle_total) : -1;
+  out->edge_set_matches_oracle = with_oracle ? (!h.set_mismatch && count == oracle_count) : -1;
+}
+
+}  // namespace
+}  // namespace mstgpu
+
 extern "C" {
 
 const char* mst_gpu_last_error(void) { return t_last_error.c_str(); }
@@ -1371,6 +1434,63 @@ int mst_gpu_boruvka_emulated(const mst_edges_soa_t* edges, int num_shards, uint3
     EmulatedExchanger ex;
     RunOut o = run_sharded(parts, ex, edges->n, edges->m, out_ids, stats);
     return finish_status(o, out_count, out_total_weight);
+  });
+}
+
+int mst_gpu_verify(const mst_edges_soa_t* edges, const uint32_t* ids, uint64_t count, const uint32_t* oracle_ids,
+                   uint64_t oracle_count, uint64_t oracle_total, mst_verify_t* report) {
+  return guarded([&]() -> int {
+    if (!edges || !report) throw MstError{MST_ERR_INVALID_ARG, "NULL argument"};
+    validate_common(edges->n, edges->m);
+    if (edges->m && (!edges->src || !edges->dst || !edges->w))
+      throw MstError{MST_ERR_INVALID_ARG, "edge arrays are NULL"};
+    if (count && !ids) throw MstError{MST_ERR_INVALID_ARG, "ids is NULL"};
+    if (oracle_count && !oracle_ids) throw MstError{MST_ERR_INVALID_ARG, "oracle_ids is NULL"};
+    const int dev = current_device_checked();
+    const uint32_t *src = edges->src, *dst = edges->dst, *w = edges->w;
+    if (!edges->on_device && edges->m) {
+      Workspace& ws = workspace(dev, 0);
+      std::lock_guard<std::mutex> lock(ws.mu);
+      MST_CUDA_CHECK(cudaSetDevice(dev));
+      uint32_t* d_src = ws.get<uint32_t>("in_src", edges->m);
+      uint32_t* d_dst = ws.get<uint32_t>("in_dst", edges->m);
+      uint32_t* d_w = ws.get<uint32_t>("in_w", edges->m);
+      copy_h2d(ws, d_src, src, edges->m * 4);
+      copy_h2d(ws, d_dst, dst, edges->m * 4);
+      copy_h2d(ws, d_w, w, edges->m * 4);
+      src = d_src;
+      dst = d_dst;
+      w = d_w;
+    }
+    run_verify(VSoa{src, dst, w}, edges->n, edges->m, edges->on_device, ids, count, oracle_ids, oracle_count,
+               oracle_total, report);
+    set_last_error("");
+    return MST_OK;
+  });
+}
+
+int mst_gpu_verify_aos(uint32_t n, uint64_t m, const mst_edge_t* edges, int on_device, const uint32_t* ids,
+                       uint64_t count, const uint32_t* oracle_ids, uint64_t oracle_count, uint64_t oracle_total,
+                       mst_verify_t* report) {
+  return guarded([&]() -> int {
+    if (!report) throw MstError{MST_ERR_INVALID_ARG, "NULL argument"};
+    validate_common(n, m);
+    if (m && !edges) throw MstError{MST_ERR_INVALID_ARG, "edges is NULL"};
+    if (count && !ids) throw MstError{MST_ERR_INVALID_ARG, "ids is NULL"};
+    if (oracle_count && !oracle_ids) throw MstError{MST_ERR_INVALID_ARG, "oracle_ids is NULL"};
+    const int dev = current_device_checked();
+    const uint4* e4 = reinterpret_cast<const uint4*>(edges);
+    if (!on_device && m) {
+      Workspace& ws = workspace(dev, 0);
+      std::lock_guard<std::mutex> lock(ws.mu);
+      MST_CUDA_CHECK(cudaSetDevice(dev));
+      uint4* d = ws.get<uint4>("in_aos", m);
+      copy_h2d(ws, d, e4, m * 16);
+      e4 = d;
+    }
+    run_verify(VAos{e4}, n, m, on_device, ids, count, oracle_ids, oracle_count, oracle_total, report);
+    set_last_error("");
+    return MST_OK;
   });
 }
 

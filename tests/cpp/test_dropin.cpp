@@ -6,6 +6,7 @@
 //
 //   test_dropin          full suite (needs a GPU)
 //   test_dropin --cpu    argument / no-device behaviour only
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -56,6 +57,65 @@ static void same_as_oracle(Graph& g, int gpus = 1) {
   const VerifyReport rep = verify_mst(g, r, oracle);
   CHECK(rep.all_ok());
   if (!rep.all_ok()) std::fprintf(stderr, "  %s\n", rep.details.c_str());
+  CHECK(verify_mst_gpu(g, r, oracle).all_ok());
+}
+
+// verify_mst_gpu must report exactly what the reference's verify_mst does
+// (verify.cpp:15-57): the five flags and the details line.
+static void same_report(const Graph& g, const MstResult& r, const MstResult& oracle) {
+  const VerifyReport a = verify_mst(g, r, oracle);
+  const VerifyReport b = verify_mst_gpu(g, r, oracle);
+  CHECK(a.is_spanning == b.is_spanning);
+  CHECK(a.is_acyclic == b.is_acyclic);
+  CHECK(a.edge_count_ok == b.edge_count_ok);
+  CHECK(a.weight_matches_oracle == b.weight_matches_oracle);
+  CHECK(a.edge_set_matches_oracle == b.edge_set_matches_oracle);
+  CHECK(a.details == b.details);
+  if (a.details != b.details) std::fprintf(stderr, "  ref: %s\n  gpu: %s\n", a.details.c_str(), b.details.c_str());
+}
+
+static void verifier_cases() {
+  Graph g = generate_graph(3000, 6, 2);
+  const MstResult oracle = kruskal_oracle(g);
+  same_report(g, oracle, oracle);
+  MstResult r = oracle;
+  r.mst_edges.pop_back();  // one edge short: not spanning
+  same_report(g, r, oracle);
+  r = oracle;
+  r.mst_edges.back() = r.mst_edges.front();  // duplicate: a cycle, one short
+  same_report(g, r, oracle);
+  r = oracle;
+  std::vector<bool> in(static_cast<std::size_t>(g.edge_count()), false);
+  for (EdgeId e : oracle.mst_edges) in[static_cast<std::size_t>(e)] = true;
+  EdgeId other = 0;
+  while (in[static_cast<std::size_t>(other)]) ++other;
+  r.mst_edges[r.mst_edges.size() / 2] = other;  // a non-MST edge swapped in
+  same_report(g, r, oracle);
+  r = oracle;
+  std::reverse(r.mst_edges.begin(), r.mst_edges.end());  // order does not matter
+  same_report(g, r, oracle);
+  r = oracle;
+  r.total_weight += 1;  // the result's own total disagrees with its edges
+  same_report(g, r, oracle);
+  r = oracle;
+  r.mst_edges.push_back(g.edge_count());  // outside [0, m)
+  CHECK(throws<std::out_of_range>([&] { verify_mst(g, r, oracle); }));
+  CHECK(throws<std::out_of_range>([&] { verify_mst_gpu(g, r, oracle); }));
+}
+
+// binary SoA round trip through the reference's build_graph (host only)
+static void io_cases() {
+  Graph g = generate_graph(3000, 6, 5);
+  const std::string path = "/tmp/test_dropin_soa.mstb";
+  save_graph_soa(g, path);
+  const Graph h = load_graph_soa(path);
+  CHECK(h.vertex_count() == g.vertex_count() && h.edge_count() == g.edge_count());
+  bool same = true;
+  for (EdgeId i = 0; i < g.edge_count(); ++i)
+    same = same && h.edge(i).src == g.edge(i).src && h.edge(i).dest == g.edge(i).dest &&
+           h.edge(i).weight == g.edge(i).weight;
+  CHECK(same);
+  std::remove(path.c_str());
 }
 
 int main(int argc, char** argv) {
@@ -65,6 +125,7 @@ int main(int argc, char** argv) {
     CHECK(throws<std::invalid_argument>([&] { boruvka_gpu(g, 0); }));   // boruvka_parallel.cpp:86
     CHECK(throws<std::invalid_argument>([&] { boruvka_gpu(g, -2); }));
   }
+  io_cases();  // host-only: no device needed
   if (cpu_only) {
     Graph g = triangle();
     CHECK(throws<WorkerPanic>([&] { boruvka_gpu(g); }));  // no device: loud, no CPU fallback
@@ -142,6 +203,7 @@ int main(int argc, char** argv) {
       CHECK(r.mst_edges.size() == k.n - 1);
     }
   }
+  verifier_cases();
   std::printf("drop-in checks: %d passed, %d failed\n", g_pass, g_fail);
   return g_fail ? 1 : 0;
 }
