@@ -343,6 +343,7 @@ void init_counters(Workspace& ws, DevCounters* d_ctr, uint32_t n, uint64_t m) {
   h.stop_round = kNoStop;
   h.phase_end = kNoStop;
   h.pivot = 0xFFFFFFFFu;
+  h.fin_round = kNoStop;
   MST_CUDA_CHECK(cudaMemcpyAsync(d_ctr, &h, sizeof(DevCounters), cudaMemcpyHostToDevice, ws.stream));
 }
 
@@ -661,13 +662,32 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
         trace = ws.get<unsigned long long>("tail_trace", 512);
         MST_CUDA_CHECK(cudaMemsetAsync(trace, 0, 512 * 8, s));
       }
-      TailArgs ta{{E[0], E[1]}, {minb[0], minb[1]}, parent, rootlabel, L, mst, bcount, M, flags, trace, d_ctr, n, r,
-                  (int)light};
+      // finisher hand-off (plain loop / phase D only): cleared pair table
+      const bool fin = !light && !tail_v2 && env_int("MST_FINISH", 0) != 0;
+      unsigned long long* fin_table = nullptr;
+      if (fin) {
+        fin_table = ws.get<unsigned long long>("fin_table", 2ull * kFinTableSlots);
+        MST_CUDA_CHECK(cudaMemsetAsync(fin_table, 0xFF, 16ull * kFinTableSlots, s));
+        MST_CUDA_CHECK(cudaMemsetAsync(&d_ctr->fin_round, 0xFF, sizeof(unsigned int), s));
+      }
+      TailArgs ta{{E[0], E[1]}, {minb[0], minb[1]}, parent, rootlabel, L, mst, bcount, M, flags, trace,
+                  fin_table, kFinTableSlots - 1ull, d_ctr, n, r, (int)light};
       void* args[] = {&ta};
       hot_begin(kHotTail, r, light);
       MST_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)kt, G, kBlock, args, 0, s));
-      tmark();
       ++launches;
+      if (fin) {
+        static const bool attr_set = [] {
+          MST_CUDA_CHECK(cudaFuncSetAttribute(k_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, kFinSmem));
+          return true;
+        }();
+        (void)attr_set;
+        FinArgs fa{{E[0], E[1]}, mst, flags, trace ? trace + 448 : nullptr, d_ctr, n};
+        k_finish<<<1, kFinThreads, kFinSmem, s>>>(fa);
+        MST_CUDA_CHECK(cudaGetLastError());
+        ++launches;
+      }
+      tmark();
       MST_CUDA_CHECK(cudaMemcpyAsync(&ws.h_snap[kMaxR - 1], d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
       MST_CUDA_CHECK(cudaStreamSynchronize(s));
       const DevCounters& snap = ws.h_snap[kMaxR - 1];
@@ -675,8 +695,15 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
         std::vector<unsigned long long> tt(512);
         MST_CUDA_CHECK(cudaMemcpy(tt.data(), trace, 512 * 8, cudaMemcpyDeviceToHost));
         fprintf(stderr, "tail r0=%d G=%u:", r, G);
-        for (int i = 1; i < 512 && tt[i]; ++i) fprintf(stderr, " %.1f", (tt[i] - tt[i - 1]) * 1e-3);
+        for (int i = 1; i < 448 && tt[i]; ++i) fprintf(stderr, " %.1f", (tt[i] - tt[i - 1]) * 1e-3);
         fprintf(stderr, " (us per phase: H1 H2 L C1 C2 per round)\n");
+        if (tt[448]) {
+          int last = 0;
+          while (last + 1 < 448 && tt[last + 1]) ++last;
+          fprintf(stderr, "finish: hand-off %.1f |", (tt[448] - tt[last]) * 1e-3);
+          for (int i = 449; i < 512 && tt[i]; ++i) fprintf(stderr, " %.1f", (tt[i] - tt[i - 1]) * 1e-3);
+          fprintf(stderr, " (us: load, then per round: min hook jump label relabel)\n");
+        }
       }
       if (snap.err || snap.stop_round != kNoStop) break;
       if (light && snap.phase_end != kNoStop) {

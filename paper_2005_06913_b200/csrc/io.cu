@@ -27,6 +27,9 @@
 #include <charconv>
 #include <cstring>
 #include <limits>
+#include <map>
+#include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -166,6 +169,31 @@ void pwrite_all(int fd, const void* src, size_t len, uint64_t off, const std::st
     if (r <= 0) fail(MST_ERR_IO, path + ": write failed");
     done += (size_t)r;
   }
+}
+
+struct Staging {
+  static constexpr size_t kChunk = 32u << 20;
+  std::mutex mu;
+  void* buf[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  cudaStream_t stream = nullptr;
+};
+
+Staging& staging_for(int dev) {
+  static std::mutex mu;
+  static std::map<int, std::unique_ptr<Staging>> pool;
+  std::lock_guard<std::mutex> lock(mu);
+  auto& slot = pool[dev];
+  if (!slot) {
+    auto s = std::make_unique<Staging>();
+    MST_CUDA_CHECK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+      MST_CUDA_CHECK(cudaHostAlloc(&s->buf[b], Staging::kChunk, cudaHostAllocDefault));
+      MST_CUDA_CHECK(cudaEventCreateWithFlags(&s->ev[b], cudaEventDisableTiming));
+    }
+    slot = std::move(s);
+  }
+  return *slot;
 }
 
 }  // namespace
@@ -394,46 +422,28 @@ int mst_io_load_soa(const char* path, uint32_t n, uint64_t m, uint32_t* src, uin
       return MST_OK;
     }
     // file -> two pinned chunks -> HBM: the read of chunk k+1 overlaps the
-    // copy of chunk k
-    constexpr size_t kChunk = 32u << 20;
-    void* stage[2] = {nullptr, nullptr};
-    cudaStream_t s = nullptr;
-    cudaEvent_t ev[2] = {nullptr, nullptr};
-    auto cleanup = [&]() {
-      if (s) cudaStreamSynchronize(s);
-      for (int b = 0; b < 2; ++b) {
-        if (stage[b]) cudaFreeHost(stage[b]);
-        if (ev[b]) cudaEventDestroy(ev[b]);
+    // copy of chunk k. The staging pair lives for the process (one per
+    // device), so small files do not pay for pinned allocations.
+    int dev = 0;
+    MST_CUDA_CHECK(cudaGetDevice(&dev));
+    Staging& sg = staging_for(dev);
+    std::lock_guard<std::mutex> lock(sg.mu);
+    bool busy[2] = {false, false};
+    uint64_t k = 0;
+    for (int a = 0; a < 3; ++a) {
+      const uint64_t bytes = m * 4;
+      for (uint64_t off = 0; off < bytes; off += Staging::kChunk, ++k) {
+        const int b = (int)(k & 1);
+        const size_t len = (size_t)std::min<uint64_t>(Staging::kChunk, bytes - off);
+        if (busy[b]) MST_CUDA_CHECK(cudaEventSynchronize(sg.ev[b]));
+        pread_all(f.fd, sg.buf[b], len, offs[a] + off, P);
+        MST_CUDA_CHECK(cudaMemcpyAsync(reinterpret_cast<char*>(outs[a]) + off, sg.buf[b], len,
+                                       cudaMemcpyHostToDevice, sg.stream));
+        MST_CUDA_CHECK(cudaEventRecord(sg.ev[b], sg.stream));
+        busy[b] = true;
       }
-      if (s) cudaStreamDestroy(s);
-    };
-    try {
-      MST_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-      for (int b = 0; b < 2; ++b) {
-        MST_CUDA_CHECK(cudaHostAlloc(&stage[b], kChunk, cudaHostAllocDefault));
-        MST_CUDA_CHECK(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
-      }
-      bool busy[2] = {false, false};
-      uint64_t k = 0;
-      for (int a = 0; a < 3; ++a) {
-        const uint64_t bytes = m * 4;
-        for (uint64_t off = 0; off < bytes; off += kChunk, ++k) {
-          const int b = (int)(k & 1);
-          const size_t len = (size_t)std::min<uint64_t>(kChunk, bytes - off);
-          if (busy[b]) MST_CUDA_CHECK(cudaEventSynchronize(ev[b]));
-          pread_all(f.fd, stage[b], len, offs[a] + off, P);
-          MST_CUDA_CHECK(cudaMemcpyAsync(reinterpret_cast<char*>(outs[a]) + off, stage[b], len,
-                                         cudaMemcpyHostToDevice, s));
-          MST_CUDA_CHECK(cudaEventRecord(ev[b], s));
-          busy[b] = true;
-        }
-      }
-      MST_CUDA_CHECK(cudaStreamSynchronize(s));
-    } catch (...) {
-      cleanup();
-      throw;
     }
-    cleanup();
+    MST_CUDA_CHECK(cudaStreamSynchronize(sg.stream));
     return MST_OK;
   });
 }

@@ -70,6 +70,9 @@ struct DevCounters {
   unsigned int live[kMaxR];        // tail v2: live edges entering round r
   unsigned int mst_fill;           // tail v2: next free MST slot
   unsigned int pair_abort[kMaxR];  // table overflowed: keep every edge this round
+  unsigned int fin_round;          // round handed from k_tail to k_finish (kNoStop: none)
+  unsigned int fin_m;              // edges of the deduplicated list k_finish starts from
+  unsigned int fin_pairs[kMaxR];   // distinct component pairs seen by k_tail's dedup
 };
 
 
@@ -1165,6 +1168,8 @@ struct TailArgs {
   uint32_t* M;       // light phase: entry-label -> current-label map (n[r0] entries)
   uint8_t* flags;    // MST edge flags (sorted output)
   unsigned long long* trace;  // optional: globaltimer stamps at phase boundaries (block 0)
+  unsigned long long* fin_table;  // finisher hand-off: pair table ({pair, key} slots), cleared
+  unsigned long long fin_mask;    // slots - 1
   DevCounters* ctr;
   uint32_t n_orig;
   int r0;
@@ -1172,6 +1177,58 @@ struct TailArgs {
 };
 
 constexpr uint32_t kTailSmemMin = 4096;  // block-local min table entries (32 KB)
+
+// ------------------------------ finisher -----------------------------------
+// The last rounds have few components but, on meshes and R-MAT cores, still
+// many parallel edges between them, and every grid-wide step costs a grid
+// sync plus a chain of L2 round trips (~4 us). Once n_r <= kFinC, k_tail
+// keeps only the lightest edge of every component pair (cycle property:
+// exact) in an ordered compaction and, if at most kFinE pairs remain, hands
+// off to k_finish: ONE block that runs every remaining round in shared
+// memory (__syncthreads instead of grid syncs, smem atomics instead of L2).
+// Keys stay (w << 32 | position) over an order-preserving list, so ties
+// fall exactly as in the grid-wide rounds.
+constexpr uint32_t kFinC = 8192;   // components (u16 labels)
+constexpr uint32_t kFinE = 15872;  // deduplicated edges
+constexpr int kFinThreads = 1024;
+constexpr uint32_t kFinSmem = kFinC * (8 + 2 + 2) + kFinE * 8;
+constexpr uint32_t kFinTableSlots = 1u << 15;  // >= 2 x kFinE
+constexpr uint32_t kFinOverflow = 1u << 24;
+
+// Insert pair(x, y) with key into the finisher table; 1 if the pair is new,
+// kFinOverflow if no slot was found.
+__device__ __forceinline__ uint32_t fin_insert(unsigned long long* t, unsigned long long mask, uint32_t x,
+                                               uint32_t y, unsigned long long key) {
+  const unsigned long long pair = ((unsigned long long)min(x, y) << 32) | max(x, y);
+  unsigned long long h = pair_hash(pair) & mask;
+  for (int probe = 0; probe < kPairProbes; ++probe) {
+    unsigned long long cur = __ldcg(t + 2 * h);
+    uint32_t fresh = 0;
+    if (cur == kNoKey) {
+      cur = atomicCAS(t + 2 * h, kNoKey, pair);
+      fresh = cur == kNoKey;
+      if (fresh) cur = pair;
+    }
+    if (cur == pair) {
+      if (key < __ldcg(t + 2 * h + 1)) atomicMin(t + 2 * h + 1, key);
+      return fresh;
+    }
+    h = (h + 1) & mask;
+  }
+  return kFinOverflow;
+}
+
+__device__ __forceinline__ bool fin_keep(const unsigned long long* t, unsigned long long mask, uint32_t x,
+                                         uint32_t y, unsigned long long key) {
+  const unsigned long long pair = ((unsigned long long)min(x, y) << 32) | max(x, y);
+  unsigned long long h = pair_hash(pair) & mask;
+  for (int probe = 0; probe < kPairProbes; ++probe) {
+    const ulonglong2 slot = __ldcg(reinterpret_cast<const ulonglong2*>(t) + h);
+    if (slot.x == pair) return slot.y == key;
+    h = (h + 1) & mask;
+  }
+  return true;  // unreachable when every insert succeeded
+}
 
 // Ordered ranks of kItems striped flags per thread; returns the total.
 __device__ __forceinline__ uint32_t block_ranks(const bool (&f)[kItems], uint32_t (&rank)[kItems],
@@ -1214,7 +1271,7 @@ __device__ __forceinline__ uint32_t block_prefix(const uint32_t* bcount, uint32_
 }
 
 __device__ __forceinline__ void tail_stamp(const TailArgs& a, int& slot) {
-  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && slot < 512) {
+  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && slot < 448) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     a.trace[slot] = t;
@@ -1223,7 +1280,7 @@ __device__ __forceinline__ void tail_stamp(const TailArgs& a, int& slot) {
 }
 
 template <bool kWarpPre>
-__global__ void __launch_bounds__(kBlock) k_tail(TailArgs a) {
+__global__ void __launch_bounds__(kBlock, 2) k_tail(TailArgs a) {
   pdl_prologue();
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
@@ -1236,6 +1293,7 @@ __global__ void __launch_bounds__(kBlock) k_tail(TailArgs a) {
   const uint32_t G = gridDim.x, b = blockIdx.x;
   volatile DevCounters* vc = a.ctr;
   const uint32_t n_entry = vc->n[a.r0];
+  uint32_t fin_next = kFinC;  // finisher hand-off tried once n_r <= fin_next
   for (int r = a.r0; r < kMaxR - 1; ++r) {
     if ((uint32_t)r >= vc->stop_round || (uint32_t)r >= vc->phase_end) break;
     const uint32_t n_r = vc->n[r];
@@ -1246,6 +1304,105 @@ __global__ void __launch_bounds__(kBlock) k_tail(TailArgs a) {
     unsigned long long* mnext = (r & 1) ? a.minb[1] : a.minb[0];
     uint4* Ecur = (r & 1) ? a.E[1] : a.E[0];
     uint4* Enext = (r & 1) ? a.E[0] : a.E[1];
+    if (a.fin_table && !a.light && n_r <= fin_next) {
+      // ---- F1: lightest edge per component pair into the table
+      const uint64_t es = (m_r + G - 1) / G;
+      const uint64_t elo = min((uint64_t)b * es, m_r), ehi = min(elo + es, m_r);
+      uint32_t fresh = 0;
+      for (uint64_t base = elo; base < ehi; base += kBlock * kItems) {
+        // kItems edges in flight per thread: most pairs are already in the
+        // table, so one 16 B slot load decides and a RED min finishes
+        uint4 e[kItems];
+        ulonglong2 sl[kItems];
+        unsigned long long pr[kItems], h[kItems];
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          const uint64_t i = base + k * kBlock + threadIdx.x;
+          e[k] = i < ehi ? __ldcg(Ecur + i) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          pr[k] = ((unsigned long long)min(e[k].x, e[k].y) << 32) | max(e[k].x, e[k].y);
+          h[k] = pair_hash(pr[k]) & a.fin_mask;
+          sl[k] = __ldcg(reinterpret_cast<const ulonglong2*>(a.fin_table) + h[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          const uint64_t i = base + k * kBlock + threadIdx.x;
+          if (i >= ehi) continue;
+          const unsigned long long key = ((unsigned long long)e[k].z << 32) | (uint32_t)i;
+          if (sl[k].x == pr[k]) {
+            if (key < sl[k].y) atomicMin(a.fin_table + 2 * h[k] + 1, key);
+          } else {
+            fresh += fin_insert(a.fin_table, a.fin_mask, e[k].x, e[k].y, key);
+          }
+        }
+      }
+      fresh = warp_sum<uint32_t>(fresh);
+      if (lane_id() == 0 && fresh) atomicAdd(&a.ctr->fin_pairs[r], fresh);
+      grid.sync();
+      tail_stamp(a, slot);
+      if (vc->fin_pairs[r] <= kFinE) {
+        // ---- F2: kept edges per block; F3: ordered compaction, hand-off
+        uint32_t kept = 0;
+        for (uint64_t base = elo; base < ehi; base += kBlock * kItems) {
+          uint4 e[kItems];
+#pragma unroll
+          for (int k = 0; k < kItems; ++k) {
+            const uint64_t i = base + k * kBlock + threadIdx.x;
+            e[k] = i < ehi ? __ldcg(Ecur + i) : make_uint4(0, 0, 0, 0);
+          }
+#pragma unroll
+          for (int k = 0; k < kItems; ++k) {
+            const uint64_t i = base + k * kBlock + threadIdx.x;
+            if (i < ehi)
+              kept += fin_keep(a.fin_table, a.fin_mask, e[k].x, e[k].y,
+                               ((unsigned long long)e[k].z << 32) | (uint32_t)i);
+          }
+        }
+        kept = warp_sum<uint32_t>(kept);
+        if (lane_id() == 0) s_cnt[threadIdx.x >> 5] = kept;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          uint32_t t = 0;
+          for (int i = 0; i < kWarps; ++i) t += s_cnt[i];
+          a.bcount[b] = t;
+        }
+        __syncthreads();
+        grid.sync();
+        tail_stamp(a, slot);
+        uint32_t running = block_prefix(a.bcount, b, s_misc);
+        for (uint64_t base = elo; base < ehi; base += kBlock * kItems) {
+          bool f[kItems];
+          uint32_t rank[kItems];
+          uint4 e[kItems];
+#pragma unroll
+          for (int k = 0; k < kItems; ++k) {
+            const uint64_t i = base + k * kBlock + threadIdx.x;
+            e[k] = i < ehi ? __ldcg(Ecur + i) : make_uint4(0, 0, 0, 0);
+            f[k] = i < ehi && fin_keep(a.fin_table, a.fin_mask, e[k].x, e[k].y,
+                                       ((unsigned long long)e[k].z << 32) | (uint32_t)i);
+          }
+          const uint32_t tot = block_ranks(f, rank, s_cnt);
+#pragma unroll
+          for (int k = 0; k < kItems; ++k)
+            if (f[k]) Enext[running + rank[k]] = e[k];
+          running += tot;
+        }
+        if (b == G - 1 && threadIdx.x == 0) {
+          a.ctr->fin_m = running;
+          a.ctr->fin_round = (uint32_t)r;
+        }
+        return;  // k_finish continues from Enext
+      }
+      // too many pairs for one block: clear the table, retry once the
+      // components have shrunk 4x (the clear is ordered before the next
+      // attempt by the rounds' grid syncs)
+      for (unsigned long long i = (unsigned long long)b * kBlock + threadIdx.x; i <= a.fin_mask;
+           i += (unsigned long long)G * kBlock)
+        reinterpret_cast<ulonglong2*>(a.fin_table)[i] = make_ulonglong2(kNoKey, kNoKey);
+      fin_next = n_r / 4;
+    }
     // ---- H1: hook decisions over this block's component chunk
     const uint32_t cs = (n_r + G - 1) / G;
     const uint32_t clo = min(b * cs, n_r), chi = min(clo + cs, n_r);
@@ -1479,6 +1636,199 @@ __global__ void __launch_bounds__(kBlock) k_tail(TailArgs a) {
     }
     grid.sync();
     tail_stamp(a, slot);
+  }
+}
+
+// Exclusive block-wide scan of one value per thread (kFinThreads threads).
+__device__ __forceinline__ uint32_t fin_scan(uint32_t v, uint32_t* s_warp, uint32_t* s_total) {
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint32_t incl = warp_incl_scan(v);
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t t = s_warp[lane];
+    const uint32_t ti = warp_incl_scan(t);
+    s_warp[lane] = ti - t;
+    if (lane == 31) *s_total = ti;
+  }
+  __syncthreads();
+  const uint32_t out = s_warp[warp] + incl - v;
+  __syncthreads();
+  return out;
+}
+
+struct FinArgs {
+  const uint4* E[2];
+  uint32_t* mst;
+  uint8_t* flags;
+  unsigned long long* trace;  // optional: globaltimer at entry, after the load, after each round
+  DevCounters* ctr;
+  uint32_t n_orig;
+};
+
+__device__ __forceinline__ void fin_stamp(const FinArgs& a, int& slot) {
+  if (a.trace && threadIdx.x == 0 && slot < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[slot] = t;
+  }
+  ++slot;
+}
+
+// All remaining rounds in one block: edges {a | b << 16, w} and the per-
+// component key / parent / label arrays live in shared memory. Same hook
+// rule, MST slots, counters and verdicts as the grid-wide rounds.
+__global__ void __launch_bounds__(kFinThreads, 1) k_finish(FinArgs a) {
+  pdl_prologue();
+  volatile DevCounters* vc = a.ctr;
+  const uint32_t r0 = vc->fin_round;
+  if (r0 == kNoStop) return;
+  extern __shared__ unsigned long long fin_smem[];
+  // per component: lightest weight, then the lowest position among the edges
+  // of that weight = the (w << 32 | position) minimum, with two native 32-bit
+  // shared atomics instead of a 64-bit CAS loop
+  uint32_t* mw = reinterpret_cast<uint32_t*>(fin_smem);                 // [kFinC]
+  uint32_t* mi = mw + kFinC;                                            // [kFinC]
+  uint32_t* ab = mi + kFinC;                                            // [kFinE]
+  uint32_t* wt = ab + kFinE;                                            // [kFinE]
+  uint16_t* par = reinterpret_cast<uint16_t*>(wt + kFinE);              // [kFinC]
+  uint16_t* lab = par + kFinC;                                          // [kFinC]
+  __shared__ uint32_t s_warp[32], s_total;
+  __shared__ unsigned long long s_wsum[32];
+  const uint32_t T = kFinThreads, tid = threadIdx.x;
+  int tslot = 0;
+  fin_stamp(a, tslot);
+  const uint4* E = (r0 & 1) ? a.E[0] : a.E[1];  // k_tail's Enext of round r0
+  const uint32_t m = vc->fin_m;
+  uint32_t n = vc->n[r0];
+  for (uint32_t i = tid; i < m; i += T) {
+    const uint4 e = __ldcg(E + i);
+    ab[i] = e.x | (e.y << 16);
+    wt[i] = e.z;
+  }
+  __syncthreads();
+  fin_stamp(a, tslot);
+  unsigned long long wsum = 0;
+  uint32_t r = r0;
+  while (true) {
+    if (r + 2 >= (uint32_t)kMaxR) {
+      if (tid == 0) a.ctr->err |= 4u;  // no convergence (cannot happen: n halves per round)
+      break;
+    }
+    const uint32_t mst_base = a.n_orig - n;
+    for (uint32_t c = tid; c < n; c += T) {
+      mw[c] = kNone;
+      mi[c] = kNone;
+    }
+    __syncthreads();
+    for (uint32_t i = tid; i < m; i += T) {
+      const uint32_t e = ab[i], x = e & 0xFFFFu, y = e >> 16;
+      if (x == y) continue;
+      const uint32_t w = wt[i];
+      if (w < mw[x]) atomicMin(mw + x, w);
+      if (w < mw[y]) atomicMin(mw + y, w);
+    }
+    __syncthreads();
+    for (uint32_t i = tid; i < m; i += T) {
+      const uint32_t e = ab[i], x = e & 0xFFFFu, y = e >> 16;
+      if (x == y) continue;
+      const uint32_t w = wt[i];
+      if (w == mw[x] && i < mi[x]) atomicMin(mi + x, i);
+      if (w == mw[y] && i < mi[y]) atomicMin(mi + y, i);
+    }
+    __syncthreads();
+    fin_stamp(a, tslot);
+    // hook: partner along the lightest edge; a mutual pair (same edge) keeps
+    // the lower label as root
+    for (uint32_t c = tid; c < n; c += T) {
+      const uint32_t i = mi[c];
+      uint32_t p = c;
+      if (i != kNone) {
+        const uint32_t e = ab[i], x = e & 0xFFFFu, y = e >> 16;
+        const uint32_t o = x == c ? y : x;
+        if (!(mi[o] == i && c < o)) {
+          p = o;
+          wsum += mw[c];
+        }
+      }
+      par[c] = (uint16_t)p;
+    }
+    __syncthreads();
+    fin_stamp(a, tslot);
+    while (true) {  // pointer jumping to the roots
+      int changed = 0;
+      for (uint32_t c = tid; c < n; c += T) {
+        const uint32_t p = par[c], pp = par[p];
+        if (p != pp) {
+          par[c] = (uint16_t)pp;
+          changed = 1;
+        }
+      }
+      if (!__syncthreads_or(changed)) break;
+    }
+    fin_stamp(a, tslot);
+    // dense root labels in component order; MST slots of hooked components
+    const uint32_t per = (n + T - 1) / T, lo = min(tid * per, n), hi = min(lo + per, n);
+    uint32_t cnt = 0;
+    for (uint32_t c = lo; c < hi; ++c) cnt += par[c] == c;
+    uint32_t run = fin_scan(cnt, s_warp, &s_total);
+    const uint32_t n_next = s_total;
+    // the hooked components' edge ids: independent L2 loads, all in flight
+    constexpr int kPer = kFinC / kFinThreads;
+    uint32_t eids[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const uint32_t c = lo + j;
+      eids[j] = (c < hi && par[c] != c) ? __ldcg(&E[mi[c]].w) : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const uint32_t c = lo + j;
+      if (c >= hi) break;
+      if (par[c] == c) {
+        lab[c] = (uint16_t)run++;
+      } else {
+        a.mst[mst_base + (c - run)] = eids[j];
+        if (a.flags) a.flags[eids[j]] = 1;
+      }
+    }
+    __syncthreads();
+    for (uint32_t c = lo; c < hi; ++c)
+      if (par[c] != c) lab[c] = lab[par[c]];
+    __syncthreads();
+    fin_stamp(a, tslot);
+    if (tid == 0) a.ctr->n[r + 1] = n_next;
+    if (n_next <= 1 || n_next == n) {
+      if (tid == 0) a.ctr->stop_round = r + 1;
+      break;
+    }
+    uint32_t live = 0;
+    for (uint32_t i = tid; i < m; i += T) {
+      const uint32_t e = ab[i], x = e & 0xFFFFu, y = e >> 16;
+      if (x == y) continue;
+      const uint32_t nx = lab[x], ny = lab[y];
+      ab[i] = nx | (ny << 16);
+      live += nx != ny;
+    }
+    fin_scan(live, s_warp, &s_total);
+    const uint32_t live_total = s_total;
+    if (tid == 0) a.ctr->m[r + 1] = live_total;
+    if (live_total == 0) {
+      if (tid == 0) a.ctr->stop_round = r + 1;
+      break;
+    }
+    n = n_next;
+    ++r;
+    fin_stamp(a, tslot);
+  }
+  fin_stamp(a, tslot);
+  wsum = warp_sum<unsigned long long>(wsum);
+  if (lane_id() == 0) s_wsum[tid >> 5] = wsum;
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long t = 0;
+    for (int i = 0; i < kFinThreads / 32; ++i) t += s_wsum[i];
+    if (t) atomicAdd(&a.ctr->total_weight, t);
   }
 }
 

@@ -44,7 +44,9 @@ MODES = [dict(MST_FILTER=0), dict(MST_FILTER=1, MST_FILTER_BETA=0.3),
          dict(MST_FILTER=1, MST_FILTER_BETA=2), dict(MST_FILTER=1, MST_FILTER_BETA=50),
          # every round through the separate kernels with the pair-dedup variant armed
          dict(MST_FILTER=0, MST_TAIL=0, MST_DEDUP_MIN_EDGES=0),
-         dict(MST_FILTER=1, MST_TAIL=0, MST_DEDUP_MIN_EDGES=0)]
+         dict(MST_FILTER=1, MST_TAIL=0, MST_DEDUP_MIN_EDGES=0),
+         # the tail hands the last rounds to the one-block finisher
+         dict(MST_FILTER=0, MST_FINISH=1)]
 
 
 def _check(P, n, src, dst, w, ids, total, shards=(2, 3), modes=MODES):
