@@ -127,6 +127,30 @@ def reference_cpu(g, threads: int, runs: int):
     return times, res
 
 
+CPU_SAMPLE_EDGES = 20_000_000  # above this the CPU legs run a scaled instance (10-30 s of work)
+
+
+def cpu_sample(spec):
+    """The graph the CPU legs time: the workload itself when it is small, else
+    an instance of the same generator family and density scaled to ~16-17 M
+    edges (the unchanged reference CAS scans every edge every round, so the
+    full c3/c4 graphs would take from minutes to hours)."""
+    from paper_2005_06913_b200 import configs as C
+    m = C.edge_count(spec)
+    if m <= CPU_SAMPLE_EDGES:
+        return spec, f"full {spec.name} graph"
+    if spec.kind == 0:
+        n2 = 1 << 20
+        sub = C.uniform(n2, n2 * (spec.m // spec.n), seed=spec.seed, name=f"{spec.name}_sample_n{n2}")
+        return sub, (f"scaled {spec.name}: uniform n={n2}, m={sub.m} (same density {spec.m // spec.n}, "
+                     f"same generator and seed)")
+    if spec.kind == 2:
+        sub = C.rmat(20, spec.edgefactor, seed=spec.seed, name=f"{spec.name}_sample_s20")
+        return sub, (f"scaled {spec.name}: R-MAT scale 20, edgefactor {spec.edgefactor} (same generator, "
+                     f"parameters and seed)")
+    return spec, f"full {spec.name} graph"
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -134,7 +158,7 @@ def run_reference(args):
     from oracle import oracle as O
     from paper_2005_06913_b200 import configs as C
 
-    spec = C.CONFIGS[args.config]
+    spec, sample = cpu_sample(C.CONFIGS[args.config])
     g = C.generate_host(spec)
     m = g.edge_count()
     if not O.ref_available():
@@ -157,7 +181,7 @@ def run_reference(args):
                    "path": "mst::boruvka_cas (unchanged reference, oracle/_ref) via SURVEY §8(c) adapter",
                    "m_prime": r.m_prime, "timer": "reference MstResult::elapsed_ms"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": f"full {spec.name} graph, {args.steps} runs of boruvka_cas(T={threads})"},
+                         "sample": f"{sample}, {args.steps} runs of boruvka_cas(T={threads})"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -287,14 +311,15 @@ def run_ours(args):
     if world == 1 and not args.no_cpu_baseline:
         try:
             from oracle import oracle as O
-            hg = g if e2e is not None else C.generate_host(spec)
+            cspec, sample = cpu_sample(spec)
+            hg = g if (e2e is not None and cspec is spec) else C.generate_host(cspec)
             threads = O.hardware_threads()
             rr = reference_cpu(hg, threads, runs=1)
             if rr is not None:
                 times, res = rr
-                cpu = {"value": m / (float(np.mean(times)) / 1e3), "unit": UNIT, "cores": threads,
+                cpu = {"value": hg.edge_count() / (float(np.mean(times)) / 1e3), "unit": UNIT, "cores": threads,
                        "kind": "reference",
-                       "sample": f"full {spec.name} graph, 1 run of unchanged boruvka_cas(T={threads}) "
+                       "sample": f"{sample}, 1 run of unchanged boruvka_cas(T={threads}) "
                                  f"(m'={res.m_prime} after the §8(c) adapter), reference elapsed_ms"}
         except Exception as ex:  # reported, not fatal
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"failed: {ex}"}

@@ -51,6 +51,23 @@ def build_library(force: bool = False, verbose: bool = True) -> Path:
     return LIB
 
 
+CLI = PKG / "mstbench_gpu"
+
+
+def build_cli(force: bool = False, verbose: bool = True) -> Path:
+    """mstbench_gpu: the reference's benchmark CLI re-hosted on the C ABI."""
+    src = CSRC / "mstbench_gpu.cpp"
+    deps = [src, ROOT / "include" / "mst_gpu.h", LIB]
+    if force or _stale(CLI, deps):
+        cuda = Path(_nvcc()).resolve().parent.parent
+        cmd = [shutil.which("g++") or "g++", "-std=c++17", "-O2", "-Wall", f"-I{cuda / 'include'}", str(src),
+               "-o", str(CLI), f"-L{PKG}", "-lmstgpu", f"-L{cuda / 'lib64'}", "-lcudart", "-Wl,-rpath,$ORIGIN"]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True, cwd=str(CSRC))
+    return CLI
+
+
 def build_oracle(verbose: bool = True) -> None:
     """oracle/liboracle.so always; oracle/_ref when /root/reference exists."""
     targets = ["all"]
@@ -62,4 +79,5 @@ def build_oracle(verbose: bool = True) -> None:
 
 if __name__ == "__main__":
     build_library(force="--force" in sys.argv)
+    build_cli(force="--force" in sys.argv)
     build_oracle()

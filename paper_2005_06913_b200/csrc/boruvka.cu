@@ -598,7 +598,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   const bool dedup_on = env_int("MST_DEDUP", 1) != 0;
   const uint64_t dedup_min_edges = (uint64_t)env_double("MST_DEDUP_MIN_EDGES", 2.0e6);
   const unsigned int dedup_active = (unsigned int)env_double("MST_DEDUP_ACTIVE", 262144);
-  const uint64_t tail_edges = (uint64_t)env_double("MST_TAIL_EDGES", 6.0e6);
+  const uint64_t tail_edges = (uint64_t)env_double("MST_TAIL_EDGES", 3.0e6);
 
   // Light phase over: compose its relabel maps into a vertex -> component map,
   // run the heavy filter pass, continue with the plain loop (phase D).

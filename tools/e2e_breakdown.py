@@ -13,6 +13,7 @@ def main():
     p = argparse.ArgumentParser()
     p.add_argument("--config", default="c1")
     p.add_argument("--reps", type=int, default=5)
+    p.add_argument("--flush", action="store_true", help="512 MiB device write + sync before each call")
     a = p.parse_args()
     import numpy as np
     import torch
@@ -28,7 +29,11 @@ def main():
     info = P.GpuRunInfo()
     for _ in range(2):
         P.boruvka_gpu(g)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     for _ in range(a.reps):
+        if a.flush:
+            flush.zero_()
+            torch.cuda.synchronize()
         t0 = time.perf_counter()
         P.boruvka_gpu(g, info=info)
         wall = (time.perf_counter() - t0) * 1e3
