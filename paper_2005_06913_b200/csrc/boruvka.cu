@@ -15,6 +15,7 @@
 #include <mutex>
 #include <string>
 #include <tuple>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -343,7 +344,6 @@ void init_counters(Workspace& ws, DevCounters* d_ctr, uint32_t n, uint64_t m) {
   h.stop_round = kNoStop;
   h.phase_end = kNoStop;
   h.pivot = 0xFFFFFFFFu;
-  h.fin_round = kNoStop;
   MST_CUDA_CHECK(cudaMemcpyAsync(d_ctr, &h, sizeof(DevCounters), cudaMemcpyHostToDevice, ws.stream));
 }
 
@@ -425,15 +425,6 @@ uint32_t sort_ids(Workspace& ws, const uint32_t* d_ids, uint64_t count, uint64_t
   return launches;
 }
 
-// Warp pre-reduction (__match_any_sync + redux) before the filtered atomicMin
-// costs more than it saves on the BASELINE graphs once the read-first filter
-// is on (c1: 1.25 -> 0.96 ms without it); kept selectable for hub-heavy
-// inputs: MST_WARP_PREREDUCE=1.
-bool warp_prereduce_enabled() {
-  const char* e = getenv("MST_WARP_PREREDUCE");
-  return e && e[0] == '1';
-}
-
 // ------------------------------- single GPU ---------------------------------
 // Literal keys (w<<32 | index into this round's edge array): the hook reads
 // the winning edge directly. The host runs one round ahead of the device;
@@ -479,7 +470,9 @@ struct CompactBufs {
 };
 
 // Ordered compaction as count + emit (kernels.cuh, "two-pass ordered compaction").
-template <class View, int kMode, bool kPre>
+// min_next receives the offers for round r+1: keyed by the position in the
+// input list for every mode but the heavy filter (see k_count).
+template <class View, int kMode>
 void launch_two_pass(Workspace& ws, const CompactBufs& cb, View in, uint4* relabeled, const uint32_t* L, uint4* out,
                      unsigned long long* min_next, DevCounters* d_ctr, int r, uint64_t m_bound, uint32_t n_orig,
                      int slot, int light, int filt, PairTable pt = PairTable{nullptr, nullptr, 0}) {
@@ -493,12 +486,12 @@ void launch_two_pass(Workspace& ws, const CompactBufs& cb, View in, uint4* relab
   // armed: this launch relabels + inserts pairs if the device chose dedup
   // (decided and table cleared by k_label2), the kModeDedup pass counts
   launch_k(kcnt, gc, kBlock, ws.stream, in, kMode == kModeRelabel ? relabeled : cb.stage, L, cb.masks, cb.counts, n_orig,
-                                     d_ctr, r, fused, slot, light, pt);
+           d_ctr, r, fused, slot, light, pt, min_next, filt);
   if constexpr (!View::kOriginal) {
     if (armed) {
-      auto kdc = k_count<View, kModeDedup>;
+      auto kdc = k_count<PackedView, kModeDedup>;
       launch_k(kdc, gc, kBlock, ws.stream, PackedView{relabeled}, cb.stage, L, cb.masks, cb.counts, n_orig, d_ctr, r,
-                                        fused, slot, light, pt);
+               fused, slot, light, pt, min_next, filt);
     }
   }
   if (!fused) {
@@ -506,25 +499,30 @@ void launch_two_pass(Workspace& ws, const CompactBufs& cb, View in, uint4* relab
     const unsigned gs = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((tiles + kScanTile - 1) / kScanTile,
                                                                             (uint64_t)sm_count(dev)));
     launch_k(ksc, gs, kScanBlock, ws.stream, cb.counts, tiles, d_ctr, r, cb.st, ws.next_epoch(), light,
-                                          View::kOriginal ? 1 : 0);
+             View::kOriginal ? 1 : 0);
   }
   const unsigned ge = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)sm_count(dev) * 8));
   if (armed) {
-    auto kde = k_emit_staged<kModeDedup, kPre>;
+    auto kde = k_emit_staged<kModeDedup>;
     launch_k(kde, ge, kBlock, ws.stream, cb.stage, cb.counts, out, min_next, d_ctr, r, filt);
   }
   if (kMode == kModeRelabel) {
-    auto kem = k_emit<View, kMode, kPre>;
-    launch_k(kem, ge, kBlock, ws.stream, in, relabeled, L, cb.masks, cb.counts, out, min_next, d_ctr, r, filt,
-                                      armed ? 1 : 0, n_orig);
+    auto kem = k_emit<View, kMode>;
+    launch_k(kem, ge, kBlock, ws.stream, in, relabeled, L, cb.masks, cb.counts, out, d_ctr, r, armed ? 1 : 0, n_orig);
   } else {
-    auto kes = k_emit_staged<kMode, kPre>;
+    auto kes = k_emit_staged<kMode>;
     launch_k(kes, ge, kBlock, ws.stream, cb.stage, cb.counts, out, min_next, d_ctr, r, filt);
   }
   MST_CUDA_CHECK(cudaGetLastError());
 }
 
-template <class InView, bool kPre>
+enum { kSrcIn = 0, kSrcPairs = 1, kSrcPacked = 2 };
+struct HookSrc {
+  int kind;
+  const uint4* packed;
+};
+
+template <class InView>
 void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t wstride, uint32_t n,
                      uint64_t m, RunOut& out, bool time_hot, bool filter) {
   cudaStream_t s = ws.stream;
@@ -560,6 +558,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     tmark();
   };
 
+  double light_target = (double)m;  // expected light edges (Filter-Borůvka)
   if (filter) {
     uint32_t* hist = ws.get<uint32_t>("hist", 65536);
     MST_CUDA_CHECK(cudaMemsetAsync(hist, 0, 65536 * sizeof(uint32_t), s));
@@ -568,16 +567,17 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     launch_k(k_weight_hist, std::max(1u, samples / 1024), 256, s, wbase, wstride, m, step, samples, hist);
     const double beta = env_double("MST_FILTER_BETA", 1.5);
     const double frac = std::min(1.0, beta * (double)n / (double)m);
+    light_target = frac * (double)m;
     const uint32_t target = (uint32_t)std::max(1.0, frac * samples);
     launch_k(k_pick_pivot, 1, 1024, s, hist, target, d_ctr);
     launches += 2;
     hot_begin(kHotSplit, 0, true);
-    launch_two_pass<InView, kModeLight, kPre>(ws, cb, in, nullptr, nullptr, E[1], minb[0], d_ctr, 0, m, n,
-                                              kSlotCompact, 0, filt_for(n));
+    launch_two_pass<InView, kModeLight>(ws, cb, in, nullptr, nullptr, E[1], minb[0], d_ctr, 0, m, n,
+                                        kSlotCompact, 0, filt_for(n));
     tmark();
     launches += 2;
   } else {
-    auto kmin = k_min_round1<InView, kPre>;
+    auto kmin = k_min_round1<InView>;
     const unsigned g = (unsigned)std::max<uint64_t>(
         1, std::min<uint64_t>((m + 4 * kBlock - 1) / (4 * kBlock), (uint64_t)sm_count(dev) * blocks_per_sm(kmin)));
     hot_begin(kHotMin1, 0, false);
@@ -592,13 +592,17 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   int r = 1, loop_start = 1;
   int phase_end = 0;
   DevCounters snap_b{};  // counters at the end of the light phase
-  const int tail_mode = env_int("MST_TAIL", 1);  // 0 off, 1 compacting tail, 2 sparse-label tail
-  const bool tail_on = tail_mode != 0;
-  const bool tail_v2 = tail_mode == 2;
+  const bool tail_on = env_int("MST_TAIL", 1) != 0;
   const bool dedup_on = env_int("MST_DEDUP", 1) != 0;
   const uint64_t dedup_min_edges = (uint64_t)env_double("MST_DEDUP_MIN_EDGES", 2.0e6);
   const unsigned int dedup_active = (unsigned int)env_double("MST_DEDUP_ACTIVE", 262144);
-  const uint64_t tail_edges = (uint64_t)env_double("MST_TAIL_EDGES", 3.0e6);
+  // Tail entry (m_bound is the host's one-round-stale edge bound). Measured
+  // (tools/sweep_tail.sh): the plain loop and phase D gain from entering
+  // early (c1, c0: 6 M), the light phase from keeping the round kernels,
+  // whose pair dedup the tail lacks, a little longer (c2: 3.02 ms at 3 M vs
+  // 3.19 ms at 6 M).
+  const double tail_env = env_double("MST_TAIL_EDGES", 0.0);
+  auto tail_edges = [&]() -> uint64_t { return (uint64_t)(tail_env > 0 ? tail_env : (light ? 3.0e6 : 6.0e6)); };
 
   // Light phase over: compose its relabel maps into a vertex -> component map,
   // run the heavy filter pass, continue with the plain loop (phase D).
@@ -610,7 +614,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       // not a single light non-loop edge: run the plain loop instead
       MST_CUDA_CHECK(cudaStreamSynchronize(s));
       RunOut plain;
-      run_single_impl<InView, kPre>(ws, in, wbase, wstride, n, m, plain, time_hot, false);
+      run_single_impl<InView>(ws, in, wbase, wstride, n, m, plain, time_hot, false);
       plain.launches += launches;
       out = plain;
       return false;
@@ -627,8 +631,8 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     const int R1 = phase_end;
     hot_begin(kHotHeavy, R1, false);
     // launched as round R1-1's producer: it writes m[R1] and E/min of round R1
-    launch_two_pass<InView, kModeHeavy, kPre>(ws, cb, in, nullptr, vlabel, E[R1 & 1], minb[(R1 - 1) & 1], d_ctr,
-                                              R1 - 1, m, n, kSlotFilter, 0, filt_for(snap.n[R1]));
+    launch_two_pass<InView, kModeHeavy>(ws, cb, in, nullptr, vlabel, E[R1 & 1], minb[(R1 - 1) & 1], d_ctr,
+                                        R1 - 1, m, n, kSlotFilter, 0, filt_for(snap.n[R1]));
     tmark();
     launches += 2;
     light = false;
@@ -639,10 +643,24 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     return true;
   };
 
+  // The list round r's min-table keys index (see k_count): the caller's list
+  // in round 1 of the plain loop, the light split's / heavy filter's output
+  // in the first round after them, round 1's label pairs in round 2 of the
+  // plain loop, else round r-1's list (relabelled in place by its count pass).
+  auto hook_src = [&](int rr) -> HookSrc {
+    if (rr == 1) return filter ? HookSrc{kSrcPacked, E[1]} : HookSrc{kSrcIn, nullptr};
+    if (phase_end && rr == phase_end) return HookSrc{kSrcPacked, E[rr & 1]};
+    if (rr == 2 && !filter) return HookSrc{kSrcPairs, nullptr};
+    return HookSrc{kSrcPacked, E[(rr - 1) & 1]};
+  };
+
   while (true) {
     if (r > MST_MAX_ROUNDS) throw MstError{MST_ERR_STALL, "no convergence within MST_MAX_ROUNDS rounds"};
     const bool original_in = (r == 1 && !filter);
-    if (tail_on && !original_in && m_bound <= tail_edges) {
+    // round 1 of the light phase: the split keeps ~beta*n edges (the pivot's
+    // target), a better bound than m before its count is known
+    const uint64_t m_est = (light && r == 1) ? std::min<uint64_t>(m_bound, (uint64_t)(1.1 * light_target)) : m_bound;
+    if (tail_on && !original_in && m_est <= tail_edges()) {
       // ---- all remaining rounds in one cooperative launch
       uint32_t* M = nullptr;
       if (light) {
@@ -651,42 +669,42 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
             M, n_bound);
         ++launches;
       }
-      auto kt = tail_v2 ? k_tail2
-                        : (getenv("MST_TAIL_PREREDUCE") && getenv("MST_TAIL_PREREDUCE")[0] == '1' ? k_tail<true>
-                                                                                                  : k_tail<false>);
+      auto kt = k_tail;
       const int bps = std::max(1, std::min(blocks_per_sm(kt), env_int("MST_TAIL_BPS", 2)));
-      const unsigned G = (unsigned)(sm_count(dev) * bps);
-      uint32_t* bcount = ws.get<uint32_t>("bcount", G);
+      const unsigned G = std::min<unsigned>(kTailMaxBlocks, (unsigned)(sm_count(dev) * bps));
+      uint32_t* broots = ws.get<uint32_t>("tail_broots", G);
+      uint32_t* bkept = ws.get<uint32_t>("tail_bkept", G);
+      uint32_t* tmasks = ws.get<uint32_t>("tail_masks", n_bound / 32 + 64);
+      uint32_t* twpref = ws.get<uint32_t>("tail_wpref", n_bound / 32 + 64);
       unsigned long long* trace = nullptr;
       if (env_int("MST_TAIL_TRACE", 0)) {
         trace = ws.get<unsigned long long>("tail_trace", 512);
         MST_CUDA_CHECK(cudaMemsetAsync(trace, 0, 512 * 8, s));
       }
-      // finisher hand-off (plain loop / phase D only): cleared pair table
-      const bool fin = !light && !tail_v2 && env_int("MST_FINISH", 0) != 0;
-      unsigned long long* fin_table = nullptr;
-      if (fin) {
-        fin_table = ws.get<unsigned long long>("fin_table", 2ull * kFinTableSlots);
-        MST_CUDA_CHECK(cudaMemsetAsync(fin_table, 0xFF, 16ull * kFinTableSlots, s));
-        MST_CUDA_CHECK(cudaMemsetAsync(&d_ctr->fin_round, 0xFF, sizeof(unsigned int), s));
+      const HookSrc src = hook_src(r);
+      TailArgs ta{{E[0], E[1]}, {minb[0], minb[1]}, parent, rootlabel, L, mst, broots, bkept, tmasks, twpref, M, flags,
+                  trace, 0, nullptr, nullptr, nullptr, 0, d_ctr, n, r, (int)light};
+      if (src.kind == kSrcPacked) {
+        ta.src_kind = kTailSrcPacked;
+        ta.src0 = src.packed;
+      } else if (src.kind == kSrcPairs) {
+        ta.src_kind = kTailSrcPairs;
+        ta.src0 = E[1];
+        ta.src_w = wbase;
+        ta.src_wstride = wstride;
+      } else if constexpr (std::is_same_v<InView, SoaView>) {
+        ta.src_kind = kTailSrcSoa;
+        ta.src0 = in.src;
+        ta.src1 = in.dst;
+        ta.src_w = in.w;
+      } else {
+        ta.src_kind = kTailSrcAos;
+        ta.src0 = in.e;
       }
-      TailArgs ta{{E[0], E[1]}, {minb[0], minb[1]}, parent, rootlabel, L, mst, bcount, M, flags, trace,
-                  fin_table, kFinTableSlots - 1ull, d_ctr, n, r, (int)light};
       void* args[] = {&ta};
       hot_begin(kHotTail, r, light);
       MST_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)kt, G, kBlock, args, 0, s));
       ++launches;
-      if (fin) {
-        static const bool attr_set = [] {
-          MST_CUDA_CHECK(cudaFuncSetAttribute(k_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, kFinSmem));
-          return true;
-        }();
-        (void)attr_set;
-        FinArgs fa{{E[0], E[1]}, mst, flags, trace ? trace + 448 : nullptr, d_ctr, n};
-        k_finish<<<1, kFinThreads, kFinSmem, s>>>(fa);
-        MST_CUDA_CHECK(cudaGetLastError());
-        ++launches;
-      }
       tmark();
       MST_CUDA_CHECK(cudaMemcpyAsync(&ws.h_snap[kMaxR - 1], d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
       MST_CUDA_CHECK(cudaStreamSynchronize(s));
@@ -695,15 +713,8 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
         std::vector<unsigned long long> tt(512);
         MST_CUDA_CHECK(cudaMemcpy(tt.data(), trace, 512 * 8, cudaMemcpyDeviceToHost));
         fprintf(stderr, "tail r0=%d G=%u:", r, G);
-        for (int i = 1; i < 448 && tt[i]; ++i) fprintf(stderr, " %.1f", (tt[i] - tt[i - 1]) * 1e-3);
-        fprintf(stderr, " (us per phase: H1 H2 L C1 C2 per round)\n");
-        if (tt[448]) {
-          int last = 0;
-          while (last + 1 < 448 && tt[last + 1]) ++last;
-          fprintf(stderr, "finish: hand-off %.1f |", (tt[448] - tt[last]) * 1e-3);
-          for (int i = 449; i < 512 && tt[i]; ++i) fprintf(stderr, " %.1f", (tt[i] - tt[i - 1]) * 1e-3);
-          fprintf(stderr, " (us: load, then per round: min hook jump label relabel)\n");
-        }
+        for (int i = 1; i < 512 && tt[i]; ++i) fprintf(stderr, " %.1f", (tt[i] - tt[i - 1]) * 1e-3);
+        fprintf(stderr, " (us per phase: A B C per round)\n");
       }
       if (snap.err || snap.stop_round != kNoStop) break;
       if (light && snap.phase_end != kNoStop) {
@@ -719,16 +730,18 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     {
       const uint64_t ht = tiles_of(n_bound);
       const int hfused = ht <= kFusedScanMaxTiles ? 1 : 0;
-      if (original_in) {
-        auto kd = k_hook_decide<InView>;
+      const HookSrc src = hook_src(r);
+      auto launch_hook = [&](auto view) {
+        auto kd = k_hook_decide<decltype(view)>;
         launch_k(kd, (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ht, (uint64_t)sm_count(dev) * blocks_per_sm(kd))),
-                 kBlock, s, in, mcur, parent, rootlabel, hmasks, hcounts, d_ctr, r, hfused, (int)light, hslot);
-      } else {
-        auto kd = k_hook_decide<PackedView>;
-        launch_k(kd, (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ht, (uint64_t)sm_count(dev) * blocks_per_sm(kd))),
-                 kBlock, s, PackedView{E[r & 1]}, mcur, parent, rootlabel, hmasks, hcounts, d_ctr, r, hfused,
-                 (int)light, hslot);
-      }
+                 kBlock, s, view, mcur, parent, rootlabel, hmasks, hcounts, d_ctr, r, hfused, (int)light, hslot);
+      };
+      if (src.kind == kSrcIn)
+        launch_hook(in);
+      else if (src.kind == kSrcPairs)
+        launch_hook(PairsView<InView>{reinterpret_cast<const uint2*>(E[1]), in});
+      else
+        launch_hook(PackedView{src.packed});
       if (!hfused)
         launch_k(k_scan_counts<kScanRoots>,
                  (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((ht + kScanTile - 1) / kScanTile, (uint64_t)sm_count(dev))),
@@ -757,11 +770,11 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     hot_begin(kHotCompact, r, light);
     if (original_in) {
       // plain round 1: relabelled copy of the caller's list in E[1], compacted into E[0]
-      launch_two_pass<InView, kModeRelabel, kPre>(ws, cb, in, E[1], Lr, Eout, mnext, d_ctr, r, m_bound, n,
-                                                  kSlotCompact, (int)light, filt_for(n_bound));
+      launch_two_pass<InView, kModeRelabel>(ws, cb, in, E[1], Lr, Eout, mnext, d_ctr, r, m_bound, n,
+                                            kSlotCompact, (int)light, filt_for(n_bound));
     } else {
-      launch_two_pass<PackedView, kModeRelabel, kPre>(ws, cb, PackedView{E[r & 1]}, E[r & 1], Lr, Eout, mnext, d_ctr,
-                                                      r, m_bound, n, kSlotCompact, (int)light, filt_for(n_bound), pt);
+      launch_two_pass<PackedView, kModeRelabel>(ws, cb, PackedView{E[r & 1]}, E[r & 1], Lr, Eout, mnext, d_ctr,
+                                                r, m_bound, n, kSlotCompact, (int)light, filt_for(n_bound), pt);
     }
     tmark();
     launches += 5;
@@ -933,22 +946,13 @@ RunOut run_single(const SingleArgs& a, mst_stats_t* stats) {
   MST_CUDA_CHECK(cudaEventRecord(e1, s));
 
   RunOut o;
-  const bool pre = warp_prereduce_enabled();
   if (a.kind == 0) {
     SoaView v{src, dst, w, 0};
-    const bool filt = filter_mode(a.n, a.m);
-    if (pre)
-      run_single_impl<SoaView, true>(ws, v, w, 1, a.n, a.m, o, a.time_hot, filt);
-    else
-      run_single_impl<SoaView, false>(ws, v, w, 1, a.n, a.m, o, a.time_hot, filt);
+    run_single_impl<SoaView>(ws, v, w, 1, a.n, a.m, o, a.time_hot, filter_mode(a.n, a.m));
   } else {
     AosView v{reinterpret_cast<const uint4*>(aos), 0};
     const uint32_t* wb = reinterpret_cast<const uint32_t*>(aos) + 2;
-    const bool filt = filter_mode(a.n, a.m);
-    if (pre)
-      run_single_impl<AosView, true>(ws, v, wb, 4, a.n, a.m, o, a.time_hot, filt);
-    else
-      run_single_impl<AosView, false>(ws, v, wb, 4, a.n, a.m, o, a.time_hot, filt);
+    run_single_impl<AosView>(ws, v, wb, 4, a.n, a.m, o, a.time_hot, filter_mode(a.n, a.m));
   }
   check_err_bits(o.err);
   uint32_t* d_mst = ws.get<uint32_t>("mst", a.n);
@@ -1037,7 +1041,6 @@ struct NcclExchanger : Exchanger {
   }
 };
 
-template <bool kPre>
 void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, RunOut& out) {
   const int G = (int)sh.size();
   uint32_t launches = 0;
@@ -1045,7 +1048,7 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, RunOu
     MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
     init_counters(*s.ws, s.d_ctr, n, s.m);
     MST_CUDA_CHECK(cudaMemsetAsync(s.minb[0], 0xFF, (size_t)n * 8, s.ws->stream));
-    auto kmin = k_min_round1<SoaView, kPre>;
+    auto kmin = k_min_round1<SoaView>;
     launch_k(kmin, persistent_grid(kmin, s.ws->device, (s.m + kBlock - 1) / kBlock), kBlock, s.ws->stream, s.in, n, s.m,
              s.minb[0], s.d_ctr, filt_for(n));
     ++launches;
@@ -1073,9 +1076,15 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, RunOu
       if (r == 1) {
         auto kk = k_shard_keys<SoaView>;
         launch_k(kk, persistent_grid(kk, s.ws->device, t), kBlock, s.ws->stream, s.in, s.minb[0], s.xch, s.own, s.d_ctr, r);
+      } else if (r == 2) {
+        // round 1's label pairs + the shard's weights (see k_count)
+        auto kk = k_shard_keys<PairsView<SoaView>>;
+        launch_k(kk, persistent_grid(kk, s.ws->device, t), kBlock, s.ws->stream,
+                 PairsView<SoaView>{reinterpret_cast<const uint2*>(s.E[1]), s.in}, s.minb[1], s.xch, s.own, s.d_ctr,
+                 r);
       } else {
         auto kk = k_shard_keys<PackedView>;
-        launch_k(kk, persistent_grid(kk, s.ws->device, t), kBlock, s.ws->stream, PackedView{s.E[r & 1]},
+        launch_k(kk, persistent_grid(kk, s.ws->device, t), kBlock, s.ws->stream, PackedView{s.E[(r - 1) & 1]},
                  s.minb[(r - 1) & 1], s.xch, s.own, s.d_ctr, r);
       }
     }
@@ -1116,10 +1125,10 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, RunOu
                            ws.get<uint4>("stage", kCTile)};
       uint4* Eout = s.E[(r + 1) & 1];
       if (r == 1)
-        launch_two_pass<SoaView, kModeRelabel, kPre>(ws, cb, s.in, s.E[1], s.L, Eout, mnext, s.d_ctr, r, m_bound, n,
+        launch_two_pass<SoaView, kModeRelabel>(ws, cb, s.in, s.E[1], s.L, Eout, mnext, s.d_ctr, r, m_bound, n,
                                                      kSlotCompact, (int)kPhaseSharded, filt_for(n_bound));
       else
-        launch_two_pass<PackedView, kModeRelabel, kPre>(ws, cb, PackedView{s.E[r & 1]}, s.E[r & 1], s.L, Eout, mnext,
+        launch_two_pass<PackedView, kModeRelabel>(ws, cb, PackedView{s.E[r & 1]}, s.E[r & 1], s.L, Eout, mnext,
                                                         s.d_ctr, r, m_bound, n, kSlotCompact, (int)kPhaseSharded,
                                                         filt_for(n_bound));
       launches += 5;
@@ -1233,10 +1242,7 @@ RunOut run_sharded(const std::vector<PartSpec>& parts, Exchanger& ex, uint32_t n
   cudaEvent_t e2 = sh[0].ws->tev[sh[0].ws->tev.size() - 2];
   MST_CUDA_CHECK(cudaEventRecord(e1, sh[0].ws->stream));
   RunOut o;
-  if (warp_prereduce_enabled())
-    run_sharded_rounds<true>(sh, ex, n, o);
-  else
-    run_sharded_rounds<false>(sh, ex, n, o);
+  run_sharded_rounds(sh, ex, n, o);
   check_err_bits(o.err);
   Workspace& ws0 = *sh[0].ws;
   MST_CUDA_CHECK(cudaSetDevice(ws0.device));
@@ -1631,8 +1637,7 @@ int mst_gpu_round1_min(const mst_edges_soa_t* edges, uint64_t* out_min) {
     auto* mn = ws.get<unsigned long long>("minA", n);
     init_counters(ws, d_ctr, n, m);
     MST_CUDA_CHECK(cudaMemsetAsync(mn, 0xFF, (size_t)n * 8, ws.stream));
-    auto kmin = warp_prereduce_enabled() ? k_min_round1<SoaView, true>
-                                         : k_min_round1<SoaView, false>;
+    auto kmin = k_min_round1<SoaView>;
     const unsigned g = (unsigned)std::max<uint64_t>(
         1, std::min<uint64_t>((m + 4 * kBlock - 1) / (4 * kBlock), (uint64_t)sm_count(dev) * blocks_per_sm(kmin)));
     kmin<<<g, kBlock, 0, ws.stream>>>(SoaView{src, dst, w, 0}, n, m, mn, d_ctr, filt_for(n));

@@ -66,13 +66,7 @@ struct DevCounters {
   unsigned int dedup[kMaxR];      // round r's compaction keeps one edge per component pair
   unsigned long long pair_mask[kMaxR];
   unsigned int pair_count[kMaxR];  // distinct pairs inserted
-  unsigned int hooks[kMaxR];       // tail v2: hooks per round
-  unsigned int live[kMaxR];        // tail v2: live edges entering round r
-  unsigned int mst_fill;           // tail v2: next free MST slot
   unsigned int pair_abort[kMaxR];  // table overflowed: keep every edge this round
-  unsigned int fin_round;          // round handed from k_tail to k_finish (kNoStop: none)
-  unsigned int fin_m;              // edges of the deduplicated list k_finish starts from
-  unsigned int fin_pairs[kMaxR];   // distinct component pairs seen by k_tail's dedup
 };
 
 
@@ -142,6 +136,20 @@ struct PackedView {
     return __ldcs(reinterpret_cast<const uint32_t*>(e + i) + 2);
   }
   static constexpr uint32_t base = 0;
+};
+
+// Round 1's relabelled list when the input was the caller's list: the count
+// pass leaves 8 B label pairs at each input position; weight and id come
+// from the caller's list. Round 2's hook gathers through this view.
+template <class In>
+struct PairsView {
+  const uint2* __restrict__ xy;
+  In in;
+  static constexpr bool kOriginal = false;
+  __device__ __forceinline__ EdgeRec gather(uint64_t i) const {
+    const uint2 p = __ldcg(xy + i);
+    return EdgeRec{p.x, p.y, in.weight(i), in.base + (uint32_t)i, true};
+  }
 };
 
 // ------------------------------ primitives ---------------------------------
@@ -224,24 +232,11 @@ __device__ __forceinline__ uint32_t lookback(unsigned long long* status, uint32_
 }
 
 // Filtered 64-bit min: read first (a stale read is never below the true
-// value, so skipping is always safe), atomic only when it can win. With
-// kWarpPre, lanes of a warp that target the same component first reduce
-// to one candidate (__match_any_sync + redux.sync), so hub components see
-// one atomic per warp instead of up to 32.
-template <bool kWarpPre>
+// value, so skipping is always safe), atomic only when it can win. (A
+// warp-level pre-reduction with __match_any_sync + redux.sync measured
+// slower on every config and was removed.)
 __device__ __forceinline__ void offer(unsigned long long* table, uint32_t c, uint64_t key,
                                       bool valid, bool filt = true) {
-  if (kWarpPre) {
-    const unsigned act = __ballot_sync(0xffffffffu, valid);
-    if (!valid) return;
-    const unsigned grp = __match_any_sync(act, c);
-    if (__popc(grp) > 1) {
-      const uint32_t hi = (uint32_t)(key >> 32), lo = (uint32_t)key;
-      const uint32_t mhi = __reduce_min_sync(grp, hi);
-      const uint32_t mlo = __reduce_min_sync(grp, hi == mhi ? lo : 0xFFFFFFFFu);
-      if (hi != mhi || lo != mlo) return;
-    }
-  }
   if (!valid) return;
   // Large (DRAM-resident) tables: a fire-and-forget RED; the read-first
   // filter would put a dependent DRAM round trip on the critical path.
@@ -310,7 +305,7 @@ __device__ __forceinline__ uint32_t find_root(uint32_t* parent, uint32_t c) {
 
 // Lightest incident edge per vertex over the caller's list, literal keys
 // (w<<32 | index in the list).
-template <class View, bool kWarpPre>
+template <class View>
 __global__ void __launch_bounds__(kBlock) k_min_round1(View v, uint32_t n, uint64_t m,
                                                        unsigned long long* __restrict__ minimum,
                                                        DevCounters* ctr, int filt) {
@@ -342,8 +337,8 @@ __global__ void __launch_bounds__(kBlock) k_min_round1(View v, uint32_t n, uint6
         }
       }
       const uint64_t key = ((uint64_t)e[k].w << 32) | (uint32_t)i;
-      offer<kWarpPre>(minimum, e[k].a, key, valid, filt);
-      offer<kWarpPre>(minimum, e[k].b, key, valid, filt);
+      offer(minimum, e[k].a, key, valid, filt);
+      offer(minimum, e[k].b, key, valid, filt);
     }
   }
   if (err) atomicOr(&ctr->err, err);
@@ -593,7 +588,8 @@ __global__ void __launch_bounds__(kBlock) k_count(View in, uint4* __restrict__ r
                                                   const uint32_t* __restrict__ L,
                                                   uint32_t* __restrict__ masks, uint32_t* __restrict__ counts,
                                                   uint32_t n_orig, DevCounters* ctr, int r, int fused, int slot,
-                                                  int light_phase, PairTable pt) {
+                                                  int light_phase, PairTable pt,
+                                                  unsigned long long* __restrict__ min_next, int filt) {
   pdl_prologue();
   __shared__ uint32_t s_cnt[kWarps];
   __shared__ uint32_t s_slot[kCItems * kWarps];
@@ -627,6 +623,7 @@ __global__ void __launch_bounds__(kBlock) k_count(View in, uint4* __restrict__ r
     for (int k = 0; k < kCItems; ++k) {
       const uint64_t i = (uint64_t)tile * kCTile + k * kBlock + threadIdx.x;
       keep[k] = false;
+      uint32_t ox = e[k].a, oy = e[k].b;  // the endpoint labels of round r+1
       if (i < m_r) {
         bool ok = true;
         if (View::kOriginal) {
@@ -649,15 +646,28 @@ __global__ void __launch_bounds__(kBlock) k_count(View in, uint4* __restrict__ r
             keep[k] = e[k].a != e[k].b;
           }
         } else if (ok) {
-          const uint32_t x = __ldg(L + e[k].a), y = __ldg(L + e[k].b);
-          keep[k] = x != y;
+          ox = __ldg(L + e[k].a);
+          oy = __ldg(L + e[k].b);
+          keep[k] = ox != oy;
           if (View::kOriginal)
-            __stcs(reinterpret_cast<uint2*>(relabeled) + i, make_uint2(x, y));
+            __stcs(reinterpret_cast<uint2*>(relabeled) + i, make_uint2(ox, oy));
           else
-            __stcs(reinterpret_cast<uint2*>(relabeled + i), make_uint2(x, y));
+            __stcs(reinterpret_cast<uint2*>(relabeled + i), make_uint2(ox, oy));
         } else if (View::kOriginal && kMode == kModeRelabel) {
           __stcs(reinterpret_cast<uint2*>(relabeled) + i, make_uint2(0, 0));  // rejected edge: a self-loop
         }
+      }
+      // Offers for round r+1, keyed by the position in THIS list (the
+      // relabelled input, which round r+1's hook gathers from), so they
+      // need no output position and leave the emit pass a pure copy. The
+      // light split and the heavy filter keep few, scattered survivors of a
+      // DRAM-sized stream: their offers are made by output position in
+      // k_emit_staged, where they do not stall the stream (c3 split: 1.8 ms
+      // there vs 3.1 ms here).
+      if ((kMode == kModeRelabel || kMode == kModeDedup) && keep[k]) {
+        const unsigned long long key = ((unsigned long long)e[k].w << 32) | (uint32_t)i;
+        offer(min_next, ox, key, true, filt);
+        offer(min_next, oy, key, true, filt);
       }
       bal[k] = __ballot_sync(0xffffffffu, keep[k]);
       if (lane == 0) s_slot[k * kWarps + warp] = __popc(bal[k]);
@@ -709,13 +719,12 @@ __global__ void __launch_bounds__(kBlock) k_count(View in, uint4* __restrict__ r
   }
 }
 
-template <class View, int kMode, bool kWarpPre>
+template <class View, int kMode>
 __global__ void __launch_bounds__(kBlock) k_emit(View in, const uint4* __restrict__ relabeled,
                                                  const uint32_t* __restrict__ L,
                                                  const uint32_t* __restrict__ masks,
                                                  const uint32_t* __restrict__ offsets, uint4* __restrict__ out,
-                                                 unsigned long long* __restrict__ min_next, DevCounters* ctr,
-                                                 int r, int filt, int dedup_armed, uint32_t n_orig) {
+                                                 DevCounters* ctr, int r, int dedup_armed, uint32_t n_orig) {
   pdl_prologue();
   __shared__ uint32_t s_scan[kCItems * kWarps];
   const uint32_t stop = ctr->stop_round;
@@ -791,17 +800,15 @@ __global__ void __launch_bounds__(kBlock) k_emit(View in, const uint4* __restric
     for (int k = 0; k < kCItems; ++k) {
       const uint32_t j = prefix + s_scan[k * kWarps + warp] + __popc(bal[k] & lt);
       if (keep[k]) __stcs(out + j, e[k]);
-      const unsigned long long key = ((unsigned long long)e[k].z << 32) | j;
-      offer<kWarpPre>(min_next, e[k].x, key, keep[k], filt);
-      offer<kWarpPre>(min_next, e[k].y, key, keep[k], filt);
     }
     __syncthreads();
   }
 }
 
 // Emit of the staged modes: tile t's survivors sit at stage[t*kCTile ..
-// t*kCTile + count); copy them to their final slots and make the offers.
-template <int kMode, bool kWarpPre>
+// t*kCTile + count); copy them to their final slots (and, for the light
+// split and the heavy filter, make the offers by output position).
+template <int kMode>
 __global__ void __launch_bounds__(kBlock) k_emit_staged(const uint4* __restrict__ stage,
                                                         const uint32_t* __restrict__ offsets, uint4* __restrict__ out,
                                                         unsigned long long* __restrict__ min_next, DevCounters* ctr,
@@ -822,9 +829,11 @@ __global__ void __launch_bounds__(kBlock) k_emit_staged(const uint4* __restrict_
       const bool v = j < cnt;
       const uint4 e = v ? __ldcs(stage + (uint64_t)tile * kCTile + j) : make_uint4(0, 0, 0, 0);
       if (v) __stcs(out + off + j, e);
-      const unsigned long long key = ((unsigned long long)e.z << 32) | (off + j);
-      offer<kWarpPre>(min_next, e.x, key, v, filt);
-      offer<kWarpPre>(min_next, e.y, key, v, filt);
+      if (kMode == kModeHeavy || kMode == kModeLight) {
+        const unsigned long long key = ((unsigned long long)e.z << 32) | (off + j);
+        offer(min_next, e.x, key, v, filt);
+        offer(min_next, e.y, key, v, filt);
+      }
     }
   }
 }
@@ -1152,24 +1161,41 @@ __global__ void __launch_bounds__(kBlock) k_label2(uint32_t* __restrict__ parent
 
 // Once a round has few live edges, per-round kernel launches, ramp-up/tail
 // effects and look-back latency dominate. k_tail runs all remaining rounds
-// in ONE cooperative launch: every phase of a round (hook decide, hook emit,
-// label, relabel+count, compact+offer) is a grid-wide step separated by
-// grid.sync(), and ordered compaction uses per-block chunk counts instead of
-// a look-back (all blocks are co-resident). Semantics match k_hook_decide /
-// k_label2 / k_count + k_emit exactly (same counters, same literal keys).
+// in ONE cooperative launch (all blocks co-resident), three grid-wide steps
+// per round, same hook rule, counters, keys and verdicts as the round
+// kernels:
+//   A: ordered compaction of round r-1's relabelled list into E_r (per-block
+//      chunk counts, no look-back) AND round r's hook decisions: the keys
+//      index round r-1's list (offers are keyed by input position, see
+//      k_count), so the hook does not wait for the compaction. Each block
+//      records its chunk's root bitmask and per-word root prefixes.
+//   B: dense labels: roots_before(x) = block prefix + word prefix + popc,
+//      root finding (path halving), MST slots of the hooked components,
+//      clear of the next min table.
+//   C: relabel E_r in place, count the kept edges per block and make the
+//      offers (w << 32 | position in E_r) for round r+1 (aggregated in a
+//      block-local shared-memory table when <= kTailSmemMin components).
 struct TailArgs {
   uint4* E[2];
   unsigned long long* minb[2];
   uint32_t* parent;
-  uint32_t* rootlabel;
+  uint32_t* rootlabel;  // MST edge id of each hooked component (stash)
   uint32_t* L;
   uint32_t* mst;
-  uint32_t* bcount;  // [gridDim.x]
-  uint32_t* M;       // light phase: entry-label -> current-label map (n[r0] entries)
-  uint8_t* flags;    // MST edge flags (sorted output)
+  uint32_t* broots;     // [gridDim.x] roots per block chunk (A -> B)
+  uint32_t* bkept;      // [gridDim.x] kept edges per block chunk (C -> A)
+  uint32_t* masks;      // root bitmask, one word per 32 components
+  uint32_t* wpref;      // roots of the block's chunk before each word
+  uint32_t* M;          // light phase: entry-label -> current-label map (n[r0] entries)
+  uint8_t* flags;       // MST edge flags (sorted output)
   unsigned long long* trace;  // optional: globaltimer stamps at phase boundaries (block 0)
-  unsigned long long* fin_table;  // finisher hand-off: pair table ({pair, key} slots), cleared
-  unsigned long long fin_mask;    // slots - 1
+  // the list the entry round's keys index (kTailSrc*): a packed list, round
+  // 1's label pairs with the caller's weights, or the caller's SoA / AoS list
+  int src_kind;
+  const void* src0;         // packed / pairs / SoA src / AoS records
+  const uint32_t* src1;     // SoA dst
+  const uint32_t* src_w;    // weights (pairs, SoA)
+  uint32_t src_wstride;
   DevCounters* ctr;
   uint32_t n_orig;
   int r0;
@@ -1177,58 +1203,7 @@ struct TailArgs {
 };
 
 constexpr uint32_t kTailSmemMin = 4096;  // block-local min table entries (32 KB)
-
-// ------------------------------ finisher -----------------------------------
-// The last rounds have few components but, on meshes and R-MAT cores, still
-// many parallel edges between them, and every grid-wide step costs a grid
-// sync plus a chain of L2 round trips (~4 us). Once n_r <= kFinC, k_tail
-// keeps only the lightest edge of every component pair (cycle property:
-// exact) in an ordered compaction and, if at most kFinE pairs remain, hands
-// off to k_finish: ONE block that runs every remaining round in shared
-// memory (__syncthreads instead of grid syncs, smem atomics instead of L2).
-// Keys stay (w << 32 | position) over an order-preserving list, so ties
-// fall exactly as in the grid-wide rounds.
-constexpr uint32_t kFinC = 8192;   // components (u16 labels)
-constexpr uint32_t kFinE = 15872;  // deduplicated edges
-constexpr int kFinThreads = 1024;
-constexpr uint32_t kFinSmem = kFinC * (8 + 2 + 2) + kFinE * 8;
-constexpr uint32_t kFinTableSlots = 1u << 15;  // >= 2 x kFinE
-constexpr uint32_t kFinOverflow = 1u << 24;
-
-// Insert pair(x, y) with key into the finisher table; 1 if the pair is new,
-// kFinOverflow if no slot was found.
-__device__ __forceinline__ uint32_t fin_insert(unsigned long long* t, unsigned long long mask, uint32_t x,
-                                               uint32_t y, unsigned long long key) {
-  const unsigned long long pair = ((unsigned long long)min(x, y) << 32) | max(x, y);
-  unsigned long long h = pair_hash(pair) & mask;
-  for (int probe = 0; probe < kPairProbes; ++probe) {
-    unsigned long long cur = __ldcg(t + 2 * h);
-    uint32_t fresh = 0;
-    if (cur == kNoKey) {
-      cur = atomicCAS(t + 2 * h, kNoKey, pair);
-      fresh = cur == kNoKey;
-      if (fresh) cur = pair;
-    }
-    if (cur == pair) {
-      if (key < __ldcg(t + 2 * h + 1)) atomicMin(t + 2 * h + 1, key);
-      return fresh;
-    }
-    h = (h + 1) & mask;
-  }
-  return kFinOverflow;
-}
-
-__device__ __forceinline__ bool fin_keep(const unsigned long long* t, unsigned long long mask, uint32_t x,
-                                         uint32_t y, unsigned long long key) {
-  const unsigned long long pair = ((unsigned long long)min(x, y) << 32) | max(x, y);
-  unsigned long long h = pair_hash(pair) & mask;
-  for (int probe = 0; probe < kPairProbes; ++probe) {
-    const ulonglong2 slot = __ldcg(reinterpret_cast<const ulonglong2*>(t) + h);
-    if (slot.x == pair) return slot.y == key;
-    h = (h + 1) & mask;
-  }
-  return true;  // unreachable when every insert succeeded
-}
+constexpr uint32_t kTailMaxBlocks = 1024;
 
 // Ordered ranks of kItems striped flags per thread; returns the total.
 __device__ __forceinline__ uint32_t block_ranks(const bool (&f)[kItems], uint32_t (&rank)[kItems],
@@ -1256,22 +1231,35 @@ __device__ __forceinline__ uint32_t block_ranks(const bool (&f)[kItems], uint32_
   return total;
 }
 
-// Sum of bcount[0..b) (exclusive block prefix), computed by warp 0, broadcast.
-__device__ __forceinline__ uint32_t block_prefix(const uint32_t* bcount, uint32_t b, uint32_t* s_out) {
-  if (threadIdx.x < 32) {
-    uint32_t s = 0;
-    for (uint32_t i = threadIdx.x; i < b; i += 32) s += __ldcg(bcount + i);
-    s = warp_sum<uint32_t>(s);
-    if (threadIdx.x == 0) *s_out = s;
+// Exclusive prefix of cnt[0..G) into s_pre[0..G] (s_pre[G] = total), by the
+// whole block.
+__device__ __forceinline__ void block_scan_array(const uint32_t* cnt, uint32_t G, uint32_t* s_pre,
+                                                 uint32_t* s_warp) {
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  uint32_t carry = 0;
+  for (uint32_t base = 0; base < G; base += kBlock) {
+    const uint32_t i = base + threadIdx.x;
+    const uint32_t v = i < G ? __ldcg(cnt + i) : 0u;
+    const uint32_t incl = warp_incl_scan(v);
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t t = lane < kWarps ? s_warp[lane] : 0u;
+      const uint32_t ti = warp_incl_scan(t);
+      if (lane < kWarps) s_warp[lane] = ti - t;
+      if (lane == kWarps - 1) s_warp[kWarps] = ti;
+    }
+    __syncthreads();
+    if (i < G) s_pre[i] = carry + s_warp[warp] + incl - v;
+    carry += s_warp[kWarps];
+    __syncthreads();
   }
+  if (threadIdx.x == 0) s_pre[G] = carry;
   __syncthreads();
-  const uint32_t v = *s_out;
-  __syncthreads();
-  return v;
 }
 
 __device__ __forceinline__ void tail_stamp(const TailArgs& a, int& slot) {
-  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && slot < 448) {
+  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && slot < 512) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     a.trace[slot] = t;
@@ -1279,7 +1267,26 @@ __device__ __forceinline__ void tail_stamp(const TailArgs& a, int& slot) {
   ++slot;
 }
 
-template <bool kWarpPre>
+enum { kTailSrcPacked = 0, kTailSrcPairs = 1, kTailSrcSoa = 2, kTailSrcAos = 3 };
+
+// Edge i of the list the entry round's keys index, as {a, b, w, id}.
+__device__ __forceinline__ uint4 tail_entry_edge(const TailArgs& a, uint32_t i) {
+  switch (a.src_kind) {
+    case kTailSrcPacked:
+      return __ldcg(static_cast<const uint4*>(a.src0) + i);
+    case kTailSrcPairs: {
+      const uint2 p = __ldcg(static_cast<const uint2*>(a.src0) + i);
+      return make_uint4(p.x, p.y, __ldg(a.src_w + (uint64_t)i * a.src_wstride), i);
+    }
+    case kTailSrcSoa:
+      return make_uint4(__ldg(static_cast<const uint32_t*>(a.src0) + i), __ldg(a.src1 + i), __ldg(a.src_w + i), i);
+    default: {
+      const uint4 v = __ldg(static_cast<const uint4*>(a.src0) + i);
+      return make_uint4(v.x, v.y, v.z, i);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kBlock, 2) k_tail(TailArgs a) {
   pdl_prologue();
   namespace cg = cooperative_groups;
@@ -1287,140 +1294,68 @@ __global__ void __launch_bounds__(kBlock, 2) k_tail(TailArgs a) {
   int slot = 0;
   tail_stamp(a, slot);
   __shared__ uint32_t s_cnt[kItems * kWarps + 1];
-  __shared__ uint32_t s_misc[2];
+  __shared__ uint32_t s_warp[kWarps + 1];
+  __shared__ uint32_t s_bpre[kTailMaxBlocks + 1];
   __shared__ unsigned long long s_wsum[kWarps];
   __shared__ unsigned long long s_min[kTailSmemMin];
   const uint32_t G = gridDim.x, b = blockIdx.x;
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   volatile DevCounters* vc = a.ctr;
   const uint32_t n_entry = vc->n[a.r0];
-  uint32_t fin_next = kFinC;  // finisher hand-off tried once n_r <= fin_next
   for (int r = a.r0; r < kMaxR - 1; ++r) {
     if ((uint32_t)r >= vc->stop_round || (uint32_t)r >= vc->phase_end) break;
     const uint32_t n_r = vc->n[r];
-    const uint64_t m_r = vc->m[r];
     const uint32_t mst_base = a.n_orig - n_r;
     // ternaries, not a dynamic index: keeps TailArgs out of local memory
     const unsigned long long* mcur = (r & 1) ? a.minb[0] : a.minb[1];
     unsigned long long* mnext = (r & 1) ? a.minb[1] : a.minb[0];
     uint4* Ecur = (r & 1) ? a.E[1] : a.E[0];
-    uint4* Enext = (r & 1) ? a.E[0] : a.E[1];
-    if (a.fin_table && !a.light && n_r <= fin_next) {
-      // ---- F1: lightest edge per component pair into the table
-      const uint64_t es = (m_r + G - 1) / G;
-      const uint64_t elo = min((uint64_t)b * es, m_r), ehi = min(elo + es, m_r);
-      uint32_t fresh = 0;
+    uint4* Eprev = (r & 1) ? a.E[0] : a.E[1];
+    // ---- A1: ordered compaction of round r-1's relabelled list into E_r
+    if (r > a.r0) {
+      const uint64_t m_prev = vc->m[r - 1];
+      const uint64_t es = (m_prev + G - 1) / G;
+      const uint64_t elo = min((uint64_t)b * es, m_prev), ehi = min(elo + es, m_prev);
+      block_scan_array(a.bkept, G, s_bpre, s_warp);
+      uint32_t running = s_bpre[b];
+      if (b == G - 1 && threadIdx.x == 0) a.ctr->m[r] = s_bpre[G];
       for (uint64_t base = elo; base < ehi; base += kBlock * kItems) {
-        // kItems edges in flight per thread: most pairs are already in the
-        // table, so one 16 B slot load decides and a RED min finishes
+        bool f[kItems];
+        uint32_t rank[kItems];
         uint4 e[kItems];
-        ulonglong2 sl[kItems];
-        unsigned long long pr[kItems], h[kItems];
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
           const uint64_t i = base + k * kBlock + threadIdx.x;
-          e[k] = i < ehi ? __ldcg(Ecur + i) : make_uint4(0, 0, 0, 0);
+          e[k] = i < ehi ? __ldcg(Eprev + i) : make_uint4(0, 0, 0, 0);
+          f[k] = i < ehi && e[k].x != e[k].y;
         }
+        const uint32_t tot = block_ranks(f, rank, s_cnt);
 #pragma unroll
-        for (int k = 0; k < kItems; ++k) {
-          pr[k] = ((unsigned long long)min(e[k].x, e[k].y) << 32) | max(e[k].x, e[k].y);
-          h[k] = pair_hash(pr[k]) & a.fin_mask;
-          sl[k] = __ldcg(reinterpret_cast<const ulonglong2*>(a.fin_table) + h[k]);
-        }
-#pragma unroll
-        for (int k = 0; k < kItems; ++k) {
-          const uint64_t i = base + k * kBlock + threadIdx.x;
-          if (i >= ehi) continue;
-          const unsigned long long key = ((unsigned long long)e[k].z << 32) | (uint32_t)i;
-          if (sl[k].x == pr[k]) {
-            if (key < sl[k].y) atomicMin(a.fin_table + 2 * h[k] + 1, key);
-          } else {
-            fresh += fin_insert(a.fin_table, a.fin_mask, e[k].x, e[k].y, key);
-          }
-        }
+        for (int k = 0; k < kItems; ++k)
+          if (f[k]) Ecur[running + rank[k]] = e[k];
+        running += tot;
       }
-      fresh = warp_sum<uint32_t>(fresh);
-      if (lane_id() == 0 && fresh) atomicAdd(&a.ctr->fin_pairs[r], fresh);
-      grid.sync();
-      tail_stamp(a, slot);
-      if (vc->fin_pairs[r] <= kFinE) {
-        // ---- F2: kept edges per block; F3: ordered compaction, hand-off
-        uint32_t kept = 0;
-        for (uint64_t base = elo; base < ehi; base += kBlock * kItems) {
-          uint4 e[kItems];
-#pragma unroll
-          for (int k = 0; k < kItems; ++k) {
-            const uint64_t i = base + k * kBlock + threadIdx.x;
-            e[k] = i < ehi ? __ldcg(Ecur + i) : make_uint4(0, 0, 0, 0);
-          }
-#pragma unroll
-          for (int k = 0; k < kItems; ++k) {
-            const uint64_t i = base + k * kBlock + threadIdx.x;
-            if (i < ehi)
-              kept += fin_keep(a.fin_table, a.fin_mask, e[k].x, e[k].y,
-                               ((unsigned long long)e[k].z << 32) | (uint32_t)i);
-          }
-        }
-        kept = warp_sum<uint32_t>(kept);
-        if (lane_id() == 0) s_cnt[threadIdx.x >> 5] = kept;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-          uint32_t t = 0;
-          for (int i = 0; i < kWarps; ++i) t += s_cnt[i];
-          a.bcount[b] = t;
-        }
-        __syncthreads();
-        grid.sync();
-        tail_stamp(a, slot);
-        uint32_t running = block_prefix(a.bcount, b, s_misc);
-        for (uint64_t base = elo; base < ehi; base += kBlock * kItems) {
-          bool f[kItems];
-          uint32_t rank[kItems];
-          uint4 e[kItems];
-#pragma unroll
-          for (int k = 0; k < kItems; ++k) {
-            const uint64_t i = base + k * kBlock + threadIdx.x;
-            e[k] = i < ehi ? __ldcg(Ecur + i) : make_uint4(0, 0, 0, 0);
-            f[k] = i < ehi && fin_keep(a.fin_table, a.fin_mask, e[k].x, e[k].y,
-                                       ((unsigned long long)e[k].z << 32) | (uint32_t)i);
-          }
-          const uint32_t tot = block_ranks(f, rank, s_cnt);
-#pragma unroll
-          for (int k = 0; k < kItems; ++k)
-            if (f[k]) Enext[running + rank[k]] = e[k];
-          running += tot;
-        }
-        if (b == G - 1 && threadIdx.x == 0) {
-          a.ctr->fin_m = running;
-          a.ctr->fin_round = (uint32_t)r;
-        }
-        return;  // k_finish continues from Enext
-      }
-      // too many pairs for one block: clear the table, retry once the
-      // components have shrunk 4x (the clear is ordered before the next
-      // attempt by the rounds' grid syncs)
-      for (unsigned long long i = (unsigned long long)b * kBlock + threadIdx.x; i <= a.fin_mask;
-           i += (unsigned long long)G * kBlock)
-        reinterpret_cast<ulonglong2*>(a.fin_table)[i] = make_ulonglong2(kNoKey, kNoKey);
-      fin_next = n_r / 4;
     }
-    // ---- H1: hook decisions over this block's component chunk
-    const uint32_t cs = (n_r + G - 1) / G;
-    const uint32_t clo = min(b * cs, n_r), chi = min(clo + cs, n_r);
+    // ---- A2: hook decisions over this block's chunk (a multiple of 32
+    // components, so root-mask words never straddle chunks)
+    const uint32_t cs = (((n_r + G - 1) / G) + 31u) & ~31u;
     {
-      uint32_t roots = 0;
+      const uint32_t clo = min(b * cs, n_r), chi = min(clo + cs, n_r);
+      uint32_t running = 0;
       unsigned long long wsum = 0;
       for (uint32_t base = clo; base < chi; base += kBlock * kItems) {
         unsigned long long key[kItems];
         uint4 e[kItems];
-        bool act[kItems];
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
           const uint32_t c = base + k * kBlock + threadIdx.x;
-          act[k] = c < chi;
-          key[k] = act[k] ? mcur[c] : kNoKey;
+          key[k] = c < chi ? __ldcg(mcur + c) : kNoKey;
         }
 #pragma unroll
-        for (int k = 0; k < kItems; ++k) e[k] = key[k] != kNoKey ? Ecur[(uint32_t)key[k]] : make_uint4(0, 0, 0, 0);
+        for (int k = 0; k < kItems; ++k) {
+          e[k] = make_uint4(0, 0, 0, 0);
+          if (key[k] != kNoKey) e[k] = r == a.r0 ? tail_entry_edge(a, (uint32_t)key[k]) : __ldcg(Eprev + (uint32_t)key[k]);
+        }
         unsigned long long okey[kItems];
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
@@ -1428,11 +1363,12 @@ __global__ void __launch_bounds__(kBlock, 2) k_tail(TailArgs a) {
           const uint32_t o = (e[k].x == c) ? e[k].y : e[k].x;
           okey[k] = key[k] != kNoKey ? __ldcg(mcur + o) : kNoKey;
         }
+        unsigned bal[kItems];
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
           const uint32_t c = base + k * kBlock + threadIdx.x;
           bool isroot = false;
-          if (act[k]) {
+          if (c < chi) {
             if (key[k] == kNoKey) {
               isroot = true;
               a.parent[c] = c;
@@ -1441,115 +1377,132 @@ __global__ void __launch_bounds__(kBlock, 2) k_tail(TailArgs a) {
               isroot = okey[k] == key[k] && c < o;
               a.parent[c] = isroot ? c : o;
               if (!isroot) {
-                a.rootlabel[c] = e[k].w;  // stash the MST edge id until its slot is known
+                a.rootlabel[c] = e[k].w;  // the MST edge id, placed in B
                 wsum += (uint32_t)(key[k] >> 32);
               }
             }
           }
-          roots += __popc(__ballot_sync(0xffffffffu, isroot));
+          bal[k] = __ballot_sync(0xffffffffu, isroot);
+          if (lane == 0) s_cnt[k * kWarps + warp] = __popc(bal[k]);
         }
-      }
-      wsum = warp_sum<unsigned long long>(wsum);
-      if (lane_id() == 0) {
-        s_wsum[threadIdx.x >> 5] = wsum;
-        s_cnt[threadIdx.x >> 5] = roots;
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        unsigned long long t = 0;
-        uint32_t rc = 0;
-        for (int i = 0; i < kWarps; ++i) {
-          t += s_wsum[i];
-          rc += s_cnt[i];
+        __syncthreads();
+        if (warp == 0) {
+          const uint32_t v = s_cnt[lane];
+          const uint32_t incl = warp_incl_scan(v);
+          s_cnt[lane] = incl - v;
+          if (lane == 31) s_cnt[32] = incl;
         }
-        if (t) atomicAdd(&a.ctr->total_weight, t);
-        a.bcount[b] = rc;
-      }
-      __syncthreads();
-    }
-    grid.sync();
-    tail_stamp(a, slot);
-    // ---- H2: dense root labels and MST slots, in component order
-    {
-      uint32_t running = block_prefix(a.bcount, b, s_misc);
-      const uint32_t start_prefix = running;
-      for (uint32_t base = clo; base < chi; base += kBlock * kItems) {
-        bool f[kItems];
-        uint32_t rank[kItems];
+        __syncthreads();
+        if (lane == 0) {
 #pragma unroll
-        for (int k = 0; k < kItems; ++k) {
-          const uint32_t c = base + k * kBlock + threadIdx.x;
-          f[k] = c < chi && __ldcg(a.parent + c) == c;
-        }
-        const uint32_t tot = block_ranks(f, rank, s_cnt);
-#pragma unroll
-        for (int k = 0; k < kItems; ++k) {
-          const uint32_t c = base + k * kBlock + threadIdx.x;
-          if (c < chi) {
-            const uint32_t before = running + rank[k];
-            if (f[k])
-              a.rootlabel[c] = before;
-            else
-            {
-              const uint32_t eid = a.rootlabel[c];
-              a.mst[mst_base + (c - before)] = eid;
-              if (a.flags) a.flags[eid] = 1;
+          for (int k = 0; k < kItems; ++k) {
+            const uint32_t c0 = base + k * kBlock + warp * 32;
+            if (c0 < chi) {
+              a.masks[c0 >> 5] = bal[k];
+              a.wpref[c0 >> 5] = running + s_cnt[k * kWarps + warp];
             }
           }
         }
-        running += tot;
+        running += s_cnt[32];
+        __syncthreads();
       }
-      if (b == G - 1 && threadIdx.x == 0) {
-        (void)start_prefix;
-        const uint32_t roots = running;
-        a.ctr->n[r + 1] = roots;
-        if (roots <= 1) {
-          a.ctr->stop_round = (uint32_t)r + 1;
-        } else if (roots == n_r) {
-          if (a.light)
-            a.ctr->phase_end = (uint32_t)r;
-          else
-            a.ctr->stop_round = (uint32_t)r + 1;
-        }
+      wsum = warp_sum<unsigned long long>(wsum);
+      if (lane == 0) s_wsum[warp] = wsum;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int i = 0; i < kWarps; ++i) t += s_wsum[i];
+        if (t) atomicAdd(&a.ctr->total_weight, t);
+        a.broots[b] = running;
       }
     }
     grid.sync();
     tail_stamp(a, slot);
-    if ((uint32_t)r + 1 >= vc->stop_round || (uint32_t)r >= vc->phase_end) break;
-    const uint32_t n_next = vc->n[r + 1];
-    // ---- L: labels via root finding, clear the next min table
+    // ---- B: dense labels, MST slots, next min table
+    if (r > a.r0 && vc->m[r] == 0) {
+      // round r-1 kept no edge: the same verdict the round kernels' edge
+      // scan gives (scan_verdict)
+      if (b == 0 && threadIdx.x == 0) {
+        if (a.light)
+          a.ctr->phase_end = (uint32_t)r;
+        else
+          a.ctr->stop_round = (uint32_t)r;
+      }
+      break;
+    }
+    block_scan_array(a.broots, G, s_bpre, s_warp);
+    const uint32_t n_next = s_bpre[G];
+    bool stop_now = false, phase_now = false;
+    if (n_next <= 1) {
+      stop_now = true;
+    } else if (n_next == n_r) {
+      // no live edge anywhere: done (a forest), or the light phase ends
+      if (a.light)
+        phase_now = true;
+      else
+        stop_now = true;
+    }
+    if (b == 0 && threadIdx.x == 0) {
+      a.ctr->n[r + 1] = n_next;
+      if (stop_now) a.ctr->stop_round = (uint32_t)r + 1;
+      if (phase_now) a.ctr->phase_end = (uint32_t)r;
+    }
+    if (phase_now) break;  // the host composes the maps; nothing of round r is kept
     for (uint32_t base = b * kBlock * kItems; base < n_r; base += G * kBlock * kItems) {
       uint32_t c[kItems], root[kItems];
-      bool v[kItems];
+      bool v[kItems], walk[kItems], isroot[kItems];
 #pragma unroll
       for (int k = 0; k < kItems; ++k) {
         c[k] = base + k * kBlock + threadIdx.x;
         v[k] = c[k] < n_r;
+        isroot[k] = v[k] && ((__ldcg(a.masks + (c[k] >> 5)) >> (c[k] & 31)) & 1u);
+        walk[k] = v[k] && !isroot[k] && !stop_now;
       }
-      find_roots<kItems>(a.parent, c, v, root);
+#pragma unroll
+      for (int k = 0; k < kItems; ++k) {
+        if (!v[k] || isroot[k]) continue;
+        const uint32_t x = c[k], w = x >> 5;
+        const uint32_t before = s_bpre[x / cs] + __ldcg(a.wpref + w) +
+                                __popc(__ldcg(a.masks + w) & ((1u << (x & 31)) - 1u));
+        const uint32_t eid = __ldcg(a.rootlabel + x);
+        a.mst[mst_base + (x - before)] = eid;
+        if (a.flags) a.flags[eid] = 1;
+      }
+      if (stop_now) continue;
+      find_roots<kItems>(a.parent, c, walk, root);
 #pragma unroll
       for (int k = 0; k < kItems; ++k) {
         if (!v[k]) continue;
-        a.L[c[k]] = __ldcg(a.rootlabel + root[k]);
+        const uint32_t x = isroot[k] ? c[k] : root[k], w = x >> 5;
+        a.L[c[k]] = s_bpre[x / cs] + __ldcg(a.wpref + w) + __popc(__ldcg(a.masks + w) & ((1u << (x & 31)) - 1u));
         if (c[k] < n_next) mnext[c[k]] = kNoKey;
       }
     }
     grid.sync();
     tail_stamp(a, slot);
-    // ---- C1: relabel in place, count kept per block (+ light-phase map update)
+    if (stop_now) break;
+    // ---- C: relabel E_r in place, count kept per block, offers for round r+1
     if (a.light) {
       for (uint32_t x = b * kBlock + threadIdx.x; x < n_entry; x += G * kBlock) a.M[x] = __ldcg(a.L + a.M[x]);
     }
-    const uint64_t es = (m_r + G - 1) / G;
-    const uint64_t elo = min((uint64_t)b * es, m_r), ehi = min(elo + es, m_r);
     {
+      const uint64_t m_r = vc->m[r];
+      const uint64_t es = (m_r + G - 1) / G;
+      const uint64_t elo = min((uint64_t)b * es, m_r), ehi = min(elo + es, m_r);
+      // Few components left: offers hammer a handful of lines. Aggregate them
+      // in a block-local shared-memory table and flush once per block.
+      const bool local = n_next <= kTailSmemMin;
+      if (local) {
+        for (uint32_t c = threadIdx.x; c < n_next; c += kBlock) s_min[c] = kNoKey;
+        __syncthreads();
+      }
       uint32_t kept = 0;
       for (uint64_t base = elo; base < ehi; base += kBlock * kItems) {
-        uint2 e[kItems];
+        uint4 e[kItems];
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
           const uint64_t i = base + k * kBlock + threadIdx.x;
-          e[k] = i < ehi ? __ldcg(reinterpret_cast<const uint2*>(Ecur + i)) : make_uint2(0, 0);
+          e[k] = i < ehi ? __ldcg(Ecur + i) : make_uint4(0, 0, 0, 0);
         }
         uint32_t x[kItems], y[kItems];
 #pragma unroll
@@ -1561,61 +1514,27 @@ __global__ void __launch_bounds__(kBlock, 2) k_tail(TailArgs a) {
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
           const uint64_t i = base + k * kBlock + threadIdx.x;
-          if (i < ehi) {
-            *reinterpret_cast<uint2*>(Ecur + i) = make_uint2(x[k], y[k]);
-            kept += (x[k] != y[k]);
+          if (i >= ehi) continue;
+          *reinterpret_cast<uint2*>(Ecur + i) = make_uint2(x[k], y[k]);
+          if (x[k] == y[k]) continue;
+          ++kept;
+          const unsigned long long key = ((unsigned long long)e[k].z << 32) | (uint32_t)i;
+          if (local) {
+            if (key < s_min[x[k]]) atomicMin(s_min + x[k], key);
+            if (key < s_min[y[k]]) atomicMin(s_min + y[k], key);
+          } else {
+            offer(mnext, x[k], key, true, true);
+            offer(mnext, y[k], key, true, true);
           }
         }
       }
       kept = warp_sum<uint32_t>(kept);
-      if (lane_id() == 0) s_cnt[threadIdx.x >> 5] = kept;
+      if (lane == 0) s_cnt[warp] = kept;
       __syncthreads();
       if (threadIdx.x == 0) {
         uint32_t t = 0;
         for (int i = 0; i < kWarps; ++i) t += s_cnt[i];
-        a.bcount[b] = t;
-      }
-      __syncthreads();
-    }
-    grid.sync();
-    tail_stamp(a, slot);
-    // ---- C2: ordered compaction + offers for round r+1
-    {
-      // Few components left: offers hammer a handful of lines. Aggregate them
-      // in a block-local shared-memory table and flush once per block.
-      const bool local = n_next <= kTailSmemMin;
-      if (local) {
-        for (uint32_t c = threadIdx.x; c < n_next; c += kBlock) s_min[c] = kNoKey;
-        __syncthreads();
-      }
-      uint32_t running = block_prefix(a.bcount, b, s_misc);
-      for (uint64_t base = elo; base < ehi; base += kBlock * kItems) {
-        bool f[kItems];
-        uint32_t rank[kItems];
-        uint4 e[kItems];
-#pragma unroll
-        for (int k = 0; k < kItems; ++k) {
-          const uint64_t i = base + k * kBlock + threadIdx.x;
-          e[k] = i < ehi ? __ldcg(Ecur + i) : make_uint4(0, 0, 0, 0);
-          f[k] = i < ehi && e[k].x != e[k].y;
-        }
-        const uint32_t tot = block_ranks(f, rank, s_cnt);
-#pragma unroll
-        for (int k = 0; k < kItems; ++k) {
-          const uint32_t j = running + rank[k];
-          if (f[k]) Enext[j] = e[k];
-          const unsigned long long key = ((unsigned long long)e[k].z << 32) | j;
-          if (local) {
-            if (f[k]) {
-              atomicMin(s_min + e[k].x, key);
-              atomicMin(s_min + e[k].y, key);
-            }
-          } else {
-            offer<kWarpPre>(mnext, e[k].x, key, f[k], true);
-            offer<kWarpPre>(mnext, e[k].y, key, f[k], true);
-          }
-        }
-        running += tot;
+        a.bkept[b] = t;
       }
       if (local) {
         __syncthreads();
@@ -1624,467 +1543,9 @@ __global__ void __launch_bounds__(kBlock, 2) k_tail(TailArgs a) {
           if (v != kNoKey && v < __ldcg(mnext + c)) atomicMin(mnext + c, v);
         }
       }
-      if (b == G - 1 && threadIdx.x == 0) {
-        a.ctr->m[r + 1] = running;
-        if (running == 0) {
-          if (a.light)
-            a.ctr->phase_end = (uint32_t)r + 1;
-          else if (a.ctr->stop_round == kNoStop)
-            a.ctr->stop_round = (uint32_t)r + 1;
-        }
-      }
     }
     grid.sync();
     tail_stamp(a, slot);
-  }
-}
-
-// Exclusive block-wide scan of one value per thread (kFinThreads threads).
-__device__ __forceinline__ uint32_t fin_scan(uint32_t v, uint32_t* s_warp, uint32_t* s_total) {
-  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-  const uint32_t incl = warp_incl_scan(v);
-  if (lane == 31) s_warp[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    const uint32_t t = s_warp[lane];
-    const uint32_t ti = warp_incl_scan(t);
-    s_warp[lane] = ti - t;
-    if (lane == 31) *s_total = ti;
-  }
-  __syncthreads();
-  const uint32_t out = s_warp[warp] + incl - v;
-  __syncthreads();
-  return out;
-}
-
-struct FinArgs {
-  const uint4* E[2];
-  uint32_t* mst;
-  uint8_t* flags;
-  unsigned long long* trace;  // optional: globaltimer at entry, after the load, after each round
-  DevCounters* ctr;
-  uint32_t n_orig;
-};
-
-__device__ __forceinline__ void fin_stamp(const FinArgs& a, int& slot) {
-  if (a.trace && threadIdx.x == 0 && slot < 64) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    a.trace[slot] = t;
-  }
-  ++slot;
-}
-
-// All remaining rounds in one block: edges {a | b << 16, w} and the per-
-// component key / parent / label arrays live in shared memory. Same hook
-// rule, MST slots, counters and verdicts as the grid-wide rounds.
-__global__ void __launch_bounds__(kFinThreads, 1) k_finish(FinArgs a) {
-  pdl_prologue();
-  volatile DevCounters* vc = a.ctr;
-  const uint32_t r0 = vc->fin_round;
-  if (r0 == kNoStop) return;
-  extern __shared__ unsigned long long fin_smem[];
-  // per component: lightest weight, then the lowest position among the edges
-  // of that weight = the (w << 32 | position) minimum, with two native 32-bit
-  // shared atomics instead of a 64-bit CAS loop
-  uint32_t* mw = reinterpret_cast<uint32_t*>(fin_smem);                 // [kFinC]
-  uint32_t* mi = mw + kFinC;                                            // [kFinC]
-  uint32_t* ab = mi + kFinC;                                            // [kFinE]
-  uint32_t* wt = ab + kFinE;                                            // [kFinE]
-  uint16_t* par = reinterpret_cast<uint16_t*>(wt + kFinE);              // [kFinC]
-  uint16_t* lab = par + kFinC;                                          // [kFinC]
-  __shared__ uint32_t s_warp[32], s_total;
-  __shared__ unsigned long long s_wsum[32];
-  const uint32_t T = kFinThreads, tid = threadIdx.x;
-  int tslot = 0;
-  fin_stamp(a, tslot);
-  const uint4* E = (r0 & 1) ? a.E[0] : a.E[1];  // k_tail's Enext of round r0
-  const uint32_t m = vc->fin_m;
-  uint32_t n = vc->n[r0];
-  for (uint32_t i = tid; i < m; i += T) {
-    const uint4 e = __ldcg(E + i);
-    ab[i] = e.x | (e.y << 16);
-    wt[i] = e.z;
-  }
-  __syncthreads();
-  fin_stamp(a, tslot);
-  unsigned long long wsum = 0;
-  uint32_t r = r0;
-  while (true) {
-    if (r + 2 >= (uint32_t)kMaxR) {
-      if (tid == 0) a.ctr->err |= 4u;  // no convergence (cannot happen: n halves per round)
-      break;
-    }
-    const uint32_t mst_base = a.n_orig - n;
-    for (uint32_t c = tid; c < n; c += T) {
-      mw[c] = kNone;
-      mi[c] = kNone;
-    }
-    __syncthreads();
-    for (uint32_t i = tid; i < m; i += T) {
-      const uint32_t e = ab[i], x = e & 0xFFFFu, y = e >> 16;
-      if (x == y) continue;
-      const uint32_t w = wt[i];
-      if (w < mw[x]) atomicMin(mw + x, w);
-      if (w < mw[y]) atomicMin(mw + y, w);
-    }
-    __syncthreads();
-    for (uint32_t i = tid; i < m; i += T) {
-      const uint32_t e = ab[i], x = e & 0xFFFFu, y = e >> 16;
-      if (x == y) continue;
-      const uint32_t w = wt[i];
-      if (w == mw[x] && i < mi[x]) atomicMin(mi + x, i);
-      if (w == mw[y] && i < mi[y]) atomicMin(mi + y, i);
-    }
-    __syncthreads();
-    fin_stamp(a, tslot);
-    // hook: partner along the lightest edge; a mutual pair (same edge) keeps
-    // the lower label as root
-    for (uint32_t c = tid; c < n; c += T) {
-      const uint32_t i = mi[c];
-      uint32_t p = c;
-      if (i != kNone) {
-        const uint32_t e = ab[i], x = e & 0xFFFFu, y = e >> 16;
-        const uint32_t o = x == c ? y : x;
-        if (!(mi[o] == i && c < o)) {
-          p = o;
-          wsum += mw[c];
-        }
-      }
-      par[c] = (uint16_t)p;
-    }
-    __syncthreads();
-    fin_stamp(a, tslot);
-    while (true) {  // pointer jumping to the roots
-      int changed = 0;
-      for (uint32_t c = tid; c < n; c += T) {
-        const uint32_t p = par[c], pp = par[p];
-        if (p != pp) {
-          par[c] = (uint16_t)pp;
-          changed = 1;
-        }
-      }
-      if (!__syncthreads_or(changed)) break;
-    }
-    fin_stamp(a, tslot);
-    // dense root labels in component order; MST slots of hooked components
-    const uint32_t per = (n + T - 1) / T, lo = min(tid * per, n), hi = min(lo + per, n);
-    uint32_t cnt = 0;
-    for (uint32_t c = lo; c < hi; ++c) cnt += par[c] == c;
-    uint32_t run = fin_scan(cnt, s_warp, &s_total);
-    const uint32_t n_next = s_total;
-    // the hooked components' edge ids: independent L2 loads, all in flight
-    constexpr int kPer = kFinC / kFinThreads;
-    uint32_t eids[kPer];
-#pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-      const uint32_t c = lo + j;
-      eids[j] = (c < hi && par[c] != c) ? __ldcg(&E[mi[c]].w) : 0u;
-    }
-#pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-      const uint32_t c = lo + j;
-      if (c >= hi) break;
-      if (par[c] == c) {
-        lab[c] = (uint16_t)run++;
-      } else {
-        a.mst[mst_base + (c - run)] = eids[j];
-        if (a.flags) a.flags[eids[j]] = 1;
-      }
-    }
-    __syncthreads();
-    for (uint32_t c = lo; c < hi; ++c)
-      if (par[c] != c) lab[c] = lab[par[c]];
-    __syncthreads();
-    fin_stamp(a, tslot);
-    if (tid == 0) a.ctr->n[r + 1] = n_next;
-    if (n_next <= 1 || n_next == n) {
-      if (tid == 0) a.ctr->stop_round = r + 1;
-      break;
-    }
-    uint32_t live = 0;
-    for (uint32_t i = tid; i < m; i += T) {
-      const uint32_t e = ab[i], x = e & 0xFFFFu, y = e >> 16;
-      if (x == y) continue;
-      const uint32_t nx = lab[x], ny = lab[y];
-      ab[i] = nx | (ny << 16);
-      live += nx != ny;
-    }
-    fin_scan(live, s_warp, &s_total);
-    const uint32_t live_total = s_total;
-    if (tid == 0) a.ctr->m[r + 1] = live_total;
-    if (live_total == 0) {
-      if (tid == 0) a.ctr->stop_round = r + 1;
-      break;
-    }
-    n = n_next;
-    ++r;
-    fin_stamp(a, tslot);
-  }
-  fin_stamp(a, tslot);
-  wsum = warp_sum<unsigned long long>(wsum);
-  if (lane_id() == 0) s_wsum[tid >> 5] = wsum;
-  __syncthreads();
-  if (tid == 0) {
-    unsigned long long t = 0;
-    for (int i = 0; i < kFinThreads / 32; ++i) t += s_wsum[i];
-    if (t) atomicAdd(&a.ctr->total_weight, t);
-  }
-}
-
-// Tail v2: sparse labels, no compaction, two grid-wide steps per round.
-// Components keep their tail-entry label (a root id in [0, n0)); a round is
-//   H: every live root reads its key, the winning edge (whose endpoints were
-//      rewritten to current roots by the previous C step) and the partner's
-//      key, hooks (parent[c] = partner) unless it is the lower end of a
-//      mutual pair, and appends its MST edge at an atomically taken slot
-//      (the output is sorted by the bitmap pass anyway); clears the next
-//      min table;
-//   C: every live edge rewrites its endpoints to their current roots (path
-//      halving finds), drops out once both agree, and offers
-//      (w<<32 | entry index) to both roots (block-local smem table when the
-//      id space is small).
-// Entry: dense labels [0, n0) and the round-r0 min table, exactly as the
-// round kernels leave them. On exit in the light phase the roots are
-// densified (one prefix) so the filter pass and phase D see dense labels.
-__global__ void __launch_bounds__(kBlock) k_tail2(TailArgs a) {
-  pdl_prologue();
-  namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
-  __shared__ unsigned long long s_min[kTailSmemMin];
-  __shared__ uint32_t s_red[kWarps];
-  __shared__ unsigned long long s_wred[kWarps];
-  __shared__ uint32_t s_misc[2];
-  const uint32_t G = gridDim.x, b = blockIdx.x;
-  const uint64_t T = (uint64_t)G * kBlock;
-  const uint64_t tid = (uint64_t)b * kBlock + threadIdx.x;
-  volatile DevCounters* vc = a.ctr;
-  const int r0 = a.r0;
-  int slot = 0;
-  tail_stamp(a, slot);
-  if ((uint32_t)r0 >= vc->stop_round || (uint32_t)r0 >= vc->phase_end) return;  // uniform
-  const uint32_t n0 = vc->n[r0];
-  const uint64_t m0 = vc->m[r0];
-  uint4* E = (r0 & 1) ? a.E[1] : a.E[0];
-  for (uint64_t c = tid; c < n0; c += T) a.parent[c] = (uint32_t)c;
-  if (tid == 0) a.ctr->mst_fill = a.n_orig - n0;
-  grid.sync();
-  int r = r0;
-  bool densify = false;
-  for (; r < kMaxR - 2; ++r) {
-    const unsigned long long* mcur = (r & 1) ? a.minb[0] : a.minb[1];
-    unsigned long long* mnext = (r & 1) ? a.minb[1] : a.minb[0];
-    // ---- H: hooks
-    uint32_t hooks = 0;
-    unsigned long long wsum = 0;
-    for (uint64_t base = (uint64_t)b * kBlock * kItems; base < n0; base += T * kItems) {
-      uint32_t c[kItems];
-      unsigned long long key[kItems], okey[kItems];
-      uint4 e[kItems];
-      bool live[kItems];
-#pragma unroll
-      for (int k = 0; k < kItems; ++k) {
-        c[k] = (uint32_t)(base + k * kBlock + threadIdx.x);
-        live[k] = c[k] < n0 && __ldcg(a.parent + c[k]) == c[k];
-        if (c[k] < n0) mnext[c[k]] = kNoKey;
-        key[k] = live[k] ? __ldcg(mcur + c[k]) : kNoKey;
-      }
-#pragma unroll
-      for (int k = 0; k < kItems; ++k) e[k] = key[k] != kNoKey ? __ldcg(E + (uint32_t)key[k]) : make_uint4(0, 0, 0, 0);
-#pragma unroll
-      for (int k = 0; k < kItems; ++k) {
-        const uint32_t o = e[k].x == c[k] ? e[k].y : e[k].x;
-        okey[k] = key[k] != kNoKey ? __ldcg(mcur + o) : kNoKey;
-      }
-#pragma unroll
-      for (int k = 0; k < kItems; ++k) {
-        bool hook = false;
-        uint32_t o = 0;
-        if (key[k] != kNoKey) {
-          o = e[k].x == c[k] ? e[k].y : e[k].x;
-          hook = !(okey[k] == key[k] && c[k] < o);
-        }
-        const unsigned bal = __ballot_sync(0xffffffffu, hook);
-        if (bal) {
-          const uint32_t lane = lane_id();
-          uint32_t basepos = 0;
-          if (lane == __ffs(bal) - 1) basepos = atomicAdd(&a.ctr->mst_fill, (uint32_t)__popc(bal));
-          basepos = __shfl_sync(0xffffffffu, basepos, __ffs(bal) - 1);
-          if (hook) {
-            a.parent[c[k]] = o;
-            a.mst[basepos + __popc(bal & lanemask_lt())] = e[k].w;
-            if (a.flags) a.flags[e[k].w] = 1;
-            wsum += (uint32_t)(key[k] >> 32);
-          }
-          hooks += __popc(bal) * (lane == 0);
-        }
-      }
-    }
-    hooks = warp_sum<uint32_t>(hooks);
-    wsum = warp_sum<unsigned long long>(wsum);
-    if (lane_id() == 0) {
-      s_red[threadIdx.x >> 5] = hooks;
-      s_wred[threadIdx.x >> 5] = wsum;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint32_t h = 0;
-      unsigned long long ws = 0;
-      for (int i = 0; i < kWarps; ++i) {
-        h += s_red[i];
-        ws += s_wred[i];
-      }
-      if (h) atomicAdd(&a.ctr->hooks[r], h);
-      if (ws) atomicAdd(&a.ctr->total_weight, ws);
-    }
-    grid.sync();
-    tail_stamp(a, slot);
-    const uint32_t n_r = vc->n[r];
-    const uint32_t n_next = n_r - vc->hooks[r];
-    if (tid == 0) {
-      a.ctr->n[r + 1] = n_next;
-      if (n_next <= 1) {
-        a.ctr->stop_round = (uint32_t)r + 1;
-      } else if (n_next == n_r) {
-        if (a.light)
-          a.ctr->phase_end = (uint32_t)r;
-        else
-          a.ctr->stop_round = (uint32_t)r + 1;
-      }
-    }
-    if (n_next <= 1 || (n_next == n_r && !a.light)) break;
-    if (n_next == n_r) {  // light phase with nothing left to hook: densify below
-      densify = true;
-      break;
-    }
-    // ---- C: relabel live edges to current roots, offer for round r+1
-    const bool local = n0 <= kTailSmemMin;
-    if (local) {
-      for (uint32_t c = threadIdx.x; c < n0; c += kBlock) s_min[c] = kNoKey;
-      __syncthreads();
-    }
-    uint32_t live = 0;
-    for (uint64_t base = (uint64_t)b * kBlock * kItems; base < m0; base += T * kItems) {
-      uint4 e[kItems];
-      bool v[kItems];
-#pragma unroll
-      for (int k = 0; k < kItems; ++k) {
-        const uint64_t i = base + k * kBlock + threadIdx.x;
-        e[k] = i < m0 ? __ldcg(E + i) : make_uint4(0, 0, 0, 0);
-        v[k] = i < m0 && e[k].x != e[k].y;
-      }
-      uint32_t xs[kItems], ys[kItems], rx[kItems], ry[kItems];
-#pragma unroll
-      for (int k = 0; k < kItems; ++k) {
-        xs[k] = e[k].x;
-        ys[k] = e[k].y;
-      }
-      find_roots<kItems>(a.parent, xs, v, rx);
-      find_roots<kItems>(a.parent, ys, v, ry);
-#pragma unroll
-      for (int k = 0; k < kItems; ++k) {
-        if (!v[k]) continue;
-        const uint64_t i = base + k * kBlock + threadIdx.x;
-        if (rx[k] != e[k].x || ry[k] != e[k].y) *reinterpret_cast<uint2*>(E + i) = make_uint2(rx[k], ry[k]);
-        if (rx[k] == ry[k]) continue;
-        ++live;
-        const unsigned long long key = ((unsigned long long)e[k].z << 32) | (uint32_t)i;
-        if (local) {
-          atomicMin(s_min + rx[k], key);
-          atomicMin(s_min + ry[k], key);
-        } else {
-          if (key < __ldcg(mnext + rx[k])) atomicMin(mnext + rx[k], key);
-          if (key < __ldcg(mnext + ry[k])) atomicMin(mnext + ry[k], key);
-        }
-      }
-    }
-    if (local) {
-      __syncthreads();
-      for (uint32_t c = threadIdx.x; c < n0; c += kBlock) {
-        const unsigned long long v = s_min[c];
-        if (v != kNoKey && v < __ldcg(mnext + c)) atomicMin(mnext + c, v);
-      }
-    }
-    live = warp_sum<uint32_t>(live);
-    if (lane_id() == 0) s_red[threadIdx.x >> 5] = live;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint32_t t = 0;
-      for (int i = 0; i < kWarps; ++i) t += s_red[i];
-      if (t) atomicAdd(&a.ctr->live[r + 1], t);
-    }
-    grid.sync();
-    tail_stamp(a, slot);
-    const uint32_t lv = vc->live[r + 1];
-    if (tid == 0) {
-      a.ctr->m[r + 1] = lv;
-      if (lv == 0) {
-        if (a.light)
-          a.ctr->phase_end = (uint32_t)r + 1;
-        else if (a.ctr->stop_round == kNoStop)
-          a.ctr->stop_round = (uint32_t)r + 1;
-      }
-    }
-    if (lv == 0) {
-      densify = a.light != 0;
-      break;
-    }
-  }
-  if (!densify) return;
-  // ---- light-phase exit: dense labels for the roots, entry-label map M,
-  // clear the min table of the round the filter pass feeds
-  const int R1 = (int)vc->phase_end;
-  const uint32_t cs = (n0 + G - 1) / G;
-  const uint32_t clo = min(b * cs, n0), chi = min(clo + cs, n0);
-  {
-    uint32_t roots = 0;
-    for (uint32_t c = clo + threadIdx.x; c < chi; c += kBlock) roots += __ldcg(a.parent + c) == c;
-    roots = warp_sum<uint32_t>(roots);
-    if (lane_id() == 0) s_red[threadIdx.x >> 5] = roots;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint32_t t = 0;
-      for (int i = 0; i < kWarps; ++i) t += s_red[i];
-      a.bcount[b] = t;
-    }
-  }
-  grid.sync();
-  {
-    uint32_t running = block_prefix(a.bcount, b, s_misc);
-    for (uint32_t base = clo; base < chi; base += kBlock) {
-      const uint32_t c = base + threadIdx.x;
-      const bool f = c < chi && __ldcg(a.parent + c) == c;
-      const unsigned bal = __ballot_sync(0xffffffffu, f);
-      if (lane_id() == 0) s_red[threadIdx.x >> 5] = __popc(bal);
-      __syncthreads();
-      uint32_t before = running, tot = 0;
-      for (int i = 0; i < kWarps; ++i) {
-        before += i < (int)(threadIdx.x >> 5) ? s_red[i] : 0u;
-        tot += s_red[i];
-      }
-      if (f) a.rootlabel[c] = before + __popc(bal & lanemask_lt());
-      running += tot;
-      __syncthreads();
-    }
-  }
-  grid.sync();
-  const uint32_t n_final = vc->n[R1];
-  unsigned long long* mR1 = (R1 & 1) ? a.minb[0] : a.minb[1];
-  for (uint64_t base = (uint64_t)b * kBlock * kItems; base < n0; base += T * kItems) {
-    uint32_t c[kItems], root[kItems];
-    bool v[kItems];
-#pragma unroll
-    for (int k = 0; k < kItems; ++k) {
-      c[k] = (uint32_t)(base + k * kBlock + threadIdx.x);
-      v[k] = c[k] < n0;
-    }
-    find_roots<kItems>(a.parent, c, v, root);
-#pragma unroll
-    for (int k = 0; k < kItems; ++k) {
-      if (!v[k]) continue;
-      a.M[c[k]] = __ldcg(a.rootlabel + root[k]);
-      if (c[k] < n_final) mR1[c[k]] = kNoKey;
-    }
   }
 }
 

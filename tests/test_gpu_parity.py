@@ -45,8 +45,8 @@ MODES = [dict(MST_FILTER=0), dict(MST_FILTER=1, MST_FILTER_BETA=0.3),
          # every round through the separate kernels with the pair-dedup variant armed
          dict(MST_FILTER=0, MST_TAIL=0, MST_DEDUP_MIN_EDGES=0),
          dict(MST_FILTER=1, MST_TAIL=0, MST_DEDUP_MIN_EDGES=0),
-         # the tail hands the last rounds to the one-block finisher
-         dict(MST_FILTER=0, MST_FINISH=1)]
+         # the tail megakernel with one block per SM (other chunk sizes)
+         dict(MST_FILTER=0, MST_TAIL_BPS=1, MST_TAIL_EDGES=1e9)]
 
 
 def _check(P, n, src, dst, w, ids, total, shards=(2, 3), modes=MODES):
