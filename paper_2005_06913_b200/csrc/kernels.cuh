@@ -36,7 +36,7 @@ constexpr int kBlock = 256;
 constexpr int kWarps = kBlock / 32;
 constexpr int kItems = 4;                // per thread, component tiles (hook)
 constexpr int kTile = kBlock * kItems;   // elements per tile (striped)
-constexpr int kCItems = 8;               // per thread, edge tiles (compaction)
+constexpr int kCItems = 4;               // per thread, edge tiles (compaction)
 constexpr int kCTile = kBlock * kCItems;
 
 constexpr int kMaxR = MST_MAX_ROUNDS + 2;
