@@ -990,6 +990,7 @@ struct Shard {
   unsigned long long* minb[2]{};
   unsigned long long *xch = nullptr, *own = nullptr;
   uint32_t *parent = nullptr, *rootlabel = nullptr, *L = nullptr, *partner = nullptr, *mst = nullptr;
+  uint32_t* hist = nullptr;  // Filter-Borůvka: weight histogram (summed across shards)
   uint4* E[2]{};
   DevCounters* d_ctr = nullptr;
   unsigned long long* st = nullptr;
@@ -999,16 +1000,17 @@ struct Exchanger {
   virtual ~Exchanger() = default;
   virtual void min_u64(std::vector<Shard>& sh, unsigned long long* Shard::*buf, uint64_t count) = 0;
   virtual void min_u32(std::vector<Shard>& sh, uint32_t* Shard::*buf, uint64_t count) = 0;
+  virtual void sum_u32(std::vector<Shard>& sh, uint32_t* Shard::*buf, uint64_t count) = 0;
 };
 
 // All shards on one device, one stream: an element-wise min kernel.
 struct EmulatedExchanger : Exchanger {
-  template <class T>
+  template <class T, bool kSum = false>
   static void run(std::vector<Shard>& sh, T* Shard::*buf, uint64_t count) {
     if (sh.size() == 1 || count == 0) return;
     ShardPtrs<T, 8> p{};
     for (size_t i = 0; i < sh.size(); ++i) p.p[i] = sh[i].*buf;
-    k_shard_min<T><<<(unsigned)std::min<uint64_t>((count + 255) / 256, 4096), 256, 0, sh[0].ws->stream>>>(
+    k_shard_min<T, kSum><<<(unsigned)std::min<uint64_t>((count + 255) / 256, 4096), 256, 0, sh[0].ws->stream>>>(
         p, (int)sh.size(), count);
     MST_CUDA_CHECK(cudaGetLastError());
   }
@@ -1016,6 +1018,9 @@ struct EmulatedExchanger : Exchanger {
     run(sh, buf, count);
   }
   void min_u32(std::vector<Shard>& sh, uint32_t* Shard::*buf, uint64_t count) override { run(sh, buf, count); }
+  void sum_u32(std::vector<Shard>& sh, uint32_t* Shard::*buf, uint64_t count) override {
+    run<uint32_t, true>(sh, buf, count);
+  }
 };
 
 // NCCL: one communicator per shard (single process driving several GPUs via
@@ -1023,13 +1028,13 @@ struct EmulatedExchanger : Exchanger {
 struct NcclExchanger : Exchanger {
   std::vector<ncclComm_t> comms;
   template <class T>
-  void run(std::vector<Shard>& sh, T* Shard::*buf, uint64_t count, ncclDataType_t type) {
+  void run(std::vector<Shard>& sh, T* Shard::*buf, uint64_t count, ncclDataType_t type, ncclRedOp_t op = ncclMin) {
     if (count == 0) return;
     MST_NCCL_CHECK(nccl().GroupStart());
     for (size_t i = 0; i < sh.size(); ++i) {
       MST_CUDA_CHECK(cudaSetDevice(sh[i].ws->device));
       T* p = sh[i].*buf;
-      MST_NCCL_CHECK(nccl().AllReduce(p, p, count, type, ncclMin, comms[i], sh[i].ws->stream));
+      MST_NCCL_CHECK(nccl().AllReduce(p, p, count, type, op, comms[i], sh[i].ws->stream));
     }
     MST_NCCL_CHECK(nccl().GroupEnd());
   }
@@ -1039,19 +1044,64 @@ struct NcclExchanger : Exchanger {
   void min_u32(std::vector<Shard>& sh, uint32_t* Shard::*buf, uint64_t count) override {
     run(sh, buf, count, ncclUint32);
   }
+  void sum_u32(std::vector<Shard>& sh, uint32_t* Shard::*buf, uint64_t count) override {
+    run(sh, buf, count, ncclUint32, ncclSum);
+  }
 };
 
-void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, RunOut& out) {
+// The sharded loop (kernels.cuh "sharded exchange"). With filter, the
+// Filter-Borůvka phases run sharded too: the weight histograms are summed
+// across shards so every shard picks the same pivot, each shard splits and
+// later filters its own edges, and the light-phase relabel maps are
+// replicated like every other piece of component state.
+void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, uint64_t m_total, bool filter,
+                        RunOut& out) {
   const int G = (int)sh.size();
   uint32_t launches = 0;
   for (auto& s : sh) {
     MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
     init_counters(*s.ws, s.d_ctr, n, s.m);
     MST_CUDA_CHECK(cudaMemsetAsync(s.minb[0], 0xFF, (size_t)n * 8, s.ws->stream));
-    auto kmin = k_min_round1<SoaView>;
-    launch_k(kmin, persistent_grid(kmin, s.ws->device, (s.m + kBlock - 1) / kBlock), kBlock, s.ws->stream, s.in, n, s.m,
-             s.minb[0], s.d_ctr, filt_for(n));
-    ++launches;
+  }
+  if (filter) {
+    // pivot from the summed histogram of every shard's weight sample
+    const uint64_t total_samples_target = std::min<uint64_t>(m_total, 1u << 20);
+    uint64_t total_samples = 0;
+    for (auto& s : sh) {
+      MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
+      s.hist = s.ws->get<uint32_t>("hist", 65536);
+      MST_CUDA_CHECK(cudaMemsetAsync(s.hist, 0, 65536 * sizeof(uint32_t), s.ws->stream));
+      const uint32_t samples = (uint32_t)std::min<uint64_t>(
+          s.m, std::max<uint64_t>(1, total_samples_target * s.m / std::max<uint64_t>(m_total, 1)));
+      if (s.m) {
+        const uint64_t step = std::max<uint64_t>(1, s.m / samples);
+        launch_k(k_weight_hist, std::max(1u, samples / 1024), 256, s.ws->stream, s.in.w, 1u, s.m, step, samples, s.hist);
+        total_samples += samples;
+      }
+    }
+    ex.sum_u32(sh, &Shard::hist, 65536);
+    const double beta = env_double("MST_FILTER_BETA", 1.5);
+    const double frac = std::min(1.0, beta * (double)n / (double)std::max<uint64_t>(m_total, 1));
+    const uint32_t target = (uint32_t)std::max(1.0, frac * (double)total_samples);
+    for (auto& s : sh) {
+      MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
+      Workspace& ws = *s.ws;
+      launch_k(k_pick_pivot, 1, 1024, ws.stream, s.hist, target, s.d_ctr);
+      const CompactBufs cb{ws.get<uint32_t>("tile_counts", tiles_c(s.m)),
+                           ws.get<uint32_t>("tile_masks", tiles_c(s.m) * kCItems * kWarps), s.st,
+                           ws.get<uint4>("stage", tiles_c(s.m) * kCTile)};
+      launch_two_pass<SoaView, kModeLight>(ws, cb, s.in, nullptr, nullptr, s.E[1], s.minb[0], s.d_ctr, 0, s.m, n,
+                                           kSlotCompact, (int)kPhaseSharded, filt_for(n));
+      launches += 4;
+    }
+  } else {
+    for (auto& s : sh) {
+      MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
+      auto kmin = k_min_round1<SoaView>;
+      launch_k(kmin, persistent_grid(kmin, s.ws->device, (s.m + kBlock - 1) / kBlock), kBlock, s.ws->stream, s.in, n,
+               s.m, s.minb[0], s.d_ctr, filt_for(n));
+      ++launches;
+    }
   }
   // errors (range) are checked before the first exchange
   for (auto& s : sh) {
@@ -1064,29 +1114,35 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, RunOu
       return;
     }
   }
+  bool light = filter;
+  int R1 = 0;                  // first round after the heavy filter
+  std::vector<int> levels;     // light rounds whose relabel map ("Llvl<r>") is kept
   uint64_t n_bound = n;
   int r = 1;
   int stop = 0;
   while (true) {
     if (r >= MST_MAX_ROUNDS) throw MstError{MST_ERR_STALL, "no convergence within MST_MAX_ROUNDS rounds"};
-    // 1. local literal keys -> (w, global id) keys + owned partners; exchange
+    // 1. local literal keys -> (w, global id) keys + owned partners; exchange.
+    // The keys index the list named by the single-device rule (run_single_impl
+    // hook_src).
     for (auto& s : sh) {
       MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
       const uint64_t t = (n_bound + kBlock - 1) / kBlock;
-      if (r == 1) {
-        auto kk = k_shard_keys<SoaView>;
-        launch_k(kk, persistent_grid(kk, s.ws->device, t), kBlock, s.ws->stream, s.in, s.minb[0], s.xch, s.own, s.d_ctr, r);
-      } else if (r == 2) {
-        // round 1's label pairs + the shard's weights (see k_count)
-        auto kk = k_shard_keys<PairsView<SoaView>>;
-        launch_k(kk, persistent_grid(kk, s.ws->device, t), kBlock, s.ws->stream,
-                 PairsView<SoaView>{reinterpret_cast<const uint2*>(s.E[1]), s.in}, s.minb[1], s.xch, s.own, s.d_ctr,
-                 r);
-      } else {
-        auto kk = k_shard_keys<PackedView>;
-        launch_k(kk, persistent_grid(kk, s.ws->device, t), kBlock, s.ws->stream, PackedView{s.E[(r - 1) & 1]},
-                 s.minb[(r - 1) & 1], s.xch, s.own, s.d_ctr, r);
-      }
+      unsigned long long* mcur = s.minb[(r - 1) & 1];
+      auto keys = [&](auto view) {
+        auto kk = k_shard_keys<decltype(view)>;
+        launch_k(kk, persistent_grid(kk, s.ws->device, t), kBlock, s.ws->stream, view, mcur, s.xch, s.own, s.d_ctr, r);
+      };
+      if (r == 1 && !filter)
+        keys(s.in);
+      else if (r == 1)
+        keys(PackedView{s.E[1]});
+      else if (r == R1)
+        keys(PackedView{s.E[r & 1]});
+      else if (r == 2 && !filter)
+        keys(PairsView<SoaView>{reinterpret_cast<const uint2*>(s.E[1]), s.in});
+      else
+        keys(PackedView{s.E[(r - 1) & 1]});
     }
     ex.min_u64(sh, &Shard::xch, n_bound);
     for (auto& s : sh) {
@@ -1104,52 +1160,102 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, RunOu
       cudaStream_t st = ws.stream;
       const uint64_t ht = tiles_of(n_bound);
       const int hfused = ht <= kFusedScanMaxTiles ? 1 : 0;
+      const int phase = light ? (int)kPhaseLight : (int)kPhasePlain;
       uint32_t* hcounts = ws.get<uint32_t>("hook_counts", tiles_of(n));
       uint32_t* hmasks = ws.get<uint32_t>("hook_masks", tiles_of(n) * kItems * kWarps);
       uint32_t* hslot = ws.get<uint32_t>("hook_slotpref", tiles_of(n) * kItems * kWarps);
       auto kd = k_hook_decide<PartnerView, true>;
       launch_k(kd, persistent_grid(kd, dev, ht), kBlock, st, PartnerView{s.partner}, s.xch, s.parent, s.rootlabel, hmasks,
-               hcounts, s.d_ctr, r, hfused, (int)kPhasePlain, hslot);
+               hcounts, s.d_ctr, r, hfused, phase, hslot);
       if (!hfused)
         launch_k(k_scan_counts<kScanRoots>,
                  (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((ht + kScanTile - 1) / kScanTile, (uint64_t)sm_count(dev))),
-                 kScanBlock, st, hcounts, ht, s.d_ctr, r, s.st, ws.next_epoch(), (int)kPhasePlain, 0);
+                 kScanBlock, st, hcounts, ht, s.d_ctr, r, s.st, ws.next_epoch(), phase, 0);
       unsigned long long* mnext = s.minb[r & 1];
-      launch_k(k_label2, persistent_grid(k_label2, dev, ht), kBlock, st, s.parent, s.rootlabel, hmasks, hslot, hcounts, s.L,
+      uint32_t* Lr = light ? ws.get<uint32_t>("Llvl" + std::to_string(r), n_bound) : s.L;
+      launch_k(k_label2, persistent_grid(k_label2, dev, ht), kBlock, st, s.parent, s.rootlabel, hmasks, hslot, hcounts, Lr,
                mnext, s.mst, (uint8_t*)nullptr, n, s.d_ctr, r, (unsigned long long*)nullptr, 0ull, 0u);
       MST_CUDA_CHECK(cudaMemcpyAsync(&ws.h_snap[r], s.d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, st));
       MST_CUDA_CHECK(cudaEventRecord(ws.ev[r], st));
-      const uint64_t m_bound = r == 1 ? s.m : ws.h_snap[r - 1].m[r];
+      const uint64_t m_bound = (r == 1 && !filter) ? s.m : (r == 1 || r == R1) ? s.m : ws.h_snap[r - 1].m[r];
       const CompactBufs cb{ws.get<uint32_t>("tile_counts", tiles_c(s.m)),
                            ws.get<uint32_t>("tile_masks", tiles_c(s.m) * kCItems * kWarps), s.st,
-                           ws.get<uint4>("stage", kCTile)};
+                           ws.get<uint4>("stage", tiles_c(s.m) * kCTile)};
       uint4* Eout = s.E[(r + 1) & 1];
-      if (r == 1)
-        launch_two_pass<SoaView, kModeRelabel>(ws, cb, s.in, s.E[1], s.L, Eout, mnext, s.d_ctr, r, m_bound, n,
-                                                     kSlotCompact, (int)kPhaseSharded, filt_for(n_bound));
+      if (r == 1 && !filter)
+        launch_two_pass<SoaView, kModeRelabel>(ws, cb, s.in, s.E[1], Lr, Eout, mnext, s.d_ctr, r, m_bound, n,
+                                               kSlotCompact, (int)kPhaseSharded, filt_for(n_bound));
       else
-        launch_two_pass<PackedView, kModeRelabel>(ws, cb, PackedView{s.E[r & 1]}, s.E[r & 1], s.L, Eout, mnext,
-                                                        s.d_ctr, r, m_bound, n, kSlotCompact, (int)kPhaseSharded,
-                                                        filt_for(n_bound));
+        launch_two_pass<PackedView, kModeRelabel>(ws, cb, PackedView{s.E[r & 1]}, s.E[r & 1], Lr, Eout, mnext,
+                                                  s.d_ctr, r, m_bound, n, kSlotCompact, (int)kPhaseSharded,
+                                                  filt_for(n_bound));
       launches += 5;
       MST_CUDA_CHECK(cudaGetLastError());
     }
+    if (light) levels.push_back(r);
     // verdict after label (identical on every shard: replicated hook)
-    uint32_t verdict = kNoStop;
+    uint32_t verdict = kNoStop, pend = kNoStop;
     uint32_t n_next = 0;
     for (int g = 0; g < G; ++g) {
       MST_CUDA_CHECK(cudaEventSynchronize(sh[g].ws->ev[r]));
       const DevCounters& snap = sh[g].ws->h_snap[r];
       if (g == 0) {
         verdict = snap.stop_round;
+        pend = snap.phase_end;
         n_next = snap.n[r + 1];
-      } else if (snap.stop_round != verdict || snap.n[r + 1] != n_next) {
+      } else if (snap.stop_round != verdict || snap.phase_end != pend || snap.n[r + 1] != n_next) {
         throw MstError{MST_ERR_STALL, "replicated hook diverged between shards"};
       }
     }
+    if (env_int("MST_DEBUG_ROUNDS", 0))
+      fprintf(stderr, "shard round %2d: n=%llu next=%u light=%d stop=%d phase_end=%d m0=%llu\n", r,
+              (unsigned long long)n_bound, n_next, (int)light, (int)verdict, (int)pend,
+              (unsigned long long)sh[0].ws->h_snap[r].m[r]);
     if (verdict != kNoStop && (int)verdict <= r + 1) {
       stop = (int)verdict;
       break;
+    }
+    if (light && pend != kNoStop && (int)pend <= r) {
+      // light phase over at round r (no light edge left between components)
+      const int pe = (int)pend;
+      if (pe == 1) {
+        // not a single light hook: the plain sharded loop instead
+        for (auto& s : sh) {
+          MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
+          MST_CUDA_CHECK(cudaStreamSynchronize(s.ws->stream));
+        }
+        run_sharded_rounds(sh, ex, n, m_total, false, out);
+        out.launches += launches;
+        return;
+      }
+      while (!levels.empty() && levels.back() >= pe) levels.pop_back();
+      R1 = pe;
+      for (auto& s : sh) {
+        MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
+        Workspace& ws = *s.ws;
+        const DevCounters& snap = ws.h_snap[r];
+        for (int k = (int)levels.size() - 2; k >= 0; --k) {
+          const unsigned g = (unsigned)std::max<uint64_t>(
+              1, std::min<uint64_t>((snap.n[levels[k]] + 255) / 256, (uint64_t)sm_count(ws.device) * 8));
+          launch_k(k_compose, g, 256, ws.stream, ws.get<uint32_t>("Llvl" + std::to_string(levels[k]), 1),
+                   (const uint32_t*)ws.get<uint32_t>("Llvl" + std::to_string(levels[k + 1]), 1), s.d_ctr, levels[k]);
+          ++launches;
+        }
+        const uint32_t* vlabel = levels.empty() ? nullptr : ws.get<uint32_t>("Llvl" + std::to_string(levels[0]), 1);
+        MST_CUDA_CHECK(cudaMemsetAsync(&s.d_ctr->phase_end, 0xFF, sizeof(unsigned int), ws.stream));
+        const CompactBufs cb{ws.get<uint32_t>("tile_counts", tiles_c(s.m)),
+                             ws.get<uint32_t>("tile_masks", tiles_c(s.m) * kCItems * kWarps), s.st,
+                             ws.get<uint4>("stage", tiles_c(s.m) * kCTile)};
+        // launched as round R1-1's producer: m[R1], E and the min table of round R1
+        launch_two_pass<SoaView, kModeHeavy>(ws, cb, s.in, nullptr, vlabel, s.E[R1 & 1], s.minb[(R1 - 1) & 1], s.d_ctr,
+                                             R1 - 1, s.m, n, kSlotFilter, (int)kPhaseSharded, filt_for(snap.n[R1]));
+        launches += 2;
+        MST_CUDA_CHECK(cudaStreamSynchronize(ws.stream));
+      }
+      light = false;
+      n_bound = sh[0].ws->h_snap[r].n[R1];
+      r = R1;
+      continue;
     }
     // the compaction's kept count m[r+1] sizes the next round's passes
     for (auto& s : sh) {
@@ -1242,7 +1348,7 @@ RunOut run_sharded(const std::vector<PartSpec>& parts, Exchanger& ex, uint32_t n
   cudaEvent_t e2 = sh[0].ws->tev[sh[0].ws->tev.size() - 2];
   MST_CUDA_CHECK(cudaEventRecord(e1, sh[0].ws->stream));
   RunOut o;
-  run_sharded_rounds(sh, ex, n, o);
+  run_sharded_rounds(sh, ex, n, m_total, filter_mode(n, m_total), o);
   check_err_bits(o.err);
   Workspace& ws0 = *sh[0].ws;
   MST_CUDA_CHECK(cudaSetDevice(ws0.device));

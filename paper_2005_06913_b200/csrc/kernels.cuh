@@ -67,6 +67,7 @@ struct DevCounters {
   unsigned long long pair_mask[kMaxR];
   unsigned int pair_count[kMaxR];  // distinct pairs inserted
   unsigned int pair_abort[kMaxR];  // table overflowed: keep every edge this round
+  unsigned int dedup_fail;         // some dedup attempt overflowed (sticky, see k_label2)
 };
 
 
@@ -482,7 +483,13 @@ __device__ __forceinline__ void fused_scan_if_last(uint32_t* counts, uint32_t T,
   if (*s_flag) {
     __threadfence();
     const uint32_t total = block_scan_counts(counts, T, s_warp);
-    if (threadIdx.x == 0) scan_verdict<kKind>(ctr, r, total, light_phase);
+    if (threadIdx.x == 0) {
+      scan_verdict<kKind>(ctr, r, total, light_phase);
+      // every block has checked in: re-arm the counter, so a round index
+      // that runs twice (the light phase's last round is phase D's first)
+      // finds it at zero
+      ctr->done[r][slot] = 0;
+    }
   }
 }
 
@@ -565,7 +572,10 @@ __device__ __forceinline__ void dedup_insert(uint4* __restrict__ E, const uint32
       }
     }
     fresh = warp_sum<uint32_t>(fresh);
-    if (lane_id() == 0 && fresh && atomicAdd(&ctr->pair_count[r], fresh) + fresh > limit) *abort_flag = 1;
+    if (lane_id() == 0 && fresh && atomicAdd(&ctr->pair_count[r], fresh) + fresh > limit) {
+      *abort_flag = 1;
+      ctr->dedup_fail = 1;
+    }
   }
 }
 
@@ -1106,7 +1116,11 @@ __global__ void __launch_bounds__(kBlock) k_label2(uint32_t* __restrict__ parent
     // "pair dedup"); tried when few active components carry many edges each
     const unsigned long long K = ctr->active[r];
     const unsigned long long m_r = ctr->m[r];
-    const bool use = K <= dedup_active && m_r >= 8 * K && m_r >= 4096;
+    // after an overflowed attempt (pairs mostly distinct: uniform graphs),
+    // try again only once K(K-1)/2 pairs guarantee an 8x reduction;
+    // R-MAT's repeated hub pairs keep succeeding and are not held back
+    const bool doubtful = ctr->dedup_fail && K * (K - 1) / 2 > m_r / 8;
+    const bool use = K <= dedup_active && m_r >= 8 * K && m_r >= 4096 && !doubtful;
     unsigned long long P = 1024;
     while (P < m_r / 4 && P < pair_cap) P <<= 1;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -1564,7 +1578,8 @@ struct ShardPtrs {
   T* p[kMaxShards];
 };
 
-template <class T>
+// Emulated allreduce over the shard buffers (min, or sum for histograms).
+template <class T, bool kSum = false>
 __global__ void k_shard_min(ShardPtrs<T, 8> bufs, int shards, uint64_t count) {
   pdl_prologue();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -1572,7 +1587,7 @@ __global__ void k_shard_min(ShardPtrs<T, 8> bufs, int shards, uint64_t count) {
     T v = bufs.p[0][i];
     for (int s = 1; s < shards; ++s) {
       const T x = bufs.p[s][i];
-      v = x < v ? x : v;
+      v = kSum ? v + x : (x < v ? x : v);
     }
     for (int s = 0; s < shards; ++s) bufs.p[s][i] = v;
   }

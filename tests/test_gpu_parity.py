@@ -59,9 +59,12 @@ def _check(P, n, src, dst, w, ids, total, shards=(2, 3), modes=MODES):
             a = P.boruvka_gpu_aos(n, g.to_aos())
             assert a.mst_edges.tolist() == list(ids) and a.total_weight == int(total)
     for s in shards:
-        e = P.boruvka_gpu_emulated(g, s)
-        assert e.mst_edges.tolist() == list(ids), f"{s}-shard edge set differs"
-        assert e.total_weight == int(total)
+        # the sharded loop, plain and with sharded Filter-Boruvka
+        for f in (0, 1):
+            with _env(MST_FILTER=f):
+                e = P.boruvka_gpu_emulated(g, s)
+            assert e.mst_edges.tolist() == list(ids), f"{s}-shard edge set differs (filter={f})"
+            assert e.total_weight == int(total)
 
 
 def test_small_golden_graphs(mst):
@@ -130,10 +133,12 @@ def test_edge_cases(mst, oracle_mod):
         with _env(**mode):
             r = P.boruvka_gpu(P.Graph(n, src, dst, w))
             assert r.mst_edges.tolist() == k.ids.tolist() and r.total_weight == k.total_weight
-    # the sharded exchange breaks ties by global id too
+    # the sharded exchange breaks ties by global id too (plain and filtered)
     for s in (2, 3, 8):
-        e = P.boruvka_gpu_emulated(P.Graph(n, src, dst, w), s)
-        assert e.mst_edges.tolist() == k.ids.tolist() and e.total_weight == k.total_weight
+        for f in (0, 1):
+            with _env(MST_FILTER=f):
+                e = P.boruvka_gpu_emulated(P.Graph(n, src, dst, w), s)
+            assert e.mst_edges.tolist() == k.ids.tolist() and e.total_weight == k.total_weight
     # all weights equal (the filter pivot then splits nothing off)
     w0 = np.zeros(m, dtype=np.uint32)
     k = O.kruskal(n, src, dst, w0)
@@ -258,6 +263,9 @@ def test_c3_full_size(mst, oracle_mod):
     assert v["total_weight"] == r.total_weight
     k = O.kruskal(g.n, g.src, g.dst, g.w)
     assert np.array_equal(r.mst_edges, k.ids.astype(np.int64)) and r.total_weight == k.total_weight
+    # the sharded loop with sharded Filter-Boruvka at full size
+    e = P.boruvka_gpu_emulated(g, 2)
+    assert np.array_equal(e.mst_edges, r.mst_edges) and e.total_weight == r.total_weight
 
 
 @pytest.mark.skipif(os.environ.get("MST_FULL_PARITY") != "1", reason="set MST_FULL_PARITY=1 (c4, ~1.1 B edges)")
