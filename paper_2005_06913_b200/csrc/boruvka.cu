@@ -102,6 +102,10 @@ struct Workspace {
   unsigned long long* status = nullptr;
   size_t status_words = 0;
   uint32_t epoch = 1;
+  // tail pair-dedup table: slots tagged (call epoch, round); cleared only
+  // when it grows or the 10-bit epoch wraps
+  uint32_t pair_epoch = 0;
+  size_t pair_slots = 0;
   DevCounters* h_snap = nullptr;  // pinned, kMaxR + 1 snapshots
   // pinned staging for pageable host buffers (two chunks, ping-pong)
   static constexpr size_t kStageBytes = 32u << 20;
@@ -133,6 +137,7 @@ struct Workspace {
     cudaStreamSynchronize(stream);
     for (auto& kv : bufs) cudaFree(kv.second.p);
     bufs.clear();
+    pair_slots = 0;
     if (status) cudaFree(status);
     status = nullptr;
     status_words = 0;
@@ -594,8 +599,12 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   DevCounters snap_b{};  // counters at the end of the light phase
   const bool tail_on = env_int("MST_TAIL", 1) != 0;
   const bool dedup_on = env_int("MST_DEDUP", 1) != 0;
+  // off by default: the tail's inserts are latency-bound at 2 CTAs/SM (c1
+  // round 3: 106 us for 3.0 M edges), slower than what they save
+  const bool tail_dedup_on = dedup_on && env_int("MST_TAIL_DEDUP", 0) != 0;
   const uint64_t dedup_min_edges = (uint64_t)env_double("MST_DEDUP_MIN_EDGES", 2.0e6);
   const unsigned int dedup_active = (unsigned int)env_double("MST_DEDUP_ACTIVE", 262144);
+  const unsigned int pair_div = (unsigned int)std::max(1, env_int("MST_DEDUP_TABLE_DIV", 4));
   // Tail entry (m_bound is the host's one-round-stale edge bound). Measured
   // (tools/sweep_tail.sh): the plain loop and phase D gain from entering
   // early (c1, c0: 6 M), the light phase from keeping the round kernels,
@@ -684,6 +693,21 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       const HookSrc src = hook_src(r);
       TailArgs ta{{E[0], E[1]}, {minb[0], minb[1]}, parent, rootlabel, L, mst, broots, bkept, tmasks, twpref, M, flags,
                   trace, 0, nullptr, nullptr, nullptr, 0, d_ctr, n, r, (int)light};
+      if (tail_dedup_on) {
+        // per-round table mask <= next_pow2(m_r / 2) <= this
+        const size_t slots = (size_t)std::max<unsigned long long>(1024, next_pow2(std::max<uint64_t>(m_bound / 2, 1)));
+        ulonglong2* pairs = ws.get<ulonglong2>("tail_pairs", slots);
+        if (slots > ws.pair_slots || ws.pair_epoch >= 1022) {
+          ws.pair_slots = std::max(ws.pair_slots, slots);
+          MST_CUDA_CHECK(cudaMemsetAsync(pairs, 0xFF, ws.pair_slots * sizeof(ulonglong2), s));
+          ws.pair_epoch = 0;
+        }
+        ta.pairs = pairs;
+        ta.pair_cap = slots;
+        ta.pair_epoch = ++ws.pair_epoch;
+        ta.dedup_ratio = (uint32_t)env_int("MST_TAIL_DEDUP_RATIO", 4);
+        ta.dedup_min = (uint32_t)env_double("MST_TAIL_DEDUP_MIN", 16384);
+      }
       if (src.kind == kSrcPacked) {
         ta.src_kind = kTailSrcPacked;
         ta.src0 = src.packed;
@@ -765,7 +789,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       const unsigned g = (unsigned)std::max<uint64_t>(
           1, std::min<uint64_t>(tiles_of(n_bound), (uint64_t)sm_count(dev) * blocks_per_sm(k_label2)));
       launch_k(k_label2, g, kBlock, s, parent, rootlabel, hmasks, hslot, hcounts, Lr, mnext, mst, flags, n, d_ctr, r,
-               pt.pairs, pt.cap, dedup_active);
+               pt.pairs, pt.cap, dedup_active, pair_div);
     }
     hot_begin(kHotCompact, r, light);
     if (original_in) {
@@ -1174,7 +1198,7 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, uint6
       unsigned long long* mnext = s.minb[r & 1];
       uint32_t* Lr = light ? ws.get<uint32_t>("Llvl" + std::to_string(r), n_bound) : s.L;
       launch_k(k_label2, persistent_grid(k_label2, dev, ht), kBlock, st, s.parent, s.rootlabel, hmasks, hslot, hcounts, Lr,
-               mnext, s.mst, (uint8_t*)nullptr, n, s.d_ctr, r, (unsigned long long*)nullptr, 0ull, 0u);
+               mnext, s.mst, (uint8_t*)nullptr, n, s.d_ctr, r, (unsigned long long*)nullptr, 0ull, 0u, 4u);
       MST_CUDA_CHECK(cudaMemcpyAsync(&ws.h_snap[r], s.d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, st));
       MST_CUDA_CHECK(cudaEventRecord(ws.ev[r], st));
       const uint64_t m_bound = (r == 1 && !filter) ? s.m : (r == 1 || r == R1) ? s.m : ws.h_snap[r - 1].m[r];

@@ -1104,7 +1104,7 @@ __global__ void __launch_bounds__(kBlock) k_label2(uint32_t* __restrict__ parent
                                                    uint32_t* __restrict__ mst, uint8_t* __restrict__ flags,
                                                    uint32_t n_orig, DevCounters* ctr, int r,
                                                    unsigned long long* pair_keys, unsigned long long pair_cap,
-                                                   unsigned int dedup_active) {
+                                                   unsigned int dedup_active, unsigned int pair_div) {
   pdl_prologue();
   if ((uint32_t)r >= ctr->stop_round || (uint32_t)r >= ctr->phase_end) return;
   const bool labels = (uint32_t)r + 1 < ctr->stop_round;  // the last hook round only emits MST slots
@@ -1122,7 +1122,7 @@ __global__ void __launch_bounds__(kBlock) k_label2(uint32_t* __restrict__ parent
     const bool doubtful = ctr->dedup_fail && K * (K - 1) / 2 > m_r / 8;
     const bool use = K <= dedup_active && m_r >= 8 * K && m_r >= 4096 && !doubtful;
     unsigned long long P = 1024;
-    while (P < m_r / 4 && P < pair_cap) P <<= 1;
+    while (P < m_r / pair_div && P < pair_cap) P <<= 1;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       ctr->dedup[r] = use ? 1u : 0u;
       ctr->pair_mask[r] = P - 1;
@@ -1178,17 +1178,30 @@ __global__ void __launch_bounds__(kBlock) k_label2(uint32_t* __restrict__ parent
 // in ONE cooperative launch (all blocks co-resident), three grid-wide steps
 // per round, same hook rule, counters, keys and verdicts as the round
 // kernels:
-//   A: ordered compaction of round r-1's relabelled list into E_r (per-block
-//      chunk counts, no look-back) AND round r's hook decisions: the keys
-//      index round r-1's list (offers are keyed by input position, see
-//      k_count), so the hook does not wait for the compaction. Each block
+//   A: round r's hook decisions over the block's component chunk; each block
 //      records its chunk's root bitmask and per-word root prefixes.
 //   B: dense labels: roots_before(x) = block prefix + word prefix + popc,
 //      root finding (path halving), MST slots of the hooked components,
 //      clear of the next min table.
-//   C: relabel E_r in place, count the kept edges per block and make the
-//      offers (w << 32 | position in E_r) for round r+1 (aggregated in a
-//      block-local shared-memory table when <= kTailSmemMin components).
+//   C: relabel + compact the block's own SEGMENT of the edge list in place
+//      and make the offers (w << 32 | new position) for round r+1
+//      (aggregated in a block-local shared-memory table when <=
+//      kTailSmemMin components remain).
+// The list is segmented: block b owns positions [b*es, b*es + len_b) of
+// the entry list for the whole launch and compacts its segment in place, so
+// no cross-block prefix and no second pass over the edges is needed.
+// Segments keep list order, so position order is still edge-id order (the
+// tie rule of the keys).
+//
+// Pair dedup (C0, optional per round): when the live edges outnumber the
+// next round's components (m_r >= ratio * n_{r+1}), many edges join the
+// same two components (grids and other low-genus graphs: <= 3 n_{r+1}
+// distinct pairs; R-MAT cores). C0 relabels in place and records each
+// pair's lightest key in a hash table; C then keeps only that edge (cycle
+// property: exact). Slots carry a 16-bit tag (call epoch, round) in the
+// pair word, so the table is never cleared between rounds; a slot is claimed
+// with a 128-bit CAS of {pair, key}. A round whose dedup removed < half the
+// edges turns it off until K(K-1)/2 <= m_r/4 guarantees the gain.
 struct TailArgs {
   uint4* E[2];
   unsigned long long* minb[2];
@@ -1197,7 +1210,7 @@ struct TailArgs {
   uint32_t* L;
   uint32_t* mst;
   uint32_t* broots;     // [gridDim.x] roots per block chunk (A -> B)
-  uint32_t* bkept;      // [gridDim.x] kept edges per block chunk (C -> A)
+  uint32_t* bkept;      // unused (kept for the layout)
   uint32_t* masks;      // root bitmask, one word per 32 components
   uint32_t* wpref;      // roots of the block's chunk before each word
   uint32_t* M;          // light phase: entry-label -> current-label map (n[r0] entries)
@@ -1214,10 +1227,18 @@ struct TailArgs {
   uint32_t n_orig;
   int r0;
   int light;
+  // pair dedup (pairs == nullptr: off)
+  ulonglong2* pairs;
+  unsigned long long pair_cap;  // slots, power of two
+  uint32_t pair_epoch;          // 1..1022, tag = epoch << 6 | round
+  uint32_t dedup_ratio;
+  uint32_t dedup_min;
 };
 
 constexpr uint32_t kTailSmemMin = 4096;  // block-local min table entries (32 KB)
 constexpr uint32_t kTailMaxBlocks = 1024;
+constexpr uint32_t kTailPairLabelBits = 24;
+constexpr int kTailPairProbes = 64;
 
 // Ordered ranks of kItems striped flags per thread; returns the total.
 __device__ __forceinline__ uint32_t block_ranks(const bool (&f)[kItems], uint32_t (&rank)[kItems],
@@ -1301,6 +1322,124 @@ __device__ __forceinline__ uint4 tail_entry_edge(const TailArgs& a, uint32_t i) 
   }
 }
 
+// Tagged pair word: tag(16) | min label(24) | max label(24).
+__device__ __forceinline__ unsigned long long tail_pair_word(uint32_t tag, uint32_t x, uint32_t y) {
+  const uint32_t lo = min(x, y), hi = max(x, y);
+  return ((unsigned long long)tag << 48) | ((unsigned long long)lo << kTailPairLabelBits) | hi;
+}
+
+// Record key as a candidate minimum of its pair. A failed insert (64 probes
+// over slots owned by other pairs this round) leaves the pair absent, so
+// every edge of it is kept by tail_pair_keep: always safe.
+__device__ __forceinline__ void tail_pair_insert(ulonglong2* t, unsigned long long mask, unsigned long long pw,
+                                                 unsigned long long key) {
+  const unsigned long long tag = pw >> 48;
+  unsigned long long h = pair_hash(pw) & mask;
+  ulonglong2 s = __ldcg(t + h);
+  for (int probe = 0; probe < kTailPairProbes;) {
+    if (s.x == pw) {
+      if (key < s.y) atomicMin(&t[h].y, key);
+      return;
+    }
+    if ((s.x >> 48) == tag) {  // another pair of this round
+      h = (h + 1) & mask;
+      ++probe;
+      s = __ldcg(t + h);
+      continue;
+    }
+    // empty for this round (stale tag): claim it with {pair, key}
+    const ulonglong2 want = make_ulonglong2(pw, key);
+    const ulonglong2 got = atomicCAS(t + h, s, want);
+    if (got.x == s.x && got.y == s.y) return;
+    s = got;  // lost the race: look at the winner's slot again
+  }
+}
+
+__device__ __forceinline__ bool tail_pair_keep(const ulonglong2* t, unsigned long long mask, unsigned long long pw,
+                                               unsigned long long key) {
+  const unsigned long long tag = pw >> 48;
+  unsigned long long h = pair_hash(pw) & mask;
+  for (int probe = 0; probe < kTailPairProbes; ++probe) {
+    const ulonglong2 s = __ldcg(t + h);
+    if (s.x == pw) return key <= s.y;
+    if ((s.x >> 48) != tag) return true;
+    h = (h + 1) & mask;
+  }
+  return true;
+}
+
+// kItems inserts with their first probes in flight together (slot loads,
+// then the CASes); the rare unresolved ones finish one by one.
+__device__ __forceinline__ void tail_pair_insert_batch(ulonglong2* t, unsigned long long mask,
+                                                       const unsigned long long (&pw)[kItems],
+                                                       const unsigned long long (&key)[kItems],
+                                                       const bool (&v)[kItems]) {
+  unsigned long long h[kItems];
+  ulonglong2 s[kItems], got[kItems];
+  bool todo[kItems], cas[kItems];
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) {
+    todo[k] = v[k];
+    h[k] = pair_hash(pw[k]) & mask;
+    s[k] = todo[k] ? __ldcg(t + h[k]) : make_ulonglong2(0, 0);
+  }
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) {
+    cas[k] = false;
+    if (!todo[k]) continue;
+    if (s[k].x == pw[k]) {
+      if (key[k] < s[k].y) atomicMin(&t[h[k]].y, key[k]);
+      todo[k] = false;
+    } else if ((s[k].x >> 48) != (pw[k] >> 48)) {
+      got[k] = atomicCAS(t + h[k], s[k], make_ulonglong2(pw[k], key[k]));
+      cas[k] = true;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kItems; ++k)
+    if (cas[k] && got[k].x == s[k].x && got[k].y == s[k].y) todo[k] = false;
+#pragma unroll
+  for (int k = 0; k < kItems; ++k)
+    if (todo[k]) tail_pair_insert(t, mask, pw[k], key[k]);
+}
+
+__device__ __forceinline__ void tail_pair_keep_batch(const ulonglong2* t, unsigned long long mask,
+                                                     const unsigned long long (&pw)[kItems],
+                                                     const unsigned long long (&key)[kItems], bool (&f)[kItems]) {
+  unsigned long long h[kItems];
+  ulonglong2 s[kItems];
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) {
+    h[k] = pair_hash(pw[k]) & mask;
+    s[k] = f[k] ? __ldcg(t + h[k]) : make_ulonglong2(0, 0);
+  }
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) {
+    if (!f[k]) continue;
+    if (s[k].x == pw[k])
+      f[k] = key[k] <= s[k].y;
+    else if ((s[k].x >> 48) == (pw[k] >> 48))
+      f[k] = tail_pair_keep(t, mask, pw[k], key[k]);  // probe on (rare)
+  }
+}
+
+// 2*kItems filtered offers with their reads in flight together.
+__device__ __forceinline__ void offer_batch(unsigned long long* table, const uint4 (&e)[kItems],
+                                            const unsigned long long (&key)[kItems], const bool (&f)[kItems]) {
+  unsigned long long cx[kItems], cy[kItems];
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) {
+    cx[k] = f[k] ? __ldcg(table + e[k].x) : 0ull;
+    cy[k] = f[k] ? __ldcg(table + e[k].y) : 0ull;
+  }
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) {
+    if (!f[k]) continue;
+    if (key[k] < cx[k]) atomicMin(table + e[k].x, key[k]);
+    if (key[k] < cy[k]) atomicMin(table + e[k].y, key[k]);
+  }
+}
+
 __global__ void __launch_bounds__(kBlock, 2) k_tail(TailArgs a) {
   pdl_prologue();
   namespace cg = cooperative_groups;
@@ -1316,41 +1455,34 @@ __global__ void __launch_bounds__(kBlock, 2) k_tail(TailArgs a) {
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   volatile DevCounters* vc = a.ctr;
   const uint32_t n_entry = vc->n[a.r0];
+  // this block's segment of the (single, in place) edge list
+  uint4* const E = (a.r0 & 1) ? a.E[1] : a.E[0];
+  const uint64_t m_entry = vc->m[a.r0];
+  const uint64_t es = (m_entry + G - 1) / G;
+  const uint64_t seg_lo = min((uint64_t)b * es, m_entry);
+  uint64_t seg_len = min(seg_lo + es, m_entry) - seg_lo;
+  bool dedup_off = false;  // identical on every block (from global counters)
+  int last_dedup = -1;
   for (int r = a.r0; r < kMaxR - 1; ++r) {
     if ((uint32_t)r >= vc->stop_round || (uint32_t)r >= vc->phase_end) break;
+    if (r > a.r0 && vc->m[r] == 0) {
+      // round r-1 kept no edge: the same verdict the round kernels' edge
+      // scan gives (scan_verdict)
+      if (b == 0 && threadIdx.x == 0) {
+        if (a.light)
+          a.ctr->phase_end = (uint32_t)r;
+        else
+          a.ctr->stop_round = (uint32_t)r;
+      }
+      break;
+    }
+    if (last_dedup == r - 1 && 2 * vc->m[r] > vc->m[r - 1]) dedup_off = true;
     const uint32_t n_r = vc->n[r];
     const uint32_t mst_base = a.n_orig - n_r;
     // ternaries, not a dynamic index: keeps TailArgs out of local memory
     const unsigned long long* mcur = (r & 1) ? a.minb[0] : a.minb[1];
     unsigned long long* mnext = (r & 1) ? a.minb[1] : a.minb[0];
-    uint4* Ecur = (r & 1) ? a.E[1] : a.E[0];
-    uint4* Eprev = (r & 1) ? a.E[0] : a.E[1];
-    // ---- A1: ordered compaction of round r-1's relabelled list into E_r
-    if (r > a.r0) {
-      const uint64_t m_prev = vc->m[r - 1];
-      const uint64_t es = (m_prev + G - 1) / G;
-      const uint64_t elo = min((uint64_t)b * es, m_prev), ehi = min(elo + es, m_prev);
-      block_scan_array(a.bkept, G, s_bpre, s_warp);
-      uint32_t running = s_bpre[b];
-      if (b == G - 1 && threadIdx.x == 0) a.ctr->m[r] = s_bpre[G];
-      for (uint64_t base = elo; base < ehi; base += kBlock * kItems) {
-        bool f[kItems];
-        uint32_t rank[kItems];
-        uint4 e[kItems];
-#pragma unroll
-        for (int k = 0; k < kItems; ++k) {
-          const uint64_t i = base + k * kBlock + threadIdx.x;
-          e[k] = i < ehi ? __ldcg(Eprev + i) : make_uint4(0, 0, 0, 0);
-          f[k] = i < ehi && e[k].x != e[k].y;
-        }
-        const uint32_t tot = block_ranks(f, rank, s_cnt);
-#pragma unroll
-        for (int k = 0; k < kItems; ++k)
-          if (f[k]) Ecur[running + rank[k]] = e[k];
-        running += tot;
-      }
-    }
-    // ---- A2: hook decisions over this block's chunk (a multiple of 32
+    // ---- A: hook decisions over this block's chunk (a multiple of 32
     // components, so root-mask words never straddle chunks)
     const uint32_t cs = (((n_r + G - 1) / G) + 31u) & ~31u;
     {
@@ -1368,7 +1500,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_tail(TailArgs a) {
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
           e[k] = make_uint4(0, 0, 0, 0);
-          if (key[k] != kNoKey) e[k] = r == a.r0 ? tail_entry_edge(a, (uint32_t)key[k]) : __ldcg(Eprev + (uint32_t)key[k]);
+          if (key[k] != kNoKey) e[k] = r == a.r0 ? tail_entry_edge(a, (uint32_t)key[k]) : __ldcg(E + (uint32_t)key[k]);
         }
         unsigned long long okey[kItems];
 #pragma unroll
@@ -1433,17 +1565,6 @@ __global__ void __launch_bounds__(kBlock, 2) k_tail(TailArgs a) {
     grid.sync();
     tail_stamp(a, slot);
     // ---- B: dense labels, MST slots, next min table
-    if (r > a.r0 && vc->m[r] == 0) {
-      // round r-1 kept no edge: the same verdict the round kernels' edge
-      // scan gives (scan_verdict)
-      if (b == 0 && threadIdx.x == 0) {
-        if (a.light)
-          a.ctr->phase_end = (uint32_t)r;
-        else
-          a.ctr->stop_round = (uint32_t)r;
-      }
-      break;
-    }
     block_scan_array(a.broots, G, s_bpre, s_warp);
     const uint32_t n_next = s_bpre[G];
     bool stop_now = false, phase_now = false;
@@ -1458,6 +1579,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_tail(TailArgs a) {
     }
     if (b == 0 && threadIdx.x == 0) {
       a.ctr->n[r + 1] = n_next;
+      a.ctr->m[r + 1] = 0;  // C adds every block's kept count
       if (stop_now) a.ctr->stop_round = (uint32_t)r + 1;
       if (phase_now) a.ctr->phase_end = (uint32_t)r;
     }
@@ -1495,14 +1617,56 @@ __global__ void __launch_bounds__(kBlock, 2) k_tail(TailArgs a) {
     grid.sync();
     tail_stamp(a, slot);
     if (stop_now) break;
-    // ---- C: relabel E_r in place, count kept per block, offers for round r+1
     if (a.light) {
       for (uint32_t x = b * kBlock + threadIdx.x; x < n_entry; x += G * kBlock) a.M[x] = __ldcg(a.L + a.M[x]);
     }
+    // ---- C0 (optional): relabel in place + each pair's lightest key
+    const uint64_t m_r = vc->m[r];
+    const bool dedup = a.pairs != nullptr && n_next < (1u << kTailPairLabelBits) && m_r >= a.dedup_min &&
+                       m_r >= (uint64_t)a.dedup_ratio * n_next &&
+                       (!dedup_off || (uint64_t)n_next * (n_next - 1) / 2 <= m_r / 4);
+    const uint32_t tag = (a.pair_epoch << 6) | ((uint32_t)r & 63u);
+    unsigned long long pmask = 0;
+    if (dedup) {
+      unsigned long long cap = 1024;
+      while (cap < m_r / 2 && cap < a.pair_cap) cap <<= 1;
+      pmask = min(cap, a.pair_cap) - 1;
+      last_dedup = r;
+      for (uint64_t base = seg_lo; base < seg_lo + seg_len; base += kBlock * kItems) {
+        uint4 e[kItems];
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          const uint64_t i = base + k * kBlock + threadIdx.x;
+          e[k] = i < seg_lo + seg_len ? __ldcg(E + i) : make_uint4(0, 0, 0, 0);
+        }
+        uint32_t x[kItems], y[kItems];
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          const uint64_t i = base + k * kBlock + threadIdx.x;
+          x[k] = i < seg_lo + seg_len ? __ldcg(a.L + e[k].x) : 0u;
+          y[k] = i < seg_lo + seg_len ? __ldcg(a.L + e[k].y) : 0u;
+        }
+        unsigned long long pw[kItems], key[kItems];
+        bool v[kItems];
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          const uint64_t i = base + k * kBlock + threadIdx.x;
+          v[k] = i < seg_lo + seg_len && x[k] != y[k];
+          pw[k] = tail_pair_word(tag, x[k], y[k]);
+          key[k] = ((unsigned long long)e[k].z << 32) | (uint32_t)i;
+        }
+        tail_pair_insert_batch(a.pairs, pmask, pw, key, v);
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          const uint64_t i = base + k * kBlock + threadIdx.x;
+          if (i < seg_lo + seg_len) *reinterpret_cast<uint2*>(E + i) = make_uint2(x[k], y[k]);
+        }
+      }
+      grid.sync();
+      tail_stamp(a, slot);
+    }
+    // ---- C: relabel + compact the segment in place, offers for round r+1
     {
-      const uint64_t m_r = vc->m[r];
-      const uint64_t es = (m_r + G - 1) / G;
-      const uint64_t elo = min((uint64_t)b * es, m_r), ehi = min(elo + es, m_r);
       // Few components left: offers hammer a handful of lines. Aggregate them
       // in a block-local shared-memory table and flush once per block.
       const bool local = n_next <= kTailSmemMin;
@@ -1510,46 +1674,63 @@ __global__ void __launch_bounds__(kBlock, 2) k_tail(TailArgs a) {
         for (uint32_t c = threadIdx.x; c < n_next; c += kBlock) s_min[c] = kNoKey;
         __syncthreads();
       }
-      uint32_t kept = 0;
-      for (uint64_t base = elo; base < ehi; base += kBlock * kItems) {
+      const uint64_t seg_hi = seg_lo + seg_len;
+      uint64_t out = seg_lo;
+      for (uint64_t base = seg_lo; base < seg_hi; base += kBlock * kItems) {
         uint4 e[kItems];
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
           const uint64_t i = base + k * kBlock + threadIdx.x;
-          e[k] = i < ehi ? __ldcg(Ecur + i) : make_uint4(0, 0, 0, 0);
+          e[k] = i < seg_hi ? __ldcg(E + i) : make_uint4(0, 0, 0, 0);
         }
-        uint32_t x[kItems], y[kItems];
+        bool f[kItems];
+        if (!dedup) {
 #pragma unroll
-        for (int k = 0; k < kItems; ++k) {
-          const uint64_t i = base + k * kBlock + threadIdx.x;
-          x[k] = i < ehi ? __ldcg(a.L + e[k].x) : 0u;
-          y[k] = i < ehi ? __ldcg(a.L + e[k].y) : 0u;
-        }
-#pragma unroll
-        for (int k = 0; k < kItems; ++k) {
-          const uint64_t i = base + k * kBlock + threadIdx.x;
-          if (i >= ehi) continue;
-          *reinterpret_cast<uint2*>(Ecur + i) = make_uint2(x[k], y[k]);
-          if (x[k] == y[k]) continue;
-          ++kept;
-          const unsigned long long key = ((unsigned long long)e[k].z << 32) | (uint32_t)i;
-          if (local) {
-            if (key < s_min[x[k]]) atomicMin(s_min + x[k], key);
-            if (key < s_min[y[k]]) atomicMin(s_min + y[k], key);
-          } else {
-            offer(mnext, x[k], key, true, true);
-            offer(mnext, y[k], key, true, true);
+          for (int k = 0; k < kItems; ++k) {
+            const uint64_t i = base + k * kBlock + threadIdx.x;
+            if (i < seg_hi) {
+              e[k].x = __ldcg(a.L + e[k].x);
+              e[k].y = __ldcg(a.L + e[k].y);
+            }
           }
         }
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          const uint64_t i = base + k * kBlock + threadIdx.x;
+          f[k] = i < seg_hi && e[k].x != e[k].y;
+        }
+        if (dedup) {
+          unsigned long long pw[kItems], key[kItems];
+#pragma unroll
+          for (int k = 0; k < kItems; ++k) {
+            pw[k] = tail_pair_word(tag, e[k].x, e[k].y);
+            key[k] = ((unsigned long long)e[k].z << 32) | (uint32_t)(base + k * kBlock + threadIdx.x);
+          }
+          tail_pair_keep_batch(a.pairs, pmask, pw, key, f);
+        }
+        uint32_t rank[kItems];
+        const uint32_t tot = block_ranks(f, rank, s_cnt);  // every load of the tile is done
+        unsigned long long key[kItems];
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          const uint64_t j = out + rank[k];
+          key[k] = ((unsigned long long)e[k].z << 32) | (uint32_t)j;
+          if (f[k]) E[j] = e[k];
+        }
+        if (local) {
+#pragma unroll
+          for (int k = 0; k < kItems; ++k) {
+            if (!f[k]) continue;
+            if (key[k] < s_min[e[k].x]) atomicMin(s_min + e[k].x, key[k]);
+            if (key[k] < s_min[e[k].y]) atomicMin(s_min + e[k].y, key[k]);
+          }
+        } else {
+          offer_batch(mnext, e, key, f);
+        }
+        out += tot;
       }
-      kept = warp_sum<uint32_t>(kept);
-      if (lane == 0) s_cnt[warp] = kept;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        uint32_t t = 0;
-        for (int i = 0; i < kWarps; ++i) t += s_cnt[i];
-        a.bkept[b] = t;
-      }
+      seg_len = out - seg_lo;
+      if (threadIdx.x == 0 && seg_len) atomicAdd(const_cast<unsigned long long*>(&a.ctr->m[r + 1]), seg_len);
       if (local) {
         __syncthreads();
         for (uint32_t c = threadIdx.x; c < n_next; c += kBlock) {
