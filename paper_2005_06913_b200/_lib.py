@@ -13,7 +13,9 @@ from pathlib import Path
 
 PKG_DIR = Path(__file__).resolve().parent
 REPO_ROOT = PKG_DIR.parent
-LIB_PATH = PKG_DIR / "libmstgpu.so"
+# MST_GPU_LIB: another build of the same library (A/B timing of two
+# versions in tools/, e.g. tools/ab/); the product path is the in-tree one
+LIB_PATH = Path(os.environ["MST_GPU_LIB"]) if os.environ.get("MST_GPU_LIB") else PKG_DIR / "libmstgpu.so"
 HEADER = REPO_ROOT / "include" / "mst_gpu.h"
 
 MST_OK = 0

@@ -311,12 +311,38 @@ unsigned long long next_pow2(unsigned long long x) {
 // wins, because hub / giant-component entries are hot — unfiltered REDs to
 // one address serialise at its L2 slice (c4: 172 -> 53 ms with the filter).
 // MST_FILTER_TABLE_MB=<size> turns it off for tables above that size.
-int filt_for(uint64_t table_entries) {
+// Offer mode per call site (kernels.cuh offer_both): 0 plain REDs, 1
+// read-first one offer at a time, 2 read-first with a thread's reads batched
+// (more memory-level parallelism; but a batch's reads all miss its own
+// atomics, which costs on hub-heavy tables). MST_OFFER_<SITE>=0|1|2
+// overrides. Defaults from tools/sweep_offer.sh and tools/ab2.sh (one
+// B200, c0-c4): batched for round 1 and for the round compactions of the
+// plain loop (sparse graphs: c1 -11 % with both); one at a time for the
+// light split, the heavy filter and the compactions of Filter-Boruvka's
+// phases, whose survivors concentrate on hubs (batched: c2 +3 %, c3 +1.5 %,
+// c4 +1.7 %).
+enum OfferSite { kSiteMin1 = 0, kSiteSplit = 1, kSiteCount = 2, kSiteHeavy = 3, kSiteCount_ = 4 };
+int filt_for(uint64_t table_entries, int site = kSiteCount, bool dense = true) {
   static const long long limit = [] {
     const char* e = getenv("MST_FILTER_TABLE_MB");
     return (long long)((e && *e) ? atof(e) : 1.0e7) << 20;
   }();
-  return table_entries * 8 <= (uint64_t)limit ? 1 : 0;
+  auto env_mode = [](const char* name) {
+    const char* e = getenv(name);
+    return e && *e ? atoi(e) : -1;
+  };
+  static const int mode[kSiteCount_] = {env_mode("MST_OFFER_MIN1"), env_mode("MST_OFFER_SPLIT"),
+                                        env_mode("MST_OFFER_COUNT"), env_mode("MST_OFFER_HEAVY")};
+  if (table_entries * 8 > (uint64_t)limit) return 0;
+  if (mode[site] >= 0) return mode[site];
+  switch (site) {
+    case kSiteMin1:
+      return 2;
+    case kSiteCount:
+      return dense ? 1 : 2;
+    default:
+      return 1;
+  }
 }
 
 double ms_between(cudaEvent_t a, cudaEvent_t b) {
@@ -485,7 +511,7 @@ void launch_two_pass(Workspace& ws, const CompactBufs& cb, View in, uint4* relab
   const uint64_t tiles = tiles_c(m_bound);
   const int fused = tiles <= kFusedScanMaxTiles ? 1 : 0;  // small: the last count block scans
   const bool armed = kMode == kModeRelabel && !View::kOriginal && pt.pairs != nullptr;
-  auto kcnt = k_count<View, kMode>;
+  auto kcnt = filt == 2 ? k_count<View, kMode, true> : k_count<View, kMode, false>;
   const unsigned gc = (unsigned)std::max<uint64_t>(
       1, std::min<uint64_t>(tiles, (uint64_t)sm_count(dev) * blocks_per_sm(kcnt)));
   // armed: this launch relabels + inserts pairs if the device chose dedup
@@ -515,7 +541,7 @@ void launch_two_pass(Workspace& ws, const CompactBufs& cb, View in, uint4* relab
     auto kem = k_emit<View, kMode>;
     launch_k(kem, ge, kBlock, ws.stream, in, relabeled, L, cb.masks, cb.counts, out, d_ctr, r, armed ? 1 : 0, n_orig);
   } else {
-    auto kes = k_emit_staged<kMode>;
+    auto kes = filt == 2 ? k_emit_staged<kMode, true> : k_emit_staged<kMode, false>;
     launch_k(kes, ge, kBlock, ws.stream, cb.stage, cb.counts, out, min_next, d_ctr, r, filt);
   }
   MST_CUDA_CHECK(cudaGetLastError());
@@ -578,7 +604,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     launches += 2;
     hot_begin(kHotSplit, 0, true);
     launch_two_pass<InView, kModeLight>(ws, cb, in, nullptr, nullptr, E[1], minb[0], d_ctr, 0, m, n,
-                                        kSlotCompact, 0, filt_for(n));
+                                        kSlotCompact, 0, filt_for(n, kSiteSplit));
     tmark();
     launches += 2;
   } else {
@@ -586,7 +612,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     const unsigned g = (unsigned)std::max<uint64_t>(
         1, std::min<uint64_t>((m + 4 * kBlock - 1) / (4 * kBlock), (uint64_t)sm_count(dev) * blocks_per_sm(kmin)));
     hot_begin(kHotMin1, 0, false);
-    launch_k(kmin, g, kBlock, s, in, n, m, minb[0], d_ctr, filt_for(n));
+    launch_k(kmin, g, kBlock, s, in, n, m, minb[0], d_ctr, filt_for(n, kSiteMin1));
     tmark();
     ++launches;
   }
@@ -611,6 +637,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   // whose pair dedup the tail lacks, a little longer (c2: 3.02 ms at 3 M vs
   // 3.19 ms at 6 M).
   const double tail_env = env_double("MST_TAIL_EDGES", 0.0);
+  const uint64_t tail_comps = (uint64_t)env_double("MST_TAIL_COMPS", 8.0e6);
   auto tail_edges = [&]() -> uint64_t { return (uint64_t)(tail_env > 0 ? tail_env : (light ? 3.0e6 : 6.0e6)); };
 
   // Light phase over: compose its relabel maps into a vertex -> component map,
@@ -641,7 +668,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     hot_begin(kHotHeavy, R1, false);
     // launched as round R1-1's producer: it writes m[R1] and E/min of round R1
     launch_two_pass<InView, kModeHeavy>(ws, cb, in, nullptr, vlabel, E[R1 & 1], minb[(R1 - 1) & 1], d_ctr,
-                                        R1 - 1, m, n, kSlotFilter, 0, filt_for(snap.n[R1]));
+                                        R1 - 1, m, n, kSlotFilter, 0, filt_for(snap.n[R1], kSiteHeavy));
     tmark();
     launches += 2;
     light = false;
@@ -669,7 +696,10 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     // round 1 of the light phase: the split keeps ~beta*n edges (the pivot's
     // target), a better bound than m before its count is known
     const uint64_t m_est = (light && r == 1) ? std::min<uint64_t>(m_bound, (uint64_t)(1.1 * light_target)) : m_bound;
-    if (tail_on && !original_in && m_est <= tail_edges()) {
+    // the tail runs at 2 CTAs/SM: its component phases are latency-bound when
+    // n_r is huge (c4's light phase ends with 47 M components and 406 edges:
+    // 1.2 ms in the tail vs 0.3 ms of round kernels)
+    if (tail_on && !original_in && m_est <= tail_edges() && n_bound <= tail_comps) {
       // ---- all remaining rounds in one cooperative launch
       uint32_t* M = nullptr;
       if (light) {
@@ -795,10 +825,10 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     if (original_in) {
       // plain round 1: relabelled copy of the caller's list in E[1], compacted into E[0]
       launch_two_pass<InView, kModeRelabel>(ws, cb, in, E[1], Lr, Eout, mnext, d_ctr, r, m_bound, n,
-                                            kSlotCompact, (int)light, filt_for(n_bound));
+                                            kSlotCompact, (int)light, filt_for(n_bound, kSiteCount, filter));
     } else {
       launch_two_pass<PackedView, kModeRelabel>(ws, cb, PackedView{E[r & 1]}, E[r & 1], Lr, Eout, mnext, d_ctr,
-                                                r, m_bound, n, kSlotCompact, (int)light, filt_for(n_bound), pt);
+                                                r, m_bound, n, kSlotCompact, (int)light, filt_for(n_bound, kSiteCount, filter), pt);
     }
     tmark();
     launches += 5;
@@ -1115,7 +1145,7 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, uint6
                            ws.get<uint32_t>("tile_masks", tiles_c(s.m) * kCItems * kWarps), s.st,
                            ws.get<uint4>("stage", tiles_c(s.m) * kCTile)};
       launch_two_pass<SoaView, kModeLight>(ws, cb, s.in, nullptr, nullptr, s.E[1], s.minb[0], s.d_ctr, 0, s.m, n,
-                                           kSlotCompact, (int)kPhaseSharded, filt_for(n));
+                                           kSlotCompact, (int)kPhaseSharded, filt_for(n, kSiteSplit));
       launches += 4;
     }
   } else {
@@ -1123,7 +1153,7 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, uint6
       MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
       auto kmin = k_min_round1<SoaView>;
       launch_k(kmin, persistent_grid(kmin, s.ws->device, (s.m + kBlock - 1) / kBlock), kBlock, s.ws->stream, s.in, n,
-               s.m, s.minb[0], s.d_ctr, filt_for(n));
+               s.m, s.minb[0], s.d_ctr, filt_for(n, kSiteMin1));
       ++launches;
     }
   }
@@ -1208,11 +1238,11 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, uint6
       uint4* Eout = s.E[(r + 1) & 1];
       if (r == 1 && !filter)
         launch_two_pass<SoaView, kModeRelabel>(ws, cb, s.in, s.E[1], Lr, Eout, mnext, s.d_ctr, r, m_bound, n,
-                                               kSlotCompact, (int)kPhaseSharded, filt_for(n_bound));
+                                               kSlotCompact, (int)kPhaseSharded, filt_for(n_bound, kSiteCount, filter));
       else
         launch_two_pass<PackedView, kModeRelabel>(ws, cb, PackedView{s.E[r & 1]}, s.E[r & 1], Lr, Eout, mnext,
                                                   s.d_ctr, r, m_bound, n, kSlotCompact, (int)kPhaseSharded,
-                                                  filt_for(n_bound));
+                                                  filt_for(n_bound, kSiteCount, filter));
       launches += 5;
       MST_CUDA_CHECK(cudaGetLastError());
     }
@@ -1272,7 +1302,7 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, uint6
                              ws.get<uint4>("stage", tiles_c(s.m) * kCTile)};
         // launched as round R1-1's producer: m[R1], E and the min table of round R1
         launch_two_pass<SoaView, kModeHeavy>(ws, cb, s.in, nullptr, vlabel, s.E[R1 & 1], s.minb[(R1 - 1) & 1], s.d_ctr,
-                                             R1 - 1, s.m, n, kSlotFilter, (int)kPhaseSharded, filt_for(snap.n[R1]));
+                                             R1 - 1, s.m, n, kSlotFilter, (int)kPhaseSharded, filt_for(snap.n[R1], kSiteHeavy));
         launches += 2;
         MST_CUDA_CHECK(cudaStreamSynchronize(ws.stream));
       }
@@ -1770,7 +1800,7 @@ int mst_gpu_round1_min(const mst_edges_soa_t* edges, uint64_t* out_min) {
     auto kmin = k_min_round1<SoaView>;
     const unsigned g = (unsigned)std::max<uint64_t>(
         1, std::min<uint64_t>((m + 4 * kBlock - 1) / (4 * kBlock), (uint64_t)sm_count(dev) * blocks_per_sm(kmin)));
-    kmin<<<g, kBlock, 0, ws.stream>>>(SoaView{src, dst, w, 0}, n, m, mn, d_ctr, filt_for(n));
+    kmin<<<g, kBlock, 0, ws.stream>>>(SoaView{src, dst, w, 0}, n, m, mn, d_ctr, filt_for(n, kSiteMin1));
     MST_CUDA_CHECK(cudaGetLastError());
     MST_CUDA_CHECK(cudaMemcpyAsync(out_min, mn, (size_t)n * 8, cudaMemcpyDeviceToHost, ws.stream));
     MST_CUDA_CHECK(cudaMemcpyAsync(&ws.h_snap[0], d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost,

@@ -249,6 +249,43 @@ __device__ __forceinline__ void offer(unsigned long long* table, uint32_t c, uin
   }
 }
 
+// K edges' offers to both endpoints with all filter reads in flight together,
+// then the atomics. (Offer by offer, each read waits behind the previous
+// item's atomic on the same table: 2K serial L2 round trips per thread.)
+// filt: 0 = plain REDs, 1 = read-first one offer at a time (each read sees
+// the previous atomics: best for hot hub entries), 2 = read-first batched.
+template <int K>
+__device__ __forceinline__ void offer_both(unsigned long long* table, const uint32_t (&x)[K], const uint32_t (&y)[K],
+                                           const unsigned long long (&key)[K], const bool (&valid)[K], int filt) {
+  if (filt == 1) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      offer(table, x[k], key[k], valid[k], true);
+      offer(table, y[k], key[k], valid[k], true);
+    }
+  } else if (filt == 2) {
+    unsigned long long cx[K], cy[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      cx[k] = valid[k] ? __ldcg(table + x[k]) : 0ull;
+      cy[k] = valid[k] ? __ldcg(table + y[k]) : 0ull;
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (!valid[k]) continue;
+      if (key[k] < cx[k]) atomicMin(table + x[k], key[k]);
+      if (key[k] < cy[k]) atomicMin(table + y[k], key[k]);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (!valid[k]) continue;
+      atomicMin(table + x[k], key[k]);
+      atomicMin(table + y[k], key[k]);
+    }
+  }
+}
+
 // kU independent root walks interleaved step by step (path halving), so each
 // thread keeps kU dependent-load chains in flight instead of one.
 template <int kU>
@@ -322,25 +359,29 @@ __global__ void __launch_bounds__(kBlock) k_min_round1(View v, uint32_t n, uint6
       e[k] = EdgeRec{0, 0, 0, 0, false};
       if (i < m) e[k] = v.stream(i);
     }
+    uint32_t xa[kU], xb[kU];
+    unsigned long long key[kU];
+    bool valid[kU];
 #pragma unroll
     for (int k = 0; k < kU; ++k) {
       const uint64_t i = base + k * kBlock + threadIdx.x;
-      bool valid = i < m;
-      if (valid) {
+      valid[k] = i < m;
+      if (valid[k]) {
         if (e[k].a >= n || e[k].b >= n) {
           err |= kErrRange;
-          valid = false;
+          valid[k] = false;
         } else if (!e[k].ok) {
           err |= kErrWeight;
-          valid = false;
+          valid[k] = false;
         } else if (e[k].a == e[k].b) {
-          valid = false;  // self-loop: never in an MST
+          valid[k] = false;  // self-loop: never in an MST
         }
       }
-      const uint64_t key = ((uint64_t)e[k].w << 32) | (uint32_t)i;
-      offer(minimum, e[k].a, key, valid, filt);
-      offer(minimum, e[k].b, key, valid, filt);
+      xa[k] = e[k].a;
+      xb[k] = e[k].b;
+      key[k] = ((unsigned long long)e[k].w << 32) | (uint32_t)i;
     }
+    offer_both<kU>(minimum, xa, xb, key, valid, filt);
   }
   if (err) atomicOr(&ctr->err, err);
 }
@@ -593,7 +634,7 @@ __device__ __forceinline__ bool pair_keep(const PairTable& t, unsigned long long
   return true;
 }
 
-template <class View, int kMode>
+template <class View, int kMode, bool kBatch = false>
 __global__ void __launch_bounds__(kBlock) k_count(View in, uint4* __restrict__ relabeled,
                                                   const uint32_t* __restrict__ L,
                                                   uint32_t* __restrict__ masks, uint32_t* __restrict__ counts,
@@ -629,6 +670,8 @@ __global__ void __launch_bounds__(kBlock) k_count(View in, uint4* __restrict__ r
     uint32_t err = 0, cnt = 0;
     bool keep[kCItems];
     unsigned bal[kCItems];
+    uint32_t ofx[kCItems], ofy[kCItems];
+    unsigned long long okey[kCItems];
 #pragma unroll
     for (int k = 0; k < kCItems; ++k) {
       const uint64_t i = (uint64_t)tile * kCTile + k * kBlock + threadIdx.x;
@@ -674,15 +717,20 @@ __global__ void __launch_bounds__(kBlock) k_count(View in, uint4* __restrict__ r
       // DRAM-sized stream: their offers are made by output position in
       // k_emit_staged, where they do not stall the stream (c3 split: 1.8 ms
       // there vs 3.1 ms here).
-      if ((kMode == kModeRelabel || kMode == kModeDedup) && keep[k]) {
-        const unsigned long long key = ((unsigned long long)e[k].w << 32) | (uint32_t)i;
-        offer(min_next, ox, key, true, filt);
-        offer(min_next, oy, key, true, filt);
+      ofx[k] = ox;
+      ofy[k] = oy;
+      okey[k] = ((unsigned long long)e[k].w << 32) | (uint32_t)i;
+      if ((kMode == kModeRelabel || kMode == kModeDedup) && !kBatch && keep[k]) {
+        // one offer at a time, as each edge is decided (hub-heavy tables)
+        offer(min_next, ox, okey[k], true, filt != 0);
+        offer(min_next, oy, okey[k], true, filt != 0);
       }
       bal[k] = __ballot_sync(0xffffffffu, keep[k]);
       if (lane == 0) s_slot[k * kWarps + warp] = __popc(bal[k]);
       cnt += __popc(bal[k]);
     }
+    if ((kMode == kModeRelabel || kMode == kModeDedup) && kBatch)
+      offer_both<kCItems>(min_next, ofx, ofy, okey, keep, 2);
     if (err) atomicOr(&ctr->err, err);
     if (lane == 0) s_cnt[warp] = cnt;
     __syncthreads();
@@ -818,7 +866,7 @@ __global__ void __launch_bounds__(kBlock) k_emit(View in, const uint4* __restric
 // Emit of the staged modes: tile t's survivors sit at stage[t*kCTile ..
 // t*kCTile + count); copy them to their final slots (and, for the light
 // split and the heavy filter, make the offers by output position).
-template <int kMode>
+template <int kMode, bool kBatch = false>
 __global__ void __launch_bounds__(kBlock) k_emit_staged(const uint4* __restrict__ stage,
                                                         const uint32_t* __restrict__ offsets, uint4* __restrict__ out,
                                                         unsigned long long* __restrict__ min_next, DevCounters* ctr,
@@ -834,16 +882,40 @@ __global__ void __launch_bounds__(kBlock) k_emit_staged(const uint4* __restrict_
     const uint32_t off = __ldg(offsets + tile);
     const uint32_t end = tile + 1 < ntiles ? __ldg(offsets + tile + 1) : total;
     const uint32_t cnt = end - off;
-    for (uint32_t base = 0; base < cnt; base += kBlock) {
-      const uint32_t j = base + threadIdx.x;
-      const bool v = j < cnt;
-      const uint4 e = v ? __ldcs(stage + (uint64_t)tile * kCTile + j) : make_uint4(0, 0, 0, 0);
-      if (v) __stcs(out + off + j, e);
-      if (kMode == kModeHeavy || kMode == kModeLight) {
-        const unsigned long long key = ((unsigned long long)e.z << 32) | (off + j);
-        offer(min_next, e.x, key, v, filt);
-        offer(min_next, e.y, key, v, filt);
+    if constexpr (!kBatch) {
+      for (uint32_t base = 0; base < cnt; base += kBlock) {
+        const uint32_t j = base + threadIdx.x;
+        const bool v = j < cnt;
+        const uint4 e = v ? __ldcs(stage + (uint64_t)tile * kCTile + j) : make_uint4(0, 0, 0, 0);
+        if (v) __stcs(out + off + j, e);
+        if (kMode == kModeHeavy || kMode == kModeLight) {
+          const unsigned long long key = ((unsigned long long)e.z << 32) | (off + j);
+          offer(min_next, e.x, key, v, filt != 0);
+          offer(min_next, e.y, key, v, filt != 0);
+        }
       }
+      continue;
+    }
+    for (uint32_t base = 0; base < cnt; base += kBlock * kCItems) {
+      uint4 e[kCItems];
+      bool v[kCItems];
+      uint32_t x[kCItems], y[kCItems];
+      unsigned long long key[kCItems];
+#pragma unroll
+      for (int k = 0; k < kCItems; ++k) {
+        const uint32_t j = base + k * kBlock + threadIdx.x;
+        v[k] = j < cnt;
+        e[k] = v[k] ? __ldcs(stage + (uint64_t)tile * kCTile + j) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int k = 0; k < kCItems; ++k) {
+        const uint32_t j = base + k * kBlock + threadIdx.x;
+        if (v[k]) __stcs(out + off + j, e[k]);
+        x[k] = e[k].x;
+        y[k] = e[k].y;
+        key[k] = ((unsigned long long)e[k].z << 32) | (off + j);
+      }
+      if (kMode == kModeHeavy || kMode == kModeLight) offer_both<kCItems>(min_next, x, y, key, v, 2);
     }
   }
 }
