@@ -32,6 +32,30 @@
 
 namespace mstgpu {
 
+// Minimum resident blocks per SM for the round kernels (register caps):
+// these kernels are memory-latency bound, so more resident warps = more
+// loads in flight. 0 = ptxas's own choice. Overridable at build time (A/B).
+#define MST_LB_(n) MST_LB_SEL_(n)
+#define MST_LB_SEL_(n) MST_LB_##n
+#define MST_LB_0 __launch_bounds__(256)
+#define MST_LB_5 __launch_bounds__(256, 5)
+#define MST_LB_6 __launch_bounds__(256, 6)
+#define MST_LB_8 __launch_bounds__(256, 8)
+#ifndef MST_MINB_MIN1
+#define MST_MINB_MIN1 0
+#endif
+#ifndef MST_MINB_HOOK
+#define MST_MINB_HOOK 0
+#endif
+#ifndef MST_MINB_LABEL
+#define MST_MINB_LABEL 0
+#endif
+#ifndef MST_MINB_COUNT
+#define MST_MINB_COUNT 0
+#endif
+#ifndef MST_MINB_EMIT
+#define MST_MINB_EMIT 0
+#endif
 constexpr int kBlock = 256;
 constexpr int kWarps = kBlock / 32;
 constexpr int kItems = 4;                // per thread, component tiles (hook)
@@ -100,6 +124,10 @@ struct SoaView {
   __device__ __forceinline__ EdgeRec gather(uint64_t i) const {
     return EdgeRec{__ldg(src + i), __ldg(dst + i), __ldg(w + i), base + (uint32_t)i, true};
   }
+  // endpoints and id only (the hook has the weight in its key)
+  __device__ __forceinline__ EdgeRec gather_ends(uint64_t i) const {
+    return EdgeRec{__ldg(src + i), __ldg(dst + i), 0u, base + (uint32_t)i, true};
+  }
   __device__ __forceinline__ uint32_t weight(uint64_t i) const { return __ldcs(w + i); }
 };
 
@@ -116,6 +144,7 @@ struct AosView {
     const uint4 v = __ldg(e + i);
     return EdgeRec{v.x, v.y, v.z, base + (uint32_t)i, v.w == 0};
   }
+  __device__ __forceinline__ EdgeRec gather_ends(uint64_t i) const { return gather(i); }
   __device__ __forceinline__ uint32_t weight(uint64_t i) const {
     return __ldcs(reinterpret_cast<const uint32_t*>(e + i) + 2);
   }
@@ -133,6 +162,7 @@ struct PackedView {
     const uint4 v = __ldg(e + i);
     return EdgeRec{v.x, v.y, v.z, v.w, true};
   }
+  __device__ __forceinline__ EdgeRec gather_ends(uint64_t i) const { return gather(i); }
   __device__ __forceinline__ uint32_t weight(uint64_t i) const {
     return __ldcs(reinterpret_cast<const uint32_t*>(e + i) + 2);
   }
@@ -150,6 +180,10 @@ struct PairsView {
   __device__ __forceinline__ EdgeRec gather(uint64_t i) const {
     const uint2 p = __ldcg(xy + i);
     return EdgeRec{p.x, p.y, in.weight(i), in.base + (uint32_t)i, true};
+  }
+  __device__ __forceinline__ EdgeRec gather_ends(uint64_t i) const {
+    const uint2 p = __ldcg(xy + i);
+    return EdgeRec{p.x, p.y, 0u, in.base + (uint32_t)i, true};
   }
 };
 
@@ -344,7 +378,7 @@ __device__ __forceinline__ uint32_t find_root(uint32_t* parent, uint32_t c) {
 // Lightest incident edge per vertex over the caller's list, literal keys
 // (w<<32 | index in the list).
 template <class View>
-__global__ void __launch_bounds__(kBlock) k_min_round1(View v, uint32_t n, uint64_t m,
+__global__ void MST_LB_(MST_MINB_MIN1) k_min_round1(View v, uint32_t n, uint64_t m,
                                                        unsigned long long* __restrict__ minimum,
                                                        DevCounters* ctr, int filt) {
   pdl_prologue();
@@ -635,7 +669,7 @@ __device__ __forceinline__ bool pair_keep(const PairTable& t, unsigned long long
 }
 
 template <class View, int kMode, bool kBatch = false>
-__global__ void __launch_bounds__(kBlock) k_count(View in, uint4* __restrict__ relabeled,
+__global__ void MST_LB_(MST_MINB_COUNT) k_count(View in, uint4* __restrict__ relabeled,
                                                   const uint32_t* __restrict__ L,
                                                   uint32_t* __restrict__ masks, uint32_t* __restrict__ counts,
                                                   uint32_t n_orig, DevCounters* ctr, int r, int fused, int slot,
@@ -778,7 +812,7 @@ __global__ void __launch_bounds__(kBlock) k_count(View in, uint4* __restrict__ r
 }
 
 template <class View, int kMode>
-__global__ void __launch_bounds__(kBlock) k_emit(View in, const uint4* __restrict__ relabeled,
+__global__ void MST_LB_(MST_MINB_EMIT) k_emit(View in, const uint4* __restrict__ relabeled,
                                                  const uint32_t* __restrict__ L,
                                                  const uint32_t* __restrict__ masks,
                                                  const uint32_t* __restrict__ offsets, uint4* __restrict__ out,
@@ -1047,7 +1081,7 @@ __global__ void __launch_bounds__(kBlock) k_shard_partner(const unsigned long lo
 // key (w << 32 | global edge id) and E.partner[c] the other endpoint's label
 // of that edge (all-reduced too), so nothing is gathered from an edge list.
 template <class View, bool kExchanged = false>
-__global__ void __launch_bounds__(kBlock) k_hook_decide(View E, const unsigned long long* __restrict__ minimum,
+__global__ void MST_LB_(MST_MINB_HOOK) k_hook_decide(View E, const unsigned long long* __restrict__ minimum,
                                                         uint32_t* __restrict__ parent, uint32_t* __restrict__ rootlabel,
                                                         uint32_t* __restrict__ masks, uint32_t* __restrict__ counts,
                                                         DevCounters* ctr, int r, int fused, int light_phase,
@@ -1077,7 +1111,7 @@ __global__ void __launch_bounds__(kBlock) k_hook_decide(View E, const unsigned l
         const uint32_t c = (uint32_t)((uint64_t)tile * kTile + k * kBlock + threadIdx.x);
         if (key[k] != kNoKey) e[k] = EdgeRec{c, __ldg(E.partner + c), (uint32_t)(key[k] >> 32), (uint32_t)key[k], true};
       } else {
-        if (key[k] != kNoKey) e[k] = E.gather((uint32_t)key[k]);
+        if (key[k] != kNoKey) e[k] = E.gather_ends((uint32_t)key[k]);
       }
     }
 #pragma unroll
@@ -1168,7 +1202,7 @@ __device__ __forceinline__ uint32_t roots_before(uint32_t x, const uint32_t* __r
   return __ldg(offsets + t) + __ldg(slotpref + (uint64_t)t * 32 + slot) + __popc(m & ((1u << lane) - 1u));
 }
 
-__global__ void __launch_bounds__(kBlock) k_label2(uint32_t* __restrict__ parent, const uint32_t* __restrict__ stash,
+__global__ void MST_LB_(MST_MINB_LABEL) k_label2(uint32_t* __restrict__ parent, const uint32_t* __restrict__ stash,
                                                    const uint32_t* __restrict__ masks,
                                                    const uint32_t* __restrict__ slotpref,
                                                    const uint32_t* __restrict__ offsets, uint32_t* __restrict__ L,
@@ -1376,17 +1410,18 @@ __device__ __forceinline__ void tail_stamp(const TailArgs& a, int& slot) {
 
 enum { kTailSrcPacked = 0, kTailSrcPairs = 1, kTailSrcSoa = 2, kTailSrcAos = 3 };
 
-// Edge i of the list the entry round's keys index, as {a, b, w, id}.
+// Edge i of the list the entry round's keys index, as {a, b, -, id} (the
+// hook has the weight in its key).
 __device__ __forceinline__ uint4 tail_entry_edge(const TailArgs& a, uint32_t i) {
   switch (a.src_kind) {
     case kTailSrcPacked:
       return __ldcg(static_cast<const uint4*>(a.src0) + i);
     case kTailSrcPairs: {
       const uint2 p = __ldcg(static_cast<const uint2*>(a.src0) + i);
-      return make_uint4(p.x, p.y, __ldg(a.src_w + (uint64_t)i * a.src_wstride), i);
+      return make_uint4(p.x, p.y, 0u, i);
     }
     case kTailSrcSoa:
-      return make_uint4(__ldg(static_cast<const uint32_t*>(a.src0) + i), __ldg(a.src1 + i), __ldg(a.src_w + i), i);
+      return make_uint4(__ldg(static_cast<const uint32_t*>(a.src0) + i), __ldg(a.src1 + i), 0u, i);
     default: {
       const uint4 v = __ldg(static_cast<const uint4*>(a.src0) + i);
       return make_uint4(v.x, v.y, v.z, i);
@@ -1535,21 +1570,17 @@ __global__ void __launch_bounds__(kBlock, 2) k_tail(TailArgs a) {
   uint64_t seg_len = min(seg_lo + es, m_entry) - seg_lo;
   bool dedup_off = false;  // identical on every block (from global counters)
   int last_dedup = -1;
+  // Round state kept in registers: every block derives n_{r+1} and the
+  // verdicts from the same data, and only this kernel changes them while it
+  // runs, so no counter is re-read at the top of a round (each read is a
+  // dependent L2 round trip on the critical path of a tiny round).
+  if ((uint32_t)a.r0 >= vc->stop_round || (uint32_t)a.r0 >= vc->phase_end) return;
+  uint32_t n_r = n_entry;
+  uint64_t m_prev = m_entry;  // live edges entering round r-1 (dedup statistics)
   for (int r = a.r0; r < kMaxR - 1; ++r) {
-    if ((uint32_t)r >= vc->stop_round || (uint32_t)r >= vc->phase_end) break;
-    if (r > a.r0 && vc->m[r] == 0) {
-      // round r-1 kept no edge: the same verdict the round kernels' edge
-      // scan gives (scan_verdict)
-      if (b == 0 && threadIdx.x == 0) {
-        if (a.light)
-          a.ctr->phase_end = (uint32_t)r;
-        else
-          a.ctr->stop_round = (uint32_t)r;
-      }
-      break;
-    }
-    if (last_dedup == r - 1 && 2 * vc->m[r] > vc->m[r - 1]) dedup_off = true;
-    const uint32_t n_r = vc->n[r];
+    // edges kept by round r-1 (C's atomics, complete at the last grid.sync);
+    // issued here, first used after A
+    const uint64_t m_r = r > a.r0 ? __ldcg(reinterpret_cast<const unsigned long long*>(&a.ctr->m[r])) : m_entry;
     const uint32_t mst_base = a.n_orig - n_r;
     // ternaries, not a dynamic index: keeps TailArgs out of local memory
     const unsigned long long* mcur = (r & 1) ? a.minb[0] : a.minb[1];
@@ -1637,6 +1668,18 @@ __global__ void __launch_bounds__(kBlock, 2) k_tail(TailArgs a) {
     grid.sync();
     tail_stamp(a, slot);
     // ---- B: dense labels, MST slots, next min table
+    if (r > a.r0 && m_r == 0) {
+      // round r-1 kept no edge: the same verdict the round kernels' edge
+      // scan gives (scan_verdict)
+      if (b == 0 && threadIdx.x == 0) {
+        if (a.light)
+          a.ctr->phase_end = (uint32_t)r;
+        else
+          a.ctr->stop_round = (uint32_t)r;
+      }
+      break;
+    }
+    if (last_dedup == r - 1 && 2 * m_r > m_prev) dedup_off = true;
     block_scan_array(a.broots, G, s_bpre, s_warp);
     const uint32_t n_next = s_bpre[G];
     bool stop_now = false, phase_now = false;
@@ -1693,7 +1736,6 @@ __global__ void __launch_bounds__(kBlock, 2) k_tail(TailArgs a) {
       for (uint32_t x = b * kBlock + threadIdx.x; x < n_entry; x += G * kBlock) a.M[x] = __ldcg(a.L + a.M[x]);
     }
     // ---- C0 (optional): relabel in place + each pair's lightest key
-    const uint64_t m_r = vc->m[r];
     const bool dedup = a.pairs != nullptr && n_next < (1u << kTailPairLabelBits) && m_r >= a.dedup_min &&
                        m_r >= (uint64_t)a.dedup_ratio * n_next &&
                        (!dedup_off || (uint64_t)n_next * (n_next - 1) / 2 <= m_r / 4);
@@ -1813,6 +1855,8 @@ __global__ void __launch_bounds__(kBlock, 2) k_tail(TailArgs a) {
     }
     grid.sync();
     tail_stamp(a, slot);
+    n_r = n_next;
+    m_prev = m_r;
   }
 }
 
@@ -1974,6 +2018,7 @@ __global__ void __launch_bounds__(kBlock) k_flags_emit(const uint8_t* __restrict
                                                        uint32_t* __restrict__ out) {
   pdl_prologue();
   __shared__ uint32_t s_scan[32];
+  __shared__ uint32_t s_stage[kWarps][32 * 16];
   const uint32_t ntiles = (uint32_t)((m + kFlagTile - 1) / kFlagTile);
   const uint64_t nvec = (m + 15) / 16;
   const uint4* v4 = reinterpret_cast<const uint4*>(flags);
@@ -2000,9 +2045,13 @@ __global__ void __launch_bounds__(kBlock) k_flags_emit(const uint8_t* __restrict
     const uint32_t prefix = __ldg(offsets + tile);
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
-      if (!cnt[k]) continue;
+      // a warp's ids for item k are one contiguous run of <= 512: stage them
+      // in shared memory, then store the run coalesced (lane-by-lane stores
+      // from the bit loop hit one sector per lane per store)
+      const uint32_t wtot = __shfl_sync(0xffffffffu, incl[k], 31);
+      if (!wtot) continue;
       const uint64_t i = (uint64_t)tile * kTile + k * kBlock + threadIdx.x;
-      uint32_t pos = prefix + s_scan[k * kWarps + warp] + incl[k] - cnt[k];
+      uint32_t pos = incl[k] - cnt[k];
       const uint32_t words[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -2010,9 +2059,13 @@ __global__ void __launch_bounds__(kBlock) k_flags_emit(const uint8_t* __restrict
         while (wd) {
           const int byte = (__ffs(wd) - 1) >> 3;
           wd &= ~(0xFFu << (byte * 8));
-          out[pos++] = (uint32_t)(i * 16 + q * 4 + byte);
+          s_stage[warp][pos++] = (uint32_t)(i * 16 + q * 4 + byte);
         }
       }
+      __syncwarp();
+      uint32_t* dst = out + prefix + s_scan[k * kWarps + warp];
+      for (uint32_t j = lane; j < wtot; j += 32) __stcs(dst + j, s_stage[warp][j]);
+      __syncwarp();
     }
     __syncthreads();
   }
