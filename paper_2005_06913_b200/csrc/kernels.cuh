@@ -1547,7 +1547,10 @@ __device__ __forceinline__ void offer_batch(unsigned long long* table, const uin
   }
 }
 
-__global__ void __launch_bounds__(kBlock, 2) k_tail(TailArgs a) {
+#ifndef MST_TAIL_MINB
+#define MST_TAIL_MINB 2
+#endif
+__global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
   pdl_prologue();
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
