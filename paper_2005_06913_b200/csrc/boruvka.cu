@@ -112,6 +112,8 @@ struct Workspace {
   void* hstage[2] = {nullptr, nullptr};
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};
   bool stage_busy[2] = {false, false};
+  cudaStream_t copy_stream = nullptr;  // pipelined host -> device copies
+  cudaEvent_t chunk_ev[16] = {};
   std::vector<cudaEvent_t> ev;    // per-round events
   std::vector<cudaEvent_t> tev;   // timing events (hot kernels)
 
@@ -119,6 +121,8 @@ struct Workspace {
     device = dev;
     MST_CUDA_CHECK(cudaSetDevice(dev));
     MST_CUDA_CHECK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    MST_CUDA_CHECK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+    for (auto& e : chunk_ev) MST_CUDA_CHECK(cudaEventCreate(&e));
     MST_CUDA_CHECK(cudaMallocHost(&h_snap, sizeof(DevCounters) * (kMaxR + 1)));
     ev.resize(kMaxR + 1);
     for (auto& e : ev) MST_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -553,9 +557,18 @@ struct HookSrc {
   const uint4* packed;
 };
 
+// Pipelined host copy of the caller's list: chunk j = edges [bound[j],
+// bound[j+1]) is on the device once ev[j] has completed.
+struct CopyChunks {
+  static constexpr int kMax = 16;
+  int count = 0;
+  uint64_t bound[kMax + 1];
+  cudaEvent_t ev[kMax];
+};
+
 template <class InView>
 void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t wstride, uint32_t n,
-                     uint64_t m, RunOut& out, bool time_hot, bool filter) {
+                     uint64_t m, RunOut& out, bool time_hot, bool filter, const CopyChunks* chunks = nullptr) {
   cudaStream_t s = ws.stream;
   auto* d_ctr = ws.get<DevCounters>("ctr", 1);
   unsigned long long* minb[2] = {ws.get<unsigned long long>("minA", n),
@@ -563,7 +576,9 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   uint32_t* parent = ws.get<uint32_t>("parent", n);
   uint32_t* rootlabel = ws.get<uint32_t>("rootlabel", n);
   uint32_t* L = ws.get<uint32_t>("label", n);
-  uint32_t* mst = ws.get<uint32_t>("mst", n);
+  // single GPU: the sorted output comes from the per-edge flags, so no MST
+  // slot array is written (the sharded loop keeps one, see Shard::mst)
+  uint32_t* mst = nullptr;
   uint4* E[2] = {ws.get<uint4>("E0", m), ws.get<uint4>("E1", m)};
   unsigned long long* st = ws.status_array(std::max(tiles_of(m), tiles_of(n)));
   const int dev = ws.device;
@@ -609,12 +624,19 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     launches += 2;
   } else {
     auto kmin = k_min_round1<InView>;
-    const unsigned g = (unsigned)std::max<uint64_t>(
-        1, std::min<uint64_t>((m + 4 * kBlock - 1) / (4 * kBlock), (uint64_t)sm_count(dev) * blocks_per_sm(kmin)));
     hot_begin(kHotMin1, 0, false);
-    launch_k(kmin, g, kBlock, s, in, n, m, minb[0], d_ctr, filt_for(n, kSiteMin1));
+    // one launch per host-copy chunk when the caller's list is still
+    // arriving (run_single's pipelined H2D), else one over the whole list
+    const int nch = chunks ? chunks->count : 1;
+    for (int j = 0; j < nch; ++j) {
+      const uint64_t lo = chunks ? chunks->bound[j] : 0, hi = chunks ? chunks->bound[j + 1] : m;
+      if (chunks) MST_CUDA_CHECK(cudaStreamWaitEvent(s, chunks->ev[j], 0));
+      const unsigned g = (unsigned)std::max<uint64_t>(
+          1, std::min<uint64_t>((hi - lo + 4 * kBlock - 1) / (4 * kBlock), (uint64_t)sm_count(dev) * blocks_per_sm(kmin)));
+      launch_k(kmin, g, kBlock, s, in, n, lo, hi, minb[0], d_ctr, filt_for(n, kSiteMin1));
+      ++launches;
+    }
     tmark();
-    ++launches;
   }
 
   bool light = filter;
@@ -980,14 +1002,40 @@ RunOut run_single(const SingleArgs& a, mst_stats_t* stats) {
   const uint32_t* dst = a.dst;
   const uint32_t* w = a.w;
   const mst_edge_t* aos = a.aos;
+  // Pinned SoA input on the plain loop: copy in chunks on the copy stream
+  // while round 1's min pass consumes the chunks that have landed (and the
+  // table clears run), so the H2D hides that work. Off by default: measured
+  // on c1 (tools/exp9.sh), 24 chunk copies move the 100 MB in 1.94 ms vs
+  // 1.83 ms for three whole-array copies, more than the ~45 us they hide.
+  CopyChunks chunks;
+  const bool pipelined = !a.on_device && a.kind == 0 && a.m >= (4u << 20) && !filter_mode(a.n, a.m) &&
+                         env_int("MST_PIPELINE_H2D", 0) != 0 && host_is_pinned(a.src) && host_is_pinned(a.dst) &&
+                         host_is_pinned(a.w);
   if (!a.on_device && a.m > 0) {
     if (a.kind == 0) {
       uint32_t* d_src = ws.get<uint32_t>("in_src", a.m);
       uint32_t* d_dst = ws.get<uint32_t>("in_dst", a.m);
       uint32_t* d_w = ws.get<uint32_t>("in_w", a.m);
-      copy_h2d(ws, d_src, a.src, a.m * 4);
-      copy_h2d(ws, d_dst, a.dst, a.m * 4);
-      copy_h2d(ws, d_w, a.w, a.m * 4);
+      if (pipelined) {
+        // the copies may not overwrite the buffers before earlier work on
+        // the compute stream is done with them
+        MST_CUDA_CHECK(cudaStreamWaitEvent(ws.copy_stream, e0, 0));
+        const uint64_t per = std::max<uint64_t>(1u << 20, (a.m + CopyChunks::kMax - 1) / CopyChunks::kMax);
+        chunks.count = (int)((a.m + per - 1) / per);
+        for (int j = 0; j <= chunks.count; ++j) chunks.bound[j] = std::min<uint64_t>(a.m, (uint64_t)j * per);
+        for (int j = 0; j < chunks.count; ++j) {
+          const uint64_t lo = chunks.bound[j], len = (chunks.bound[j + 1] - lo) * 4;
+          MST_CUDA_CHECK(cudaMemcpyAsync(d_src + lo, a.src + lo, len, cudaMemcpyHostToDevice, ws.copy_stream));
+          MST_CUDA_CHECK(cudaMemcpyAsync(d_dst + lo, a.dst + lo, len, cudaMemcpyHostToDevice, ws.copy_stream));
+          MST_CUDA_CHECK(cudaMemcpyAsync(d_w + lo, a.w + lo, len, cudaMemcpyHostToDevice, ws.copy_stream));
+          chunks.ev[j] = ws.chunk_ev[j];
+          MST_CUDA_CHECK(cudaEventRecord(chunks.ev[j], ws.copy_stream));
+        }
+      } else {
+        copy_h2d(ws, d_src, a.src, a.m * 4);
+        copy_h2d(ws, d_dst, a.dst, a.m * 4);
+        copy_h2d(ws, d_w, a.w, a.m * 4);
+      }
       src = d_src;
       dst = d_dst;
       w = d_w;
@@ -1002,17 +1050,16 @@ RunOut run_single(const SingleArgs& a, mst_stats_t* stats) {
   RunOut o;
   if (a.kind == 0) {
     SoaView v{src, dst, w, 0};
-    run_single_impl<SoaView>(ws, v, w, 1, a.n, a.m, o, a.time_hot, filter_mode(a.n, a.m));
+    run_single_impl<SoaView>(ws, v, w, 1, a.n, a.m, o, a.time_hot, filter_mode(a.n, a.m),
+                             chunks.count ? &chunks : nullptr);
   } else {
     AosView v{reinterpret_cast<const uint4*>(aos), 0};
     const uint32_t* wb = reinterpret_cast<const uint32_t*>(aos) + 2;
     run_single_impl<AosView>(ws, v, wb, 4, a.n, a.m, o, a.time_hot, filter_mode(a.n, a.m));
   }
   check_err_bits(o.err);
-  uint32_t* d_mst = ws.get<uint32_t>("mst", a.n);
   uint32_t* d_sorted = a.device_out ? a.out_ids : ws.get<uint32_t>("sorted", a.n);
   auto* d_ctr = ws.get<DevCounters>("ctr", 1);
-  (void)d_mst;
   o.launches += sort_from_flags(ws, ws.get<uint8_t>("mst_flags", a.m + 16), std::max<uint64_t>(a.m, 1), d_sorted,
                                 d_ctr);
   MST_CUDA_CHECK(cudaEventRecord(e2, s));
@@ -1022,8 +1069,15 @@ RunOut run_single(const SingleArgs& a, mst_stats_t* stats) {
   MST_CUDA_CHECK(cudaStreamSynchronize(s));
   if (stats) {
     fill_stats(stats, o);
-    stats->ms_h2d = ms_between(e0, e1);
-    stats->ms_device = ms_between(e1, e2);
+    if (chunks.count) {
+      // pipelined: h2d = until the last chunk landed, device = what remained
+      const cudaEvent_t last = chunks.ev[chunks.count - 1];
+      stats->ms_h2d = ms_between(e0, last);
+      stats->ms_device = ms_between(last, e2);
+    } else {
+      stats->ms_h2d = ms_between(e0, e1);
+      stats->ms_device = ms_between(e1, e2);
+    }
     stats->ms_d2h = ms_between(e2, e3);
     stats->ms_total = std::chrono::duration<double, std::milli>(Clock::now() - t_start).count();
   }
@@ -1152,7 +1206,7 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, uint6
     for (auto& s : sh) {
       MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
       auto kmin = k_min_round1<SoaView>;
-      launch_k(kmin, persistent_grid(kmin, s.ws->device, (s.m + kBlock - 1) / kBlock), kBlock, s.ws->stream, s.in, n,
+      launch_k(kmin, persistent_grid(kmin, s.ws->device, (s.m + kBlock - 1) / kBlock), kBlock, s.ws->stream, s.in, n, (uint64_t)0,
                s.m, s.minb[0], s.d_ctr, filt_for(n, kSiteMin1));
       ++launches;
     }
@@ -1800,7 +1854,7 @@ int mst_gpu_round1_min(const mst_edges_soa_t* edges, uint64_t* out_min) {
     auto kmin = k_min_round1<SoaView>;
     const unsigned g = (unsigned)std::max<uint64_t>(
         1, std::min<uint64_t>((m + 4 * kBlock - 1) / (4 * kBlock), (uint64_t)sm_count(dev) * blocks_per_sm(kmin)));
-    kmin<<<g, kBlock, 0, ws.stream>>>(SoaView{src, dst, w, 0}, n, m, mn, d_ctr, filt_for(n, kSiteMin1));
+    kmin<<<g, kBlock, 0, ws.stream>>>(SoaView{src, dst, w, 0}, n, (uint64_t)0, m, mn, d_ctr, filt_for(n, kSiteMin1));
     MST_CUDA_CHECK(cudaGetLastError());
     MST_CUDA_CHECK(cudaMemcpyAsync(out_min, mn, (size_t)n * 8, cudaMemcpyDeviceToHost, ws.stream));
     MST_CUDA_CHECK(cudaMemcpyAsync(&ws.h_snap[0], d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost,

@@ -377,15 +377,16 @@ __device__ __forceinline__ uint32_t find_root(uint32_t* parent, uint32_t c) {
 
 // Lightest incident edge per vertex over the caller's list, literal keys
 // (w<<32 | index in the list).
+// Edges [lo, m) of the list (lo > 0: a later chunk of a pipelined host copy).
 template <class View>
-__global__ void MST_LB_(MST_MINB_MIN1) k_min_round1(View v, uint32_t n, uint64_t m,
+__global__ void MST_LB_(MST_MINB_MIN1) k_min_round1(View v, uint32_t n, uint64_t lo, uint64_t m,
                                                        unsigned long long* __restrict__ minimum,
                                                        DevCounters* ctr, int filt) {
   pdl_prologue();
   constexpr int kU = 4;
   const uint64_t stride = (uint64_t)gridDim.x * kBlock * kU;
   uint32_t err = 0;
-  for (uint64_t base = (uint64_t)blockIdx.x * kBlock * kU; base < m; base += stride) {
+  for (uint64_t base = lo + (uint64_t)blockIdx.x * kBlock * kU; base < m; base += stride) {
     EdgeRec e[kU];
 #pragma unroll
     for (int k = 0; k < kU; ++k) {
@@ -928,28 +929,28 @@ __global__ void __launch_bounds__(kBlock) k_emit_staged(const uint4* __restrict_
           offer(min_next, e.y, key, v, filt != 0);
         }
       }
-      continue;
-    }
-    for (uint32_t base = 0; base < cnt; base += kBlock * kCItems) {
-      uint4 e[kCItems];
-      bool v[kCItems];
-      uint32_t x[kCItems], y[kCItems];
-      unsigned long long key[kCItems];
+    } else {
+      for (uint32_t base = 0; base < cnt; base += kBlock * kCItems) {
+        uint4 e[kCItems];
+        bool v[kCItems];
+        uint32_t x[kCItems], y[kCItems];
+        unsigned long long key[kCItems];
 #pragma unroll
-      for (int k = 0; k < kCItems; ++k) {
-        const uint32_t j = base + k * kBlock + threadIdx.x;
-        v[k] = j < cnt;
-        e[k] = v[k] ? __ldcs(stage + (uint64_t)tile * kCTile + j) : make_uint4(0, 0, 0, 0);
-      }
+        for (int k = 0; k < kCItems; ++k) {
+          const uint32_t j = base + k * kBlock + threadIdx.x;
+          v[k] = j < cnt;
+          e[k] = v[k] ? __ldcs(stage + (uint64_t)tile * kCTile + j) : make_uint4(0, 0, 0, 0);
+        }
 #pragma unroll
-      for (int k = 0; k < kCItems; ++k) {
-        const uint32_t j = base + k * kBlock + threadIdx.x;
-        if (v[k]) __stcs(out + off + j, e[k]);
-        x[k] = e[k].x;
-        y[k] = e[k].y;
-        key[k] = ((unsigned long long)e[k].z << 32) | (off + j);
+        for (int k = 0; k < kCItems; ++k) {
+          const uint32_t j = base + k * kBlock + threadIdx.x;
+          if (v[k]) __stcs(out + off + j, e[k]);
+          x[k] = e[k].x;
+          y[k] = e[k].y;
+          key[k] = ((unsigned long long)e[k].z << 32) | (off + j);
+        }
+        if (kMode == kModeHeavy || kMode == kModeLight) offer_both<kCItems>(min_next, x, y, key, v, 2);
       }
-      if (kMode == kModeHeavy || kMode == kModeLight) offer_both<kCItems>(min_next, x, y, key, v, 2);
     }
   }
 }
@@ -1260,7 +1261,7 @@ __global__ void MST_LB_(MST_MINB_LABEL) k_label2(uint32_t* __restrict__ parent, 
     for (int k = 0; k < kItems; ++k) {
       if (!v[k] || isroot[k]) continue;
       const uint32_t eid = __ldg(stash + c[k]);
-      mst[mst_base + (c[k] - own[k])] = eid;
+      if (mst) mst[mst_base + (c[k] - own[k])] = eid;  // the sharded loop's slots (single GPU: flags only)
       if (flags) flags[eid] = 1;
     }
     if (!labels) continue;
@@ -1719,7 +1720,7 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
         const uint32_t before = s_bpre[x / cs] + __ldcg(a.wpref + w) +
                                 __popc(__ldcg(a.masks + w) & ((1u << (x & 31)) - 1u));
         const uint32_t eid = __ldcg(a.rootlabel + x);
-        a.mst[mst_base + (x - before)] = eid;
+        if (a.mst) a.mst[mst_base + (x - before)] = eid;
         if (a.flags) a.flags[eid] = 1;
       }
       if (stop_now) continue;

@@ -336,3 +336,25 @@ def test_nccl_rank_path_single_rank(mst, oracle_mod):
             assert r.mst_edges.tolist() == k.ids.tolist() and r.total_weight == k.total_weight
     finally:
         comm.close()
+
+
+def test_pipelined_host_copy(mst, oracle_mod):
+    """Pinned SoA host arrays on the plain loop: chunked H2D on a copy stream
+    with round 1's min pass per landed chunk (run_single's pipelined path)."""
+    import torch
+    from paper_2005_06913_b200 import configs as C
+    P, O = mst, oracle_mod
+    for spec in (C.CONFIGS["c1"], C.uniform(3_000_000, 5_000_000, seed=9)):
+        g0 = C.generate_host(spec)
+        k = O.kruskal(g0.n, g0.src, g0.dst, g0.w)
+        pins = [torch.empty(g0.edge_count(), dtype=torch.int32, pin_memory=True) for _ in range(3)]
+        for t, arr in zip(pins, (g0.src, g0.dst, g0.w)):
+            t.numpy().view(np.uint32)[:] = arr
+        g = P.Graph(g0.n, *(t.numpy().view(np.uint32) for t in pins))
+        for mode in (dict(MST_PIPELINE_H2D=1), dict(MST_PIPELINE_H2D=0)):
+            with _env(**mode):
+                for _ in range(2):  # back to back: the copies must wait for the previous call
+                    info = P.GpuRunInfo()
+                    r = P.boruvka_gpu(g, info=info)
+                    assert np.array_equal(r.mst_edges, k.ids.astype(np.int64)) and r.total_weight == k.total_weight
+                    assert info.ms_h2d > 0 and info.ms_device > 0
