@@ -1566,12 +1566,15 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   volatile DevCounters* vc = a.ctr;
   const uint32_t n_entry = vc->n[a.r0];
-  // this block's segment of the (single, in place) edge list
+  // this WARP's segment of the (single, in place) edge list: a share of its
+  // block's chunk, compacted with ballot ranks (no block barrier)
   uint4* const E = (a.r0 & 1) ? a.E[1] : a.E[0];
   const uint64_t m_entry = vc->m[a.r0];
   const uint64_t es = (m_entry + G - 1) / G;
-  const uint64_t seg_lo = min((uint64_t)b * es, m_entry);
-  uint64_t seg_len = min(seg_lo + es, m_entry) - seg_lo;
+  const uint64_t blo = min((uint64_t)b * es, m_entry), bhi = min(blo + es, m_entry);
+  const uint64_t wes = (bhi - blo + kWarps - 1) / kWarps;
+  const uint64_t seg_lo = min(blo + warp * wes, bhi);
+  uint64_t seg_len = min(seg_lo + wes, bhi) - seg_lo;
   bool dedup_off = false;  // identical on every block (from global counters)
   int last_dedup = -1;
   // Round state kept in registers: every block derives n_{r+1} and the
@@ -1750,17 +1753,17 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
       while (cap < m_r / 2 && cap < a.pair_cap) cap <<= 1;
       pmask = min(cap, a.pair_cap) - 1;
       last_dedup = r;
-      for (uint64_t base = seg_lo; base < seg_lo + seg_len; base += kBlock * kItems) {
+      for (uint64_t base = seg_lo; base < seg_lo + seg_len; base += 32 * kItems) {
         uint4 e[kItems];
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
-          const uint64_t i = base + k * kBlock + threadIdx.x;
+          const uint64_t i = base + k * 32 + lane;
           e[k] = i < seg_lo + seg_len ? __ldcg(E + i) : make_uint4(0, 0, 0, 0);
         }
         uint32_t x[kItems], y[kItems];
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
-          const uint64_t i = base + k * kBlock + threadIdx.x;
+          const uint64_t i = base + k * 32 + lane;
           x[k] = i < seg_lo + seg_len ? __ldcg(a.L + e[k].x) : 0u;
           y[k] = i < seg_lo + seg_len ? __ldcg(a.L + e[k].y) : 0u;
         }
@@ -1768,7 +1771,7 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
         bool v[kItems];
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
-          const uint64_t i = base + k * kBlock + threadIdx.x;
+          const uint64_t i = base + k * 32 + lane;
           v[k] = i < seg_lo + seg_len && x[k] != y[k];
           pw[k] = tail_pair_word(tag, x[k], y[k]);
           key[k] = ((unsigned long long)e[k].z << 32) | (uint32_t)i;
@@ -1776,7 +1779,7 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
         tail_pair_insert_batch(a.pairs, pmask, pw, key, v);
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
-          const uint64_t i = base + k * kBlock + threadIdx.x;
+          const uint64_t i = base + k * 32 + lane;
           if (i < seg_lo + seg_len) *reinterpret_cast<uint2*>(E + i) = make_uint2(x[k], y[k]);
         }
       }
@@ -1794,18 +1797,19 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
       }
       const uint64_t seg_hi = seg_lo + seg_len;
       uint64_t out = seg_lo;
-      for (uint64_t base = seg_lo; base < seg_hi; base += kBlock * kItems) {
+      const uint32_t lt = lanemask_lt();
+      for (uint64_t base = seg_lo; base < seg_hi; base += 32 * kItems) {
         uint4 e[kItems];
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
-          const uint64_t i = base + k * kBlock + threadIdx.x;
+          const uint64_t i = base + k * 32 + lane;
           e[k] = i < seg_hi ? __ldcg(E + i) : make_uint4(0, 0, 0, 0);
         }
         bool f[kItems];
         if (!dedup) {
 #pragma unroll
           for (int k = 0; k < kItems; ++k) {
-            const uint64_t i = base + k * kBlock + threadIdx.x;
+            const uint64_t i = base + k * 32 + lane;
             if (i < seg_hi) {
               e[k].x = __ldcg(a.L + e[k].x);
               e[k].y = __ldcg(a.L + e[k].y);
@@ -1814,7 +1818,7 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
         }
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
-          const uint64_t i = base + k * kBlock + threadIdx.x;
+          const uint64_t i = base + k * 32 + lane;
           f[k] = i < seg_hi && e[k].x != e[k].y;
         }
         if (dedup) {
@@ -1822,12 +1826,20 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
 #pragma unroll
           for (int k = 0; k < kItems; ++k) {
             pw[k] = tail_pair_word(tag, e[k].x, e[k].y);
-            key[k] = ((unsigned long long)e[k].z << 32) | (uint32_t)(base + k * kBlock + threadIdx.x);
+            key[k] = ((unsigned long long)e[k].z << 32) | (uint32_t)(base + k * 32 + lane);
           }
           tail_pair_keep_batch(a.pairs, pmask, pw, key, f);
         }
-        uint32_t rank[kItems];
-        const uint32_t tot = block_ranks(f, rank, s_cnt);  // every load of the tile is done
+        // ordered ranks within the warp's tile (positions are k-major); the
+        // ballots need every lane's loads, so the in-place stores below never
+        // overwrite an unread edge
+        uint32_t rank[kItems], tot = 0;
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          const unsigned bal = __ballot_sync(0xffffffffu, f[k]);
+          rank[k] = tot + __popc(bal & lt);
+          tot += __popc(bal);
+        }
         unsigned long long key[kItems];
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
@@ -1848,7 +1860,7 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
         out += tot;
       }
       seg_len = out - seg_lo;
-      if (threadIdx.x == 0 && seg_len) atomicAdd(const_cast<unsigned long long*>(&a.ctr->m[r + 1]), seg_len);
+      if (lane == 0 && seg_len) atomicAdd(const_cast<unsigned long long*>(&a.ctr->m[r + 1]), seg_len);
       if (local) {
         __syncthreads();
         for (uint32_t c = threadIdx.x; c < n_next; c += kBlock) {
