@@ -510,7 +510,8 @@ struct CompactBufs {
 template <class View, int kMode>
 void launch_two_pass(Workspace& ws, const CompactBufs& cb, View in, uint4* relabeled, const uint32_t* L, uint4* out,
                      unsigned long long* min_next, DevCounters* d_ctr, int r, uint64_t m_bound, uint32_t n_orig,
-                     int slot, int light, int filt, PairTable pt = PairTable{nullptr, nullptr, 0}) {
+                     int slot, int light, int filt, PairTable pt = PairTable{nullptr, nullptr, 0},
+                     bool emit = true) {
   const int dev = ws.device;
   const uint64_t tiles = tiles_c(m_bound);
   const int fused = tiles <= kFusedScanMaxTiles ? 1 : 0;  // small: the last count block scans
@@ -536,6 +537,10 @@ void launch_two_pass(Workspace& ws, const CompactBufs& cb, View in, uint4* relab
     launch_k(ksc, gs, kScanBlock, ws.stream, cb.counts, tiles, d_ctr, r, cb.st, ws.next_epoch(), light,
              View::kOriginal ? 1 : 0);
   }
+  if (!emit) {  // count + scan only (round 1 of the lazy plain loop)
+    MST_CUDA_CHECK(cudaGetLastError());
+    return;
+  }
   const unsigned ge = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)sm_count(dev) * 8));
   if (armed) {
     auto kde = k_emit_staged<kModeDedup>;
@@ -554,7 +559,7 @@ void launch_two_pass(Workspace& ws, const CompactBufs& cb, View in, uint4* relab
 enum { kSrcIn = 0, kSrcPairs = 1, kSrcPacked = 2 };
 struct HookSrc {
   int kind;
-  const uint4* packed;
+  const uint4* packed;  // kSrcPacked: the list; kSrcPairs: the uint2 pair list
 };
 
 // Pipelined host copy of the caller's list: chunk j = edges [bound[j],
@@ -662,6 +667,14 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   const uint64_t tail_comps = (uint64_t)env_double("MST_TAIL_COMPS", 8.0e6);
   auto tail_edges = [&]() -> uint64_t { return (uint64_t)(tail_env > 0 ? tail_env : (light ? 3.0e6 : 6.0e6)); };
 
+  // Lazy round 1 (plain loop): round 1 stops after its count pass, whose
+  // relabelled label pairs (one per caller edge) are round 2's edge list;
+  // round 2 compacts them. Saves round 1's emit pass (c1: 32 us). Not when
+  // round 2 enters the tail, which needs a compacted list.
+  const bool lazy1 = !filter && env_int("MST_LAZY_ROUND1", 1) != 0 &&
+                     !(tail_on && m <= tail_edges() && (uint64_t)n <= tail_comps);
+  const uint4* P1 = lazy1 ? reinterpret_cast<const uint4*>(ws.get<uint2>("pairs1", m)) : E[1];
+
   // Light phase over: compose its relabel maps into a vertex -> component map,
   // run the heavy filter pass, continue with the plain loop (phase D).
   // Returns false when the run was restarted in plain mode.
@@ -708,7 +721,8 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   auto hook_src = [&](int rr) -> HookSrc {
     if (rr == 1) return filter ? HookSrc{kSrcPacked, E[1]} : HookSrc{kSrcIn, nullptr};
     if (phase_end && rr == phase_end) return HookSrc{kSrcPacked, E[rr & 1]};
-    if (rr == 2 && !filter) return HookSrc{kSrcPairs, nullptr};
+    if (rr == 2 && !filter) return HookSrc{kSrcPairs, P1};
+    if (rr == 3 && lazy1) return HookSrc{kSrcPairs, P1};  // round 2 relabelled the pairs in place
     return HookSrc{kSrcPacked, E[(rr - 1) & 1]};
   };
 
@@ -765,7 +779,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
         ta.src0 = src.packed;
       } else if (src.kind == kSrcPairs) {
         ta.src_kind = kTailSrcPairs;
-        ta.src0 = E[1];
+        ta.src0 = src.packed;
         ta.src_w = wbase;
         ta.src_wstride = wstride;
       } else if constexpr (std::is_same_v<InView, SoaView>) {
@@ -815,7 +829,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       if (src.kind == kSrcIn)
         launch_hook(in);
       else if (src.kind == kSrcPairs)
-        launch_hook(PairsView<InView>{reinterpret_cast<const uint2*>(E[1]), in});
+        launch_hook(PairsView<InView>{reinterpret_cast<const uint2*>(src.packed), in});
       else
         launch_hook(PackedView{src.packed});
       if (!hfused)
@@ -831,7 +845,8 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     }
     // pair dedup is armed for big rounds; k_label2 decides on the device
     PairTable pt{nullptr, nullptr, 0};
-    if (!original_in && dedup_on && m_bound >= dedup_min_edges) {
+    const bool lazy2 = lazy1 && r == 2;  // round 2 over round 1's uncompacted pairs
+    if (!original_in && !lazy2 && dedup_on && m_bound >= dedup_min_edges) {
       const unsigned long long cap = std::min<unsigned long long>(1ull << 25, next_pow2(m_bound / 2));
       unsigned long long* tab = ws.get<unsigned long long>("pair_table", 2 * cap);
       pt = PairTable{tab, nullptr, cap};
@@ -845,9 +860,16 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     }
     hot_begin(kHotCompact, r, light);
     if (original_in) {
-      // plain round 1: relabelled copy of the caller's list in E[1], compacted into E[0]
-      launch_two_pass<InView, kModeRelabel>(ws, cb, in, E[1], Lr, Eout, mnext, d_ctr, r, m_bound, n,
-                                            kSlotCompact, (int)light, filt_for(n_bound, kSiteCount, filter));
+      // plain round 1: label pairs of the caller's list in P1 (lazy: that is
+      // round 2's list), else compacted into E[0]
+      launch_two_pass<InView, kModeRelabel>(ws, cb, in, const_cast<uint4*>(P1), Lr, Eout, mnext, d_ctr, r, m_bound, n,
+                                            kSlotCompact, (int)light, filt_for(n_bound, kSiteCount, filter),
+                                            PairTable{nullptr, nullptr, 0}, !lazy1);
+    } else if (lazy2) {
+      using PV = PairsInView<InView>;
+      launch_two_pass<PV, kModeRelabel>(ws, cb, PV{reinterpret_cast<const uint2*>(P1), in, in.base},
+                                        const_cast<uint4*>(P1), Lr, Eout, mnext, d_ctr, r, m, n, kSlotCompact,
+                                        (int)light, filt_for(n_bound, kSiteCount, filter));
     } else {
       launch_two_pass<PackedView, kModeRelabel>(ws, cb, PackedView{E[r & 1]}, E[r & 1], Lr, Eout, mnext, d_ctr,
                                                 r, m_bound, n, kSlotCompact, (int)light, filt_for(n_bound, kSiteCount, filter), pt);

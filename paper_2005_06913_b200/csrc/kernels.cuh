@@ -118,6 +118,7 @@ struct SoaView {
   const uint32_t* __restrict__ w;
   uint32_t base;
   static constexpr bool kOriginal = true;
+  static constexpr bool kMayBeDead = false;
   __device__ __forceinline__ EdgeRec stream(uint64_t i) const {
     return EdgeRec{__ldcs(src + i), __ldcs(dst + i), __ldcs(w + i), base + (uint32_t)i, true};
   }
@@ -136,6 +137,7 @@ struct AosView {
   const uint4* __restrict__ e;
   uint32_t base;
   static constexpr bool kOriginal = true;
+  static constexpr bool kMayBeDead = false;
   __device__ __forceinline__ EdgeRec stream(uint64_t i) const {
     const uint4 v = __ldcs(e + i);
     return EdgeRec{v.x, v.y, v.z, base + (uint32_t)i, v.w == 0};
@@ -154,6 +156,7 @@ struct AosView {
 struct PackedView {
   const uint4* __restrict__ e;
   static constexpr bool kOriginal = false;
+  static constexpr bool kMayBeDead = false;
   __device__ __forceinline__ EdgeRec stream(uint64_t i) const {
     const uint4 v = __ldcs(e + i);
     return EdgeRec{v.x, v.y, v.z, v.w, true};
@@ -177,6 +180,7 @@ struct PairsView {
   const uint2* __restrict__ xy;
   In in;
   static constexpr bool kOriginal = false;
+  static constexpr bool kMayBeDead = false;
   __device__ __forceinline__ EdgeRec gather(uint64_t i) const {
     const uint2 p = __ldcg(xy + i);
     return EdgeRec{p.x, p.y, in.weight(i), in.base + (uint32_t)i, true};
@@ -185,6 +189,27 @@ struct PairsView {
     const uint2 p = __ldcg(xy + i);
     return EdgeRec{p.x, p.y, 0u, in.base + (uint32_t)i, true};
   }
+};
+
+// Round 2 of the plain loop over round 1's label pairs, uncompacted (round
+// 1 skips its emit pass): the pair list IS round 2's edge list, indexed like
+// the caller's list (positions = edge ids), with the weights read from the
+// caller's list. Round 1's dead edges are the pairs with a == b; round 2's
+// count pass skips them and relabels the live pairs in place, so round 3's
+// hook gathers from the same list (PairsView).
+template <class In>
+struct PairsInView {
+  const uint2* __restrict__ xy;
+  In in;
+  uint32_t base;
+  static constexpr bool kOriginal = true;
+  static constexpr bool kMayBeDead = true;
+  __device__ __forceinline__ EdgeRec stream(uint64_t i) const {
+    const uint2 p = __ldcg(xy + i);
+    return EdgeRec{p.x, p.y, in.weight(i), base + (uint32_t)i, true};
+  }
+  __device__ __forceinline__ EdgeRec gather(uint64_t i) const { return stream(i); }
+  __device__ __forceinline__ uint32_t weight(uint64_t i) const { return in.weight(i); }
 };
 
 // ------------------------------ primitives ---------------------------------
@@ -733,6 +758,8 @@ __global__ void MST_LB_(MST_MINB_COUNT) k_count(View in, uint4* __restrict__ rel
             }
             keep[k] = e[k].a != e[k].b;
           }
+        } else if (View::kMayBeDead && e[k].a == e[k].b) {
+          // dead since an earlier round: no gather, no write (stays a == b)
         } else if (ok) {
           ox = __ldg(L + e[k].a);
           oy = __ldg(L + e[k].b);
@@ -1036,6 +1063,7 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_counts(uint32_t* __restrict
 // loop (same keys, same tie order, MST ids straight from the keys).
 struct PartnerView {
   static constexpr bool kOriginal = false;
+  static constexpr bool kMayBeDead = false;
   const uint32_t* partner;
 };
 
