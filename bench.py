@@ -208,7 +208,8 @@ def run_ours(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     n, m, s_full, d_full, w_full = C.generate_torch(spec, device=f"cuda:{local}")
-    lo, hi = D.shard_range(m, rank, world)
+    strat = D.strategy(m, world)
+    lo, hi = D.shard_range(m, rank, world) if strat == "sharded" else (0, m)
     s, d, w = s_full[lo:hi], d_full[lo:hi], w_full[lo:hi]
     out = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
@@ -219,7 +220,7 @@ def run_ours(args):
         if args.flush == "write+read":
             flush_rd.sum()
     stream = torch.cuda.current_stream()
-    comm = D.RankComm.from_torch(local) if world > 1 else None
+    comm = D.RankComm.from_torch(local) if strat == "sharded" else None
 
     def one_step(info=None, hot=None):
         if comm is None:
@@ -353,7 +354,10 @@ def run_ours(args):
                    "rounds": info.rounds, "live_edges": info.live_edges, "live_comps": info.live_comps,
                    "l2": ("flushed between timed steps: 512 MiB write + 256 MiB read of another buffer (clean lines)"
                           if args.flush == "write+read" else "flushed (512 MiB write) between timed steps"),
-                   "parallelism": f"edge-sharded x{world}" if world > 1 else "single GPU"},
+                   "parallelism": (f"edge-sharded x{world}" if strat == "sharded" else
+                                   f"replicated x{world}: m < {D.SHARD_MIN_EDGES >> 20} Mi edges, every rank runs "
+                                   "the single-GPU MST of the whole graph (sharding adds two allreduces per "
+                                   "round to a latency-bound loop)" if world > 1 else "single GPU")},
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,

@@ -20,6 +20,22 @@ from . import _lib as L
 from .api import GpuRunInfo, MstResult, WorkerPanic, _finish
 
 
+# Below this many edges one GPU's MST is a few hundred microseconds of
+# latency-bound rounds (c1: 0.69 ms for 8.4 M edges) and an edge-sharded run,
+# which adds two allreduces per round, cannot beat it: every rank then runs
+# the single-GPU MST of the whole graph (replicas, no data-path collective).
+# Larger graphs (c2-c4) are edge-sharded. MST_SHARD_MIN_EDGES overrides.
+SHARD_MIN_EDGES = 32 << 20
+
+
+def strategy(m: int, world: int) -> str:
+    """'sharded' (edge slices + per-round allreduce) or 'replicated'."""
+    import os
+
+    thr = int(float(os.environ.get("MST_SHARD_MIN_EDGES", SHARD_MIN_EDGES)))
+    return "sharded" if world > 1 and m >= thr else "replicated"
+
+
 def shard_range(m: int, rank: int, world: int) -> tuple[int, int]:
     """[lo, hi) of the global edge list owned by `rank` (edge_start analogue)."""
     if world < 1 or not 0 <= rank < world:

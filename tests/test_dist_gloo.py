@@ -115,3 +115,16 @@ def test_sharded_model_single_rank_matches_oracle(oracle_mod):
         assert got.tolist() == ids and tot == total
         # 3 shards in one process: allreduce = elementwise min over shards
         # is exercised by the gloo test; here shards are emulated serially
+
+
+def test_bench_strategy_threshold(monkeypatch):
+    """bench.py --gpus N: small graphs run replicas, large ones are sharded."""
+    from paper_2005_06913_b200 import dist as D
+    monkeypatch.delenv("MST_SHARD_MIN_EDGES", raising=False)
+    assert D.strategy(8_384_512, 8) == "replicated"      # c1
+    assert D.strategy(4_000_000, 2) == "replicated"      # c0
+    assert D.strategy(71_301_398, 2) == "sharded"        # c2
+    assert D.strategy(268_435_456, 8) == "sharded"       # c3
+    assert D.strategy(268_435_456, 1) == "replicated"    # one GPU: the single-GPU path
+    monkeypatch.setenv("MST_SHARD_MIN_EDGES", "1e6")
+    assert D.strategy(8_384_512, 2) == "sharded"
