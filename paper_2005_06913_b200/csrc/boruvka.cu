@@ -283,15 +283,15 @@ int sm_count(int device) {
 }
 
 template <class K>
-int blocks_per_sm(K kernel) {
+int blocks_per_sm(K kernel, size_t dyn_smem = 0) {
   static std::mutex mu;
-  static std::map<const void*, int> cache;
+  static std::map<std::pair<const void*, size_t>, int> cache;
   std::lock_guard<std::mutex> g(mu);
-  const void* key = reinterpret_cast<const void*>(kernel);
+  const std::pair<const void*, size_t> key{reinterpret_cast<const void*>(kernel), dyn_smem};
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   int nb = 0;
-  MST_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, kBlock, 0));
+  MST_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, kBlock, dyn_smem));
   cache[key] = std::max(nb, 1);
   return cache[key];
 }
@@ -745,7 +745,8 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
         ++launches;
       }
       auto kt = k_tail;
-      const int bps = std::max(1, std::min(blocks_per_sm(kt), env_int("MST_TAIL_BPS", 2)));
+      const size_t tail_smem = 0;  // all static (< 48 KB)
+      const int bps = std::max(1, std::min(blocks_per_sm(kt, tail_smem), env_int("MST_TAIL_BPS", 2)));
       const unsigned G = std::min<unsigned>(kTailMaxBlocks, (unsigned)(sm_count(dev) * bps));
       uint32_t* broots = ws.get<uint32_t>("tail_broots", G);
       uint32_t* bkept = ws.get<uint32_t>("tail_bkept", G);
@@ -759,6 +760,12 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       const HookSrc src = hook_src(r);
       TailArgs ta{{E[0], E[1]}, {minb[0], minb[1]}, parent, rootlabel, L, mst, broots, bkept, tmasks, twpref, M, flags,
                   trace, 0, nullptr, nullptr, nullptr, 0, d_ctr, n, r, (int)light};
+      if (env_int("MST_TAIL_TINY", 1)) {
+        // three rotating min tables for the one-sync rounds (k_tail "tiny")
+        unsigned long long* tiny = ws.get<unsigned long long>("tail_tiny", 3 * kTailSmemMin);
+        MST_CUDA_CHECK(cudaMemsetAsync(tiny, 0xFF, 3 * kTailSmemMin * sizeof(unsigned long long), s));
+        for (int k = 0; k < 3; ++k) ta.tiny[k] = tiny + k * kTailSmemMin;
+      }
       if (tail_dedup_on) {
         // per-round table mask <= next_pow2(m_r / 2) <= this
         const size_t slots = (size_t)std::max<unsigned long long>(1024, next_pow2(std::max<uint64_t>(m_bound / 2, 1)));
@@ -793,7 +800,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       }
       void* args[] = {&ta};
       hot_begin(kHotTail, r, light);
-      MST_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)kt, G, kBlock, args, 0, s));
+      MST_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)kt, G, kBlock, args, tail_smem, s));
       ++launches;
       tmark();
       MST_CUDA_CHECK(cudaMemcpyAsync(&ws.h_snap[kMaxR - 1], d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));

@@ -1368,9 +1368,12 @@ struct TailArgs {
   uint32_t pair_epoch;          // 1..1022, tag = epoch << 6 | round
   uint32_t dedup_ratio;
   uint32_t dedup_min;
+  // tiny rounds (n_r <= kTailSmemMin, plain loop): three rotating min tables,
+  // cleared by the host before the launch (nullptr: off)
+  unsigned long long* tiny[3];
 };
 
-constexpr uint32_t kTailSmemMin = 4096;  // block-local min table entries (32 KB)
+constexpr uint32_t kTailSmemMin = 2048;  // block-local min table entries (16 KB); tiny rounds up to this
 constexpr uint32_t kTailMaxBlocks = 1024;
 constexpr uint32_t kTailPairLabelBits = 24;
 constexpr int kTailPairProbes = 64;
@@ -1589,6 +1592,9 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
   __shared__ uint32_t s_warp[kWarps + 1];
   __shared__ uint32_t s_bpre[kTailMaxBlocks + 1];
   __shared__ unsigned long long s_wsum[kWarps];
+  __shared__ uint32_t s_par[kTailSmemMin];             // tiny rounds: parent / root per component
+  __shared__ uint32_t s_mask[kTailSmemMin / 32];       // tiny rounds: root bitmask
+  __shared__ uint32_t s_wpre[kTailSmemMin / 32 + 1];   // tiny rounds: roots before each mask word
   __shared__ unsigned long long s_min[kTailSmemMin];
   const uint32_t G = gridDim.x, b = blockIdx.x;
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
@@ -1611,6 +1617,7 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
   // dependent L2 round trip on the critical path of a tiny round).
   if ((uint32_t)a.r0 >= vc->stop_round || (uint32_t)a.r0 >= vc->phase_end) return;
   uint32_t n_r = n_entry;
+  int tiny_rounds = 0;
   uint64_t m_prev = m_entry;  // live edges entering round r-1 (dedup statistics)
   for (int r = a.r0; r < kMaxR - 1; ++r) {
     // edges kept by round r-1 (C's atomics, complete at the last grid.sync);
@@ -1620,6 +1627,165 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
     // ternaries, not a dynamic index: keeps TailArgs out of local memory
     const unsigned long long* mcur = (r & 1) ? a.minb[0] : a.minb[1];
     unsigned long long* mnext = (r & 1) ? a.minb[1] : a.minb[0];
+    // ---- tiny round (n_r <= kTailSmemMin, plain loop): every block makes
+    // the hook decisions and finds the roots of ALL components itself, in
+    // shared memory (the same rule, the same dense labels as A + B), then
+    // relabels its segment from shared memory: ONE grid sync per round
+    // instead of three. Min tables rotate through three small buffers: round
+    // r reads T[r%3] (the first tiny round: the normal table), offers into
+    // T[(r+1)%3] and clears T[(r+2)%3], which every block finished reading
+    // before the previous round's sync.
+    if (a.tiny[0] != nullptr && !a.light && r > a.r0 && n_r <= kTailSmemMin) {
+      const int rr = r % 3;
+      const unsigned long long* tcur =
+          (tiny_rounds == 0) ? mcur : (rr == 0 ? a.tiny[0] : rr == 1 ? a.tiny[1] : a.tiny[2]);
+      unsigned long long* tnext = rr == 0 ? a.tiny[1] : rr == 1 ? a.tiny[2] : a.tiny[0];
+      unsigned long long* tclear = rr == 0 ? a.tiny[2] : rr == 1 ? a.tiny[0] : a.tiny[1];
+      ++tiny_rounds;
+      if (m_r == 0) {  // round r-1 kept no edge (scan_verdict)
+        if (b == 0 && threadIdx.x == 0) a.ctr->stop_round = (uint32_t)r;
+        break;
+      }
+      for (uint32_t c = threadIdx.x; c < n_r; c += kBlock) s_min[c] = __ldcg(tcur + c);
+      for (uint32_t c = b * kBlock + threadIdx.x; c < n_r; c += G * kBlock) tclear[c] = kNoKey;
+      __syncthreads();
+      // hook (same rule as A): partner, mutual pair -> lower label is root
+      unsigned long long wsum = 0;
+      for (uint32_t base = 0; base < n_r; base += kBlock * kItems) {
+        unsigned long long key[kItems];
+        uint4 e[kItems];
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {  // the gathers of kItems components in flight together
+          const uint32_t c = base + k * kBlock + threadIdx.x;
+          key[k] = c < n_r ? s_min[c] : kNoKey;
+          e[k] = key[k] != kNoKey ? __ldcg(E + (uint32_t)key[k]) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          const uint32_t c = base + k * kBlock + threadIdx.x;
+          bool isroot = false;
+          if (c < n_r) {
+            if (key[k] == kNoKey) {
+              isroot = true;
+              s_par[c] = c;
+            } else {
+              const uint32_t o = (e[k].x == c) ? e[k].y : e[k].x;
+              isroot = s_min[o] == key[k] && c < o;
+              s_par[c] = isroot ? c : o;
+              if (!isroot && b == 0) {  // block 0 records the MST edge (flags, weight)
+                if (a.flags) a.flags[e[k].w] = 1;
+                wsum += (uint32_t)(key[k] >> 32);
+              }
+            }
+          }
+          const unsigned bal = __ballot_sync(0xffffffffu, isroot);
+          const uint32_t c0 = base + k * kBlock + warp * 32;
+          if (lane == 0 && c0 < n_r) s_mask[c0 >> 5] = bal;
+        }
+      }
+      __syncthreads();
+      if (warp == 0) {  // roots before each mask word (<= 64 words)
+        constexpr int kW = (kTailSmemMin / 32 + 31) / 32;
+        const uint32_t words = (n_r + 31) / 32;
+        uint32_t v[kW], sum = 0;
+#pragma unroll
+        for (int j = 0; j < kW; ++j) {
+          const uint32_t wi = lane * kW + j;
+          v[j] = wi < words ? __popc(s_mask[wi]) : 0u;
+          sum += v[j];
+        }
+        const uint32_t incl = warp_incl_scan(sum);
+        uint32_t run = incl - sum;
+#pragma unroll
+        for (int j = 0; j < kW; ++j) {
+          const uint32_t wi = lane * kW + j;
+          if (wi < words) s_wpre[wi] = run;
+          run += v[j];
+        }
+        if (lane == 31) s_wpre[kTailSmemMin / 32] = incl;
+      }
+      // root finding in shared memory (path halving: every value ever
+      // stored is an ancestor, so the races are benign)
+      for (uint32_t c = threadIdx.x; c < n_r; c += kBlock) {
+        uint32_t x = c, p = s_par[x];
+        while (p != x) {
+          const uint32_t gp = s_par[p];
+          if (gp == p) {
+            x = p;
+            break;
+          }
+          s_par[x] = gp;
+          x = gp;
+          p = s_par[x];
+        }
+        s_par[c] = x;  // the root
+      }
+      __syncthreads();
+      const uint32_t n_next = s_wpre[kTailSmemMin / 32];
+      const bool stop_now = n_next <= 1 || n_next == n_r;
+      if (b == 0) {
+        wsum = warp_sum<unsigned long long>(wsum);
+        if (lane == 0 && wsum) atomicAdd(&a.ctr->total_weight, wsum);
+        if (threadIdx.x == 0) {
+          a.ctr->n[r + 1] = n_next;
+          a.ctr->m[r + 2] = 0;  // the next round's kept counter (used after the sync)
+          if (stop_now) a.ctr->stop_round = (uint32_t)r + 1;
+        }
+      }
+      tail_stamp(a, slot);
+      if (stop_now) break;
+      // relabel + compact the warp's segment in place, offers aggregated in
+      // shared memory and flushed into T[(r+1)%3]
+      for (uint32_t c = threadIdx.x; c < n_next; c += kBlock) s_min[c] = kNoKey;
+      __syncthreads();
+      const uint64_t seg_hi = seg_lo + seg_len;
+      uint64_t out = seg_lo;
+      const uint32_t lt = lanemask_lt();
+      for (uint64_t base = seg_lo; base < seg_hi; base += 32 * kItems) {
+        uint4 e[kItems];
+        bool f[kItems];
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          const uint64_t i = base + k * 32 + lane;
+          e[k] = i < seg_hi ? __ldcg(E + i) : make_uint4(0, 0, 0, 0);
+          if (i < seg_hi) {
+            const uint32_t ra = s_par[e[k].x], rb = s_par[e[k].y];
+            e[k].x = s_wpre[ra >> 5] + __popc(s_mask[ra >> 5] & ((1u << (ra & 31)) - 1u));
+            e[k].y = s_wpre[rb >> 5] + __popc(s_mask[rb >> 5] & ((1u << (rb & 31)) - 1u));
+          }
+          f[k] = i < seg_hi && e[k].x != e[k].y;
+        }
+        uint32_t rank[kItems], tot = 0;
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          const unsigned bal = __ballot_sync(0xffffffffu, f[k]);
+          rank[k] = tot + __popc(bal & lt);
+          tot += __popc(bal);
+        }
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          if (!f[k]) continue;
+          const uint64_t j = out + rank[k];
+          E[j] = e[k];
+          const unsigned long long key = ((unsigned long long)e[k].z << 32) | (uint32_t)j;
+          if (key < s_min[e[k].x]) atomicMin(s_min + e[k].x, key);
+          if (key < s_min[e[k].y]) atomicMin(s_min + e[k].y, key);
+        }
+        out += tot;
+      }
+      seg_len = out - seg_lo;
+      if (lane == 0 && seg_len) atomicAdd(const_cast<unsigned long long*>(&a.ctr->m[r + 1]), seg_len);
+      __syncthreads();
+      for (uint32_t c = threadIdx.x; c < n_next; c += kBlock) {
+        const unsigned long long v = s_min[c];
+        if (v != kNoKey && v < __ldcg(tnext + c)) atomicMin(tnext + c, v);
+      }
+      grid.sync();
+      tail_stamp(a, slot);
+      n_r = n_next;
+      m_prev = m_r;
+      continue;
+    }
     // ---- A: hook decisions over this block's chunk (a multiple of 32
     // components, so root-mask words never straddle chunks)
     const uint32_t cs = (((n_r + G - 1) / G) + 31u) & ~31u;
@@ -1730,6 +1896,7 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
     if (b == 0 && threadIdx.x == 0) {
       a.ctr->n[r + 1] = n_next;
       a.ctr->m[r + 1] = 0;  // C adds every block's kept count
+      a.ctr->m[r + 2] = 0;  // (a tiny round r+1 adds into m[r+2] without a prior sync)
       if (stop_now) a.ctr->stop_round = (uint32_t)r + 1;
       if (phase_now) a.ctr->phase_end = (uint32_t)r;
     }
