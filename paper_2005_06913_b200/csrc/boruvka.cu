@@ -1034,7 +1034,7 @@ RunOut run_single(const SingleArgs& a, mst_stats_t* stats) {
   // Pinned SoA input on the plain loop: copy in chunks on the copy stream
   // while round 1's min pass consumes the chunks that have landed (and the
   // table clears run), so the H2D hides that work. Off by default: measured
-  // on c1 (tools/exp9.sh), 24 chunk copies move the 100 MB in 1.94 ms vs
+  // on c1 (tools/exp_pipeline_h2d.sh), 24 chunk copies move the 100 MB in 1.94 ms vs
   // 1.83 ms for three whole-array copies, more than the ~45 us they hide.
   CopyChunks chunks;
   const bool pipelined = !a.on_device && a.kind == 0 && a.m >= (4u << 20) && !filter_mode(a.n, a.m) &&

@@ -20,10 +20,13 @@
 //                        filtered 64-bit atomicMin (the edge scan + offer,
 //                        boruvka_parallel.cpp:150-167).
 //
-// Round 1 reads the caller's edge list directly (k_min_round1 + the two
-// passes over the original view). Filter-Boruvka, pair dedup, the tail
-// megakernel, the sorted output and the sharded exchange are described at
-// their kernels below.
+// Round 1 reads the caller's edge list directly (k_min_round1 + the count
+// pass over the original view; in the plain loop its label pairs are round
+// 2's list, PairsInView). Offers are read-first 64-bit atomicMins, batched
+// per thread where that pays (offer_both). Filter-Boruvka, pair dedup, the
+// tail megakernel (segmented in-place compaction, one-sync tiny rounds),
+// the sorted output and the sharded exchange are described at their
+// kernels below.
 #pragma once
 
 #include <cooperative_groups.h>
@@ -1345,7 +1348,7 @@ struct TailArgs {
   uint32_t* L;
   uint32_t* mst;
   uint32_t* broots;     // [gridDim.x] roots per block chunk (A -> B)
-  uint32_t* bkept;      // unused (kept for the layout)
+  uint32_t* bkept;      // unused (the segmented list needs no per-block counts)
   uint32_t* masks;      // root bitmask, one word per 32 components
   uint32_t* wpref;      // roots of the block's chunk before each word
   uint32_t* M;          // light phase: entry-label -> current-label map (n[r0] entries)

@@ -47,6 +47,8 @@ MODES = [dict(MST_FILTER=0), dict(MST_FILTER=1, MST_FILTER_BETA=0.3),
          dict(MST_FILTER=1, MST_TAIL=0, MST_DEDUP_MIN_EDGES=0),
          # the tail megakernel with one block per SM (other chunk sizes)
          dict(MST_FILTER=0, MST_TAIL_BPS=1, MST_TAIL_EDGES=1e9),
+         # the tail without its one-sync tiny rounds (three phases every round)
+         dict(MST_FILTER=0, MST_TAIL_EDGES=1e9, MST_TAIL_TINY=0),
          # the tail's tagged pair dedup (opt-in) forced on in every round
          dict(MST_FILTER=0, MST_TAIL_EDGES=1e9, MST_TAIL_DEDUP=1, MST_TAIL_DEDUP_MIN=0, MST_TAIL_DEDUP_RATIO=1),
          dict(MST_FILTER=1, MST_TAIL_EDGES=1e9, MST_TAIL_DEDUP=1, MST_TAIL_DEDUP_MIN=0, MST_TAIL_DEDUP_RATIO=1)]
@@ -242,7 +244,7 @@ def test_baseline_configs_full_size(mst, oracle_mod, cfg):
     g = C.generate_host(C.CONFIGS[cfg])
     k = O.kruskal(g.n, g.src, g.dst, g.w)
     assert k.ids.size == g.n - 1
-    for mode in (MODES[0], MODES[2], MODES[5], MODES[7]):
+    for mode in (MODES[0], MODES[2], MODES[5], MODES[7], MODES[8]):
         with _env(**mode):
             info = P.GpuRunInfo()
             r = P.boruvka_gpu(g, info=info)
