@@ -669,6 +669,13 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   // 3.19 ms at 6 M).
   const double tail_env = env_double("MST_TAIL_EDGES", 0.0);
   const uint64_t tail_comps = (uint64_t)env_double("MST_TAIL_COMPS", 8.0e6);
+  // Few components but many edges (uniform graphs collapse their components
+  // long before their edges): every offer of a round kernel then hits one of
+  // a few thousand table entries and the atomics serialise (uniform m/n = 8:
+  // ~0.7 ms per such round); the tail aggregates those offers per block in
+  // shared memory (4.1 -> 1.2 ms). So the tail also takes over once
+  // n_r <= tail_small_n, whatever the edge count.
+  const uint64_t tail_small_n = (uint64_t)env_double("MST_TAIL_SMALL_N", 65536);
   auto tail_edges = [&]() -> uint64_t { return (uint64_t)(tail_env > 0 ? tail_env : (light ? 3.0e6 : 6.0e6)); };
 
   // Lazy round 1 (plain loop): round 1 stops after its count pass, whose
@@ -676,7 +683,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   // round 2 compacts them. Saves round 1's emit pass (c1: 32 us). Not when
   // round 2 enters the tail, which needs a compacted list.
   const bool lazy1 = !filter && env_int("MST_LAZY_ROUND1", 1) != 0 &&
-                     !(tail_on && m <= tail_edges() && (uint64_t)n <= tail_comps);
+                     !(tail_on && (m <= tail_edges() || (uint64_t)n <= tail_small_n) && (uint64_t)n <= tail_comps);
   const uint4* P1 = lazy1 ? reinterpret_cast<const uint4*>(ws.get<uint2>("pairs1", m)) : E[1];
 
   // Light phase over: compose its relabel maps into a vertex -> component map,
@@ -739,7 +746,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     // the tail runs at 2 CTAs/SM: its component phases are latency-bound when
     // n_r is huge (c4's light phase ends with 47 M components and 406 edges:
     // 1.2 ms in the tail vs 0.3 ms of round kernels)
-    if (tail_on && !original_in && m_est <= tail_edges() && n_bound <= tail_comps) {
+    if (tail_on && !original_in && (m_est <= tail_edges() || n_bound <= tail_small_n) && n_bound <= tail_comps) {
       // ---- all remaining rounds in one cooperative launch
       uint32_t* M = nullptr;
       if (light) {
