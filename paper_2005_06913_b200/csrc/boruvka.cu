@@ -661,7 +661,10 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   const bool tail_dedup_on = dedup_on && env_int("MST_TAIL_DEDUP", 0) != 0;
   const uint64_t dedup_min_edges = (uint64_t)env_double("MST_DEDUP_MIN_EDGES", 2.0e6);
   const unsigned int dedup_active = (unsigned int)env_double("MST_DEDUP_ACTIVE", 262144);
-  const unsigned int pair_div = (unsigned int)std::max(1, env_int("MST_DEDUP_TABLE_DIV", 4));
+  // low byte: table slots >= m_r / div; bit 8: retry after an overflowed
+  // attempt without waiting for the K(K-1)/2 <= m_r/8 guarantee
+  const unsigned int pair_div = (unsigned int)std::max(1, std::min(255, env_int("MST_DEDUP_TABLE_DIV", 4))) |
+                                (env_int("MST_DEDUP_RETRY", 0) ? 0x100u : 0u);
   // Tail entry (m_bound is the host's one-round-stale edge bound). Measured
   // (tools/sweep_tail.sh): the plain loop and phase D gain from entering
   // early (c1, c0: 6 M), the light phase from keeping the round kernels,
