@@ -335,8 +335,9 @@ int filt_for(uint64_t table_entries, int site = kSiteCount, bool dense = true) {
     const char* e = getenv(name);
     return e && *e ? atoi(e) : -1;
   };
-  static const int mode[kSiteCount_] = {env_mode("MST_OFFER_MIN1"), env_mode("MST_OFFER_SPLIT"),
-                                        env_mode("MST_OFFER_COUNT"), env_mode("MST_OFFER_HEAVY")};
+  // read per call (a few getenv per round), so a process can switch modes
+  const int mode[kSiteCount_] = {env_mode("MST_OFFER_MIN1"), env_mode("MST_OFFER_SPLIT"),
+                                 env_mode("MST_OFFER_COUNT"), env_mode("MST_OFFER_HEAVY")};
   if (table_entries * 8 > (uint64_t)limit) return 0;
   if (mode[site] >= 0) return mode[site];
   switch (site) {
