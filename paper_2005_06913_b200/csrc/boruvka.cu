@@ -425,7 +425,10 @@ uint32_t sort_from_flags(Workspace& ws, const uint8_t* flags, uint64_t m, uint32
                                     1, std::min<uint64_t>((tiles + kScanTile - 1) / kScanTile, (uint64_t)sm_count(ws.device))), kScanBlock, ws.stream, counts, tiles, d_ctr, 0, st, ws.next_epoch(), 0, 0);
     ++launches;
   }
-  launch_k(k_flags_emit, g, kBlock, ws.stream, flags, m, counts, d_sorted);
+  // the emit's own residency (more registers + 16 KB of staging per block)
+  const unsigned ge = (unsigned)std::max<uint64_t>(
+      1, std::min<uint64_t>(tiles, (uint64_t)sm_count(ws.device) * blocks_per_sm(k_flags_emit)));
+  launch_k(k_flags_emit, ge, kBlock, ws.stream, flags, m, counts, d_sorted);
   MST_CUDA_CHECK(cudaGetLastError());
   return launches;
 }
