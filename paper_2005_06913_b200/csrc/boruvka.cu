@@ -670,8 +670,9 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   const unsigned int pair_div = (unsigned int)std::max(1, std::min(255, env_int("MST_DEDUP_TABLE_DIV", 4))) |
                                 (env_int("MST_DEDUP_RETRY", 0) ? 0x100u : 0u);
   // Tail entry (m_bound is the host's one-round-stale edge bound). Measured
-  // (tools/sweep_tail.sh): the plain loop and phase D gain from entering
-  // early (c1, c0: 6 M), the light phase from keeping the round kernels,
+  // (tools/sweep_tail.sh, tools/sweep_tail2.sh): the plain loop and phase D
+  // gain from entering early (12 M: c1's round 2 with 5.1 M edges runs in
+  // the segmented tail, 0.631 -> 0.602 ms), the light phase from keeping the round kernels,
   // whose pair dedup the tail lacks, a little longer (c2: 3.02 ms at 3 M vs
   // 3.19 ms at 6 M).
   const double tail_env = env_double("MST_TAIL_EDGES", 0.0);
@@ -683,7 +684,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   // shared memory (4.1 -> 1.2 ms). So the tail also takes over once
   // n_r <= tail_small_n, whatever the edge count.
   const uint64_t tail_small_n = (uint64_t)env_double("MST_TAIL_SMALL_N", 65536);
-  auto tail_edges = [&]() -> uint64_t { return (uint64_t)(tail_env > 0 ? tail_env : (light ? 3.0e6 : 6.0e6)); };
+  auto tail_edges = [&]() -> uint64_t { return (uint64_t)(tail_env > 0 ? tail_env : (light ? 3.0e6 : 12.0e6)); };
 
   // Lazy round 1 (plain loop): round 1 stops after its count pass, whose
   // relabelled label pairs (one per caller edge) are round 2's edge list;
