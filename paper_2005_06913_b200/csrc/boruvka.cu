@@ -850,7 +850,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       auto launch_hook = [&](auto view) {
         auto kd = k_hook_decide<decltype(view)>;
         launch_k(kd, (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ht, (uint64_t)sm_count(dev) * blocks_per_sm(kd))),
-                 kBlock, s, view, mcur, parent, rootlabel, hmasks, hcounts, d_ctr, r, hfused, (int)light, hslot);
+                 kBlock, s, view, mcur, parent, rootlabel, hmasks, hcounts, d_ctr, r, hfused, (int)light, hslot, flags);
       };
       if (src.kind == kSrcIn)
         launch_hook(in);
@@ -1322,7 +1322,7 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, uint6
       uint32_t* hslot = ws.get<uint32_t>("hook_slotpref", tiles_of(n) * kItems * kWarps);
       auto kd = k_hook_decide<PartnerView, true>;
       launch_k(kd, persistent_grid(kd, dev, ht), kBlock, st, PartnerView{s.partner}, s.xch, s.parent, s.rootlabel, hmasks,
-               hcounts, s.d_ctr, r, hfused, phase, hslot);
+               hcounts, s.d_ctr, r, hfused, phase, hslot, (uint8_t*)nullptr);
       if (!hfused)
         launch_k(k_scan_counts<kScanRoots>,
                  (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((ht + kScanTile - 1) / kScanTile, (uint64_t)sm_count(dev))),

@@ -1117,7 +1117,8 @@ __global__ void MST_LB_(MST_MINB_HOOK) k_hook_decide(View E, const unsigned long
                                                         uint32_t* __restrict__ parent, uint32_t* __restrict__ rootlabel,
                                                         uint32_t* __restrict__ masks, uint32_t* __restrict__ counts,
                                                         DevCounters* ctr, int r, int fused, int light_phase,
-                                                        uint32_t* __restrict__ slotpref) {
+                                                        uint32_t* __restrict__ slotpref,
+                                                        uint8_t* __restrict__ flags = nullptr) {
   pdl_prologue();
   __shared__ uint32_t s_cnt[kWarps];
   __shared__ uint32_t s_slot[kItems * kWarps];
@@ -1167,7 +1168,12 @@ __global__ void MST_LB_(MST_MINB_HOOK) k_hook_decide(View E, const unsigned long
           parent[c] = isroot ? (uint32_t)c : o;
           ++active;
           if (!isroot) {
-            rootlabel[c] = e[k].eid;  // stash the MST edge id until its slot is known
+            // single GPU: the MST flag right here; the sharded loop stashes
+            // the id for its MST slot (placed by k_label2)
+            if (flags)
+              flags[e[k].eid] = 1;
+            else
+              rootlabel[c] = e[k].eid;
             wsum += (uint32_t)(key[k] >> 32);
           }
         }
@@ -1290,9 +1296,9 @@ __global__ void MST_LB_(MST_MINB_LABEL) k_label2(uint32_t* __restrict__ parent, 
     }
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
-      if (!v[k] || isroot[k]) continue;
+      if (!mst || !v[k] || isroot[k]) continue;  // single GPU: flags set by the hook
       const uint32_t eid = __ldg(stash + c[k]);
-      if (mst) mst[mst_base + (c[k] - own[k])] = eid;  // the sharded loop's slots (single GPU: flags only)
+      mst[mst_base + (c[k] - own[k])] = eid;  // the sharded loop's slots
       if (flags) flags[eid] = 1;
     }
     if (!labels) continue;
@@ -1830,7 +1836,10 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
               isroot = okey[k] == key[k] && c < o;
               a.parent[c] = isroot ? c : o;
               if (!isroot) {
-                a.rootlabel[c] = e[k].w;  // the MST edge id, placed in B
+                if (a.flags)
+                  a.flags[e[k].w] = 1;  // the MST edge
+                else
+                  a.rootlabel[c] = e[k].w;  // the MST edge id, placed in B
                 wsum += (uint32_t)(key[k] >> 32);
               }
             }
@@ -1916,12 +1925,12 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
       }
 #pragma unroll
       for (int k = 0; k < kItems; ++k) {
-        if (!v[k] || isroot[k]) continue;
+        if (!a.mst || !v[k] || isroot[k]) continue;  // flags: set in A
         const uint32_t x = c[k], w = x >> 5;
         const uint32_t before = s_bpre[x / cs] + __ldcg(a.wpref + w) +
                                 __popc(__ldcg(a.masks + w) & ((1u << (x & 31)) - 1u));
         const uint32_t eid = __ldcg(a.rootlabel + x);
-        if (a.mst) a.mst[mst_base + (x - before)] = eid;
+        a.mst[mst_base + (x - before)] = eid;
         if (a.flags) a.flags[eid] = 1;
       }
       if (stop_now) continue;
