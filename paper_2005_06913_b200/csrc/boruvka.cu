@@ -1068,7 +1068,8 @@ RunOut run_single(const SingleArgs& a, mst_stats_t* stats) {
         // the copies may not overwrite the buffers before earlier work on
         // the compute stream is done with them
         MST_CUDA_CHECK(cudaStreamWaitEvent(ws.copy_stream, e0, 0));
-        const uint64_t per = std::max<uint64_t>(1u << 20, (a.m + CopyChunks::kMax - 1) / CopyChunks::kMax);
+        const int want = std::max(1, std::min(CopyChunks::kMax, env_int("MST_PIPELINE_CHUNKS", 16)));
+        const uint64_t per = std::max<uint64_t>(1u << 20, (a.m + want - 1) / want);
         chunks.count = (int)((a.m + per - 1) / per);
         for (int j = 0; j <= chunks.count; ++j) chunks.bound[j] = std::min<uint64_t>(a.m, (uint64_t)j * per);
         for (int j = 0; j < chunks.count; ++j) {
