@@ -690,7 +690,14 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   // relabelled label pairs (one per caller edge) are round 2's edge list;
   // round 2 compacts them. Saves round 1's emit pass (c1: 32 us). Not when
   // round 2 enters the tail, which needs a compacted list.
-  const bool lazy1 = !filter && env_int("MST_LAZY_ROUND1", 1) != 0 &&
+  // Round 1 handed to the tail at its phase C (plain loop, SoA input): the
+  // round kernels do round 1's min / hook / label at full occupancy, the
+  // tail's first pass relabels + compacts + offers straight from the caller's
+  // list, replacing round 1's count + emit passes.
+  const bool start_c_ok = tail_on && !filter && std::is_same<InView, SoaView>::value &&
+                          env_int("MST_TAIL_START_C", 1) != 0 && m <= (32ull << 20) && n <= (16u << 20);
+  bool tail_c_pending = false;
+  const bool lazy1 = !start_c_ok && !filter && env_int("MST_LAZY_ROUND1", 1) != 0 &&
                      !(tail_on && (m <= tail_edges() || (uint64_t)n <= tail_small_n) && (uint64_t)n <= tail_comps);
   const uint4* P1 = lazy1 ? reinterpret_cast<const uint4*>(ws.get<uint2>("pairs1", m)) : E[1];
 
@@ -754,7 +761,8 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     // the tail runs at 2 CTAs/SM: its component phases are latency-bound when
     // n_r is huge (c4's light phase ends with 47 M components and 406 edges:
     // 1.2 ms in the tail vs 0.3 ms of round kernels)
-    if (tail_on && !original_in && (m_est <= tail_edges() || n_bound <= tail_small_n) && n_bound <= tail_comps) {
+    if (tail_c_pending ||
+        (tail_on && !original_in && (m_est <= tail_edges() || n_bound <= tail_small_n) && n_bound <= tail_comps)) {
       // ---- all remaining rounds in one cooperative launch
       uint32_t* M = nullptr;
       if (light) {
@@ -779,6 +787,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       const HookSrc src = hook_src(r);
       TailArgs ta{{E[0], E[1]}, {minb[0], minb[1]}, parent, rootlabel, L, mst, broots, bkept, tmasks, twpref, M, flags,
                   trace, 0, nullptr, nullptr, nullptr, 0, d_ctr, n, r, (int)light};
+      ta.start_c = tail_c_pending ? 1 : 0;
       if (env_int("MST_TAIL_TINY", 1)) {
         // three rotating min tables for the one-sync rounds (k_tail "tiny")
         unsigned long long* tiny = ws.get<unsigned long long>("tail_tiny", 3 * kTailSmemMin);
@@ -884,6 +893,10 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       launch_k(k_label2, g, kBlock, s, parent, rootlabel, hmasks, hslot, hcounts, Lr, mnext, mst, flags, n, d_ctr, r,
                pt.pairs, pt.cap, dedup_active, pair_div);
     }
+    if (original_in && start_c_ok) {  // round 1's compaction: the tail's first phase C
+      tail_c_pending = true;
+      continue;
+    }
     hot_begin(kHotCompact, r, light);
     if (original_in) {
       // plain round 1: label pairs of the caller's list in P1 (lazy: that is
@@ -949,7 +962,8 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
         // algorithmic: one 16 B read per live edge, one 16 B write per kept edge
         const int last = (h.light && phase_end) ? phase_end : stop;
         const DevCounters& cc = (h.light && phase_end) ? snap_b : c;
-        for (int rr = h.r; rr + 1 < last && rr < kMaxR - 1; ++rr) bytes += 16ull * cc.m[rr] + 16ull * cc.m[rr + 1];
+        for (int rr = h.r; rr + 1 < last && rr < kMaxR - 1; ++rr)
+          bytes += ((rr == 1 && !filter) ? 12ull : 16ull) * cc.m[rr] + 16ull * cc.m[rr + 1];
       } else {
         const bool ran = h.r + 1 < stop && (!h.light || phase_end == 0 || h.r < phase_end);
         if (!ran) continue;

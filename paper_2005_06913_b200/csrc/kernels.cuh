@@ -1380,6 +1380,10 @@ struct TailArgs {
   // tiny rounds (n_r <= kTailSmemMin, plain loop): three rotating min tables,
   // cleared by the host before the launch (nullptr: off)
   unsigned long long* tiny[3];
+  // start_c: round r0 = 1 of the plain loop had its min / hook / label done by
+  // the round kernels; the launch starts at its phase C, reading the caller's
+  // SoA list (src0 / src1 / src_w) in place of round 1's count + emit passes
+  int start_c;
 };
 
 constexpr uint32_t kTailSmemMin = 2048;  // block-local min table entries (16 KB); tiny rounds up to this
@@ -1612,7 +1616,7 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
   // this WARP's segment of the (single, in place) edge list: a share of its
   // block's chunk, compacted with ballot ranks (no block barrier)
   uint4* const E = (a.r0 & 1) ? a.E[1] : a.E[0];
-  const uint64_t m_entry = vc->m[a.r0];
+  const uint64_t m_entry = a.start_c ? vc->m[0] : vc->m[a.r0];
   const uint64_t es = (m_entry + G - 1) / G;
   const uint64_t blo = min((uint64_t)b * es, m_entry), bhi = min(blo + es, m_entry);
   const uint64_t wes = (bhi - blo + kWarps - 1) / kWarps;
@@ -1625,6 +1629,7 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
   // runs, so no counter is re-read at the top of a round (each read is a
   // dependent L2 round trip on the critical path of a tiny round).
   if ((uint32_t)a.r0 >= vc->stop_round || (uint32_t)a.r0 >= vc->phase_end) return;
+  if (a.start_c && (uint32_t)a.r0 + 1 >= vc->stop_round) return;  // round r0's hook finished the MST
   uint32_t n_r = n_entry;
   int tiny_rounds = 0;
   uint64_t m_prev = m_entry;  // live edges entering round r-1 (dedup statistics)
@@ -1795,6 +1800,11 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
       m_prev = m_r;
       continue;
     }
+    uint32_t n_next = 0;
+    bool stop_now = false, phase_now = false;
+    const bool first_c = a.start_c && r == a.r0;
+    if (first_c) n_next = vc->n[r + 1];  // the round kernels' hook + label ran round r0
+    if (!first_c) {
     // ---- A: hook decisions over this block's chunk (a multiple of 32
     // components, so root-mask words never straddle chunks)
     const uint32_t cs = (((n_r + G - 1) / G) + 31u) & ~31u;
@@ -1894,8 +1904,7 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
     }
     if (last_dedup == r - 1 && 2 * m_r > m_prev) dedup_off = true;
     block_scan_array(a.broots, G, s_bpre, s_warp);
-    const uint32_t n_next = s_bpre[G];
-    bool stop_now = false, phase_now = false;
+    n_next = s_bpre[G];
     if (n_next <= 1) {
       stop_now = true;
     } else if (n_next == n_r) {
@@ -1946,11 +1955,12 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
     grid.sync();
     tail_stamp(a, slot);
     if (stop_now) break;
+    }  // !first_c
     if (a.light) {
       for (uint32_t x = b * kBlock + threadIdx.x; x < n_entry; x += G * kBlock) a.M[x] = __ldcg(a.L + a.M[x]);
     }
     // ---- C0 (optional): relabel in place + each pair's lightest key
-    const bool dedup = a.pairs != nullptr && n_next < (1u << kTailPairLabelBits) && m_r >= a.dedup_min &&
+    const bool dedup = a.pairs != nullptr && !first_c && n_next < (1u << kTailPairLabelBits) && m_r >= a.dedup_min &&
                        m_r >= (uint64_t)a.dedup_ratio * n_next &&
                        (!dedup_off || (uint64_t)n_next * (n_next - 1) / 2 <= m_r / 4);
     const uint32_t tag = (a.pair_epoch << 6) | ((uint32_t)r & 63u);
@@ -2007,27 +2017,38 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
       const uint32_t lt = lanemask_lt();
       for (uint64_t base = seg_lo; base < seg_hi; base += 32 * kItems) {
         uint4 e[kItems];
+        bool live[kItems];
+        if (first_c) {
+          // round 1 straight from the caller's SoA list (k_min_round1 has
+          // flagged any out-of-range endpoint; such edges are dropped here)
 #pragma unroll
-        for (int k = 0; k < kItems; ++k) {
-          const uint64_t i = base + k * 32 + lane;
-          e[k] = i < seg_hi ? __ldcg(E + i) : make_uint4(0, 0, 0, 0);
+          for (int k = 0; k < kItems; ++k) {
+            const uint64_t i = base + k * 32 + lane;
+            e[k] = i < seg_hi ? make_uint4(__ldcs(static_cast<const uint32_t*>(a.src0) + i), __ldcs(a.src1 + i),
+                                           __ldcs(a.src_w + i), (uint32_t)i)
+                              : make_uint4(0, 0, 0, 0);
+            live[k] = i < seg_hi && e[k].x < a.n_orig && e[k].y < a.n_orig;
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < kItems; ++k) {
+            const uint64_t i = base + k * 32 + lane;
+            e[k] = i < seg_hi ? __ldcg(E + i) : make_uint4(0, 0, 0, 0);
+            live[k] = i < seg_hi;
+          }
         }
         bool f[kItems];
         if (!dedup) {
 #pragma unroll
           for (int k = 0; k < kItems; ++k) {
-            const uint64_t i = base + k * 32 + lane;
-            if (i < seg_hi) {
+            if (live[k]) {
               e[k].x = __ldcg(a.L + e[k].x);
               e[k].y = __ldcg(a.L + e[k].y);
             }
           }
         }
 #pragma unroll
-        for (int k = 0; k < kItems; ++k) {
-          const uint64_t i = base + k * 32 + lane;
-          f[k] = i < seg_hi && e[k].x != e[k].y;
-        }
+        for (int k = 0; k < kItems; ++k) f[k] = live[k] && e[k].x != e[k].y;
         if (dedup) {
           unsigned long long pw[kItems], key[kItems];
 #pragma unroll
