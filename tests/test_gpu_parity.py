@@ -52,6 +52,8 @@ MODES = [dict(MST_FILTER=0), dict(MST_FILTER=1, MST_FILTER_BETA=0.3),
          # the tail's tagged pair dedup (opt-in) forced on in every round
          dict(MST_FILTER=0, MST_TAIL_EDGES=1e9, MST_TAIL_DEDUP=1, MST_TAIL_DEDUP_MIN=0, MST_TAIL_DEDUP_RATIO=1),
          dict(MST_FILTER=1, MST_TAIL_EDGES=1e9, MST_TAIL_DEDUP=1, MST_TAIL_DEDUP_MIN=0, MST_TAIL_DEDUP_RATIO=1),
+         # round 1 compacted by the round kernels, then the tail (no start at phase C)
+         dict(MST_FILTER=0, MST_TAIL_START_C=0),
          # round 1 compacted (no lazy pairs list), every round kernel offering batched / as plain REDs
          dict(MST_FILTER=0, MST_LAZY_ROUND1=0, MST_TAIL=0),
          dict(MST_FILTER=1, MST_TAIL=0, MST_OFFER_MIN1=2, MST_OFFER_SPLIT=2, MST_OFFER_COUNT=2, MST_OFFER_HEAVY=2),
