@@ -788,6 +788,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       TailArgs ta{{E[0], E[1]}, {minb[0], minb[1]}, parent, rootlabel, L, mst, broots, bkept, tmasks, twpref, M, flags,
                   trace, 0, nullptr, nullptr, nullptr, 0, d_ctr, n, r, (int)light};
       ta.start_c = tail_c_pending ? 1 : 0;
+      ta.c_soa = (tail_c_pending && r == 1) ? 1 : 0;
       if (env_int("MST_TAIL_TINY", 1)) {
         // three rotating min tables for the one-sync rounds (k_tail "tiny")
         unsigned long long* tiny = ws.get<unsigned long long>("tail_tiny", 3 * kTailSmemMin);
@@ -881,7 +882,14 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     // pair dedup is armed for big rounds; k_label2 decides on the device
     PairTable pt{nullptr, nullptr, 0};
     const bool lazy2 = lazy1 && r == 2;  // round 2 over round 1's uncompacted pairs
-    if (!original_in && !lazy2 && dedup_on && m_bound >= dedup_min_edges) {
+    // phase D's first round (Filter-Boruvka): hook + label here, then the
+    // tail starts at its phase C over the heavy survivors in place (the host
+    // knows only m here, not the survivor count: bounded by components;
+    // c2 3.04 -> 2.97 ms, c3 neutral, c4's 47 M components excluded)
+    const bool d_start_c = tail_on && !light && phase_end && r == phase_end && env_int("MST_TAIL_START_C_D", 1) != 0 &&
+                           m_bound <= (uint64_t)env_double("MST_TAIL_START_C_D_EDGES", 1e12) &&
+                           n_bound <= (16u << 20);
+    if (!original_in && !lazy2 && !d_start_c && dedup_on && m_bound >= dedup_min_edges) {
       const unsigned long long cap = std::min<unsigned long long>(1ull << 25, next_pow2(m_bound / 2));
       unsigned long long* tab = ws.get<unsigned long long>("pair_table", 2 * cap);
       pt = PairTable{tab, nullptr, cap};
@@ -893,7 +901,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       launch_k(k_label2, g, kBlock, s, parent, rootlabel, hmasks, hslot, hcounts, Lr, mnext, mst, flags, n, d_ctr, r,
                pt.pairs, pt.cap, dedup_active, pair_div);
     }
-    if (original_in && start_c_ok) {  // round 1's compaction: the tail's first phase C
+    if ((original_in && start_c_ok) || d_start_c) {  // this round's compaction: the tail's first phase C
       tail_c_pending = true;
       continue;
     }

@@ -1384,6 +1384,7 @@ struct TailArgs {
   // the round kernels; the launch starts at its phase C, reading the caller's
   // SoA list (src0 / src1 / src_w) in place of round 1's count + emit passes
   int start_c;
+  int c_soa;  // start_c's phase C reads the caller's SoA list (plain round 1), else the list E[r0 & 1]
 };
 
 constexpr uint32_t kTailSmemMin = 2048;  // block-local min table entries (16 KB); tiny rounds up to this
@@ -1616,7 +1617,7 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
   // this WARP's segment of the (single, in place) edge list: a share of its
   // block's chunk, compacted with ballot ranks (no block barrier)
   uint4* const E = (a.r0 & 1) ? a.E[1] : a.E[0];
-  const uint64_t m_entry = a.start_c ? vc->m[0] : vc->m[a.r0];
+  const uint64_t m_entry = (a.start_c && a.c_soa) ? vc->m[0] : vc->m[a.r0];
   const uint64_t es = (m_entry + G - 1) / G;
   const uint64_t blo = min((uint64_t)b * es, m_entry), bhi = min(blo + es, m_entry);
   const uint64_t wes = (bhi - blo + kWarps - 1) / kWarps;
@@ -2018,7 +2019,7 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
       for (uint64_t base = seg_lo; base < seg_hi; base += 32 * kItems) {
         uint4 e[kItems];
         bool live[kItems];
-        if (first_c) {
+        if (first_c && a.c_soa) {
           // round 1 straight from the caller's SoA list (k_min_round1 has
           // flagged any out-of-range endpoint; such edges are dropped here)
 #pragma unroll
