@@ -465,11 +465,24 @@ __global__ void k_weight_hist(const uint32_t* __restrict__ w, uint32_t wstride, 
 
 __global__ void __launch_bounds__(1024) k_pick_pivot(const uint32_t* __restrict__ hist, uint32_t target, DevCounters* ctr) {
   pdl_prologue();
-  // one block of 1024 threads: 64 bins per thread, block scan of sums
+  // one block of 1024 threads: 64 bins per thread (16 independent 16 B loads
+  // in flight, not 64 dependent ones), block scan of the sums, then the 64
+  // bins of the thread whose range holds the target are searched by 64
+  // threads at once
   __shared__ uint32_t s_sum[1024];
+  __shared__ uint32_t s_tstar, s_before, s_w0;
   const uint32_t t = threadIdx.x;
+  const uint4* h4 = reinterpret_cast<const uint4*>(hist) + t * 16;
   uint32_t sum = 0;
-  for (int i = 0; i < 64; ++i) sum += hist[t * 64 + i];
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    uint4 v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __ldg(h4 + half * 8 + i);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sum += v[i].x + v[i].y + v[i].z + v[i].w;
+  }
+  if (t == 0) s_tstar = 0xFFFFFFFFu;
   s_sum[t] = sum;
   __syncthreads();
   for (int d = 1; d < 1024; d <<= 1) {
@@ -479,16 +492,24 @@ __global__ void __launch_bounds__(1024) k_pick_pivot(const uint32_t* __restrict_
     __syncthreads();
   }
   const uint32_t before = t ? s_sum[t - 1] : 0u;
-  if (before < target && s_sum[t] >= target) {
-    uint32_t run = before;
-    for (int i = 0; i < 64; ++i) {
-      run += hist[t * 64 + i];
-      if (run >= target) {
-        const uint32_t bin = t * 64 + i;
-        ctr->pivot = bin == 0xFFFFu ? 0xFFFFFFFFu : (bin + 1) << 16;
-        break;
-      }
-    }
+  if (before < target && s_sum[t] >= target) {  // at most one thread
+    s_tstar = t;
+    s_before = before;
+  }
+  __syncthreads();
+  if (s_tstar == 0xFFFFFFFFu || t >= 64) return;  // target above the total: everything light
+  const uint32_t bin = s_tstar * 64 + t;
+  const uint32_t c = __ldg(hist + bin);
+  const uint32_t incl = warp_incl_scan(c);
+  if (t == 31) s_w0 = incl;
+  __syncwarp();
+  asm volatile("bar.sync 1, 64;" ::: "memory");  // the two searching warps only
+  const uint32_t run = s_before + incl + (t >= 32 ? s_w0 : 0u);
+  const unsigned hit = __ballot_sync(0xffffffffu, run >= target);
+  // the first bin reaching the target: the lowest hit lane of warp 0, else of warp 1
+  if (hit && (uint32_t)(__ffs(hit) - 1) == (t & 31)) {
+    const bool first = t < 32 || (s_before + s_w0 < target);
+    if (first) ctr->pivot = bin == 0xFFFFu ? 0xFFFFFFFFu : (bin + 1) << 16;
   }
 }
 
