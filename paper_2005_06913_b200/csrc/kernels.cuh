@@ -519,9 +519,26 @@ __global__ void k_compose(uint32_t* __restrict__ Lr, const uint32_t* __restrict_
                           const DevCounters* ctr, int r) {
   pdl_prologue();
   const uint32_t n_r = ctr->n[r];
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n_r; c += stride)
-    Lr[c] = __ldg(Lnext + Lr[c]);
+  // 4 items per thread: the 4 gathers of Lnext are in flight together
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * 4;
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x * 4 + threadIdx.x; base < n_r; base += stride) {
+    uint32_t x[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t c = base + (uint64_t)k * blockDim.x;
+      x[k] = c < n_r ? Lr[c] : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t c = base + (uint64_t)k * blockDim.x;
+      if (c < n_r) x[k] = __ldg(Lnext + x[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t c = base + (uint64_t)k * blockDim.x;
+      if (c < n_r) Lr[c] = x[k];
+    }
+  }
 }
 
 // ------------------------------ scan helpers -------------------------------
