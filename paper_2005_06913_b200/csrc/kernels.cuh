@@ -1996,7 +1996,18 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
     if (stop_now) break;
     }  // !first_c
     if (a.light) {
-      for (uint32_t x = b * kBlock + threadIdx.x; x < n_entry; x += G * kBlock) a.M[x] = __ldcg(a.L + a.M[x]);
+      // entry label -> current label, 4 gathers in flight per thread
+      for (uint32_t base = b * kBlock * 4 + threadIdx.x; base < n_entry; base += G * kBlock * 4) {
+        uint32_t x[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) x[k] = base + k * kBlock < n_entry ? __ldcg(a.M + base + k * kBlock) : 0u;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (base + k * kBlock < n_entry) x[k] = __ldcg(a.L + x[k]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (base + k * kBlock < n_entry) a.M[base + k * kBlock] = x[k];
+      }
     }
     // ---- C0 (optional): relabel in place + each pair's lightest key
     const bool dedup = a.pairs != nullptr && !first_c && n_next < (1u << kTailPairLabelBits) && m_r >= a.dedup_min &&
