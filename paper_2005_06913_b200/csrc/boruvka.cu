@@ -775,7 +775,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       }
       auto kt = k_tail;
       const size_t tail_smem = 0;  // all static (< 48 KB)
-      const int bps = std::max(1, std::min(blocks_per_sm(kt, tail_smem), env_int("MST_TAIL_BPS", 2)));
+      const int bps = std::max(1, std::min(blocks_per_sm(kt, tail_smem), env_int("MST_TAIL_BPS", MST_TAIL_MINB)));
       const unsigned G = std::min<unsigned>(kTailMaxBlocks, (unsigned)(sm_count(dev) * bps));
       uint32_t* broots = ws.get<uint32_t>("tail_broots", G);
       uint32_t* bkept = ws.get<uint32_t>("tail_bkept", G);

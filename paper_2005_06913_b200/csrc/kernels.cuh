@@ -1631,8 +1631,11 @@ __device__ __forceinline__ void offer_batch(unsigned long long* table, const uin
   }
 }
 
+// 3 CTAs/SM (<= 80 registers): since the tail also streams round 1's edges
+// (start at phase C) the extra warps pay: c1 -1.5 %, c2 -1 %, c3 -1 %, c4
+// neutral, c0 +2 % (tools/ab: tail3 vs 2)
 #ifndef MST_TAIL_MINB
-#define MST_TAIL_MINB 2
+#define MST_TAIL_MINB 3
 #endif
 __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
   pdl_prologue();
