@@ -1,25 +1,30 @@
 #!/usr/bin/env python
 """Benchmark of the B200 parallel Boruvka MST (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
 
 One step = one complete MST of the configured synthetic graph (all rounds,
 sorted MST ids and total weight produced). Metric: graph edges/s =
-m / MST wall time (BASELINE.json), whole job over all ranks.
+m / MST wall time (BASELINE.json), whole job over all ranks. Default
+workload: c4 (R-MAT scale 26, ~1.14 B edges), the config BASELINE.json
+quotes its scaling target on; it fits one B200.
 
 * value: device-resident — edges already in HBM when the timed region
-  starts, ids left in HBM; CUDA events on the launching stream; L2 flushed
-  (a 512 MiB write) between timed steps; max over ranks.
+  starts, ids left in HBM (N > 1: mst_gpu_boruvka_rank_device); CUDA events
+  on the launching stream; L2 flushed (a 512 MiB write) between timed
+  steps; max over ranks.
 * e2e: the same MST through the public API with HOST (pinned) edge arrays:
   H2D of src/dst/w and D2H of the sorted ids inside the timed region.
-* roofline: the edge-pass kernels (k_min_round1, k_count, k_emit), algorithmic
-  bytes per SURVEY.md §8(d) (12 B/edge round 1, 16 B/live edge later,
-  +16 B/kept edge) over their CUDA-event time, against MEASURED_PEAKS.json.
-* cpu_baseline: the unchanged reference boruvka_cas (oracle/_ref) on the
-  host cores, rank 0 at N=1, on the same graph.
+* roofline: the edge-pass kernel family (round-1 min / split / compactions /
+  heavy filter / tail), algorithmic bytes per SURVEY.md §8(d) over their
+  CUDA-event time, against MEASURED_PEAKS.json; plus the whole-MST fraction.
+* cpu_baseline (rank 0, N = 1): the unchanged reference's boruvka_seq (one
+  thread) and boruvka_cas over a thread sweep (oracle/_ref), on the workload
+  or, above 20 M edges, a scaled instance of the same generator family.
 
 --impl reference times the reference's own CPU implementation of the path
-(boruvka_cas through oracle/_ref, all host threads) on the same workload.
+(boruvka_cas through oracle/_ref, all host threads) on the same bounded
+sample, printing the same `config`; it never loads the product library.
 """
 from __future__ import annotations
 
@@ -46,9 +51,11 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--config", default="c1", choices=["c0", "c1", "c2", "c3", "c4"])
+    p.add_argument("--config", default="c4", choices=["c0", "c1", "c2", "c3", "c4"])
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--shard-min-edges", type=float, default=None,
+                   help="edge-shard at N > 1 from this many edges (default: dist.SHARD_MIN_EDGES)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--flush", default="write", choices=["write", "write+read"],
                    help="L2 flush between timed steps: a 512 MiB write, then (default) a 256 MiB read of "
@@ -116,63 +123,109 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def reference_cpu(g, threads: int, runs: int):
-    """The unchanged reference boruvka_cas (oracle/_ref) on the host cores."""
-    from oracle import oracle as O
-
-    if not O.ref_available():
-        return None
-    times = []
-    res = None
-    for _ in range(runs):
-        res = O.ref_solve(g.n, g.src, g.dst, g.w, O.ALGO_CAS, threads=threads)
-        times.append(res.elapsed_ms)
-    return times, res
-
-
-CPU_SAMPLE_EDGES = 20_000_000  # above this the CPU legs run a scaled instance (10-30 s of work)
+CPU_SAMPLE_EDGES = 20_000_000  # above this the CPU legs time a scaled instance (10-30 s of work per run)
 
 
 def cpu_sample(spec):
-    """The graph the CPU legs time: the workload itself when it is small, else
-    an instance of the same generator family and density scaled to ~16-17 M
-    edges (the unchanged reference CAS scans every edge every round, so the
-    full c3/c4 graphs would take from minutes to hours)."""
+    """(spec, description) of the graph the CPU legs time: the workload itself
+    when it is small, else the same generator family, parameters and seed
+    scaled to ~16-17 M edges. The unchanged reference CAS scans every edge in
+    every round on the host (boruvka_parallel.cpp:150), so one full c3/c4 MST
+    takes minutes to hours (DESIGN.md §5 gives the one measured full-c4 run);
+    a smaller instance of the same family also sits better in the host's
+    caches, so its edges/s is, if anything, flattering to the reference."""
     from paper_2005_06913_b200 import configs as C
-    m = C.edge_count(spec)
-    if m <= CPU_SAMPLE_EDGES:
-        return spec, f"full {spec.name} graph"
+    m = C.KNOWN_EDGES.get(spec.name)
+    if m is not None and m <= CPU_SAMPLE_EDGES:
+        return spec, f"the full {spec.name} graph (m={m})"
     if spec.kind == 0:
         n2 = 1 << 20
         sub = C.uniform(n2, n2 * (spec.m // spec.n), seed=spec.seed, name=f"{spec.name}_sample_n{n2}")
         return sub, (f"scaled {spec.name}: uniform n={n2}, m={sub.m} (same density {spec.m // spec.n}, "
-                     f"same generator and seed)")
+                     f"generator and seed)")
     if spec.kind == 2:
         sub = C.rmat(20, spec.edgefactor, seed=spec.seed, name=f"{spec.name}_sample_s20")
         return sub, (f"scaled {spec.name}: R-MAT scale 20, edgefactor {spec.edgefactor} (same generator, "
-                     f"parameters and seed)")
-    return spec, f"full {spec.name} graph"
+                     f"a/b/c/d and seed)")
+    return spec, f"the full {spec.name} graph"
+
+
+def host_graph(spec):
+    """Host arrays of a config built by the restated generator under oracle/
+    (the same bytes as the product's generators, tests/test_generators.py),
+    so the CPU legs never load the product library."""
+    from oracle import oracle as O
+    return O.generate(spec)
+
+
+def thread_sweep(hw: int):
+    ts, t = [], 1
+    while t < hw:
+        ts.append(t)
+        t *= 2
+    return ts + [hw]
+
+
+def cpu_baseline_sweep(spec):
+    """rank 0, N=1: the unchanged reference's sequential Boruvka (1 thread)
+    and CAS variant over a thread sweep (bench.cpp:105-110), each timed by its
+    own MstResult::elapsed_ms on the same sample."""
+    from oracle import oracle as O
+    if not O.ref_available():
+        return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                "sample": "unavailable: oracle/_ref/libmstref.so not built"}
+    cspec, sample = cpu_sample(spec)
+    n, src, dst, w = host_graph(cspec)
+    m = int(src.size)
+    hw, omp = O.hardware_threads(), O.omp_max_threads()
+    rows = {}
+    seq = O.ref_solve(n, src, dst, w, O.ALGO_SEQ, threads=1)
+    rows["boruvka_seq T=1"] = {"ms": seq.elapsed_ms, "edges_per_s": m / (seq.elapsed_ms / 1e3), "rounds": seq.rounds}
+    cas = None
+    for t in thread_sweep(hw):
+        cas = O.ref_solve(n, src, dst, w, O.ALGO_CAS, threads=t)
+        rows[f"boruvka_cas T={t}"] = {"ms": cas.elapsed_ms, "edges_per_s": m / (cas.elapsed_ms / 1e3),
+                                      "rounds": cas.rounds}
+    return {"value": m / (cas.elapsed_ms / 1e3), "unit": UNIT, "cores": hw, "kind": "reference",
+            "sample": (f"{sample}; n={n}, m={m} (m'={cas.m_prime} after the SURVEY 8(c) adapter); one run per "
+                       f"row of the unchanged reference; value = boruvka_cas at T={hw} (all host threads)"),
+            "hardware_concurrency": hw, "omp_get_max_threads": omp, "sweep": rows}
+
+
+def workload_config(spec):
+    """The `config` object both arms print (identical keys and values)."""
+    from paper_2005_06913_b200 import configs as C
+    m = C.KNOWN_EDGES.get(spec.name)
+    if m is None:
+        from oracle import oracle as O
+        m = O.gen_count(spec)
+    return {"workload": spec.name, "n": spec.vertices, "m": m, "seed": spec.seed}
 
 
 def run_reference(args):
+    """--impl reference: the unchanged reference boruvka_cas (oracle/_ref,
+    all host threads) through its own public API, one bounded sample of the
+    workload per step. Nothing of the product library is loaded."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
     from oracle import oracle as O
     from paper_2005_06913_b200 import configs as C
 
-    spec, sample = cpu_sample(C.CONFIGS[args.config])
-    g = C.generate_host(spec)
-    m = g.edge_count()
     if not O.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libmstref.so not built"}))
         return 0
+    spec = C.CONFIGS[args.config]
+    cspec, sample = cpu_sample(spec)
+    n, src, dst, w = host_graph(cspec)
+    m = int(src.size)
     threads = O.hardware_threads()
     for _ in range(args.warmup):
-        O.ref_solve(g.n, g.src, g.dst, g.w, O.ALGO_CAS, threads=threads)
+        O.ref_solve(n, src, dst, w, O.ALGO_CAS, threads=threads)
     times = []
+    r = None
     for _ in range(args.steps):
-        r = O.ref_solve(g.n, g.src, g.dst, g.w, O.ALGO_CAS, threads=threads)
+        r = O.ref_solve(n, src, dst, w, O.ALGO_CAS, threads=threads)
         times.append(r.elapsed_ms)
     ms = float(np.mean(times))
     value = m / (ms / 1e3)
@@ -180,12 +233,16 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded generator)",
-        "config": {"workload": spec.name, "n": g.n, "m": m, "seed": spec.seed,
-                   "path": "mst::boruvka_cas (unchanged reference, oracle/_ref) via SURVEY §8(c) adapter",
-                   "m_prime": r.m_prime, "timer": "reference MstResult::elapsed_ms"},
+        "config": workload_config(spec),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": f"{sample}, {args.steps} runs of boruvka_cas(T={threads})"},
+                         "sample": (f"{sample}; n={n}, m={m} (m'={r.m_prime} after the SURVEY 8(c) adapter); "
+                                    f"{args.steps} timed runs of boruvka_cas(T={threads}) after {args.warmup} "
+                                    "warm-up runs"),
+                         "hardware_concurrency": threads, "omp_get_max_threads": O.omp_max_threads()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "run_detail": {"path": "mst::boruvka_cas (unchanged reference, oracle/_ref) via the SURVEY 8(c) adapter",
+                       "timer": "reference MstResult::elapsed_ms", "rounds": r.rounds,
+                       "sample_n": n, "sample_m": m},
     }
     print(json.dumps(line))
     return 0
@@ -208,7 +265,7 @@ def run_ours(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     n, m, s_full, d_full, w_full = C.generate_torch(spec, device=f"cuda:{local}")
-    strat = D.strategy(m, world)
+    strat = D.strategy(m, world, args.shard_min_edges)
     lo, hi = D.shard_range(m, rank, world) if strat == "sharded" else (0, m)
     s, d, w = s_full[lo:hi], d_full[lo:hi], w_full[lo:hi]
     out = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
@@ -226,8 +283,8 @@ def run_ours(args):
         if comm is None:
             return P.boruvka_gpu_device(n, m, s.data_ptr(), d.data_ptr(), w.data_ptr(), out.data_ptr(),
                                         stream.cuda_stream, info=info, hot=hot)
-        r = comm.boruvka_ptrs(n, m, lo, hi - lo, s.data_ptr(), d.data_ptr(), w.data_ptr(), True, info)
-        return len(r.mst_edges), r.total_weight
+        return comm.boruvka_device(n, m, lo, hi - lo, s.data_ptr(), d.data_ptr(), w.data_ptr(), out.data_ptr(),
+                                   stream.cuda_stream, info)
 
     def barrier():
         if world > 1:
@@ -331,17 +388,7 @@ def run_ours(args):
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
-            from oracle import oracle as O
-            cspec, sample = cpu_sample(spec)
-            hg = g if (e2e is not None and cspec is spec) else C.generate_host(cspec)
-            threads = O.hardware_threads()
-            rr = reference_cpu(hg, threads, runs=1)
-            if rr is not None:
-                times, res = rr
-                cpu = {"value": hg.edge_count() / (float(np.mean(times)) / 1e3), "unit": UNIT, "cores": threads,
-                       "kind": "reference",
-                       "sample": f"{sample}, 1 run of unchanged boruvka_cas(T={threads}) "
-                                 f"(m'={res.m_prime} after the §8(c) adapter), reference elapsed_ms"}
+            cpu = cpu_baseline_sweep(spec)
         except Exception as ex:  # reported, not fatal
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"failed: {ex}"}
 
@@ -350,14 +397,14 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (seeded counter-based generator, BASELINE.json shape)",
-        "config": {"workload": spec.name, "n": n, "m": m, "seed": spec.seed,
-                   "rounds": info.rounds, "live_edges": info.live_edges, "live_comps": info.live_comps,
-                   "l2": ("flushed between timed steps: 512 MiB write + 256 MiB read of another buffer (clean lines)"
-                          if args.flush == "write+read" else "flushed (512 MiB write) between timed steps"),
-                   "parallelism": (f"edge-sharded x{world}" if strat == "sharded" else
-                                   f"replicated x{world}: m < {D.SHARD_MIN_EDGES >> 20} Mi edges, every rank runs "
-                                   "the single-GPU MST of the whole graph (sharding adds two allreduces per "
-                                   "round to a latency-bound loop)" if world > 1 else "single GPU")},
+        "config": workload_config(spec),
+        "run_detail": {"rounds": info.rounds, "live_edges": info.live_edges, "live_comps": info.live_comps,
+                       "l2": ("flushed between timed steps: 512 MiB write + 256 MiB read of another buffer "
+                              "(clean lines)" if args.flush == "write+read" else
+                              "flushed (512 MiB write) between timed steps"),
+                       "parallelism": (f"edge-sharded x{world}" if strat == "sharded" else
+                                       f"replicated x{world}: every rank runs the single-GPU MST of the whole "
+                                       "graph (below the sharding threshold)" if world > 1 else "single GPU")},
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,

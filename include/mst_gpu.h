@@ -139,6 +139,35 @@ int mst_gpu_boruvka_rank(mst_comm_t comm, uint32_t n, uint64_t m_total, uint64_t
                          const uint32_t* w, int on_device, uint32_t* out_ids,
                          uint64_t* out_count, uint64_t* out_total_weight, mst_stats_t* stats);
 
+/* The same with this rank's shard already in HBM (device pointers on the
+ * communicator's device) and the sorted ids left in HBM (d_out_ids, n-1
+ * entries): the multi-GPU counterpart of mst_gpu_boruvka_device. Runs on
+ * `stream` (NULL: ordered after / before the legacy default stream 0). */
+int mst_gpu_boruvka_rank_device(mst_comm_t comm, uint32_t n, uint64_t m_total, uint64_t shard_base,
+                                uint64_t shard_m, const uint32_t* d_src, const uint32_t* d_dst,
+                                const uint32_t* d_w, uint32_t* d_out_ids, void* stream,
+                                uint64_t* out_count, uint64_t* out_total_weight, mst_stats_t* stats);
+
+/* Bring-your-own collective (MPI, gloo, a test harness): the sharded loop of
+ * mst_gpu_boruvka_rank with every exchange handed to `allreduce`, which must
+ * reduce `count` elements of `host_buf` (pinned host memory, in place)
+ * across all ranks and return 0. dtype MST_DTYPE_U32 / MST_DTYPE_U64
+ * (unsigned), op MST_OP_MIN / MST_OP_SUM. Every rank makes the same calls
+ * in the same order. */
+#define MST_DTYPE_U32 0
+#define MST_DTYPE_U64 1
+#define MST_OP_MIN 0
+#define MST_OP_SUM 1
+typedef struct mst_collective {
+  int (*allreduce)(void* ctx, void* host_buf, uint64_t count, int dtype, int op);
+  void* ctx;
+  int nranks, rank, device;
+} mst_collective_t;
+int mst_gpu_boruvka_rank_cb(const mst_collective_t* coll, uint32_t n, uint64_t m_total,
+                            uint64_t shard_base, uint64_t shard_m, const uint32_t* src,
+                            const uint32_t* dst, const uint32_t* w, int on_device, uint32_t* out_ids,
+                            uint64_t* out_count, uint64_t* out_total_weight, mst_stats_t* stats);
+
 /* Device-resident timing entry (bench): edges already in HBM, result left in
  * HBM (sorted ids in d_out_ids, count/total in host outputs). Runs `reps`
  * back-to-back MSTs on `stream` (0 = legacy default stream) and returns the
@@ -197,6 +226,18 @@ int mst_io_load_soa(const char* path, uint32_t n, uint64_t m, uint32_t* src, uin
                     uint32_t* w, int on_device);
 int mst_io_save_soa(const char* path, uint32_t n, uint64_t m, const uint32_t* src,
                     const uint32_t* dst, const uint32_t* w);
+
+/* ---- tuning knobs ----
+ * Every engine knob sits in one process-wide table with its measured
+ * default (DESIGN.md §2 gives the measurements); the library never reads the
+ * environment. Knobs are named like the A/B tools' MST_* variables
+ * ("MST_FILTER", "MST_FILTER_BETA", "MST_TAIL", ...; mst_gpu_tuning_name(i)
+ * enumerates them, NULL past the last). Unknown names -> MST_ERR_INVALID_ARG.
+ * Changing a knob while another thread runs an MST is not supported. */
+int mst_gpu_set_tuning(const char* name, double value);
+int mst_gpu_get_tuning(const char* name, double* out_value);
+int mst_gpu_reset_tuning(void);
+const char* mst_gpu_tuning_name(int index);
 
 /* Frees the cached device workspaces of the calling thread's devices. */
 int mst_gpu_release_workspace(void);

@@ -51,6 +51,10 @@ def _load_oracle():
         lib.oracle_boruvka_seq.argtypes = [_u32, _u64, _vp, _vp, _vp, _vp, _u64p, _u64p, _u32p]
         lib.oracle_min_edges.argtypes = [_u32, _u64, _vp, _vp, _vp, _vp]
         lib.oracle_verify.argtypes = [_u32, _u64, _vp, _vp, _vp, _vp, _u64, _u32p, _u64p]
+        gen_args = [ctypes.c_int, _u32, _u64, _u32, _u32, _u32, _u32, ctypes.c_double, ctypes.c_double,
+                    ctypes.c_double, _u64, ctypes.c_int]
+        lib.oracle_gen_count.argtypes = gen_args + [_u64p]
+        lib.oracle_gen.argtypes = gen_args + [_vp, _vp, _vp, _u64p]
         _oracle = lib
     return _oracle
 
@@ -133,6 +137,44 @@ def verify(n: int, src, dst, w, ids) -> dict:
             "total_weight": int(total.value)}
 
 
+RMAT_ABC = (0.57, 0.19, 0.19)
+
+
+def _gen_args(spec, threads: int):
+    """spec: a paper_2005_06913_b200.configs.GenSpec (plain data; nothing of
+    the product library is loaded) or any object with the same fields."""
+    a, b, c = RMAT_ABC
+    n = spec.n
+    if spec.kind == 1:
+        n = spec.rows * spec.cols
+    elif spec.kind == 2:
+        n = 1 << spec.scale
+    return [spec.kind, n, spec.m, spec.rows, spec.cols, spec.scale, spec.edgefactor, a, b, c, spec.seed, threads]
+
+
+def gen_count(spec, threads: int = 0) -> int:
+    """Edge count of a seeded BASELINE-config graph (gen_oracle.c)."""
+    out = ctypes.c_uint64()
+    rc = _load_oracle().oracle_gen_count(*_gen_args(spec, threads), ctypes.byref(out))
+    if rc:
+        raise ValueError(f"oracle_gen_count failed with status {rc}")
+    return int(out.value)
+
+
+def generate(spec, threads: int = 0):
+    """(n, src, dst, w) of a seeded BASELINE-config graph, built by the
+    restated generator (gen_oracle.c) without the product library: the
+    same bytes as configs.generate_host / generate_device."""
+    m = gen_count(spec, threads)
+    src, dst, w = (np.empty(m, dtype=np.uint32) for _ in range(3))
+    out = ctypes.c_uint64()
+    rc = _load_oracle().oracle_gen(*_gen_args(spec, threads), _p(src), _p(dst), _p(w), ctypes.byref(out))
+    if rc or out.value != m:
+        raise ValueError(f"oracle_gen failed with status {rc}")
+    n = _gen_args(spec, threads)[1]
+    return n, src, dst, w
+
+
 def ref_generate_graph(n: int, avg_degree: int, seed: int):
     """The reference's own generate_graph (graph.cpp:143-194), unchanged."""
     lib = _load_ref()
@@ -178,6 +220,14 @@ def ref_solve(n: int, src, dst, w, algo: int = ALGO_KRUSKAL, threads: int = 1) -
         raise ValueError(f"ref_solve status {rc}: {lib.ref_last_error().decode()}")
     return OracleResult(ids[: cnt.value].copy(), int(tot.value), int(rounds.value), float(ms.value),
                         int(mp.value))
+
+
+def omp_max_threads() -> int:
+    """omp_get_max_threads() inside the reference library (mstbench.cpp:137-138)."""
+    if ref_available():
+        return int(_load_ref().ref_omp_max_threads())
+    import os
+    return os.cpu_count() or 1
 
 
 def hardware_threads() -> int:

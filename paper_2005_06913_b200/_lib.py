@@ -100,6 +100,21 @@ class MstVerify(ctypes.Structure):
 
 MST_VERIFY_NO_ORACLE = (1 << 64) - 1
 
+MST_DTYPE_U32, MST_DTYPE_U64 = 0, 1
+MST_OP_MIN, MST_OP_SUM = 0, 1
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int,
+                                ctypes.c_int)
+
+
+class MstCollective(ctypes.Structure):
+    _fields_ = [
+        ("allreduce", ALLREDUCE_FN),
+        ("ctx", ctypes.c_void_p),
+        ("nranks", ctypes.c_int),
+        ("rank", ctypes.c_int),
+        ("device", ctypes.c_int),
+    ]
+
 _SIGNATURES = {
     "mst_gpu_boruvka": (ctypes.c_int, [ctypes.POINTER(MstEdgesSoa), ctypes.c_int, ctypes.c_void_p,
                                        u64p, u64p, ctypes.POINTER(MstStats)]),
@@ -118,6 +133,14 @@ _SIGNATURES = {
                                             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
                                             ctypes.c_void_p, u64p, u64p,
                                             ctypes.POINTER(MstStats)]),
+    "mst_gpu_boruvka_rank_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64,
+                                                   ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p,
+                                                   ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                                   ctypes.c_void_p, u64p, u64p, ctypes.POINTER(MstStats)]),
+    "mst_gpu_boruvka_rank_cb": (ctypes.c_int, [ctypes.POINTER(MstCollective), ctypes.c_uint32, ctypes.c_uint64,
+                                               ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p,
+                                               ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                               ctypes.c_void_p, u64p, u64p, ctypes.POINTER(MstStats)]),
     "mst_gpu_boruvka_device": (ctypes.c_int, [ctypes.POINTER(MstEdgesSoa), ctypes.c_void_p,
                                               ctypes.c_void_p, u64p, u64p,
                                               ctypes.POINTER(MstStats),
@@ -139,6 +162,10 @@ _SIGNATURES = {
                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
     "mst_io_save_soa": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_void_p,
                                        ctypes.c_void_p, ctypes.c_void_p]),
+    "mst_gpu_set_tuning": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_double]),
+    "mst_gpu_get_tuning": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_double)]),
+    "mst_gpu_reset_tuning": (ctypes.c_int, []),
+    "mst_gpu_tuning_name": (ctypes.c_char_p, [ctypes.c_int]),
     "mst_gpu_release_workspace": (ctypes.c_int, []),
     "mst_gpu_last_error": (ctypes.c_char_p, []),
     "mst_gpu_version": (ctypes.c_char_p, []),

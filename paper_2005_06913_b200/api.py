@@ -405,3 +405,66 @@ def boruvka_gpu_device(n: int, m: int, src_ptr: int, dst_ptr: int, w_ptr: int, o
         hot["bytes"] = int(stats.hot_bytes)
     _raise_for(rc)
     return int(count.value), int(total.value)
+
+
+# ---- tuning knobs (include/mst_gpu.h "tuning knobs") ----
+
+def tuning_names() -> list[str]:
+    """Every knob of the engine's tuning table."""
+    out, i = [], 0
+    while True:
+        name = L.lib().mst_gpu_tuning_name(i)
+        if name is None:
+            return out
+        out.append(name.decode())
+        i += 1
+
+
+def set_tuning(name: str, value: float) -> None:
+    rc = L.lib().mst_gpu_set_tuning(name.encode(), float(value))
+    if rc != L.MST_OK:
+        raise ValueError(L.last_error())
+
+
+def get_tuning(name: str) -> float:
+    v = ctypes.c_double()
+    rc = L.lib().mst_gpu_get_tuning(name.encode(), ctypes.byref(v))
+    if rc != L.MST_OK:
+        raise ValueError(L.last_error())
+    return v.value
+
+
+class tuning:
+    """Context manager: set knobs for the calls inside, restore on exit.
+
+        with tuning(MST_FILTER=1, MST_FILTER_BETA=0.3):
+            boruvka_gpu(g)
+    """
+
+    def __init__(self, **knobs):
+        self.knobs = knobs
+
+    def __enter__(self):
+        self.old = {k: get_tuning(k) for k in self.knobs}
+        for k, v in self.knobs.items():
+            set_tuning(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        for k, v in self.old.items():
+            set_tuning(k, v)
+
+
+def tuning_from_env(environ=None) -> dict:
+    """A/B tools only: reset the knobs to their defaults, then apply the
+    MST_* variables of the environment that name a knob (the library itself
+    never reads the environment). Returns the applied ones."""
+    import os
+    env = os.environ if environ is None else environ
+    L.lib().mst_gpu_reset_tuning()
+    applied = {}
+    for name in tuning_names():
+        if env.get(name):
+            set_tuning(name, float(env[name]))
+            applied[name] = float(env[name])
+    return applied

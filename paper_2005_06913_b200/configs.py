@@ -75,6 +75,17 @@ CONFIGS = {
     "c4": rmat(26, 16, seed=4, name="c4_rmat26_ef16"),
 }
 
+# Edge counts of the five workloads (the R-MAT ones depend on the draws that
+# land on the diagonal); pinned by tests/test_generators.py and the GPU
+# golden-answer test against tests/golden/answers.json.
+KNOWN_EDGES = {
+    "c0_uniform_1M_4M": 4_000_000,
+    "c1_grid_2048x2048": 8_384_512,
+    "c2_rmat22_ef16": 71_301_337,
+    "c3_uniform_16.7M_268M": 268_435_456,
+    "c4_rmat26_ef16": 1_140_846_523,
+}
+
 
 def _check(rc: int) -> None:
     if rc != L.MST_OK:

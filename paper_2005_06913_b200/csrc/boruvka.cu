@@ -8,6 +8,7 @@
 #include <omp.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstring>
 #include <map>
@@ -86,6 +87,75 @@ NcclApi& nccl() {
       throw MstError{MST_ERR_NCCL, std::string(#expr " failed: ") + nccl().GetErrorString(_r)}; \
   } while (0)
 
+// ------------------------------- tuning -------------------------------------
+// Every tuning knob of the engine, in ONE table with its measured default.
+// The product path never reads the environment: a process changes a knob
+// only through mst_gpu_set_tuning (the A/B tools under tools/ and the
+// parity matrix of tests/ do; tools map their MST_* environment onto it).
+// Values are read per use with relaxed atomics, so a knob set before a call
+// holds for the whole call.
+enum Knob {
+  kKnobFilter,            // -1 auto (m >= 5n), 0 plain loop, 1 Filter-Boruvka
+  kKnobFilterBeta,        // light edges ~ beta * n
+  kKnobPivotSamples,      // sampled weights for the pivot
+  kKnobFilterTableMB,     // read-first filter off for min tables above this size
+  kKnobOfferMin1,         // offer modes per site (-1 default, 0/1/2, see filt_for)
+  kKnobOfferSplit,
+  kKnobOfferCount,
+  kKnobOfferHeavy,
+  kKnobPdl,               // programmatic dependent launch
+  kKnobTail,              // tail megakernel
+  kKnobTailEdges,         // tail entry edge bound (0: 12 M plain / 3 M light)
+  kKnobTailComps,         // tail entry component bound
+  kKnobTailSmallN,        // the tail also takes over below this many components
+  kKnobTailBps,           // tail CTAs per SM (capped by residency)
+  kKnobTailTiny,          // one-sync tiny rounds
+  kKnobTailTrace,         // globaltimer stamps of the tail phases (stderr)
+  kKnobTailStartC,        // round 1 handed to the tail at its phase C
+  kKnobTailStartCD,       // phase D's first round handed to the tail at phase C
+  kKnobTailStartCDEdges,
+  kKnobTailDedup,         // tagged pair dedup inside the tail
+  kKnobTailDedupRatio,
+  kKnobTailDedupMin,
+  kKnobDedup,             // pair dedup in the round kernels
+  kKnobDedupMinEdges,
+  kKnobDedupActive,
+  kKnobDedupTableDiv,
+  kKnobDedupRetry,
+  kKnobLazyRound1,
+  kKnobPipelineH2D,       // chunked host copy overlapping round 1's min pass
+  kKnobPipelineChunks,
+  kKnobDebugRounds,       // per-round counters on stderr
+  kKnobCount
+};
+struct KnobDef {
+  const char* name;
+  double dflt;
+};
+constexpr KnobDef kKnobDefs[kKnobCount] = {
+    {"MST_FILTER", -1},          {"MST_FILTER_BETA", 1.5},       {"MST_PIVOT_SAMPLES", 262144},
+    {"MST_FILTER_TABLE_MB", 1e7}, {"MST_OFFER_MIN1", -1},         {"MST_OFFER_SPLIT", -1},
+    {"MST_OFFER_COUNT", -1},     {"MST_OFFER_HEAVY", -1},        {"MST_PDL", 1},
+    {"MST_TAIL", 1},             {"MST_TAIL_EDGES", 0},          {"MST_TAIL_COMPS", 8e6},
+    {"MST_TAIL_SMALL_N", 65536}, {"MST_TAIL_BPS", MST_TAIL_MINB}, {"MST_TAIL_TINY", 1},
+    {"MST_TAIL_TRACE", 0},       {"MST_TAIL_START_C", 1},        {"MST_TAIL_START_C_D", 1},
+    {"MST_TAIL_START_C_D_EDGES", 1e12}, {"MST_TAIL_DEDUP", 0},   {"MST_TAIL_DEDUP_RATIO", 4},
+    {"MST_TAIL_DEDUP_MIN", 16384}, {"MST_DEDUP", 1},             {"MST_DEDUP_MIN_EDGES", 2e6},
+    {"MST_DEDUP_ACTIVE", 262144}, {"MST_DEDUP_TABLE_DIV", 4},    {"MST_DEDUP_RETRY", 0},
+    {"MST_LAZY_ROUND1", 1},      {"MST_PIPELINE_H2D", 0},        {"MST_PIPELINE_CHUNKS", 16},
+    {"MST_DEBUG_ROUNDS", 0}};
+
+std::atomic<double>* knob_table() {
+  static std::atomic<double> t[kKnobCount];
+  static std::once_flag once;
+  std::call_once(once, [] {
+    for (int k = 0; k < kKnobCount; ++k) t[k].store(kKnobDefs[k].dflt, std::memory_order_relaxed);
+  });
+  return t;
+}
+double knob(Knob k) { return knob_table()[k].load(std::memory_order_relaxed); }
+int knob_i(Knob k) { return (int)knob(k); }
+
 // ------------------------------- workspace ----------------------------------
 // One per (device, slot): named grow-only device buffers, a stream, pinned
 // counter snapshots and the look-back epoch. Reused across calls like a
@@ -116,6 +186,7 @@ struct Workspace {
   cudaEvent_t chunk_ev[16] = {};
   std::vector<cudaEvent_t> ev;    // per-round events
   std::vector<cudaEvent_t> tev;   // timing events (hot kernels)
+  cudaEvent_t join_in = nullptr, join_out = nullptr;  // ordering with the caller's legacy stream 0
 
   void init(int dev) {
     device = dev;
@@ -129,6 +200,8 @@ struct Workspace {
     tev.resize(4 * kMaxR + 8);
     for (auto& e : tev) MST_CUDA_CHECK(cudaEventCreate(&e));
     for (auto& e : stage_ev) MST_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    MST_CUDA_CHECK(cudaEventCreateWithFlags(&join_in, cudaEventDisableTiming));
+    MST_CUDA_CHECK(cudaEventCreateWithFlags(&join_out, cudaEventDisableTiming));
   }
 
   void* staging(int b) {
@@ -314,7 +387,7 @@ unsigned long long next_pow2(unsigned long long x) {
 // Read-before-atomic: always on by default. Even for DRAM-sized tables it
 // wins, because hub / giant-component entries are hot — unfiltered REDs to
 // one address serialise at its L2 slice (c4: 172 -> 53 ms with the filter).
-// MST_FILTER_TABLE_MB=<size> turns it off for tables above that size.
+// The MST_FILTER_TABLE_MB knob turns it off for tables above that size.
 // Offer mode per call site (kernels.cuh offer_both): 0 plain REDs, 1
 // read-first one offer at a time, 2 read-first with a thread's reads batched
 // (more memory-level parallelism; but a batch's reads all miss its own
@@ -327,18 +400,10 @@ unsigned long long next_pow2(unsigned long long x) {
 // c4 +1.7 %).
 enum OfferSite { kSiteMin1 = 0, kSiteSplit = 1, kSiteCount = 2, kSiteHeavy = 3, kSiteCount_ = 4 };
 int filt_for(uint64_t table_entries, int site = kSiteCount, bool dense = true) {
-  static const long long limit = [] {
-    const char* e = getenv("MST_FILTER_TABLE_MB");
-    return (long long)((e && *e) ? atof(e) : 1.0e7) << 20;
-  }();
-  auto env_mode = [](const char* name) {
-    const char* e = getenv(name);
-    return e && *e ? atoi(e) : -1;
-  };
-  // read per call (a few getenv per round), so a process can switch modes
-  const int mode[kSiteCount_] = {env_mode("MST_OFFER_MIN1"), env_mode("MST_OFFER_SPLIT"),
-                                 env_mode("MST_OFFER_COUNT"), env_mode("MST_OFFER_HEAVY")};
-  if (table_entries * 8 > (uint64_t)limit) return 0;
+  const double limit_mb = knob(kKnobFilterTableMB);
+  const int mode[kSiteCount_] = {knob_i(kKnobOfferMin1), knob_i(kKnobOfferSplit), knob_i(kKnobOfferCount),
+                                 knob_i(kKnobOfferHeavy)};
+  if ((double)table_entries * 8.0 > limit_mb * 1048576.0) return 0;
   if (mode[site] >= 0) return mode[site];
   switch (site) {
     case kSiteMin1:
@@ -385,14 +450,8 @@ void init_counters(Workspace& ws, DevCounters* d_ctr, uint32_t n, uint64_t m) {
 
 
 // Kernel launch with programmatic dependent launch (kernels.cuh pdl_prologue):
-// the next kernel's launch overlaps this one's tail. MST_PDL=0 disables it.
-bool pdl_enabled() {
-  static const int v = [] {
-    const char* e = getenv("MST_PDL");
-    return (e && *e) ? atoi(e) : 1;
-  }();
-  return v != 0;
-}
+// the next kernel's launch overlaps this one's tail. The MST_PDL knob = 0 disables it.
+bool pdl_enabled() { return knob_i(kKnobPdl) != 0; }
 
 template <typename... KArgs, typename... Args>
 void launch_k(void (*kernel)(KArgs...), unsigned grid, unsigned block, cudaStream_t s, Args... args) {
@@ -484,18 +543,8 @@ struct HotLaunch {
   bool light;
 };
 
-int env_int(const char* name, int dflt) {
-  const char* e = getenv(name);
-  return (e && *e) ? atoi(e) : dflt;
-}
-
-double env_double(const char* name, double dflt) {
-  const char* e = getenv(name);
-  return (e && *e) ? atof(e) : dflt;
-}
-
 bool filter_mode(uint32_t n, uint64_t m) {
-  const int f = env_int("MST_FILTER", -1);
+  const int f = knob_i(kKnobFilter);
   if (f >= 0) return f > 0 && m > 0;
   // m >= 5n: measured crossover (tools/filter_rule.py, one B200): uniform
   // m/n = 4 plain 0.65 vs filter 0.97 ms (c0), m/n = 6 0.92 vs 1.01, m/n = 8
@@ -623,14 +672,13 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     MST_CUDA_CHECK(cudaMemsetAsync(hist, 0, 65536 * sizeof(uint32_t), s));
     // 256 K sampled weights place a pivot at the ~beta*n/m quantile within
     // ~1 % (the light set's size is a tuning target, not a correctness one)
-    const uint32_t samples = (uint32_t)std::min<uint64_t>(m, (uint64_t)env_double("MST_PIVOT_SAMPLES", 262144));
+    const uint32_t samples = (uint32_t)std::min<uint64_t>(m, (uint64_t)knob(kKnobPivotSamples));
     const uint64_t step = std::max<uint64_t>(1, m / samples);
     launch_k(k_weight_hist, std::max(1u, samples / 1024), 256, s, wbase, wstride, m, step, samples, hist);
-    const double beta = env_double("MST_FILTER_BETA", 1.5);
+    const double beta = knob(kKnobFilterBeta);
     const double frac = std::min(1.0, beta * (double)n / (double)m);
     light_target = frac * (double)m;
-    const uint32_t target = (uint32_t)std::max(1.0, frac * samples);
-    launch_k(k_pick_pivot, 1, 1024, s, hist, target, d_ctr);
+    launch_k(k_pick_pivot, 1, 1024, s, hist, frac, d_ctr);
     launches += 2;
     hot_begin(kHotSplit, 0, true);
     launch_two_pass<InView, kModeLight>(ws, cb, in, nullptr, nullptr, E[1], minb[0], d_ctr, 0, m, n,
@@ -660,32 +708,32 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   int r = 1, loop_start = 1;
   int phase_end = 0;
   DevCounters snap_b{};  // counters at the end of the light phase
-  const bool tail_on = env_int("MST_TAIL", 1) != 0;
-  const bool dedup_on = env_int("MST_DEDUP", 1) != 0;
+  const bool tail_on = knob_i(kKnobTail) != 0;
+  const bool dedup_on = knob_i(kKnobDedup) != 0;
   // off by default: the tail's inserts are latency-bound at 2 CTAs/SM (c1
   // round 3: 106 us for 3.0 M edges), slower than what they save
-  const bool tail_dedup_on = dedup_on && env_int("MST_TAIL_DEDUP", 0) != 0;
-  const uint64_t dedup_min_edges = (uint64_t)env_double("MST_DEDUP_MIN_EDGES", 2.0e6);
-  const unsigned int dedup_active = (unsigned int)env_double("MST_DEDUP_ACTIVE", 262144);
+  const bool tail_dedup_on = dedup_on && knob_i(kKnobTailDedup) != 0;
+  const uint64_t dedup_min_edges = (uint64_t)knob(kKnobDedupMinEdges);
+  const unsigned int dedup_active = (unsigned int)knob(kKnobDedupActive);
   // low byte: table slots >= m_r / div; bit 8: retry after an overflowed
   // attempt without waiting for the K(K-1)/2 <= m_r/8 guarantee
-  const unsigned int pair_div = (unsigned int)std::max(1, std::min(255, env_int("MST_DEDUP_TABLE_DIV", 4))) |
-                                (env_int("MST_DEDUP_RETRY", 0) ? 0x100u : 0u);
+  const unsigned int pair_div = (unsigned int)std::max(1, std::min(255, knob_i(kKnobDedupTableDiv))) |
+                                (knob_i(kKnobDedupRetry) ? 0x100u : 0u);
   // Tail entry (m_bound is the host's one-round-stale edge bound). Measured
   // (tools/sweep_tail.sh, tools/sweep_tail2.sh): the plain loop and phase D
   // gain from entering early (12 M: c1's round 2 with 5.1 M edges runs in
   // the segmented tail, 0.631 -> 0.602 ms), the light phase from keeping the round kernels,
   // whose pair dedup the tail lacks, a little longer (c2: 3.02 ms at 3 M vs
   // 3.19 ms at 6 M).
-  const double tail_env = env_double("MST_TAIL_EDGES", 0.0);
-  const uint64_t tail_comps = (uint64_t)env_double("MST_TAIL_COMPS", 8.0e6);
+  const double tail_env = knob(kKnobTailEdges);
+  const uint64_t tail_comps = (uint64_t)knob(kKnobTailComps);
   // Few components but many edges (uniform graphs collapse their components
   // long before their edges): every offer of a round kernel then hits one of
   // a few thousand table entries and the atomics serialise (uniform m/n = 8:
   // ~0.7 ms per such round); the tail aggregates those offers per block in
   // shared memory (4.1 -> 1.2 ms). So the tail also takes over once
   // n_r <= tail_small_n, whatever the edge count.
-  const uint64_t tail_small_n = (uint64_t)env_double("MST_TAIL_SMALL_N", 65536);
+  const uint64_t tail_small_n = (uint64_t)knob(kKnobTailSmallN);
   auto tail_edges = [&]() -> uint64_t { return (uint64_t)(tail_env > 0 ? tail_env : (light ? 3.0e6 : 12.0e6)); };
 
   // Lazy round 1 (plain loop): round 1 stops after its count pass, whose
@@ -697,9 +745,9 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   // tail's first pass relabels + compacts + offers straight from the caller's
   // list, replacing round 1's count + emit passes.
   const bool start_c_ok = tail_on && !filter && std::is_same<InView, SoaView>::value &&
-                          env_int("MST_TAIL_START_C", 1) != 0 && m <= (32ull << 20) && n <= (16u << 20);
+                          knob_i(kKnobTailStartC) != 0 && m <= (32ull << 20) && n <= (16u << 20);
   bool tail_c_pending = false;
-  const bool lazy1 = !start_c_ok && !filter && env_int("MST_LAZY_ROUND1", 1) != 0 &&
+  const bool lazy1 = !start_c_ok && !filter && knob_i(kKnobLazyRound1) != 0 &&
                      !(tail_on && (m <= tail_edges() || (uint64_t)n <= tail_small_n) && (uint64_t)n <= tail_comps);
   const uint4* P1 = lazy1 ? reinterpret_cast<const uint4*>(ws.get<uint2>("pairs1", m)) : E[1];
 
@@ -775,14 +823,14 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       }
       auto kt = k_tail;
       const size_t tail_smem = 0;  // all static (< 48 KB)
-      const int bps = std::max(1, std::min(blocks_per_sm(kt, tail_smem), env_int("MST_TAIL_BPS", MST_TAIL_MINB)));
+      const int bps = std::max(1, std::min(blocks_per_sm(kt, tail_smem), knob_i(kKnobTailBps)));
       const unsigned G = std::min<unsigned>(kTailMaxBlocks, (unsigned)(sm_count(dev) * bps));
       uint32_t* broots = ws.get<uint32_t>("tail_broots", G);
       uint32_t* bkept = ws.get<uint32_t>("tail_bkept", G);
       uint32_t* tmasks = ws.get<uint32_t>("tail_masks", n_bound / 32 + 64);
       uint32_t* twpref = ws.get<uint32_t>("tail_wpref", n_bound / 32 + 64);
       unsigned long long* trace = nullptr;
-      if (env_int("MST_TAIL_TRACE", 0)) {
+      if (knob_i(kKnobTailTrace)) {
         trace = ws.get<unsigned long long>("tail_trace", 512);
         MST_CUDA_CHECK(cudaMemsetAsync(trace, 0, 512 * 8, s));
       }
@@ -791,7 +839,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
                   trace, 0, nullptr, nullptr, nullptr, 0, d_ctr, n, r, (int)light};
       ta.start_c = tail_c_pending ? 1 : 0;
       ta.c_soa = (tail_c_pending && r == 1) ? 1 : 0;
-      if (env_int("MST_TAIL_TINY", 1)) {
+      if (knob_i(kKnobTailTiny)) {
         // three rotating min tables for the one-sync rounds (k_tail "tiny")
         unsigned long long* tiny = ws.get<unsigned long long>("tail_tiny", 3 * kTailSmemMin);
         MST_CUDA_CHECK(cudaMemsetAsync(tiny, 0xFF, 3 * kTailSmemMin * sizeof(unsigned long long), s));
@@ -809,8 +857,8 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
         ta.pairs = pairs;
         ta.pair_cap = slots;
         ta.pair_epoch = ++ws.pair_epoch;
-        ta.dedup_ratio = (uint32_t)env_int("MST_TAIL_DEDUP_RATIO", 4);
-        ta.dedup_min = (uint32_t)env_double("MST_TAIL_DEDUP_MIN", 16384);
+        ta.dedup_ratio = (uint32_t)knob_i(kKnobTailDedupRatio);
+        ta.dedup_min = (uint32_t)knob(kKnobTailDedupMin);
       }
       if (src.kind == kSrcPacked) {
         ta.src_kind = kTailSrcPacked;
@@ -888,8 +936,8 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     // tail starts at its phase C over the heavy survivors in place (the host
     // knows only m here, not the survivor count: bounded by components;
     // c2 3.04 -> 2.97 ms, c3 neutral, c4's 47 M components excluded)
-    const bool d_start_c = tail_on && !light && phase_end && r == phase_end && env_int("MST_TAIL_START_C_D", 1) != 0 &&
-                           m_bound <= (uint64_t)env_double("MST_TAIL_START_C_D_EDGES", 1e12) &&
+    const bool d_start_c = tail_on && !light && phase_end && r == phase_end && knob_i(kKnobTailStartCD) != 0 &&
+                           m_bound <= (uint64_t)knob(kKnobTailStartCDEdges) &&
                            n_bound <= (16u << 20);
     if (!original_in && !lazy2 && !d_start_c && dedup_on && m_bound >= dedup_min_edges) {
       const unsigned long long cap = std::min<unsigned long long>(1ull << 25, next_pow2(m_bound / 2));
@@ -954,7 +1002,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   out.final_components = c.n[stop];
   out.count = (uint64_t)n - out.final_components;
   out.total_weight = c.total_weight;
-  if (env_int("MST_DEBUG_ROUNDS", 0)) {
+  if (knob_i(kKnobDebugRounds)) {
     for (int rr = 1; rr < stop && rr < kMaxR; ++rr)
       fprintf(stderr, "round %2d: n=%u m=%llu active=%u dedup=%u%s\n", rr, c.n[rr], (unsigned long long)c.m[rr],
               c.active[rr], c.dedup[rr], (phase_end && rr == phase_end) ? "  <- heavy survivors" : "");
@@ -1063,6 +1111,16 @@ RunOut run_single(const SingleArgs& a, mst_stats_t* stats) {
     ~Restore() { w.stream = s; }
   } restore{ws, saved};
   cudaStream_t s = ws.stream;
+  // Device input (or a device result) with no caller stream: the caller's
+  // work is on the legacy default stream 0, which the private non-blocking
+  // stream does not wait for. Join it both ways: the MST starts after the
+  // caller's earlier work (input writes, an L2 flush, a timing event) and
+  // stream 0's later work (timing events, consumers of the ids) waits for it.
+  const bool join_legacy = !a.user_stream && (a.on_device || a.device_out);
+  if (join_legacy) {
+    MST_CUDA_CHECK(cudaEventRecord(ws.join_in, cudaStreamLegacy));
+    MST_CUDA_CHECK(cudaStreamWaitEvent(s, ws.join_in, 0));
+  }
 
   cudaEvent_t e0, e1, e2, e3;
   e0 = ws.tev[ws.tev.size() - 4];
@@ -1081,7 +1139,7 @@ RunOut run_single(const SingleArgs& a, mst_stats_t* stats) {
   // 1.83 ms for three whole-array copies, more than the ~45 us they hide.
   CopyChunks chunks;
   const bool pipelined = !a.on_device && a.kind == 0 && a.m >= (4u << 20) && !filter_mode(a.n, a.m) &&
-                         env_int("MST_PIPELINE_H2D", 0) != 0 && host_is_pinned(a.src) && host_is_pinned(a.dst) &&
+                         knob_i(kKnobPipelineH2D) != 0 && host_is_pinned(a.src) && host_is_pinned(a.dst) &&
                          host_is_pinned(a.w);
   if (!a.on_device && a.m > 0) {
     if (a.kind == 0) {
@@ -1092,7 +1150,7 @@ RunOut run_single(const SingleArgs& a, mst_stats_t* stats) {
         // the copies may not overwrite the buffers before earlier work on
         // the compute stream is done with them
         MST_CUDA_CHECK(cudaStreamWaitEvent(ws.copy_stream, e0, 0));
-        const int want = std::max(1, std::min(CopyChunks::kMax, env_int("MST_PIPELINE_CHUNKS", 16)));
+        const int want = std::max(1, std::min(CopyChunks::kMax, knob_i(kKnobPipelineChunks)));
         const uint64_t per = std::max<uint64_t>(1u << 20, (a.m + want - 1) / want);
         chunks.count = (int)((a.m + per - 1) / per);
         for (int j = 0; j <= chunks.count; ++j) chunks.bound[j] = std::min<uint64_t>(a.m, (uint64_t)j * per);
@@ -1139,6 +1197,10 @@ RunOut run_single(const SingleArgs& a, mst_stats_t* stats) {
   if (!a.device_out && o.count)
     copy_d2h(ws, a.out_ids, d_sorted, o.count * 4);
   MST_CUDA_CHECK(cudaEventRecord(e3, s));
+  if (join_legacy) {
+    MST_CUDA_CHECK(cudaEventRecord(ws.join_out, s));
+    MST_CUDA_CHECK(cudaStreamWaitEvent(cudaStreamLegacy, ws.join_out, 0));
+  }
   MST_CUDA_CHECK(cudaStreamSynchronize(s));
   if (stats) {
     fill_stats(stats, o);
@@ -1172,6 +1234,7 @@ struct Shard {
   unsigned long long *xch = nullptr, *own = nullptr;
   uint32_t *parent = nullptr, *rootlabel = nullptr, *L = nullptr, *partner = nullptr, *mst = nullptr;
   uint32_t* hist = nullptr;  // Filter-Borůvka: weight histogram (summed across shards)
+  uint32_t* errw = nullptr;  // error bits as counts (summed across shards)
   uint4* E[2]{};
   DevCounters* d_ctr = nullptr;
   unsigned long long* st = nullptr;
@@ -1230,6 +1293,65 @@ struct NcclExchanger : Exchanger {
   }
 };
 
+// A caller-supplied collective (mst_collective_t: MPI, gloo, a test
+// harness): each exchange is staged through pinned host memory, reduced by
+// the callback in place across the ranks, and copied back. One local shard.
+struct CallbackExchanger : Exchanger {
+  mst_collective_t coll{};
+  void* host = nullptr;
+  size_t host_bytes = 0;
+  ~CallbackExchanger() override {
+    if (host) cudaFreeHost(host);
+  }
+  template <class T>
+  void run(std::vector<Shard>& sh, T* Shard::*buf, uint64_t count, int dtype, int op) {
+    if (count == 0) return;
+    Shard& s = sh.at(0);
+    const size_t bytes = count * sizeof(T);
+    if (bytes > host_bytes) {
+      MST_CUDA_CHECK(cudaStreamSynchronize(s.ws->stream));
+      if (host) MST_CUDA_CHECK(cudaFreeHost(host));
+      host = nullptr;
+      host_bytes = 0;
+      MST_CUDA_CHECK(cudaMallocHost(&host, bytes));
+      host_bytes = bytes;
+    }
+    MST_CUDA_CHECK(cudaMemcpyAsync(host, s.*buf, bytes, cudaMemcpyDeviceToHost, s.ws->stream));
+    MST_CUDA_CHECK(cudaStreamSynchronize(s.ws->stream));
+    const int rc = coll.allreduce(coll.ctx, host, count, dtype, op);
+    if (rc != 0)
+      throw MstError{MST_ERR_NCCL, "collective callback failed with status " + std::to_string(rc)};
+    MST_CUDA_CHECK(cudaMemcpyAsync(s.*buf, host, bytes, cudaMemcpyHostToDevice, s.ws->stream));
+  }
+  void min_u64(std::vector<Shard>& sh, unsigned long long* Shard::*buf, uint64_t count) override {
+    run(sh, buf, count, MST_DTYPE_U64, MST_OP_MIN);
+  }
+  void min_u32(std::vector<Shard>& sh, uint32_t* Shard::*buf, uint64_t count) override {
+    run(sh, buf, count, MST_DTYPE_U32, MST_OP_MIN);
+  }
+  void sum_u32(std::vector<Shard>& sh, uint32_t* Shard::*buf, uint64_t count) override {
+    run(sh, buf, count, MST_DTYPE_U32, MST_OP_SUM);
+  }
+};
+
+// NCCL communicators of the single-process multi-GPU entry, created once per
+// GPU count and kept for the life of the process (ncclCommInitAll costs
+// hundreds of milliseconds).
+std::vector<ncclComm_t>& cached_comms(int num_gpus) {
+  static std::mutex mu;
+  static std::map<int, std::vector<ncclComm_t>> cache;
+  std::lock_guard<std::mutex> g(mu);
+  auto& c = cache[num_gpus];
+  if (c.empty()) {
+    std::vector<ncclComm_t> comms(num_gpus);
+    std::vector<int> devs(num_gpus);
+    for (int i = 0; i < num_gpus; ++i) devs[i] = i;
+    MST_NCCL_CHECK(nccl().CommInitAll(comms.data(), num_gpus, devs.data()));
+    c = comms;
+  }
+  return c;
+}
+
 // The sharded loop (kernels.cuh "sharded exchange"). With filter, the
 // Filter-Borůvka phases run sharded too: the weight histograms are summed
 // across shards so every shard picks the same pivot, each shard splits and
@@ -1247,7 +1369,6 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, uint6
   if (filter) {
     // pivot from the summed histogram of every shard's weight sample
     const uint64_t total_samples_target = std::min<uint64_t>(m_total, 1u << 20);
-    uint64_t total_samples = 0;
     for (auto& s : sh) {
       MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
       s.hist = s.ws->get<uint32_t>("hist", 65536);
@@ -1257,17 +1378,17 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, uint6
       if (s.m) {
         const uint64_t step = std::max<uint64_t>(1, s.m / samples);
         launch_k(k_weight_hist, std::max(1u, samples / 1024), 256, s.ws->stream, s.in.w, 1u, s.m, step, samples, s.hist);
-        total_samples += samples;
       }
     }
     ex.sum_u32(sh, &Shard::hist, 65536);
-    const double beta = env_double("MST_FILTER_BETA", 1.5);
+    const double beta = knob(kKnobFilterBeta);
     const double frac = std::min(1.0, beta * (double)n / (double)std::max<uint64_t>(m_total, 1));
-    const uint32_t target = (uint32_t)std::max(1.0, frac * (double)total_samples);
     for (auto& s : sh) {
       MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
       Workspace& ws = *s.ws;
-      launch_k(k_pick_pivot, 1, 1024, ws.stream, s.hist, target, s.d_ctr);
+      // the target comes from the summed histogram's total (k_pick_pivot),
+      // identical on every rank
+      launch_k(k_pick_pivot, 1, 1024, ws.stream, s.hist, frac, s.d_ctr);
       const CompactBufs cb{ws.get<uint32_t>("tile_counts", tiles_c(s.m)),
                            ws.get<uint32_t>("tile_masks", tiles_c(s.m) * kCItems * kWarps), s.st,
                            ws.get<uint4>("stage", tiles_c(s.m) * kCTile)};
@@ -1284,23 +1405,39 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, uint6
       ++launches;
     }
   }
-  // errors (range) are checked before the first exchange
+  // errors (range / weight) are checked before the first key exchange, and
+  // summed across ranks first: a rank whose own slice is bad must not leave
+  // while the others wait in the collective
   for (auto& s : sh) {
     MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
-    MST_CUDA_CHECK(cudaMemcpyAsync(&s.ws->h_snap[0], s.d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost,
-                                   s.ws->stream));
-    MST_CUDA_CHECK(cudaStreamSynchronize(s.ws->stream));
-    if (s.ws->h_snap[0].err) {
-      out.err = s.ws->h_snap[0].err;
-      return;
-    }
+    s.errw = s.ws->get<uint32_t>("errw", 2);
+    launch_k(k_err_words, 1, 32, s.ws->stream, (const DevCounters*)s.d_ctr, s.errw);
   }
+  ex.sum_u32(sh, &Shard::errw, 2);
+  for (auto& s : sh) {
+    MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
+    uint32_t* h = reinterpret_cast<uint32_t*>(&s.ws->h_snap[0]);
+    MST_CUDA_CHECK(cudaMemcpyAsync(h, s.errw, 8, cudaMemcpyDeviceToHost, s.ws->stream));
+    MST_CUDA_CHECK(cudaStreamSynchronize(s.ws->stream));
+    const uint32_t err = (h[0] ? kErrRange : 0u) | (h[1] ? kErrWeight : 0u);
+    if (err) out.err = err;
+  }
+  if (out.err) return;
   bool light = filter;
   int R1 = 0;                  // first round after the heavy filter
+  int loop_start = 1;
   std::vector<int> levels;     // light rounds whose relabel map ("Llvl<r>") is kept
+  // The host runs one round ahead of the devices, as in the single-device
+  // loop: round r is enqueued with bounds from round r-2's counters (n and
+  // each shard's m only shrink), then round r-1's counters are read. The
+  // verdicts are replicated (same hook on the same all-reduced keys), so every
+  // rank takes the same branch and enqueues the same collectives; kernels of
+  // rounds past a stop or a light-phase end exit on the device counters, and
+  // an exchange whose count exceeds n_r only reduces entries nobody reads.
   uint64_t n_bound = n;
+  std::vector<uint64_t> m_bound(G);
+  for (int g = 0; g < G; ++g) m_bound[g] = sh[g].m;
   int r = 1;
-  int stop = 0;
   while (true) {
     if (r >= MST_MAX_ROUNDS) throw MstError{MST_ERR_STALL, "no convergence within MST_MAX_ROUNDS rounds"};
     // 1. local literal keys -> (w, global id) keys + owned partners; exchange.
@@ -1334,7 +1471,8 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, uint6
     ex.min_u32(sh, &Shard::partner, n_bound);
     launches += 2;
     // 2. replicated hook + label, local compaction (as the single-device loop)
-    for (auto& s : sh) {
+    for (int g = 0; g < G; ++g) {
+      Shard& s = sh[g];
       MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
       Workspace& ws = *s.ws;
       const int dev = ws.device;
@@ -1356,96 +1494,85 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, uint6
       uint32_t* Lr = light ? ws.get<uint32_t>("Llvl" + std::to_string(r), n_bound) : s.L;
       launch_k(k_label2, persistent_grid(k_label2, dev, ht), kBlock, st, s.parent, s.rootlabel, hmasks, hslot, hcounts, Lr,
                mnext, s.mst, (uint8_t*)nullptr, n, s.d_ctr, r, (unsigned long long*)nullptr, 0ull, 0u, 4u);
-      MST_CUDA_CHECK(cudaMemcpyAsync(&ws.h_snap[r], s.d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, st));
-      MST_CUDA_CHECK(cudaEventRecord(ws.ev[r], st));
-      const uint64_t m_bound = (r == 1 && !filter) ? s.m : (r == 1 || r == R1) ? s.m : ws.h_snap[r - 1].m[r];
       const CompactBufs cb{ws.get<uint32_t>("tile_counts", tiles_c(s.m)),
                            ws.get<uint32_t>("tile_masks", tiles_c(s.m) * kCItems * kWarps), s.st,
                            ws.get<uint4>("stage", tiles_c(s.m) * kCTile)};
       uint4* Eout = s.E[(r + 1) & 1];
       if (r == 1 && !filter)
-        launch_two_pass<SoaView, kModeRelabel>(ws, cb, s.in, s.E[1], Lr, Eout, mnext, s.d_ctr, r, m_bound, n,
+        launch_two_pass<SoaView, kModeRelabel>(ws, cb, s.in, s.E[1], Lr, Eout, mnext, s.d_ctr, r, m_bound[g], n,
                                                kSlotCompact, (int)kPhaseSharded, filt_for(n_bound, kSiteCount, filter));
       else
         launch_two_pass<PackedView, kModeRelabel>(ws, cb, PackedView{s.E[r & 1]}, s.E[r & 1], Lr, Eout, mnext,
-                                                  s.d_ctr, r, m_bound, n, kSlotCompact, (int)kPhaseSharded,
+                                                  s.d_ctr, r, m_bound[g], n, kSlotCompact, (int)kPhaseSharded,
                                                   filt_for(n_bound, kSiteCount, filter));
       launches += 5;
       MST_CUDA_CHECK(cudaGetLastError());
+      MST_CUDA_CHECK(cudaMemcpyAsync(&ws.h_snap[r], s.d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, st));
+      MST_CUDA_CHECK(cudaEventRecord(ws.ev[r], st));
     }
     if (light) levels.push_back(r);
-    // verdict after label (identical on every shard: replicated hook)
-    uint32_t verdict = kNoStop, pend = kNoStop;
-    uint32_t n_next = 0;
-    for (int g = 0; g < G; ++g) {
-      MST_CUDA_CHECK(cudaEventSynchronize(sh[g].ws->ev[r]));
-      const DevCounters& snap = sh[g].ws->h_snap[r];
-      if (g == 0) {
-        verdict = snap.stop_round;
-        pend = snap.phase_end;
-        n_next = snap.n[r + 1];
-      } else if (snap.stop_round != verdict || snap.phase_end != pend || snap.n[r + 1] != n_next) {
-        throw MstError{MST_ERR_STALL, "replicated hook diverged between shards"};
+    if (r > loop_start) {
+      // round r-1's verdict (identical on every shard: replicated hook)
+      for (int g = 0; g < G; ++g) {
+        MST_CUDA_CHECK(cudaEventSynchronize(sh[g].ws->ev[r - 1]));
+        const DevCounters& a = sh[0].ws->h_snap[r - 1];
+        const DevCounters& b = sh[g].ws->h_snap[r - 1];
+        if (b.err) out.err |= b.err;
+        if (b.stop_round != a.stop_round || b.phase_end != a.phase_end || b.n[r] != a.n[r])
+          throw MstError{MST_ERR_STALL, "replicated hook diverged between shards"};
       }
-    }
-    if (env_int("MST_DEBUG_ROUNDS", 0))
-      fprintf(stderr, "shard round %2d: n=%llu next=%u light=%d stop=%d phase_end=%d m0=%llu\n", r,
-              (unsigned long long)n_bound, n_next, (int)light, (int)verdict, (int)pend,
-              (unsigned long long)sh[0].ws->h_snap[r].m[r]);
-    if (verdict != kNoStop && (int)verdict <= r + 1) {
-      stop = (int)verdict;
-      break;
-    }
-    if (light && pend != kNoStop && (int)pend <= r) {
-      // light phase over at round r (no light edge left between components)
-      const int pe = (int)pend;
-      if (pe == 1) {
-        // not a single light hook: the plain sharded loop instead
+      const DevCounters& snap = sh[0].ws->h_snap[r - 1];
+      if (knob_i(kKnobDebugRounds))
+        fprintf(stderr, "shard round %2d: n=%u light=%d stop=%d phase_end=%d m0=%llu\n", r - 1, snap.n[r - 1],
+                (int)light, (int)snap.stop_round, (int)snap.phase_end, (unsigned long long)snap.m[r - 1]);
+      if (out.err) break;
+      if (snap.stop_round != kNoStop && (int)snap.stop_round <= r) break;
+      if (light && snap.phase_end != kNoStop && (int)snap.phase_end <= r) {
+        // light phase over (no light edge left between components)
+        const int pe = (int)snap.phase_end;
+        if (pe == 1) {
+          // not a single light hook: the plain sharded loop instead
+          for (auto& s : sh) {
+            MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
+            MST_CUDA_CHECK(cudaStreamSynchronize(s.ws->stream));
+          }
+          run_sharded_rounds(sh, ex, n, m_total, false, out);
+          out.launches += launches;
+          return;
+        }
+        while (!levels.empty() && levels.back() >= pe) levels.pop_back();
+        R1 = pe;
         for (auto& s : sh) {
           MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
-          MST_CUDA_CHECK(cudaStreamSynchronize(s.ws->stream));
+          Workspace& ws = *s.ws;
+          for (int k = (int)levels.size() - 2; k >= 0; --k) {
+            const unsigned gk = (unsigned)std::max<uint64_t>(
+                1, std::min<uint64_t>((snap.n[levels[k]] + 255) / 256, (uint64_t)sm_count(ws.device) * 8));
+            launch_k(k_compose, gk, 256, ws.stream, ws.get<uint32_t>("Llvl" + std::to_string(levels[k]), 1),
+                     (const uint32_t*)ws.get<uint32_t>("Llvl" + std::to_string(levels[k + 1]), 1), s.d_ctr, levels[k]);
+            ++launches;
+          }
+          const uint32_t* vlabel = levels.empty() ? nullptr : ws.get<uint32_t>("Llvl" + std::to_string(levels[0]), 1);
+          MST_CUDA_CHECK(cudaMemsetAsync(&s.d_ctr->phase_end, 0xFF, sizeof(unsigned int), ws.stream));
+          const CompactBufs cb{ws.get<uint32_t>("tile_counts", tiles_c(s.m)),
+                               ws.get<uint32_t>("tile_masks", tiles_c(s.m) * kCItems * kWarps), s.st,
+                               ws.get<uint4>("stage", tiles_c(s.m) * kCTile)};
+          // launched as round R1-1's producer: m[R1], E and the min table of round R1
+          launch_two_pass<SoaView, kModeHeavy>(ws, cb, s.in, nullptr, vlabel, s.E[R1 & 1], s.minb[(R1 - 1) & 1],
+                                               s.d_ctr, R1 - 1, s.m, n, kSlotFilter, (int)kPhaseSharded,
+                                               filt_for(snap.n[R1], kSiteHeavy));
+          launches += 2;
         }
-        run_sharded_rounds(sh, ex, n, m_total, false, out);
-        out.launches += launches;
-        return;
+        light = false;
+        n_bound = snap.n[R1];
+        for (int g = 0; g < G; ++g) m_bound[g] = sh[g].m;
+        r = R1;
+        loop_start = R1;
+        continue;
       }
-      while (!levels.empty() && levels.back() >= pe) levels.pop_back();
-      R1 = pe;
-      for (auto& s : sh) {
-        MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
-        Workspace& ws = *s.ws;
-        const DevCounters& snap = ws.h_snap[r];
-        for (int k = (int)levels.size() - 2; k >= 0; --k) {
-          const unsigned g = (unsigned)std::max<uint64_t>(
-              1, std::min<uint64_t>((snap.n[levels[k]] + 255) / 256, (uint64_t)sm_count(ws.device) * 8));
-          launch_k(k_compose, g, 256, ws.stream, ws.get<uint32_t>("Llvl" + std::to_string(levels[k]), 1),
-                   (const uint32_t*)ws.get<uint32_t>("Llvl" + std::to_string(levels[k + 1]), 1), s.d_ctr, levels[k]);
-          ++launches;
-        }
-        const uint32_t* vlabel = levels.empty() ? nullptr : ws.get<uint32_t>("Llvl" + std::to_string(levels[0]), 1);
-        MST_CUDA_CHECK(cudaMemsetAsync(&s.d_ctr->phase_end, 0xFF, sizeof(unsigned int), ws.stream));
-        const CompactBufs cb{ws.get<uint32_t>("tile_counts", tiles_c(s.m)),
-                             ws.get<uint32_t>("tile_masks", tiles_c(s.m) * kCItems * kWarps), s.st,
-                             ws.get<uint4>("stage", tiles_c(s.m) * kCTile)};
-        // launched as round R1-1's producer: m[R1], E and the min table of round R1
-        launch_two_pass<SoaView, kModeHeavy>(ws, cb, s.in, nullptr, vlabel, s.E[R1 & 1], s.minb[(R1 - 1) & 1], s.d_ctr,
-                                             R1 - 1, s.m, n, kSlotFilter, (int)kPhaseSharded, filt_for(snap.n[R1], kSiteHeavy));
-        launches += 2;
-        MST_CUDA_CHECK(cudaStreamSynchronize(ws.stream));
-      }
-      light = false;
-      n_bound = sh[0].ws->h_snap[r].n[R1];
-      r = R1;
-      continue;
+      n_bound = snap.n[r];
+      for (int g = 0; g < G; ++g) m_bound[g] = sh[g].ws->h_snap[r - 1].m[r];
     }
-    // the compaction's kept count m[r+1] sizes the next round's passes
-    for (auto& s : sh) {
-      MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
-      MST_CUDA_CHECK(cudaMemcpyAsync(&s.ws->h_snap[r], s.d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost,
-                                     s.ws->stream));
-      MST_CUDA_CHECK(cudaStreamSynchronize(s.ws->stream));
-    }
-    n_bound = n_next;
     ++r;
   }
   for (auto& s : sh) {
@@ -1466,6 +1593,9 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, uint6
   }
   out.err |= c.err;
   out.launches = launches;
+  if (out.err) return;
+  if (c.stop_round == kNoStop) throw MstError{MST_ERR_STALL, "sharded loop ended without a stop verdict"};
+  const int stop = (int)c.stop_round;
   out.rounds = (uint32_t)stop - 1;
   out.final_components = c.n[stop];
   out.count = (uint64_t)n - out.final_components;
@@ -1482,15 +1612,39 @@ struct PartSpec {
   int on_device;
 };
 
+// device_out: the sorted ids stay in HBM (out_ids is a device pointer on the
+// first shard's device). user_stream (one local shard only): run on the
+// caller's stream; nullptr with device input or output joins the legacy
+// stream 0 both ways (see run_single).
 RunOut run_sharded(const std::vector<PartSpec>& parts, Exchanger& ex, uint32_t n, uint64_t m_total,
-                   uint32_t* out_ids, mst_stats_t* stats) {
+                   uint32_t* out_ids, mst_stats_t* stats, bool device_out = false,
+                   cudaStream_t user_stream = nullptr) {
   const auto t_start = Clock::now();
   std::vector<Shard> sh(parts.size());
   std::vector<std::unique_lock<std::mutex>> locks;
+  struct Restore {
+    Workspace* w = nullptr;
+    cudaStream_t s = nullptr;
+    ~Restore() {
+      if (w) w->stream = s;
+    }
+  } restore;
+  bool join_legacy = false;
   for (size_t i = 0; i < parts.size(); ++i) {
     Workspace& ws = workspace(parts[i].device, parts[i].slot);
     locks.emplace_back(ws.mu);
     MST_CUDA_CHECK(cudaSetDevice(ws.device));
+    if (i == 0 && parts.size() == 1) {
+      if (user_stream) {
+        restore.w = &ws;
+        restore.s = ws.stream;
+        ws.stream = user_stream;
+      } else if (parts[0].on_device || device_out) {
+        join_legacy = true;
+        MST_CUDA_CHECK(cudaEventRecord(ws.join_in, cudaStreamLegacy));
+        MST_CUDA_CHECK(cudaStreamWaitEvent(ws.stream, ws.join_in, 0));
+      }
+    }
     Shard& s = sh[i];
     s.ws = &ws;
     s.m = parts[i].m;
@@ -1533,11 +1687,15 @@ RunOut run_sharded(const std::vector<PartSpec>& parts, Exchanger& ex, uint32_t n
   check_err_bits(o.err);
   Workspace& ws0 = *sh[0].ws;
   MST_CUDA_CHECK(cudaSetDevice(ws0.device));
-  uint32_t* d_sorted = ws0.get<uint32_t>("sorted", n);
+  uint32_t* d_sorted = device_out ? out_ids : ws0.get<uint32_t>("sorted", n);
   o.launches += sort_ids(ws0, sh[0].mst, o.count, std::max<uint64_t>(m_total, 1), d_sorted, sh[0].d_ctr);
   MST_CUDA_CHECK(cudaEventRecord(e2, ws0.stream));
-  if (o.count && out_ids)
+  if (o.count && out_ids && !device_out)
     copy_d2h(ws0, out_ids, d_sorted, o.count * 4);
+  if (join_legacy) {
+    MST_CUDA_CHECK(cudaEventRecord(ws0.join_out, ws0.stream));
+    MST_CUDA_CHECK(cudaStreamWaitEvent(cudaStreamLegacy, ws0.join_out, 0));
+  }
   for (auto& s : sh) {
     MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
     MST_CUDA_CHECK(cudaStreamSynchronize(s.ws->stream));
@@ -1597,14 +1755,17 @@ namespace {
 
 // verify.cuh: range, count, acyclic/spanning by a private concurrent
 // union-find, weight sum, and (with an oracle) weight + edge-set equality.
-template <class V>
-void run_verify(V g, uint32_t n, uint64_t m, int on_device, const uint32_t* ids, uint64_t count,
+// make_view(ws) stages host edges into verifier-private buffers (under the
+// same workspace lock as everything below) and returns the device view.
+template <class MakeView>
+void run_verify(MakeView make_view, uint32_t n, uint64_t m, int on_device, const uint32_t* ids, uint64_t count,
                 const uint32_t* oracle_ids, uint64_t oracle_count, uint64_t oracle_total, mst_verify_t* out) {
   const int dev = current_device_checked();
   Workspace& ws = workspace(dev, 0);
   std::lock_guard<std::mutex> lock(ws.mu);
   MST_CUDA_CHECK(cudaSetDevice(dev));
   cudaStream_t s = ws.stream;
+  const auto g = make_view(ws);
   if (!on_device) {
     if (count) {
       uint32_t* d = ws.get<uint32_t>("v_ids", count);
@@ -1630,7 +1791,7 @@ void run_verify(V g, uint32_t n, uint64_t m, int on_device, const uint32_t* ids,
   }
   const unsigned grid = (unsigned)sm_count(dev) * 8;
   kv_iota<<<grid, 256, 0, s>>>(parent, n);
-  if (count) kv_unite<V><<<grid, 256, 0, s>>>(g, m, ids, count, parent, bits_got, ctr);
+  if (count) kv_unite<<<grid, 256, 0, s>>>(g, n, m, ids, count, parent, bits_got, ctr);
   if (with_oracle) {
     if (oracle_count) kv_mark<<<grid, 256, 0, s>>>(oracle_ids, oracle_count, m, bits_ora, ctr);
     if (words4)
@@ -1641,7 +1802,8 @@ void run_verify(V g, uint32_t n, uint64_t m, int on_device, const uint32_t* ids,
   VerifyCounters h{};
   MST_CUDA_CHECK(cudaMemcpyAsync(&h, ctr, sizeof(h), cudaMemcpyDeviceToHost, s));
   MST_CUDA_CHECK(cudaStreamSynchronize(s));
-  if (h.range_err) throw MstError{MST_ERR_RANGE, "verify: an edge id lies outside [0, m)"};
+  if (h.range_err & 1u) throw MstError{MST_ERR_RANGE, "verify: an edge id lies outside [0, m)"};
+  if (h.range_err & 2u) throw MstError{MST_ERR_RANGE, "verify: an edge endpoint lies outside [0, n)"};
   out->edge_count_ok = count == (uint64_t)n - 1;
   out->components = (uint64_t)n - h.unions;
   out->is_acyclic = h.unions == count;
@@ -1694,16 +1856,7 @@ int mst_gpu_boruvka(const mst_edges_soa_t* edges, int num_gpus, uint32_t* out_id
                                               std::to_string(count) + " devices are visible"};
     (void)dev;
     NcclExchanger ex;
-    ex.comms.resize(num_gpus);
-    std::vector<int> devs(num_gpus);
-    for (int g = 0; g < num_gpus; ++g) devs[g] = g;
-    MST_NCCL_CHECK(nccl().CommInitAll(ex.comms.data(), num_gpus, devs.data()));
-    struct Destroy {
-      std::vector<ncclComm_t>& c;
-      ~Destroy() {
-        for (auto x : c) nccl().CommDestroy(x);
-      }
-    } destroy{ex.comms};
+    ex.comms = cached_comms(num_gpus);
     std::vector<PartSpec> parts;
     for (int g = 0; g < num_gpus; ++g) {
       const uint64_t lo = edges->m * g / num_gpus, hi = edges->m * (g + 1) / num_gpus;
@@ -1766,23 +1919,23 @@ int mst_gpu_verify(const mst_edges_soa_t* edges, const uint32_t* ids, uint64_t c
       throw MstError{MST_ERR_INVALID_ARG, "edge arrays are NULL"};
     if (count && !ids) throw MstError{MST_ERR_INVALID_ARG, "ids is NULL"};
     if (oracle_count && !oracle_ids) throw MstError{MST_ERR_INVALID_ARG, "oracle_ids is NULL"};
-    const int dev = current_device_checked();
-    const uint32_t *src = edges->src, *dst = edges->dst, *w = edges->w;
-    if (!edges->on_device && edges->m) {
-      Workspace& ws = workspace(dev, 0);
-      std::lock_guard<std::mutex> lock(ws.mu);
-      MST_CUDA_CHECK(cudaSetDevice(dev));
-      uint32_t* d_src = ws.get<uint32_t>("in_src", edges->m);
-      uint32_t* d_dst = ws.get<uint32_t>("in_dst", edges->m);
-      uint32_t* d_w = ws.get<uint32_t>("in_w", edges->m);
-      copy_h2d(ws, d_src, src, edges->m * 4);
-      copy_h2d(ws, d_dst, dst, edges->m * 4);
-      copy_h2d(ws, d_w, w, edges->m * 4);
-      src = d_src;
-      dst = d_dst;
-      w = d_w;
-    }
-    run_verify(VSoa{src, dst, w}, edges->n, edges->m, edges->on_device, ids, count, oracle_ids, oracle_count,
+    current_device_checked();
+    auto make_view = [&](Workspace& ws) {
+      const uint32_t *src = edges->src, *dst = edges->dst, *w = edges->w;
+      if (!edges->on_device && edges->m) {
+        uint32_t* d_src = ws.get<uint32_t>("v_src", edges->m);
+        uint32_t* d_dst = ws.get<uint32_t>("v_dst", edges->m);
+        uint32_t* d_w = ws.get<uint32_t>("v_w", edges->m);
+        copy_h2d(ws, d_src, src, edges->m * 4);
+        copy_h2d(ws, d_dst, dst, edges->m * 4);
+        copy_h2d(ws, d_w, w, edges->m * 4);
+        src = d_src;
+        dst = d_dst;
+        w = d_w;
+      }
+      return VSoa{src, dst, w};
+    };
+    run_verify(make_view, edges->n, edges->m, edges->on_device, ids, count, oracle_ids, oracle_count,
                oracle_total, report);
     set_last_error("");
     return MST_OK;
@@ -1798,17 +1951,17 @@ int mst_gpu_verify_aos(uint32_t n, uint64_t m, const mst_edge_t* edges, int on_d
     if (m && !edges) throw MstError{MST_ERR_INVALID_ARG, "edges is NULL"};
     if (count && !ids) throw MstError{MST_ERR_INVALID_ARG, "ids is NULL"};
     if (oracle_count && !oracle_ids) throw MstError{MST_ERR_INVALID_ARG, "oracle_ids is NULL"};
-    const int dev = current_device_checked();
-    const uint4* e4 = reinterpret_cast<const uint4*>(edges);
-    if (!on_device && m) {
-      Workspace& ws = workspace(dev, 0);
-      std::lock_guard<std::mutex> lock(ws.mu);
-      MST_CUDA_CHECK(cudaSetDevice(dev));
-      uint4* d = ws.get<uint4>("in_aos", m);
-      copy_h2d(ws, d, e4, m * 16);
-      e4 = d;
-    }
-    run_verify(VAos{e4}, n, m, on_device, ids, count, oracle_ids, oracle_count, oracle_total, report);
+    current_device_checked();
+    auto make_view = [&](Workspace& ws) {
+      const uint4* e4 = reinterpret_cast<const uint4*>(edges);
+      if (!on_device && m) {
+        uint4* d = ws.get<uint4>("v_aos", m);
+        copy_h2d(ws, d, e4, m * 16);
+        e4 = d;
+      }
+      return VAos{e4};
+    };
+    run_verify(make_view, n, m, on_device, ids, count, oracle_ids, oracle_count, oracle_total, report);
     set_last_error("");
     return MST_OK;
   });
@@ -1877,6 +2030,49 @@ int mst_gpu_boruvka_rank(mst_comm_t comm, uint32_t n, uint64_t m_total, uint64_t
   });
 }
 
+int mst_gpu_boruvka_rank_device(mst_comm_t comm, uint32_t n, uint64_t m_total, uint64_t shard_base,
+                                uint64_t shard_m, const uint32_t* d_src, const uint32_t* d_dst, const uint32_t* d_w,
+                                uint32_t* d_out_ids, void* stream, uint64_t* out_count, uint64_t* out_total_weight,
+                                mst_stats_t* stats) {
+  return guarded([&]() -> int {
+    if (!comm || !d_out_ids) throw MstError{MST_ERR_INVALID_ARG, "NULL argument"};
+    validate_common(n, m_total);
+    if (shard_base + shard_m > m_total) throw MstError{MST_ERR_INVALID_ARG, "shard outside [0, m_total)"};
+    if (shard_m && (!d_src || !d_dst || !d_w)) throw MstError{MST_ERR_INVALID_ARG, "edge arrays are NULL"};
+    current_device_checked();
+    MST_CUDA_CHECK(cudaSetDevice(comm->impl.device));
+    NcclExchanger ex;
+    ex.comms = {comm->impl.comm};
+    std::vector<PartSpec> parts{
+        PartSpec{comm->impl.device, 0, d_src, d_dst, d_w, shard_m, (uint32_t)shard_base, 1}};
+    RunOut o = run_sharded(parts, ex, n, m_total, d_out_ids, stats, true, (cudaStream_t)stream);
+    return finish_status(o, out_count, out_total_weight);
+  });
+}
+
+int mst_gpu_boruvka_rank_cb(const mst_collective_t* coll, uint32_t n, uint64_t m_total, uint64_t shard_base,
+                            uint64_t shard_m, const uint32_t* src, const uint32_t* dst, const uint32_t* w,
+                            int on_device, uint32_t* out_ids, uint64_t* out_count, uint64_t* out_total_weight,
+                            mst_stats_t* stats) {
+  return guarded([&]() -> int {
+    if (!coll || !coll->allreduce) throw MstError{MST_ERR_INVALID_ARG, "collective is NULL"};
+    if (coll->nranks < 1 || coll->rank < 0 || coll->rank >= coll->nranks)
+      throw MstError{MST_ERR_INVALID_ARG, "bad rank/nranks"};
+    validate_common(n, m_total);
+    if (shard_base + shard_m > m_total) throw MstError{MST_ERR_INVALID_ARG, "shard outside [0, m_total)"};
+    if (shard_m && (!src || !dst || !w)) throw MstError{MST_ERR_INVALID_ARG, "edge arrays are NULL"};
+    if (n > 1 && !out_ids) throw MstError{MST_ERR_INVALID_ARG, "out_ids is NULL"};
+    current_device_checked();
+    MST_CUDA_CHECK(cudaSetDevice(coll->device));
+    CallbackExchanger ex;
+    ex.coll = *coll;
+    std::vector<PartSpec> parts{
+        PartSpec{coll->device, 0, src, dst, w, shard_m, (uint32_t)shard_base, on_device}};
+    RunOut o = run_sharded(parts, ex, n, m_total, out_ids, stats);
+    return finish_status(o, out_count, out_total_weight);
+  });
+}
+
 int mst_gpu_boruvka_device(const mst_edges_soa_t* edges, uint32_t* d_out_ids, void* stream,
                            uint64_t* out_count, uint64_t* out_total_weight, mst_stats_t* stats,
                            double* ms_hot, uint32_t* hot_launches) {
@@ -1936,6 +2132,41 @@ int mst_gpu_round1_min(const mst_edges_soa_t* edges, uint64_t* out_min) {
     check_err_bits(ws.h_snap[0].err);
     return MST_OK;
   });
+}
+
+int mst_gpu_set_tuning(const char* name, double value) {
+  return guarded([&]() -> int {
+    if (!name) throw MstError{MST_ERR_INVALID_ARG, "tuning knob name is NULL"};
+    for (int k = 0; k < kKnobCount; ++k) {
+      if (std::strcmp(name, kKnobDefs[k].name) == 0) {
+        knob_table()[k].store(value, std::memory_order_relaxed);
+        return MST_OK;
+      }
+    }
+    throw MstError{MST_ERR_INVALID_ARG, std::string("unknown tuning knob: ") + name};
+  });
+}
+
+int mst_gpu_get_tuning(const char* name, double* out_value) {
+  return guarded([&]() -> int {
+    if (!name || !out_value) throw MstError{MST_ERR_INVALID_ARG, "NULL argument"};
+    for (int k = 0; k < kKnobCount; ++k) {
+      if (std::strcmp(name, kKnobDefs[k].name) == 0) {
+        *out_value = knob((Knob)k);
+        return MST_OK;
+      }
+    }
+    throw MstError{MST_ERR_INVALID_ARG, std::string("unknown tuning knob: ") + name};
+  });
+}
+
+int mst_gpu_reset_tuning(void) {
+  for (int k = 0; k < kKnobCount; ++k) knob_table()[k].store(kKnobDefs[k].dflt, std::memory_order_relaxed);
+  return MST_OK;
+}
+
+const char* mst_gpu_tuning_name(int index) {
+  return (index >= 0 && index < kKnobCount) ? kKnobDefs[index].name : nullptr;
 }
 
 int mst_gpu_release_workspace(void) {

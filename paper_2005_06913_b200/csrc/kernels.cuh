@@ -463,7 +463,10 @@ __global__ void k_weight_hist(const uint32_t* __restrict__ w, uint32_t wstride, 
   }
 }
 
-__global__ void __launch_bounds__(1024) k_pick_pivot(const uint32_t* __restrict__ hist, uint32_t target, DevCounters* ctr) {
+// target = max(1, frac * (sampled weights)), computed here from the
+// histogram's own total: in the sharded loop the histograms are summed
+// across ranks first, so every rank derives the same target and pivot.
+__global__ void __launch_bounds__(1024) k_pick_pivot(const uint32_t* __restrict__ hist, double frac, DevCounters* ctr) {
   pdl_prologue();
   // one block of 1024 threads: 64 bins per thread (16 independent 16 B loads
   // in flight, not 64 dependent ones), block scan of the sums, then the 64
@@ -491,6 +494,7 @@ __global__ void __launch_bounds__(1024) k_pick_pivot(const uint32_t* __restrict_
     s_sum[t] += v;
     __syncthreads();
   }
+  const uint32_t target = (uint32_t)fmax(1.0, frac * (double)s_sum[1023]);
   const uint32_t before = t ? s_sum[t - 1] : 0u;
   if (before < target && s_sum[t] >= target) {  // at most one thread
     s_tstar = t;
@@ -1113,7 +1117,7 @@ __global__ void __launch_bounds__(kBlock) k_shard_keys(View E, const unsigned lo
                                                        unsigned long long* __restrict__ xch,
                                                        unsigned long long* __restrict__ own, DevCounters* ctr, int r) {
   pdl_prologue();
-  if ((uint32_t)r >= ctr->stop_round) return;
+  if ((uint32_t)r >= ctr->stop_round || (uint32_t)r >= ctr->phase_end) return;
   const uint32_t n_r = ctr->n[r];
   for (uint64_t c = (uint64_t)blockIdx.x * kBlock + threadIdx.x; c < n_r; c += (uint64_t)gridDim.x * kBlock) {
     const unsigned long long key = __ldcs(minimum + c);
@@ -1133,7 +1137,7 @@ __global__ void __launch_bounds__(kBlock) k_shard_partner(const unsigned long lo
                                                           const unsigned long long* __restrict__ own,
                                                           uint32_t* __restrict__ partner, DevCounters* ctr, int r) {
   pdl_prologue();
-  if ((uint32_t)r >= ctr->stop_round) return;
+  if ((uint32_t)r >= ctr->stop_round || (uint32_t)r >= ctr->phase_end) return;
   const uint32_t n_r = ctr->n[r];
   for (uint64_t c = (uint64_t)blockIdx.x * kBlock + threadIdx.x; c < n_r; c += (uint64_t)gridDim.x * kBlock) {
     const unsigned long long x = __ldcs(xch + c), o = __ldcs(own + c);
@@ -1697,6 +1701,15 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
           (tiny_rounds == 0) ? mcur : (rr == 0 ? a.tiny[0] : rr == 1 ? a.tiny[1] : a.tiny[2]);
       unsigned long long* tnext = rr == 0 ? a.tiny[1] : rr == 1 ? a.tiny[2] : a.tiny[0];
       unsigned long long* tclear = rr == 0 ? a.tiny[2] : rr == 1 ? a.tiny[0] : a.tiny[1];
+      // the list ping-pongs between E and the other list (same segment
+      // bounds): every block gathers the min edges of ALL components from the
+      // list this round reads while other blocks already compact theirs, so a
+      // round may not overwrite the list it gathers from (the other list is
+      // free past round r0; ternaries on the kernel parameters keep this out
+      // of the register budget)
+      const bool flip = ((a.r0 ^ tiny_rounds) & 1) != 0;
+      const uint4* const Et = flip ? a.E[1] : a.E[0];
+      uint4* const Eo = flip ? a.E[0] : a.E[1];
       ++tiny_rounds;
       if (m_r == 0) {  // round r-1 kept no edge (scan_verdict)
         if (b == 0 && threadIdx.x == 0) a.ctr->stop_round = (uint32_t)r;
@@ -1714,7 +1727,7 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
         for (int k = 0; k < kItems; ++k) {  // the gathers of kItems components in flight together
           const uint32_t c = base + k * kBlock + threadIdx.x;
           key[k] = c < n_r ? s_min[c] : kNoKey;
-          e[k] = key[k] != kNoKey ? __ldcg(E + (uint32_t)key[k]) : make_uint4(0, 0, 0, 0);
+          e[k] = key[k] != kNoKey ? __ldcg(Et + (uint32_t)key[k]) : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
@@ -1803,7 +1816,7 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
           const uint64_t i = base + k * 32 + lane;
-          e[k] = i < seg_hi ? __ldcg(E + i) : make_uint4(0, 0, 0, 0);
+          e[k] = i < seg_hi ? __ldcg(Et + i) : make_uint4(0, 0, 0, 0);
           if (i < seg_hi) {
             const uint32_t ra = s_par[e[k].x], rb = s_par[e[k].y];
             e[k].x = s_wpre[ra >> 5] + __popc(s_mask[ra >> 5] & ((1u << (ra & 31)) - 1u));
@@ -1822,7 +1835,7 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
         for (int k = 0; k < kItems; ++k) {
           if (!f[k]) continue;
           const uint64_t j = out + rank[k];
-          E[j] = e[k];
+          Eo[j] = e[k];
           const unsigned long long key = ((unsigned long long)e[k].z << 32) | (uint32_t)j;
           if (key < s_min[e[k].x]) atomicMin(s_min + e[k].x, key);
           if (key < s_min[e[k].y]) atomicMin(s_min + e[k].y, key);
@@ -2155,6 +2168,13 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
     n_r = n_next;
     m_prev = m_r;
   }
+}
+
+// The error bits of a shard as one count per bit, so a sum-allreduce gives
+// every rank the union of all ranks' errors (they then stop together).
+__global__ void k_err_words(const DevCounters* ctr, uint32_t* __restrict__ out) {
+  pdl_prologue();
+  if (blockIdx.x == 0 && threadIdx.x < 2) out[threadIdx.x] = (ctr->err >> threadIdx.x) & 1u;
 }
 
 __global__ void k_iota(uint32_t* __restrict__ x, uint64_t count) {

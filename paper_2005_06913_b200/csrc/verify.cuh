@@ -69,8 +69,11 @@ __device__ __forceinline__ uint32_t v_find(uint32_t* parent, uint32_t x) {
 }
 
 // Range check, weight sum, union of the result edges and the result bitmap.
+// range_err bit 0: an id >= m; bit 1: an endpoint >= n (a malformed graph:
+// its union-find would index past parent[]).
 template <class V>
-__global__ void __launch_bounds__(256) kv_unite(V g, uint64_t m, const uint32_t* __restrict__ ids, uint64_t count,
+__global__ void __launch_bounds__(256) kv_unite(V g, uint32_t n, uint64_t m, const uint32_t* __restrict__ ids,
+                                                uint64_t count,
                                                 uint32_t* __restrict__ parent, uint32_t* __restrict__ bits,
                                                 VerifyCounters* ctr) {
   unsigned long long wsum = 0, unions = 0;
@@ -81,9 +84,14 @@ __global__ void __launch_bounds__(256) kv_unite(V g, uint64_t m, const uint32_t*
       bad = 1;
       continue;
     }
+    const uint32_t ea = g.a(e), eb = g.b(e);
+    if (ea >= n || eb >= n) {
+      bad |= 2;
+      continue;
+    }
     wsum += g.wt(e);
     if (bits) atomicOr(bits + (e >> 5), 1u << (e & 31));
-    uint32_t ra = v_find(parent, g.a(e)), rb = v_find(parent, g.b(e));
+    uint32_t ra = v_find(parent, ea), rb = v_find(parent, eb);
     while (ra != rb) {
       const uint32_t hi = ra > rb ? ra : rb, lo = ra > rb ? rb : ra;
       const uint32_t old = atomicCAS(parent + hi, hi, lo);
@@ -103,7 +111,7 @@ __global__ void __launch_bounds__(256) kv_unite(V g, uint64_t m, const uint32_t*
   if ((threadIdx.x & 31) == 0) {
     if (wsum) atomicAdd(&ctr->weight, wsum);
     if (unions) atomicAdd(&ctr->unions, unions);
-    if (bad) atomicOr(&ctr->range_err, 1u);
+    if (bad) atomicOr(&ctr->range_err, bad);
   }
 }
 

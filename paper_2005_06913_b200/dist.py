@@ -24,15 +24,13 @@ from .api import GpuRunInfo, MstResult, WorkerPanic, _finish
 # latency-bound rounds (c1: 0.69 ms for 8.4 M edges) and an edge-sharded run,
 # which adds two allreduces per round, cannot beat it: every rank then runs
 # the single-GPU MST of the whole graph (replicas, no data-path collective).
-# Larger graphs (c2-c4) are edge-sharded. MST_SHARD_MIN_EDGES overrides.
+# Larger graphs (c2-c4) are edge-sharded (bench.py --shard-min-edges overrides).
 SHARD_MIN_EDGES = 32 << 20
 
 
-def strategy(m: int, world: int) -> str:
+def strategy(m: int, world: int, min_edges: int | None = None) -> str:
     """'sharded' (edge slices + per-round allreduce) or 'replicated'."""
-    import os
-
-    thr = int(float(os.environ.get("MST_SHARD_MIN_EDGES", SHARD_MIN_EDGES)))
+    thr = SHARD_MIN_EDGES if min_edges is None else int(min_edges)
     return "sharded" if world > 1 and m >= thr else "replicated"
 
 
@@ -108,4 +106,69 @@ class RankComm:
         rc = L.lib().mst_gpu_boruvka_rank(self._h, n, m_total, shard_base, shard_m, ps, pd, pw,
                                           int(on_device), ids.ctypes.data, ctypes.byref(count),
                                           ctypes.byref(total), ctypes.byref(stats))
+        return _finish(rc, ids, count, total, stats, info)
+
+    def boruvka_device(self, n: int, m_total: int, shard_base: int, shard_m: int, ps: int, pd: int, pw: int,
+                       out_ptr: int, stream: int = 0, info: GpuRunInfo | None = None) -> tuple[int, int]:
+        """Sharded MST with this rank's slice in HBM and the sorted ids left
+        in HBM at out_ptr (n-1 u32): the device-resident multi-GPU entry.
+        Returns (count, total weight)."""
+        count, total = ctypes.c_uint64(0), ctypes.c_uint64(0)
+        stats = L.MstStats()
+        rc = L.lib().mst_gpu_boruvka_rank_device(self._h, n, m_total, shard_base, shard_m, ps, pd, pw, out_ptr,
+                                                 stream, ctypes.byref(count), ctypes.byref(total),
+                                                 ctypes.byref(stats))
+        _finish(rc, np.empty(0, dtype=np.uint32), count, total, stats, info)
+        return int(count.value), int(total.value)
+
+
+class HostCollective:
+    """mst_collective_t over torch.distributed on CPU tensors (gloo): every
+    exchange of the sharded loop is staged through host memory and reduced
+    by `dist.all_reduce` (the bring-your-own-collective entry,
+    mst_gpu_boruvka_rank_cb). Unsigned 64-bit keys are reduced as int64 with
+    the sign bit flipped, which maps unsigned order onto signed order."""
+
+    _SIGN = np.uint64(1 << 63)
+
+    def __init__(self, rank: int, world: int, device: int, group=None):
+        self.rank, self.world, self.device, self.group = rank, world, device, group
+        self.calls = 0
+        self._fn = L.ALLREDUCE_FN(self._allreduce)  # keep the thunk alive
+        self.c = L.MstCollective(self._fn, None, world, rank, device)
+
+    def _allreduce(self, ctx, buf, count, dtype, op) -> int:
+        import torch
+        import torch.distributed as dist
+        try:
+            self.calls += 1
+            if dtype == L.MST_DTYPE_U64:
+                a = np.ctypeslib.as_array(ctypes.cast(buf, ctypes.POINTER(ctypes.c_uint64)), shape=(count,))
+                t = torch.from_numpy((a ^ self._SIGN).view(np.int64).copy())
+            else:
+                a = np.ctypeslib.as_array(ctypes.cast(buf, ctypes.POINTER(ctypes.c_uint32)), shape=(count,))
+                t = torch.from_numpy(a.astype(np.int64))
+            red = dist.ReduceOp.MIN if op == L.MST_OP_MIN else dist.ReduceOp.SUM
+            dist.all_reduce(t, op=red, group=self.group)
+            r = t.numpy()
+            if dtype == L.MST_DTYPE_U64:
+                a[:] = r.view(np.uint64) ^ self._SIGN
+            else:
+                a[:] = r.astype(np.uint32)
+            return 0
+        except Exception:  # reported to the library as a failed collective
+            return 1
+
+    def boruvka(self, n: int, m_total: int, shard_base: int, src, dst, w,
+                info: GpuRunInfo | None = None) -> MstResult:
+        src = np.ascontiguousarray(src, dtype=np.uint32)
+        dst = np.ascontiguousarray(dst, dtype=np.uint32)
+        w = np.ascontiguousarray(w, dtype=np.uint32)
+        ids = np.empty(max(n - 1, 1), dtype=np.uint32)
+        count, total = ctypes.c_uint64(0), ctypes.c_uint64(0)
+        stats = L.MstStats()
+        rc = L.lib().mst_gpu_boruvka_rank_cb(ctypes.byref(self.c), n, m_total, shard_base, src.size,
+                                             src.ctypes.data if src.size else 0, dst.ctypes.data if dst.size else 0,
+                                             w.ctypes.data if w.size else 0, 0, ids.ctypes.data,
+                                             ctypes.byref(count), ctypes.byref(total), ctypes.byref(stats))
         return _finish(rc, ids, count, total, stats, info)

@@ -99,3 +99,23 @@ def test_generator_validation(lib):
         C.edge_count(C.uniform(10, 5, seed=0))  # m < n-1 cannot connect
     with pytest.raises(ValueError):
         C.edge_count(C.GenSpec(kind=7))
+
+
+def test_tuning_table(lib):
+    """Every engine knob sits in one table set through the ABI (the library
+    never reads the environment)."""
+    names = api.tuning_names()
+    assert "MST_FILTER" in names and "MST_TAIL" in names and len(names) == len(set(names))
+    assert api.get_tuning("MST_FILTER_BETA") == 1.5
+    with api.tuning(MST_FILTER_BETA=0.25, MST_TAIL=0):
+        assert api.get_tuning("MST_FILTER_BETA") == 0.25 and api.get_tuning("MST_TAIL") == 0
+    assert api.get_tuning("MST_FILTER_BETA") == 1.5 and api.get_tuning("MST_TAIL") == 1
+    with pytest.raises(ValueError, match="unknown tuning knob"):
+        api.set_tuning("MST_NO_SUCH_KNOB", 1)
+    applied = api.tuning_from_env({"MST_TAIL_TINY": "0", "PATH": "/bin"})
+    assert applied == {"MST_TAIL_TINY": 0.0} and api.get_tuning("MST_TAIL_TINY") == 0
+    lib.mst_gpu_reset_tuning()
+    assert api.get_tuning("MST_TAIL_TINY") == 1
+    import subprocess
+    out = subprocess.run(["grep", "-c", "getenv", str(L.PKG_DIR / "csrc" / "boruvka.cu")], capture_output=True, text=True)
+    assert out.stdout.strip() == "0", "the engine must not read the environment"

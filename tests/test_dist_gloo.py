@@ -117,14 +117,64 @@ def test_sharded_model_single_rank_matches_oracle(oracle_mod):
         # is exercised by the gloo test; here shards are emulated serially
 
 
-def test_bench_strategy_threshold(monkeypatch):
+def test_bench_strategy_threshold():
     """bench.py --gpus N: small graphs run replicas, large ones are sharded."""
     from paper_2005_06913_b200 import dist as D
-    monkeypatch.delenv("MST_SHARD_MIN_EDGES", raising=False)
     assert D.strategy(8_384_512, 8) == "replicated"      # c1
     assert D.strategy(4_000_000, 2) == "replicated"      # c0
     assert D.strategy(71_301_398, 2) == "sharded"        # c2
     assert D.strategy(268_435_456, 8) == "sharded"       # c3
     assert D.strategy(268_435_456, 1) == "replicated"    # one GPU: the single-GPU path
-    monkeypatch.setenv("MST_SHARD_MIN_EDGES", "1e6")
-    assert D.strategy(8_384_512, 2) == "sharded"
+    assert D.strategy(8_384_512, 2, min_edges=1_000_000) == "sharded"
+
+
+def _coll_worker(rank, world, port, queue):
+    import ctypes
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2005_06913_b200 import _lib as L
+    from paper_2005_06913_b200 import dist as D
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        coll = D.HostCollective(rank, world, device=0)
+        rng = np.random.default_rng(rank)
+        # u64 keys across the whole unsigned range, kNoKey (~0) included
+        k = rng.integers(0, 2**64 - 1, 1000, dtype=np.uint64, endpoint=True)
+        k[::7] = np.uint64(2**64 - 1)
+        k[3] = np.uint64(2**63)   # sign-bit patterns must order as unsigned
+        k[5] = np.uint64(2**63 - 1)
+        u = rng.integers(0, 2**32 - 1, 1000, dtype=np.uint64, endpoint=True).astype(np.uint32)
+        s = rng.integers(0, 1000, 1000).astype(np.uint32)
+        outs = {}
+        for name, arr, dt, op in (("k", k, L.MST_DTYPE_U64, L.MST_OP_MIN), ("u", u, L.MST_DTYPE_U32, L.MST_OP_MIN),
+                                  ("s", s, L.MST_DTYPE_U32, L.MST_OP_SUM)):
+            buf = arr.copy()
+            rc = coll.c.allreduce(None, buf.ctypes.data_as(ctypes.c_void_p), buf.size, dt, op)
+            outs[name] = (rc, buf, arr)
+        queue.put((rank, {n: (rc, b.tolist(), a.tolist()) for n, (rc, b, a) in outs.items()}))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_host_collective_reductions_two_ranks():
+    """dist.HostCollective (the mst_collective_t callback of the
+    bring-your-own-collective entry): unsigned u64 / u32 min and u32 sum
+    across two gloo ranks equal numpy's element-wise reductions."""
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_coll_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for name, red in (("k", np.minimum), ("u", np.minimum), ("s", np.add)):
+        dt = np.uint64 if name == "k" else np.uint32
+        a0, a1 = (np.array(got[r][name][2], dtype=dt) for r in (0, 1))
+        want = red(a0, a1).astype(dt)
+        for r in (0, 1):
+            rc, buf, _ = got[r][name]
+            assert rc == 0
+            assert np.array_equal(np.array(buf, dtype=dt), want), name

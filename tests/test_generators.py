@@ -77,3 +77,37 @@ def test_rmat_structure_and_skew():
     assert np.unique(pairs).size < m                 # duplicate pairs are kept
     g1 = C.generate_host(spec, threads=1)
     assert np.array_equal(g.src, g1.src) and np.array_equal(g.w, g1.w)
+
+
+@pytest.mark.parametrize("spec", [C.uniform(5000, 20000, seed=9), C.grid(33, 47, seed=1), C.rmat(13, 8, seed=4),
+                                  C.uniform(2, 1, seed=0), C.grid(1, 2, seed=3)], ids=lambda s: s.name)
+def test_oracle_generator_matches_product_bytes(spec, oracle_mod):
+    """The restated generator (oracle/gen_oracle.c: the checkers' input, no
+    product library) makes the product host generator's bytes exactly."""
+    g = C.generate_host(spec, threads=2)
+    assert oracle_mod.gen_count(spec) == g.edge_count()
+    n, s, d, w = oracle_mod.generate(spec, threads=3)
+    assert n == g.n
+    assert np.array_equal(s, g.src) and np.array_equal(d, g.dst) and np.array_equal(w, g.w)
+
+
+def test_golden_answers_pin_the_configs(oracle_mod):
+    """tests/golden/answers.json (tests/golden/make_answers.py): the input
+    hashes of the small configs still match the restated generator, and the
+    recorded answers are spanning trees of the right size."""
+    import hashlib
+    import json
+    from conftest import GOLDEN
+    ans = json.loads((GOLDEN / "answers.json").read_text())
+    assert set(ans) >= {"c0", "c1", "c2", "c3", "c4"}
+    for key in ("c0", "c1"):
+        a = ans[key]
+        n, s, d, w = oracle_mod.generate(C.CONFIGS[key])
+        assert (n, s.size) == (a["n"], a["m"])
+        for name, arr in (("src", s), ("dst", d), ("w", w)):
+            assert hashlib.sha256(arr.astype("<u4").tobytes()).hexdigest() == a[f"{name}_sha256"]
+        k = oracle_mod.kruskal(n, s, d, w)
+        assert hashlib.sha256(k.ids.astype("<u4").tobytes()).hexdigest() == a["ids_sha256"]
+        assert k.total_weight == a["total_weight"]
+    for a in ans.values():
+        assert a["count"] == a["n"] - 1

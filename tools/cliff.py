@@ -18,6 +18,7 @@ def main():
     for knobs in ({}, {"MST_DEDUP": "0"}, {"MST_TAIL_EDGES": "1.2e7"}, {"MST_TAIL_EDGES": "1.2e7", "MST_DEDUP": "0"},
                   {"MST_TAIL": "0"}):
         os.environ.update({"MST_FILTER": "0", **knobs})
+        P.api.tuning_from_env()
         info = P.GpuRunInfo()
         for _ in range(3):
             P.boruvka_gpu_device(n, m, s.data_ptr(), d.data_ptr(), w.data_ptr(), out.data_ptr(), st, info=info)

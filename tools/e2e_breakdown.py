@@ -18,6 +18,7 @@ def main():
     import numpy as np
     import torch
     import paper_2005_06913_b200 as P
+    P.api.tuning_from_env()  # MST_* knobs of the A/B scripts
     from paper_2005_06913_b200 import configs as C
 
     g0 = C.generate_host(C.CONFIGS[a.config])

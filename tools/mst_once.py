@@ -15,6 +15,7 @@ def main():
     a = p.parse_args()
     import torch
     import paper_2005_06913_b200 as P
+    P.api.tuning_from_env()  # MST_* knobs of the A/B scripts
     from paper_2005_06913_b200 import configs as C
 
     n, m, s, d, w = C.generate_torch(C.CONFIGS[a.config])

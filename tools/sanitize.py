@@ -24,6 +24,7 @@ def main():
         k = O.kruskal(g.n, g.src, g.dst, g.w)
         for mode in modes:
             os.environ.update(mode)
+            P.api.tuning_from_env()
             r = P.boruvka_gpu(g)
             for key in mode:
                 os.environ.pop(key)

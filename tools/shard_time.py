@@ -16,6 +16,7 @@ def main():
     a = p.parse_args()
     import numpy as np
     import paper_2005_06913_b200 as P
+    P.api.tuning_from_env()  # MST_* knobs of the A/B scripts
     from paper_2005_06913_b200 import configs as C
 
     g = C.generate_host(C.CONFIGS[a.config])
