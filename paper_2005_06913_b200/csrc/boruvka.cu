@@ -126,6 +126,7 @@ enum Knob {
   kKnobPipelineH2D,       // chunked host copy overlapping round 1's min pass
   kKnobPipelineChunks,
   kKnobDebugRounds,       // per-round counters on stderr
+  kKnobL2Fetch,           // cudaLimitMaxL2FetchGranularity in bytes (0: leave the device default)
   kKnobCount
 };
 struct KnobDef {
@@ -143,7 +144,7 @@ constexpr KnobDef kKnobDefs[kKnobCount] = {
     {"MST_TAIL_DEDUP_MIN", 16384}, {"MST_DEDUP", 1},             {"MST_DEDUP_MIN_EDGES", 2e6},
     {"MST_DEDUP_ACTIVE", 262144}, {"MST_DEDUP_TABLE_DIV", 4},    {"MST_DEDUP_RETRY", 0},
     {"MST_LAZY_ROUND1", 1},      {"MST_PIPELINE_H2D", 0},        {"MST_PIPELINE_CHUNKS", 16},
-    {"MST_DEBUG_ROUNDS", 0}};
+    {"MST_DEBUG_ROUNDS", 0},     {"MST_L2_FETCH", 0}};
 
 std::atomic<double>* knob_table() {
   static std::atomic<double> t[kKnobCount];
@@ -1097,9 +1098,30 @@ struct SingleArgs {
   bool time_hot;
 };
 
+// The L2 fetch granularity knob (a device-wide limit): applied when it
+// changes, per device.
+void apply_l2_fetch(int dev) {
+  static std::mutex mu;
+  static std::map<int, int> applied;
+  static std::map<int, size_t> dflt;
+  const int want = knob_i(kKnobL2Fetch);
+  std::lock_guard<std::mutex> g(mu);
+  auto it = applied.find(dev);
+  if (want <= 0 && it == applied.end()) return;
+  if (it != applied.end() && it->second == want) return;
+  if (!dflt.count(dev)) {
+    size_t d = 0;
+    MST_CUDA_CHECK(cudaDeviceGetLimit(&d, cudaLimitMaxL2FetchGranularity));
+    dflt[dev] = d;
+  }
+  MST_CUDA_CHECK(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, want > 0 ? (size_t)want : dflt[dev]));
+  applied[dev] = want;
+}
+
 RunOut run_single(const SingleArgs& a, mst_stats_t* stats) {
   const auto t_start = Clock::now();
   const int dev = current_device_checked();
+  apply_l2_fetch(dev);
   Workspace& ws = workspace(dev, 0);
   std::lock_guard<std::mutex> lock(ws.mu);
   MST_CUDA_CHECK(cudaSetDevice(dev));

@@ -8,21 +8,33 @@
 //
 //   mstbench_gpu generate --config c0..c4 --out PATH [--binary]
 //   mstbench_gpu run (--graph PATH | --config cN) --algo gpu[,gpu-device]
-//                    [--gpus 1,2,..] [--reps 5] [--warmup 1] [--verify] --csv OUT
-//   mstbench_gpu summarize --csv PATH
+//                    [--gpus 1,2,..] [--reps 5] [--warmup 1] [--verify]
+//                    [--oracle ANSWER] --csv OUT
+//   mstbench_gpu summarize --csv PATH [--baseline REF.csv]
 //   mstbench_gpu --list-presets
 //
 // Algorithms: "gpu" is mst_gpu_boruvka on host arrays (elapsed_ms = the
 // whole call, copies included, like boruvka_cas's elapsed_ms); "gpu-device"
 // keeps the edges resident in HBM and reports the device time of the MST.
 // --verify checks every trial with the GPU verifier (mst_gpu_verify): the
-// structural checks, plus weight and edge-set equality with the first
-// trial's result, which plays the role of the reference's once-computed
-// oracle; every row must also agree on the MST weight (bench.cpp:132-141).
+// structural checks (n-1 edges, acyclic, spanning) and, with --oracle, the
+// weight and the edge set against an answer file written by the pinned CPU
+// oracle (oracle/answer.py: Kruskal of oracle/mst_oracle.c), computed once
+// and reused for every trial like the reference's kruskal_oracle
+// (bench.cpp:96-102, 119-126). Every row must also agree on the MST weight
+// (bench.cpp:132-141). summarize prints per-(graph, algorithm, threads)
+// medians and, when sequential / CAS rows of the reference's own mstbench
+// are present (--baseline), the speedup table of bench.cpp:246-335 with the
+// GPU rows as the parallel algorithms.
+//
+// Answer file: "MSTANS01", u32 n, u32 0, u64 count, u64 total weight, then
+// count u32 edge ids in ascending order (little endian).
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <charconv>
+#include <cmath>
+#include <limits>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -177,6 +189,32 @@ std::vector<Row> read_csv(const std::string& path) {
   return rows;
 }
 
+struct Answer {
+  uint32_t n = 0;
+  uint64_t total = 0;
+  std::vector<uint32_t> ids;
+};
+
+Answer read_answer(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw UsageError("cannot open oracle answer " + path);
+  char magic[8];
+  uint32_t hdr[2];
+  uint64_t count = 0;
+  Answer a;
+  in.read(magic, 8);
+  in.read(reinterpret_cast<char*>(hdr), 8);
+  in.read(reinterpret_cast<char*>(&count), 8);
+  in.read(reinterpret_cast<char*>(&a.total), 8);
+  if (!in || std::memcmp(magic, "MSTANS01", 8) != 0) throw UsageError(path + ": not an MST answer file");
+  a.n = hdr[0];
+  if (count > (uint64_t)a.n) throw UsageError(path + ": corrupt answer (count > n)");
+  a.ids.resize(count);
+  in.read(reinterpret_cast<char*>(a.ids.data()), (std::streamsize)(count * 4));
+  if (!in) throw UsageError(path + ": truncated answer file");
+  return a;
+}
+
 struct Result {
   std::vector<uint32_t> ids;
   uint64_t total = 0;
@@ -270,8 +308,8 @@ void usage(std::ostream& o) {
   o << "Boruvka MST on B200: workload generator, benchmark runner, summary\n"
        "  mstbench_gpu generate --config c0..c4 --out PATH [--binary]\n"
        "  mstbench_gpu run (--graph PATH | --config cN) --algo gpu[,gpu-device] [--gpus 1,2,..]\n"
-       "                   [--reps 5] [--warmup 1] [--verify] --csv OUT\n"
-       "  mstbench_gpu summarize --csv PATH\n"
+       "                   [--reps 5] [--warmup 1] [--verify] [--oracle ANSWER] --csv OUT\n"
+       "  mstbench_gpu summarize --csv PATH [--baseline REF.csv]\n"
        "  mstbench_gpu --list-presets\n";
 }
 
@@ -305,6 +343,7 @@ int cmd_run(const Args& a) {
   const int warmup = a.has("--warmup") ? to_int(a.opt.at("--warmup"), "--warmup") : 1;
   if (reps < 1) throw UsageError("--reps must be >= 1");
   const bool verify = a.flag("--verify");
+  if (a.has("--oracle") && !verify) throw UsageError("--oracle needs --verify");
 
   HostGraph g;
   if (a.has("--config")) {
@@ -318,9 +357,17 @@ int cmd_run(const Args& a) {
             << ", library " << mst_gpu_version() << "\n";
   Runner runner(g);
   const mst_edges_soa_t host{g.n, g.m, g.src.data(), g.dst.data(), g.w.data(), 0};
-  std::vector<uint32_t> oracle_ids;
-  uint64_t oracle_total = 0;
-  bool have_oracle = false;
+  Answer oracle;
+  const bool have_oracle = a.has("--oracle");
+  if (have_oracle) {
+    oracle = read_answer(a.opt.at("--oracle"));
+    if (oracle.n != g.n)
+      throw UsageError("oracle answer is for n=" + std::to_string(oracle.n) + ", the graph has n=" + std::to_string(g.n));
+    std::cout << "# oracle: " << a.opt.at("--oracle") << " (" << oracle.ids.size() << " edges, weight " << oracle.total
+              << ")\n";
+  } else if (verify) {
+    std::cout << "# verify: structural checks only (no --oracle answer file)\n";
+  }
   std::vector<Row> rows;
   for (const std::string& algo : algos) {
     const std::vector<int> ts = algo == "gpu" ? gpus : std::vector<int>{1};
@@ -337,22 +384,20 @@ int cmd_run(const Args& a) {
         row.weight = res.total;
         row.rounds = res.rounds;
         if (verify) {
-          if (!have_oracle) {
-            oracle_ids = res.ids;
-            oracle_total = res.total;
-            have_oracle = true;
-          }
           mst_verify_t v{};
-          check(mst_gpu_verify(&host, res.ids.data(), res.ids.size(), oracle_ids.data(), oracle_ids.size(),
-                               oracle_total, &v),
+          check(mst_gpu_verify(&host, res.ids.data(), res.ids.size(), have_oracle ? oracle.ids.data() : nullptr,
+                               have_oracle ? oracle.ids.size() : 0, have_oracle ? oracle.total : MST_VERIFY_NO_ORACLE,
+                               &v),
                 "verify");
-          if (!(v.is_spanning && v.is_acyclic && v.edge_count_ok && v.weight_matches_oracle == 1 &&
-                v.edge_set_matches_oracle == 1))
+          const bool oracle_ok = !have_oracle || (v.weight_matches_oracle == 1 && v.edge_set_matches_oracle == 1);
+          if (!(v.is_spanning && v.is_acyclic && v.edge_count_ok && oracle_ok))
             throw VerifyError(g.name + "/" + algo + " T=" + std::to_string(t) + " trial " + std::to_string(trial) +
                               ": edges=" + std::to_string(res.ids.size()) + " (expected " + std::to_string(g.n - 1) +
                               "), weight=" + std::to_string(v.weight) + ", components=" +
                               std::to_string(v.components) + ", acyclic=" + (v.is_acyclic ? "yes" : "no") +
-                              ", edge_set=" + (v.edge_set_matches_oracle == 1 ? "match" : "MISMATCH"));
+                              ", edge_set=" +
+                              (!have_oracle ? "unchecked" : v.edge_set_matches_oracle == 1 ? "match" : "MISMATCH") +
+                              (have_oracle ? ", oracle weight=" + std::to_string(oracle.total) : std::string()));
           row.verified = true;
         }
         std::cout << row.graph << "," << row.algorithm << ",T=" << t << ",trial=" << trial << ": " << row.elapsed_ms
@@ -371,18 +416,68 @@ int cmd_run(const Args& a) {
   return kExitOk;
 }
 
+double median_of(std::vector<double> v) {
+  if (v.empty()) return std::numeric_limits<double>::quiet_NaN();
+  std::sort(v.begin(), v.end());
+  const size_t h = v.size() / 2;
+  return v.size() % 2 ? v[h] : (v[h - 1] + v[h]) / 2.0;
+}
+
+std::string cell(double v) {
+  if (std::isnan(v)) return "-";
+  char buf[32];
+  std::snprintf(buf, sizeof buf, "%.3f", v);
+  return buf;
+}
+
 int cmd_summarize(const Args& a) {
   if (!a.has("--csv")) throw UsageError("summarize: --csv is required");
-  const std::vector<Row> rows = read_csv(a.opt.at("--csv"));
+  std::vector<Row> rows = read_csv(a.opt.at("--csv"));
+  if (a.has("--baseline")) {
+    const std::vector<Row> base = read_csv(a.opt.at("--baseline"));
+    rows.insert(rows.end(), base.begin(), base.end());
+  }
   std::map<std::tuple<std::string, std::string, int>, std::vector<double>> by;
-  for (const Row& r : rows) by[{r.graph, r.algorithm, r.threads}].push_back(r.elapsed_ms);
+  std::vector<std::string> graph_order;
+  for (const Row& r : rows) {
+    if (std::find(graph_order.begin(), graph_order.end(), r.graph) == graph_order.end()) graph_order.push_back(r.graph);
+    by[{r.graph, r.algorithm, r.threads}].push_back(r.elapsed_ms);
+  }
   std::printf("%-16s %-12s %7s %7s %12s\n", "graph", "algorithm", "threads", "trials", "median_ms");
-  for (auto& [k, v] : by) {
-    std::sort(v.begin(), v.end());
-    const size_t h = v.size() / 2;
-    const double med = v.size() % 2 ? v[h] : (v[h - 1] + v[h]) / 2.0;
+  for (auto& [k, v] : by)
     std::printf("%-16s %-12s %7d %7zu %12.4f\n", std::get<0>(k).c_str(), std::get<1>(k).c_str(), std::get<2>(k),
-                v.size(), med);
+                v.size(), median_of(v));
+  // speedups against the reference's sequential and CAS rows
+  // (summarize_speedups / print_speedup_table, bench.cpp:246-335)
+  bool any = false;
+  for (const std::string& gname : graph_order) {
+    std::vector<double> seq, seq_opt;
+    double cas_best = std::numeric_limits<double>::quiet_NaN();
+    for (auto& [k, v] : by) {
+      if (std::get<0>(k) != gname) continue;
+      const std::string& algo = std::get<1>(k);
+      if (algo == "seq") seq.insert(seq.end(), v.begin(), v.end());
+      if (algo == "seq-opt") seq_opt.insert(seq_opt.end(), v.begin(), v.end());
+      if (algo == "cas") {
+        const double m = median_of(v);
+        if (std::isnan(cas_best) || m < cas_best) cas_best = m;
+      }
+    }
+    if (seq.empty() && seq_opt.empty() && std::isnan(cas_best)) continue;
+    if (!any) {
+      std::printf("\n%-16s %-12s %7s %12s %14s %14s\n", "graph", "algo", "threads", "vs_seq", "vs_seq_opt",
+                  "vs_best_cas");
+      any = true;
+    }
+    const double ms = median_of(seq), mo = median_of(seq_opt);
+    for (auto& [k, v] : by) {
+      if (std::get<0>(k) != gname) continue;
+      const std::string& algo = std::get<1>(k);
+      if (algo == "seq" || algo == "seq-opt") continue;
+      const double med = median_of(v);
+      std::printf("%-16s %-12s %7d %12s %14s %14s\n", gname.c_str(), algo.c_str(), std::get<2>(k),
+                  cell(ms / med).c_str(), cell(mo / med).c_str(), cell(cas_best / med).c_str());
+    }
   }
   return kExitOk;
 }
@@ -406,9 +501,10 @@ int main(int argc, char** argv) {
     }
     if (sub == "generate") return cmd_generate(Args(argc, argv, 2, {"--config", "--out"}, {"--binary"}));
     if (sub == "run")
-      return cmd_run(Args(argc, argv, 2, {"--graph", "--config", "--algo", "--gpus", "--reps", "--warmup", "--csv"},
+      return cmd_run(Args(argc, argv, 2,
+                          {"--graph", "--config", "--algo", "--gpus", "--reps", "--warmup", "--csv", "--oracle"},
                           {"--verify"}));
-    if (sub == "summarize") return cmd_summarize(Args(argc, argv, 2, {"--csv"}, {}));
+    if (sub == "summarize") return cmd_summarize(Args(argc, argv, 2, {"--csv", "--baseline"}, {}));
     throw UsageError("unknown subcommand '" + sub + "'");
   } catch (const UsageError& e) {
     std::cerr << "error: " << e.what() << "\n";
