@@ -122,6 +122,7 @@ enum Knob {
   kKnobDedupActive,
   kKnobDedupTableDiv,
   kKnobDedupRetry,
+  kKnobDedupMinRatio,     // dedup a round only when m_r >= ratio * active components
   kKnobLazyRound1,
   kKnobPipelineH2D,       // chunked host copy overlapping round 1's min pass
   kKnobPipelineChunks,
@@ -143,6 +144,7 @@ constexpr KnobDef kKnobDefs[kKnobCount] = {
     {"MST_TAIL_START_C_D_EDGES", 1e12}, {"MST_TAIL_DEDUP", 0},   {"MST_TAIL_DEDUP_RATIO", 4},
     {"MST_TAIL_DEDUP_MIN", 16384}, {"MST_DEDUP", 1},             {"MST_DEDUP_MIN_EDGES", 2e6},
     {"MST_DEDUP_ACTIVE", 262144}, {"MST_DEDUP_TABLE_DIV", 4},    {"MST_DEDUP_RETRY", 0},
+    {"MST_DEDUP_MIN_RATIO", 8},
     {"MST_LAZY_ROUND1", 1},      {"MST_PIPELINE_H2D", 0},        {"MST_PIPELINE_CHUNKS", 16},
     {"MST_DEBUG_ROUNDS", 0},     {"MST_L2_FETCH", 0}};
 
@@ -717,9 +719,11 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   const uint64_t dedup_min_edges = (uint64_t)knob(kKnobDedupMinEdges);
   const unsigned int dedup_active = (unsigned int)knob(kKnobDedupActive);
   // low byte: table slots >= m_r / div; bit 8: retry after an overflowed
-  // attempt without waiting for the K(K-1)/2 <= m_r/8 guarantee
+  // attempt without waiting for the K(K-1)/2 <= m_r/8 guarantee; bits
+  // 16-23: the minimum edges-per-active-component ratio of a dedup round
   const unsigned int pair_div = (unsigned int)std::max(1, std::min(255, knob_i(kKnobDedupTableDiv))) |
-                                (knob_i(kKnobDedupRetry) ? 0x100u : 0u);
+                                (knob_i(kKnobDedupRetry) ? 0x100u : 0u) |
+                                ((unsigned int)std::max(1, std::min(255, knob_i(kKnobDedupMinRatio))) << 16);
   // Tail entry (m_bound is the host's one-round-stale edge bound). Measured
   // (tools/sweep_tail.sh, tools/sweep_tail2.sh): the plain loop and phase D
   // gain from entering early (12 M: c1's round 2 with 5.1 M edges runs in

@@ -1306,7 +1306,7 @@ __global__ void MST_LB_(MST_MINB_LABEL) k_label2(uint32_t* __restrict__ parent, 
     // try again only once K(K-1)/2 pairs guarantee an 8x reduction;
     // R-MAT's repeated hub pairs keep succeeding and are not held back
     const bool doubtful = ctr->dedup_fail && K * (K - 1) / 2 > m_r / 8 && !(pair_div & 0x100u);
-    const bool use = K <= dedup_active && m_r >= 8 * K && m_r >= 4096 && !doubtful;
+    const bool use = K <= dedup_active && m_r >= ((pair_div >> 16) & 0xFFu) * K && m_r >= 4096 && !doubtful;
     unsigned long long P = 1024;
     while (P < m_r / (pair_div & 0xFFu) && P < pair_cap) P <<= 1;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
