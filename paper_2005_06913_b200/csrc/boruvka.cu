@@ -11,6 +11,7 @@
 #include <atomic>
 #include <chrono>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -123,11 +124,15 @@ enum Knob {
   kKnobDedupTableDiv,
   kKnobDedupRetry,
   kKnobDedupMinRatio,     // dedup a round only when m_r >= ratio * active components
+  kKnobDedupCapLog2,      // pair table slots <= 2^this
   kKnobLazyRound1,
   kKnobPipelineH2D,       // chunked host copy overlapping round 1's min pass
   kKnobPipelineChunks,
   kKnobDebugRounds,       // per-round counters on stderr
   kKnobL2Fetch,           // cudaLimitMaxL2FetchGranularity in bytes (0: leave the device default)
+  kKnobOfferCached,       // offer filter reads through L1 (bit kFiltCached) at these sites (bitmask of OfferSite)
+  kKnobRetire,            // light phase: retire isolated components (tables sized by components with edges)
+  kKnobTimeline,          // tools only: an event after every launch, per-launch stream times on stderr
   kKnobCount
 };
 struct KnobDef {
@@ -144,9 +149,10 @@ constexpr KnobDef kKnobDefs[kKnobCount] = {
     {"MST_TAIL_START_C_D_EDGES", 1e12}, {"MST_TAIL_DEDUP", 0},   {"MST_TAIL_DEDUP_RATIO", 4},
     {"MST_TAIL_DEDUP_MIN", 16384}, {"MST_DEDUP", 1},             {"MST_DEDUP_MIN_EDGES", 2e6},
     {"MST_DEDUP_ACTIVE", 262144}, {"MST_DEDUP_TABLE_DIV", 4},    {"MST_DEDUP_RETRY", 0},
-    {"MST_DEDUP_MIN_RATIO", 8},
+    {"MST_DEDUP_MIN_RATIO", 8},  {"MST_DEDUP_CAP_LOG2", 25},
     {"MST_LAZY_ROUND1", 1},      {"MST_PIPELINE_H2D", 0},        {"MST_PIPELINE_CHUNKS", 16},
-    {"MST_DEBUG_ROUNDS", 0},     {"MST_L2_FETCH", 0}};
+    {"MST_DEBUG_ROUNDS", 0},     {"MST_L2_FETCH", 0},         {"MST_OFFER_CACHED", 15},
+    {"MST_RETIRE", 1},                      {"MST_TIMELINE", 0}};
 
 std::atomic<double>* knob_table() {
   static std::atomic<double> t[kKnobCount];
@@ -180,6 +186,7 @@ struct Workspace {
   uint32_t pair_epoch = 0;
   size_t pair_slots = 0;
   DevCounters* h_snap = nullptr;  // pinned, kMaxR + 1 snapshots
+  unsigned int* h_u32 = nullptr;  // pinned, 16 words (single counters read mid-run)
   // pinned staging for pageable host buffers (two chunks, ping-pong)
   static constexpr size_t kStageBytes = 32u << 20;
   void* hstage[2] = {nullptr, nullptr};
@@ -198,6 +205,7 @@ struct Workspace {
     MST_CUDA_CHECK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
     for (auto& e : chunk_ev) MST_CUDA_CHECK(cudaEventCreate(&e));
     MST_CUDA_CHECK(cudaMallocHost(&h_snap, sizeof(DevCounters) * (kMaxR + 1)));
+    MST_CUDA_CHECK(cudaMallocHost(&h_u32, 16 * sizeof(unsigned int)));
     ev.resize(kMaxR + 1);
     for (auto& e : ev) MST_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     tev.resize(4 * kMaxR + 8);
@@ -402,7 +410,7 @@ unsigned long long next_pow2(unsigned long long x) {
 // phases, whose survivors concentrate on hubs (batched: c2 +3 %, c3 +1.5 %,
 // c4 +1.7 %).
 enum OfferSite { kSiteMin1 = 0, kSiteSplit = 1, kSiteCount = 2, kSiteHeavy = 3, kSiteCount_ = 4 };
-int filt_for(uint64_t table_entries, int site = kSiteCount, bool dense = true) {
+int filt_mode(uint64_t table_entries, int site, bool dense) {
   const double limit_mb = knob(kKnobFilterTableMB);
   const int mode[kSiteCount_] = {knob_i(kKnobOfferMin1), knob_i(kKnobOfferSplit), knob_i(kKnobOfferCount),
                                  knob_i(kKnobOfferHeavy)};
@@ -416,6 +424,10 @@ int filt_for(uint64_t table_entries, int site = kSiteCount, bool dense = true) {
     default:
       return 1;
   }
+}
+int filt_for(uint64_t table_entries, int site = kSiteCount, bool dense = true) {
+  const int f = filt_mode(table_entries, site, dense);
+  return (f != 0 && ((knob_i(kKnobOfferCached) >> site) & 1)) ? (f | kFiltCached) : f;
 }
 
 double ms_between(cudaEvent_t a, cudaEvent_t b) {
@@ -456,6 +468,39 @@ void init_counters(Workspace& ws, DevCounters* d_ctr, uint32_t n, uint64_t m) {
 // the next kernel's launch overlaps this one's tail. The MST_PDL knob = 0 disables it.
 bool pdl_enabled() { return knob_i(kKnobPdl) != 0; }
 
+// MST_TIMELINE (tools only): an event after every launch on the calling
+// thread, printed as stream-time offsets by run_single once the call is done.
+struct TimelineMark {
+  const void* fn;
+  cudaEvent_t ev;
+};
+thread_local std::vector<TimelineMark> t_timeline;
+thread_local std::vector<cudaEvent_t> t_timeline_pool;
+void timeline_mark(const void* fn, cudaStream_t s) {
+  if (!knob_i(kKnobTimeline)) return;
+  const size_t i = t_timeline.size();
+  if (i >= t_timeline_pool.size()) {
+    cudaEvent_t e;
+    MST_CUDA_CHECK(cudaEventCreate(&e));
+    t_timeline_pool.push_back(e);
+  }
+  MST_CUDA_CHECK(cudaEventRecord(t_timeline_pool[i], s));
+  t_timeline.push_back(TimelineMark{fn, t_timeline_pool[i]});
+}
+void timeline_print(cudaEvent_t start) {
+  if (t_timeline.empty()) return;
+  float prev = 0;
+  for (const TimelineMark& m : t_timeline) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, start, m.ev);
+    const char* name = "(mark)";
+    if (m.fn) cudaFuncGetName(&name, m.fn);
+    fprintf(stderr, "timeline %9.1f us  +%8.1f  %s\n", ms * 1e3, (ms - prev) * 1e3, name);
+    prev = ms;
+  }
+  t_timeline.clear();
+}
+
 template <typename... KArgs, typename... Args>
 void launch_k(void (*kernel)(KArgs...), unsigned grid, unsigned block, cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg{};
@@ -469,6 +514,7 @@ void launch_k(void (*kernel)(KArgs...), unsigned grid, unsigned block, cudaStrea
   cfg.attrs = &attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
   MST_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+  timeline_mark(reinterpret_cast<const void*>(kernel), s);
 }
 
 // Sorted id list from the per-edge flags the hook kernels set.
@@ -576,7 +622,7 @@ void launch_two_pass(Workspace& ws, const CompactBufs& cb, View in, uint4* relab
   const uint64_t tiles = tiles_c(m_bound);
   const int fused = tiles <= kFusedScanMaxTiles ? 1 : 0;  // small: the last count block scans
   const bool armed = kMode == kModeRelabel && !View::kOriginal && pt.pairs != nullptr;
-  auto kcnt = filt == 2 ? k_count<View, kMode, true> : k_count<View, kMode, false>;
+  auto kcnt = (filt & 3) == 2 ? k_count<View, kMode, true> : k_count<View, kMode, false>;
   const unsigned gc = (unsigned)std::max<uint64_t>(
       1, std::min<uint64_t>(tiles, (uint64_t)sm_count(dev) * blocks_per_sm(kcnt)));
   // armed: this launch relabels + inserts pairs if the device chose dedup
@@ -610,7 +656,7 @@ void launch_two_pass(Workspace& ws, const CompactBufs& cb, View in, uint4* relab
     auto kem = k_emit<View, kMode>;
     launch_k(kem, ge, kBlock, ws.stream, in, relabeled, L, cb.masks, cb.counts, out, d_ctr, r, armed ? 1 : 0, n_orig);
   } else {
-    auto kes = filt == 2 ? k_emit_staged<kMode, true> : k_emit_staged<kMode, false>;
+    auto kes = (filt & 3) == 2 ? k_emit_staged<kMode, true> : k_emit_staged<kMode, false>;
     launch_k(kes, ge, kBlock, ws.stream, cb.stage, cb.counts, out, min_next, d_ctr, r, filt);
   }
   MST_CUDA_CHECK(cudaGetLastError());
@@ -631,9 +677,15 @@ struct CopyChunks {
   cudaEvent_t ev[kMax];
 };
 
+// `enqueue_after` (optional) is enqueued on the stream right behind the last
+// round, before the one host sync that reads the verdict: the sorted output
+// and its copy-back need no host decision, so they follow the MST without a
+// host round trip (the verdict is checked after the sync; an error discards
+// them).
 template <class InView>
 void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t wstride, uint32_t n,
-                     uint64_t m, RunOut& out, bool time_hot, bool filter, const CopyChunks* chunks = nullptr) {
+                     uint64_t m, RunOut& out, bool time_hot, bool filter, const CopyChunks* chunks = nullptr,
+                     const std::function<void()>* enqueue_after = nullptr) {
   cudaStream_t s = ws.stream;
   auto* d_ctr = ws.get<DevCounters>("ctr", 1);
   unsigned long long* minb[2] = {ws.get<unsigned long long>("minA", n),
@@ -658,6 +710,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   MST_CUDA_CHECK(cudaMemsetAsync(minb[0], 0xFF, (size_t)n * 8, s));
   uint8_t* flags = ws.get<uint8_t>("mst_flags", m + 16);
   MST_CUDA_CHECK(cudaMemsetAsync(flags, 0, m + 16, s));
+  timeline_mark(nullptr, s);
   uint32_t launches = 0;
   int tix = 0;
   std::vector<HotLaunch> hot;
@@ -707,6 +760,17 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
 
   bool light = filter;
   std::vector<std::pair<uint32_t*, int>> levels;  // light-phase relabel maps (buffer, round)
+  // Retirement (kernels.cuh, k_ret_*): the light rounds run by the round
+  // kernels retire their isolated components into bitmap regions, one per
+  // round (sized by the host's bound on n_r), then the final region. R-MAT's
+  // light phase: 44 M of c4's 67 M vertices have no light edge, so from round
+  // 2 on the per-component tables cover ~5 M instead of ~49 M components.
+  const bool retire_ok = filter && knob_i(kKnobRetire) != 0 && n < (1u << 31);
+  const uint64_t ret_region = ((uint64_t)n + 31) / 32 + 1;  // words: one region's bound
+  constexpr uint64_t kRetRegions = 5;
+  uint32_t* ret_bits = retire_ok ? ws.get<uint32_t>("ret_bits", kRetRegions * ret_region) : nullptr;
+  std::vector<std::pair<int, uint64_t>> ret_woff;  // (round, first word) of each retiring round
+  uint64_t ret_used = 0;
   uint64_t n_bound = n, m_bound = m;
   int r = 1, loop_start = 1;
   int phase_end = 0;
@@ -766,17 +830,49 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       // not a single light non-loop edge: run the plain loop instead
       MST_CUDA_CHECK(cudaStreamSynchronize(s));
       RunOut plain;
-      run_single_impl<InView>(ws, in, wbase, wstride, n, m, plain, time_hot, false);
+      run_single_impl<InView>(ws, in, wbase, wstride, n, m, plain, time_hot, false, nullptr, enqueue_after);
       plain.launches += launches;
       out = plain;
       return false;
     }
     while (!levels.empty() && levels.back().second >= phase_end) levels.pop_back();
-    for (int k = (int)levels.size() - 2; k >= 0; --k) {
-      const unsigned g = (unsigned)std::max<uint64_t>(
-          1, std::min<uint64_t>((snap.n[levels[k].second] + 255) / 256, (uint64_t)sm_count(dev) * 8));
-      launch_k(k_compose, g, 256, s, levels[k].first, levels[k + 1].first, d_ctr, levels[k].second);
-      ++launches;
+    while (!ret_woff.empty() && ret_woff.back().first >= phase_end) ret_woff.pop_back();
+    const bool retired = !ret_woff.empty() && !levels.empty();
+    if (retired) {
+      // final region: one bit per component labelled at the phase end; the
+      // rank of a bit over all regions is the final label; the total is n[P]
+      const int P = phase_end;
+      const uint64_t woff_final = ret_used;  // after every region handed out (dropped rounds' are zero)
+      MST_CUDA_CHECK(cudaMemsetAsync(ret_bits + woff_final, 0, ret_region * 4, s));
+      launch_k(k_ret_fill_final, (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ret_region / 256 + 1, 4096)), 256,
+               s, ret_bits + woff_final, d_ctr, P);
+      const uint64_t W = woff_final + ret_region;
+      uint32_t* prefix = ws.get<uint32_t>("ret_prefix", W);
+      launch_k(k_ret_popc, (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(W / 256 + 1, (uint64_t)sm_count(dev) * 8)),
+               256, s, (const uint32_t*)ret_bits, W, prefix);
+      launch_k(k_scan_counts<kScanDense>,
+               (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((W + kScanTile - 1) / kScanTile, (uint64_t)sm_count(dev))),
+               kScanBlock, s, prefix, W, d_ctr, P, st, ws.next_epoch(), 0, 0);
+      for (int k = (int)levels.size() - 1; k >= 0; --k) {
+        uint64_t woff = 0;
+        for (const auto& rw : ret_woff)
+          if (rw.first == levels[k].second) woff = rw.second;
+        const uint32_t* Lnext = k + 1 < (int)levels.size() ? levels[k + 1].first : nullptr;
+        const unsigned g = (unsigned)std::max<uint64_t>(
+            1, std::min<uint64_t>((snap.n[levels[k].second] + 1023) / 1024, (uint64_t)sm_count(dev) * 8));
+        launch_k(k_compose_ret, g, 256, s, levels[k].first, Lnext, (const uint32_t*)ret_bits, (const uint32_t*)prefix,
+                 woff, woff_final, d_ctr, levels[k].second);
+      }
+      // the heavy filter offers into this table for all n[P] components
+      launch_k(k_fill_keys, (unsigned)(sm_count(dev) * 8), 256, s, minb[(P - 1) & 1], d_ctr, P);
+      launches += 5 + (uint32_t)levels.size();
+    } else {
+      for (int k = (int)levels.size() - 2; k >= 0; --k) {
+        const unsigned g = (unsigned)std::max<uint64_t>(
+            1, std::min<uint64_t>((snap.n[levels[k].second] + 255) / 256, (uint64_t)sm_count(dev) * 8));
+        launch_k(k_compose, g, 256, s, levels[k].first, levels[k + 1].first, d_ctr, levels[k].second);
+        ++launches;
+      }
     }
     const uint32_t* vlabel = levels.empty() ? nullptr : levels[0].first;
     MST_CUDA_CHECK(cudaMemsetAsync(&d_ctr->phase_end, 0xFF, sizeof(unsigned int), s));
@@ -790,7 +886,13 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     light = false;
     r = R1;
     loop_start = R1;
+    // retirement: n[R1] (all final components) was counted on the device
     n_bound = snap.n[R1];
+    if (retired) {
+      MST_CUDA_CHECK(cudaMemcpyAsync(ws.h_u32, &d_ctr->n[R1], sizeof(unsigned int), cudaMemcpyDeviceToHost, s));
+      MST_CUDA_CHECK(cudaStreamSynchronize(s));
+      n_bound = ws.h_u32[0];
+    }
     m_bound = m;
     return true;
   };
@@ -810,6 +912,11 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   while (true) {
     if (r > MST_MAX_ROUNDS) throw MstError{MST_ERR_STALL, "no convergence within MST_MAX_ROUNDS rounds"};
     const bool original_in = (r == 1 && !filter);
+    // after retirement n_bound counts the light components with edges only:
+    // few of them can still carry millions of edges, which the round
+    // kernels' pair dedup collapses and the tail would not (c3: 4 tail
+    // rounds over ~9 M edges, +0.8 ms), so the small-n rule stays off there
+    const bool retiring = light && !ret_woff.empty();
     // round 1 of the light phase: the split keeps ~beta*n edges (the pivot's
     // target), a better bound than m before its count is known
     const uint64_t m_est = (light && r == 1) ? std::min<uint64_t>(m_bound, (uint64_t)(1.1 * light_target)) : m_bound;
@@ -817,7 +924,8 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     // n_r is huge (c4's light phase ends with 47 M components and 406 edges:
     // 1.2 ms in the tail vs 0.3 ms of round kernels)
     if (tail_c_pending ||
-        (tail_on && !original_in && (m_est <= tail_edges() || n_bound <= tail_small_n) && n_bound <= tail_comps)) {
+        (tail_on && !original_in && (m_est <= tail_edges() || (n_bound <= tail_small_n && !retiring)) &&
+         n_bound <= tail_comps)) {
       // ---- all remaining rounds in one cooperative launch
       uint32_t* M = nullptr;
       if (light) {
@@ -843,6 +951,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       TailArgs ta{{E[0], E[1]}, {minb[0], minb[1]}, parent, rootlabel, L, mst, broots, bkept, tmasks, twpref, M, flags,
                   trace, 0, nullptr, nullptr, nullptr, 0, d_ctr, n, r, (int)light};
       ta.start_c = tail_c_pending ? 1 : 0;
+      ta.retired = (light && !ret_woff.empty()) ? 1 : 0;
       ta.c_soa = (tail_c_pending && r == 1) ? 1 : 0;
       if (knob_i(kKnobTailTiny)) {
         // three rotating min tables for the one-sync rounds (k_tail "tiny")
@@ -885,8 +994,12 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       void* args[] = {&ta};
       hot_begin(kHotTail, r, light);
       MST_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)kt, G, kBlock, args, tail_smem, s));
+      timeline_mark((const void*)kt, s);
       ++launches;
       tmark();
+      // outside the light phase the tail runs the loop to its verdict (stop,
+      // error or stall), which the epilogue reads after its one sync
+      if (!light && !trace) break;
       MST_CUDA_CHECK(cudaMemcpyAsync(&ws.h_snap[kMaxR - 1], d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
       MST_CUDA_CHECK(cudaStreamSynchronize(s));
       const DevCounters& snap = ws.h_snap[kMaxR - 1];
@@ -908,14 +1021,26 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     unsigned long long* mcur = minb[(r - 1) & 1];
     unsigned long long* mnext = minb[r & 1];
     uint4* Eout = E[(r + 1) & 1];
+    uint32_t* rb = nullptr;  // this round's retirement region (light phase)
     {
       const uint64_t ht = tiles_of(n_bound);
       const int hfused = ht <= kFusedScanMaxTiles ? 1 : 0;
       const HookSrc src = hook_src(r);
+      // a light round retires its isolated components into its own region
+      // (the last region is kept for the final one)
+      rb = nullptr;
+      const uint64_t need = (n_bound + 31) / 32;
+      if (ret_bits && light && ret_used + need + ret_region <= kRetRegions * ret_region) {
+        rb = ret_bits + ret_used;
+        MST_CUDA_CHECK(cudaMemsetAsync(rb, 0, need * 4, s));
+        ret_woff.push_back({r, ret_used});
+        ret_used += need;
+      }
+      const int hphase = (light && !ret_woff.empty()) ? (int)kPhaseLightRetire : (int)light;
       auto launch_hook = [&](auto view) {
         auto kd = k_hook_decide<decltype(view)>;
         launch_k(kd, (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ht, (uint64_t)sm_count(dev) * blocks_per_sm(kd))),
-                 kBlock, s, view, mcur, parent, rootlabel, hmasks, hcounts, d_ctr, r, hfused, (int)light, hslot, flags);
+                 kBlock, s, view, mcur, parent, rootlabel, hmasks, hcounts, d_ctr, r, hfused, hphase, hslot, flags, rb);
       };
       if (src.kind == kSrcIn)
         launch_hook(in);
@@ -926,7 +1051,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       if (!hfused)
         launch_k(k_scan_counts<kScanRoots>,
                  (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((ht + kScanTile - 1) / kScanTile, (uint64_t)sm_count(dev))),
-                 kScanBlock, s, hcounts, ht, d_ctr, r, st, ws.next_epoch(), (int)light, 0);
+                 kScanBlock, s, hcounts, ht, d_ctr, r, st, ws.next_epoch(), hphase, 0);
       launches += 1;
     }
     uint32_t* Lr = L;
@@ -945,7 +1070,8 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
                            m_bound <= (uint64_t)knob(kKnobTailStartCDEdges) &&
                            n_bound <= (16u << 20);
     if (!original_in && !lazy2 && !d_start_c && dedup_on && m_bound >= dedup_min_edges) {
-      const unsigned long long cap = std::min<unsigned long long>(1ull << 25, next_pow2(m_bound / 2));
+      const unsigned long long cap = std::min<unsigned long long>(1ull << std::max(10, std::min(30, knob_i(kKnobDedupCapLog2))),
+                                                                   next_pow2(m_bound / 2));
       unsigned long long* tab = ws.get<unsigned long long>("pair_table", 2 * cap);
       pt = PairTable{tab, nullptr, cap};
       launches += 2;
@@ -954,7 +1080,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       const unsigned g = (unsigned)std::max<uint64_t>(
           1, std::min<uint64_t>(tiles_of(n_bound), (uint64_t)sm_count(dev) * blocks_per_sm(k_label2)));
       launch_k(k_label2, g, kBlock, s, parent, rootlabel, hmasks, hslot, hcounts, Lr, mnext, mst, flags, n, d_ctr, r,
-               pt.pairs, pt.cap, dedup_active, pair_div);
+               pt.pairs, pt.cap, dedup_active, pair_div, (const uint32_t*)rb);
     }
     if ((original_in && start_c_ok) || d_start_c) {  // this round's compaction: the tail's first phase C
       tail_c_pending = true;
@@ -996,6 +1122,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     ++r;
   }
   MST_CUDA_CHECK(cudaMemcpyAsync(&out.ctr, d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
+  if (enqueue_after) (*enqueue_after)();
   MST_CUDA_CHECK(cudaStreamSynchronize(s));
   const DevCounters& c = out.ctr;
   out.err = c.err;
@@ -1205,29 +1332,37 @@ RunOut run_single(const SingleArgs& a, mst_stats_t* stats) {
   MST_CUDA_CHECK(cudaEventRecord(e1, s));
 
   RunOut o;
+  uint32_t* d_sorted = a.device_out ? a.out_ids : ws.get<uint32_t>("sorted", std::max<uint32_t>(a.n, 1));
+  auto* d_ctr = ws.get<DevCounters>("ctr", 1);
+  uint8_t* d_flags = ws.get<uint8_t>("mst_flags", a.m + 16);
+  // the sorted ids and their copy-back, enqueued behind the last round: a
+  // spanning tree has n - 1 edges, so n - 1 ids are copied (a forest's
+  // shorter list is followed by stale slots, which the caller's n - 1
+  // capacity holds and the returned count excludes)
+  uint32_t sort_launches = 0;
+  const std::function<void()> after = [&]() {
+    sort_launches = sort_from_flags(ws, d_flags, std::max<uint64_t>(a.m, 1), d_sorted, d_ctr);
+    MST_CUDA_CHECK(cudaEventRecord(e2, s));
+    if (!a.device_out && a.n > 1) copy_d2h(ws, a.out_ids, d_sorted, (uint64_t)(a.n - 1) * 4);
+    MST_CUDA_CHECK(cudaEventRecord(e3, s));
+  };
   if (a.kind == 0) {
     SoaView v{src, dst, w, 0};
     run_single_impl<SoaView>(ws, v, w, 1, a.n, a.m, o, a.time_hot, filter_mode(a.n, a.m),
-                             chunks.count ? &chunks : nullptr);
+                             chunks.count ? &chunks : nullptr, &after);
   } else {
     AosView v{reinterpret_cast<const uint4*>(aos), 0};
     const uint32_t* wb = reinterpret_cast<const uint32_t*>(aos) + 2;
-    run_single_impl<AosView>(ws, v, wb, 4, a.n, a.m, o, a.time_hot, filter_mode(a.n, a.m));
+    run_single_impl<AosView>(ws, v, wb, 4, a.n, a.m, o, a.time_hot, filter_mode(a.n, a.m), nullptr, &after);
   }
   check_err_bits(o.err);
-  uint32_t* d_sorted = a.device_out ? a.out_ids : ws.get<uint32_t>("sorted", a.n);
-  auto* d_ctr = ws.get<DevCounters>("ctr", 1);
-  o.launches += sort_from_flags(ws, ws.get<uint8_t>("mst_flags", a.m + 16), std::max<uint64_t>(a.m, 1), d_sorted,
-                                d_ctr);
-  MST_CUDA_CHECK(cudaEventRecord(e2, s));
-  if (!a.device_out && o.count)
-    copy_d2h(ws, a.out_ids, d_sorted, o.count * 4);
-  MST_CUDA_CHECK(cudaEventRecord(e3, s));
+  o.launches += sort_launches;
   if (join_legacy) {
     MST_CUDA_CHECK(cudaEventRecord(ws.join_out, s));
     MST_CUDA_CHECK(cudaStreamWaitEvent(cudaStreamLegacy, ws.join_out, 0));
   }
   MST_CUDA_CHECK(cudaStreamSynchronize(s));
+  timeline_print(e0);
   if (stats) {
     fill_stats(stats, o);
     if (chunks.count) {
@@ -1511,7 +1646,7 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, uint6
       uint32_t* hslot = ws.get<uint32_t>("hook_slotpref", tiles_of(n) * kItems * kWarps);
       auto kd = k_hook_decide<PartnerView, true>;
       launch_k(kd, persistent_grid(kd, dev, ht), kBlock, st, PartnerView{s.partner}, s.xch, s.parent, s.rootlabel, hmasks,
-               hcounts, s.d_ctr, r, hfused, phase, hslot, (uint8_t*)nullptr);
+               hcounts, s.d_ctr, r, hfused, phase, hslot, (uint8_t*)nullptr, (uint32_t*)nullptr);
       if (!hfused)
         launch_k(k_scan_counts<kScanRoots>,
                  (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((ht + kScanTile - 1) / kScanTile, (uint64_t)sm_count(dev))),
@@ -1519,7 +1654,8 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, uint6
       unsigned long long* mnext = s.minb[r & 1];
       uint32_t* Lr = light ? ws.get<uint32_t>("Llvl" + std::to_string(r), n_bound) : s.L;
       launch_k(k_label2, persistent_grid(k_label2, dev, ht), kBlock, st, s.parent, s.rootlabel, hmasks, hslot, hcounts, Lr,
-               mnext, s.mst, (uint8_t*)nullptr, n, s.d_ctr, r, (unsigned long long*)nullptr, 0ull, 0u, 4u);
+               mnext, s.mst, (uint8_t*)nullptr, n, s.d_ctr, r, (unsigned long long*)nullptr, 0ull, 0u, 4u,
+               (const uint32_t*)nullptr);
       const CompactBufs cb{ws.get<uint32_t>("tile_counts", tiles_c(s.m)),
                            ws.get<uint32_t>("tile_masks", tiles_c(s.m) * kCItems * kWarps), s.st,
                            ws.get<uint4>("stage", tiles_c(s.m) * kCTile)};

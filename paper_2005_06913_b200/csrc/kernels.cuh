@@ -68,6 +68,8 @@ constexpr int kCTile = kBlock * kCItems;
 
 constexpr int kMaxR = MST_MAX_ROUNDS + 2;
 constexpr uint64_t kNoKey = ~0ull;
+constexpr int kFiltCached = 8;  // offer filter reads through L1 (see offer)
+constexpr uint32_t kRetFlag = 0x80000000u;  // level-map entry of a retired component: kRetFlag | own index
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr uint32_t kErrRange = 1u;
 constexpr uint32_t kErrWeight = 2u;
@@ -299,12 +301,14 @@ __device__ __forceinline__ uint32_t lookback(unsigned long long* status, uint32_
 // warp-level pre-reduction with __match_any_sync + redux.sync measured
 // slower on every config and was removed.)
 __device__ __forceinline__ void offer(unsigned long long* table, uint32_t c, uint64_t key,
-                                      bool valid, bool filt = true) {
+                                      bool valid, int filt = 1) {
   if (!valid) return;
-  // Large (DRAM-resident) tables: a fire-and-forget RED; the read-first
-  // filter would put a dependent DRAM round trip on the critical path.
-  if (filt) {
-    const unsigned long long cur = __ldcg(table + c);
+  // filt & 3 == 0: a fire-and-forget RED (no dependent read on the path).
+  // filt & kFiltCached: the filter read goes through L1 (a stale copy is
+  // never below the truth either), so hot hub entries are not re-read from
+  // their one L2 slice by every offer.
+  if (filt & 3) {
+    const unsigned long long cur = (filt & kFiltCached) ? __ldca(table + c) : __ldcg(table + c);
     if (key < cur) atomicMin(table + c, (unsigned long long)key);
   } else {
     atomicMin(table + c, (unsigned long long)key);
@@ -314,23 +318,25 @@ __device__ __forceinline__ void offer(unsigned long long* table, uint32_t c, uin
 // K edges' offers to both endpoints with all filter reads in flight together,
 // then the atomics. (Offer by offer, each read waits behind the previous
 // item's atomic on the same table: 2K serial L2 round trips per thread.)
-// filt: 0 = plain REDs, 1 = read-first one offer at a time (each read sees
-// the previous atomics: best for hot hub entries), 2 = read-first batched.
+// filt & 3: 0 = plain REDs, 1 = read-first one offer at a time (each read sees
+// the previous atomics: best for hot hub entries), 2 = read-first batched;
+// | kFiltCached: filter reads through L1.
 template <int K>
 __device__ __forceinline__ void offer_both(unsigned long long* table, const uint32_t (&x)[K], const uint32_t (&y)[K],
                                            const unsigned long long (&key)[K], const bool (&valid)[K], int filt) {
-  if (filt == 1) {
+  if ((filt & 3) == 1) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      offer(table, x[k], key[k], valid[k], true);
-      offer(table, y[k], key[k], valid[k], true);
+      offer(table, x[k], key[k], valid[k], filt);
+      offer(table, y[k], key[k], valid[k], filt);
     }
-  } else if (filt == 2) {
+  } else if ((filt & 3) == 2) {
+    const bool cached = (filt & kFiltCached) != 0;
     unsigned long long cx[K], cy[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      cx[k] = valid[k] ? __ldcg(table + x[k]) : 0ull;
-      cy[k] = valid[k] ? __ldcg(table + y[k]) : 0ull;
+      cx[k] = valid[k] ? (cached ? __ldca(table + x[k]) : __ldcg(table + x[k])) : 0ull;
+      cy[k] = valid[k] ? (cached ? __ldca(table + y[k]) : __ldcg(table + y[k])) : 0ull;
     }
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -545,12 +551,88 @@ __global__ void k_compose(uint32_t* __restrict__ Lr, const uint32_t* __restrict_
   }
 }
 
+// ---- retirement (light phase): the final dense labels
+// A light round's hook may retire its isolated components (no edge left):
+// they get no label in the next round's dense space (so the tables of later
+// rounds cover only components that still have edges), their level-map
+// entry is kRetFlag | own index, and the hook records them in a bitmap
+// region of that round. At the end of the light phase the bitmap regions
+// (round 1, 2, ..., then the final region: one bit per component still
+// labelled at the phase end) enumerate every final component exactly once;
+// a component's final label is its rank in that bitmap (word prefix +
+// popcount), which the top-down composition applies.
+__global__ void k_ret_fill_final(uint32_t* __restrict__ words, const DevCounters* ctr, int P) {
+  pdl_prologue();
+  const uint32_t cnt = ctr->n[P];
+  const uint32_t nw = (cnt + 31) / 32;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += gridDim.x * blockDim.x)
+    words[i] = (i + 1) * 32 <= cnt ? 0xFFFFFFFFu : ((1u << (cnt & 31)) - 1u);
+}
+
+__global__ void k_ret_popc(const uint32_t* __restrict__ words, uint64_t nw, uint32_t* __restrict__ counts) {
+  pdl_prologue();
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += (uint64_t)gridDim.x * blockDim.x)
+    counts[i] = __popc(__ldg(words + i));
+}
+
+__device__ __forceinline__ uint32_t ret_rank(const uint32_t* __restrict__ words, const uint32_t* __restrict__ prefix,
+                                             uint64_t s) {
+  const uint64_t w = s >> 5;
+  return __ldg(prefix + w) + __popc(__ldg(words + w) & ((1u << (s & 31)) - 1u));
+}
+
+// Level r of the light phase's maps to final labels, top-down: a retired
+// entry -> its rank in region r; otherwise the top level -> the rank in the
+// final region, a lower level -> the (already final) entry of level r+1.
+__global__ void k_compose_ret(uint32_t* __restrict__ Lr, const uint32_t* __restrict__ Lnext,
+                              const uint32_t* __restrict__ words, const uint32_t* __restrict__ prefix,
+                              uint64_t woff_r, uint64_t woff_final, const DevCounters* ctr, int r) {
+  pdl_prologue();
+  const uint32_t n_r = ctr->n[r];
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * 4;
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x * 4 + threadIdx.x; base < n_r; base += stride) {
+    uint32_t x[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t c = base + (uint64_t)k * blockDim.x;
+      x[k] = c < n_r ? Lr[c] : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t c = base + (uint64_t)k * blockDim.x;
+      if (c >= n_r) continue;
+      if (x[k] & kRetFlag)
+        x[k] = ret_rank(words, prefix, woff_r * 32 + (x[k] & ~kRetFlag));
+      else if (Lnext == nullptr)
+        x[k] = ret_rank(words, prefix, woff_final * 32 + x[k]);
+      else
+        x[k] = __ldg(Lnext + x[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t c = base + (uint64_t)k * blockDim.x;
+      if (c < n_r) Lr[c] = x[k];
+    }
+  }
+}
+
+__global__ void k_fill_keys(unsigned long long* __restrict__ t, const DevCounters* ctr, int r) {
+  pdl_prologue();
+  const uint32_t cnt = ctr->n[r];
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (uint64_t)gridDim.x * blockDim.x)
+    t[i] = kNoKey;
+}
+
 // ------------------------------ scan helpers -------------------------------
 //   kScanEdges : m[r+1] = kept; none kept -> stop (or light-phase end)
 //   kScanRoots : n[r+1] = roots; <= 1 -> stop; == n[r] -> stop (or light end)
-enum { kScanEdges = 0, kScanRoots = 1, kScanPlain = 2 };
+enum { kScanEdges = 0, kScanRoots = 1, kScanPlain = 2, kScanDense = 3 };
 // the `light_phase` argument of the scans: which loop the round belongs to
-enum { kPhasePlain = 0, kPhaseLight = 1, kPhaseSharded = 2 };
+// kPhaseLightRetire: a light-phase round whose hook retires isolated
+// components (see "retirement" at k_hook_decide): its root count covers the
+// components that still have edges only, so <= 1 of them ends the light
+// phase, not the MST
+enum { kPhasePlain = 0, kPhaseLight = 1, kPhaseSharded = 2, kPhaseLightRetire = 3 };
 constexpr uint32_t kFusedScanMaxTiles = 16384;  // one block scans <= this many counts
 
 template <int kKind>
@@ -567,7 +649,16 @@ __device__ __forceinline__ void scan_verdict(DevCounters* ctr, int r, uint32_t t
     }
   } else if (kKind == kScanRoots) {
     ctr->n[r + 1] = total;
-    if (total <= 1) {
+    if (light_phase == kPhaseLightRetire) {
+      // retired components are final: nothing left with an edge ends the
+      // light phase at round r + 1 (round 1: no light edge at all, which the
+      // host answers with the plain loop); one component with edges left ends
+      // it once its last (internal) edges are dropped by the compaction
+      if (total == 0)
+        ctr->phase_end = r == 1 ? 1u : (uint32_t)r + 1;
+      else if (total == ctr->n[r])
+        ctr->phase_end = (uint32_t)r;  // no progress (a round without retirement after retiring ones)
+    } else if (total <= 1) {
       ctr->stop_round = (uint32_t)r + 1;
     } else if (total == ctr->n[r]) {
       // no live edge anywhere: done (a forest if total > 1), unless this is
@@ -577,6 +668,8 @@ __device__ __forceinline__ void scan_verdict(DevCounters* ctr, int r, uint32_t t
       else
         ctr->stop_round = (uint32_t)r + 1;
     }
+  } else if (kKind == kScanDense) {
+    ctr->n[r] = total;  // the light phase's final component count (retirement)
   } else {
     ctr->m[kMaxR - 1] = total;
   }
@@ -829,15 +922,15 @@ __global__ void MST_LB_(MST_MINB_COUNT) k_count(View in, uint4* __restrict__ rel
       okey[k] = ((unsigned long long)e[k].w << 32) | (uint32_t)i;
       if ((kMode == kModeRelabel || kMode == kModeDedup) && !kBatch && keep[k]) {
         // one offer at a time, as each edge is decided (hub-heavy tables)
-        offer(min_next, ox, okey[k], true, filt != 0);
-        offer(min_next, oy, okey[k], true, filt != 0);
+        offer(min_next, ox, okey[k], true, filt);
+        offer(min_next, oy, okey[k], true, filt);
       }
       bal[k] = __ballot_sync(0xffffffffu, keep[k]);
       if (lane == 0) s_slot[k * kWarps + warp] = __popc(bal[k]);
       cnt += __popc(bal[k]);
     }
     if ((kMode == kModeRelabel || kMode == kModeDedup) && kBatch)
-      offer_both<kCItems>(min_next, ofx, ofy, okey, keep, 2);
+      offer_both<kCItems>(min_next, ofx, ofy, okey, keep, 2 | (filt & kFiltCached));
     if (err) atomicOr(&ctr->err, err);
     if (lane == 0) s_cnt[warp] = cnt;
     __syncthreads();
@@ -997,8 +1090,8 @@ __global__ void __launch_bounds__(kBlock) k_emit_staged(const uint4* __restrict_
         if (v) __stcs(out + off + j, e);
         if (kMode == kModeHeavy || kMode == kModeLight) {
           const unsigned long long key = ((unsigned long long)e.z << 32) | (off + j);
-          offer(min_next, e.x, key, v, filt != 0);
-          offer(min_next, e.y, key, v, filt != 0);
+          offer(min_next, e.x, key, v, filt);
+          offer(min_next, e.y, key, v, filt);
         }
       }
     } else {
@@ -1021,7 +1114,7 @@ __global__ void __launch_bounds__(kBlock) k_emit_staged(const uint4* __restrict_
           y[k] = e[k].y;
           key[k] = ((unsigned long long)e[k].z << 32) | (off + j);
         }
-        if (kMode == kModeHeavy || kMode == kModeLight) offer_both<kCItems>(min_next, x, y, key, v, 2);
+        if (kMode == kModeHeavy || kMode == kModeLight) offer_both<kCItems>(min_next, x, y, key, v, 2 | (filt & kFiltCached));
       }
     }
   }
@@ -1044,7 +1137,7 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_counts(uint32_t* __restrict
   pdl_prologue();
   __shared__ uint32_t s_warp[kScanBlock / 32];
   __shared__ uint32_t s_misc[2];
-  if (kKind != kScanPlain) {
+  if (kKind == kScanEdges || kKind == kScanRoots) {
     if ((uint32_t)r >= ctr->phase_end) return;
     if (kKind == kScanEdges && (uint32_t)r + 1 >= ctr->stop_round) return;
     if (kKind == kScanRoots && (uint32_t)r >= ctr->stop_round) return;
@@ -1056,7 +1149,7 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_counts(uint32_t* __restrict
   else if (kKind == kScanEdges)
     n_items = ((count_src ? ctr->m[0] : ctr->m[r]) + (uint64_t)kCTile - 1) / kCTile;
   else
-    n_items = ntiles_max;
+    n_items = ntiles_max;  // kScanPlain, kScanDense
   const uint32_t nblocks = (uint32_t)((n_items + kScanTile - 1) / kScanTile);
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   for (uint32_t blk = blockIdx.x; blk < max(nblocks, 1u); blk += gridDim.x) {
@@ -1160,7 +1253,8 @@ __global__ void MST_LB_(MST_MINB_HOOK) k_hook_decide(View E, const unsigned long
                                                         uint32_t* __restrict__ masks, uint32_t* __restrict__ counts,
                                                         DevCounters* ctr, int r, int fused, int light_phase,
                                                         uint32_t* __restrict__ slotpref,
-                                                        uint8_t* __restrict__ flags = nullptr) {
+                                                        uint8_t* __restrict__ flags = nullptr,
+                                                        uint32_t* __restrict__ rbits = nullptr) {
   pdl_prologue();
   __shared__ uint32_t s_cnt[kWarps];
   __shared__ uint32_t s_slot[kItems * kWarps];
@@ -1199,10 +1293,13 @@ __global__ void MST_LB_(MST_MINB_HOOK) k_hook_decide(View E, const unsigned long
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
       const uint64_t c = (uint64_t)tile * kTile + k * kBlock + threadIdx.x;
-      bool isroot = false;
+      bool isroot = false, iso = false;
       if (c < n_r) {
         if (key[k] == kNoKey) {
-          isroot = true;
+          // no edge: a root; with rbits it is retired instead (final, no
+          // label in round r+1's dense space)
+          iso = rbits != nullptr;
+          isroot = !iso;
           parent[c] = (uint32_t)c;
         } else {
           const uint32_t o = (e[k].a == (uint32_t)c) ? e[k].b : e[k].a;
@@ -1221,6 +1318,11 @@ __global__ void MST_LB_(MST_MINB_HOOK) k_hook_decide(View E, const unsigned long
         }
       }
       const unsigned bal = __ballot_sync(0xffffffffu, isroot);
+      if (rbits) {
+        const unsigned rb = __ballot_sync(0xffffffffu, iso);
+        const uint64_t c0 = (uint64_t)tile * kTile + k * kBlock + warp * 32;
+        if (lane == 0 && c0 < n_r) rbits[c0 >> 5] = rb;
+      }
       if (lane == 0) {
         masks[(uint64_t)tile * (kItems * kWarps) + k * kWarps + warp] = bal;
         s_slot[k * kWarps + warp] = __popc(bal);
@@ -1290,7 +1392,8 @@ __global__ void MST_LB_(MST_MINB_LABEL) k_label2(uint32_t* __restrict__ parent, 
                                                    uint32_t* __restrict__ mst, uint8_t* __restrict__ flags,
                                                    uint32_t n_orig, DevCounters* ctr, int r,
                                                    unsigned long long* pair_keys, unsigned long long pair_cap,
-                                                   unsigned int dedup_active, unsigned int pair_div) {
+                                                   unsigned int dedup_active, unsigned int pair_div,
+                                                   const uint32_t* __restrict__ rbits = nullptr) {
   pdl_prologue();
   if ((uint32_t)r >= ctr->stop_round || (uint32_t)r >= ctr->phase_end) return;
   const bool labels = (uint32_t)r + 1 < ctr->stop_round;  // the last hook round only emits MST slots
@@ -1307,8 +1410,16 @@ __global__ void MST_LB_(MST_MINB_LABEL) k_label2(uint32_t* __restrict__ parent, 
     // R-MAT's repeated hub pairs keep succeeding and are not held back
     const bool doubtful = ctr->dedup_fail && K * (K - 1) / 2 > m_r / 8 && !(pair_div & 0x100u);
     const bool use = K <= dedup_active && m_r >= ((pair_div >> 16) & 0xFFu) * K && m_r >= 4096 && !doubtful;
+    // table >= m_r / div slots, but no more than twice the pairs the next
+    // round's n_next components can form (after retirement they are few: c4
+    // round 3, 825 components, 1 M slots in L2 instead of 32 M in DRAM:
+    // 3.3 -> 1.05 ms) and no fewer than 256 K (a few hundred hot pairs
+    // packed into a few KB serialise their inserts: c3 round 7, 0.15 vs
+    // 0.65 ms with 2 K slots)
+    const unsigned long long pairs_max = (unsigned long long)n_next * (n_next > 0 ? n_next - 1 : 0) / 2;
+    const unsigned long long want = min(m_r / (pair_div & 0xFFu), max(2 * pairs_max, 1ull << 18));
     unsigned long long P = 1024;
-    while (P < m_r / (pair_div & 0xFFu) && P < pair_cap) P <<= 1;
+    while (P < want && P < pair_cap) P <<= 1;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       ctr->dedup[r] = use ? 1u : 0u;
       ctr->pair_mask[r] = P - 1;
@@ -1326,7 +1437,7 @@ __global__ void MST_LB_(MST_MINB_LABEL) k_label2(uint32_t* __restrict__ parent, 
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const uint32_t toff = __ldg(offsets + tile);
     uint32_t c[kItems], root[kItems], own[kItems];
-    bool v[kItems], isroot[kItems];
+    bool v[kItems], isroot[kItems], iso[kItems];
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
       c[k] = tile * kTile + k * kBlock + threadIdx.x;
@@ -1335,6 +1446,7 @@ __global__ void MST_LB_(MST_MINB_LABEL) k_label2(uint32_t* __restrict__ parent, 
       const uint32_t m = __ldg(masks + (uint64_t)tile * 32 + slot);
       isroot[k] = (m >> lane) & 1u;
       own[k] = toff + __ldg(slotpref + (uint64_t)tile * 32 + slot) + __popc(m & lt);
+      iso[k] = rbits != nullptr && v[k] && ((__ldg(rbits + (c[k] >> 5)) >> lane) & 1u);
     }
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
@@ -1346,12 +1458,12 @@ __global__ void MST_LB_(MST_MINB_LABEL) k_label2(uint32_t* __restrict__ parent, 
     if (!labels) continue;
     bool walk[kItems];
 #pragma unroll
-    for (int k = 0; k < kItems; ++k) walk[k] = v[k] && !isroot[k];
+    for (int k = 0; k < kItems; ++k) walk[k] = v[k] && !isroot[k] && !iso[k];
     find_roots<kItems>(parent, c, walk, root);
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
       if (!v[k]) continue;
-      L[c[k]] = isroot[k] ? own[k] : roots_before(root[k], masks, slotpref, offsets);
+      L[c[k]] = iso[k] ? (kRetFlag | c[k]) : isroot[k] ? own[k] : roots_before(root[k], masks, slotpref, offsets);
       if (c[k] < n_next) min_next[c[k]] = kNoKey;
     }
   }
@@ -1427,6 +1539,9 @@ struct TailArgs {
   // SoA list (src0 / src1 / src_w) in place of round 1's count + emit passes
   int start_c;
   int c_soa;  // start_c's phase C reads the caller's SoA list (plain round 1), else the list E[r0 & 1]
+  // light phase after retiring round kernels: components outside the tail's
+  // label space exist, so one component left ends the light phase, not the MST
+  int retired;
 };
 
 constexpr uint32_t kTailSmemMin = 2048;  // block-local min table entries (16 KB); tiny rounds up to this
@@ -1856,7 +1971,7 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
       continue;
     }
     uint32_t n_next = 0;
-    bool stop_now = false, phase_now = false;
+    bool stop_now = false, phase_now = false, light_final = false;
     const bool first_c = a.start_c && r == a.r0;
     if (first_c) n_next = vc->n[r + 1];  // the round kernels' hook + label ran round r0
     if (!first_c) {
@@ -1960,7 +2075,8 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
     if (last_dedup == r - 1 && 2 * m_r > m_prev) dedup_off = true;
     block_scan_array(a.broots, G, s_bpre, s_warp);
     n_next = s_bpre[G];
-    if (n_next <= 1) {
+    light_final = a.light && a.retired && n_next <= 1 && n_next < n_r;
+    if (n_next <= 1 && !(a.light && a.retired)) {
       stop_now = true;
     } else if (n_next == n_r) {
       // no live edge anywhere: done (a forest), or the light phase ends
@@ -1975,6 +2091,9 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
       a.ctr->m[r + 2] = 0;  // (a tiny round r+1 adds into m[r+2] without a prior sync)
       if (stop_now) a.ctr->stop_round = (uint32_t)r + 1;
       if (phase_now) a.ctr->phase_end = (uint32_t)r;
+      // round r's merges are kept (their MST flags are set): its labels and
+      // the map update below still run, then the phase ends at round r + 1
+      if (light_final) a.ctr->phase_end = (uint32_t)r + 1;
     }
     if (phase_now) break;  // the host composes the maps; nothing of round r is kept
     for (uint32_t base = b * kBlock * kItems; base < n_r; base += G * kBlock * kItems) {
@@ -2024,6 +2143,7 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
         for (int k = 0; k < 4; ++k)
           if (base + k * kBlock < n_entry) a.M[base + k * kBlock] = x[k];
       }
+      if (light_final) break;  // the host composes the maps (phase_end = r + 1)
     }
     // ---- C0 (optional): relabel in place + each pair's lightest key
     const bool dedup = a.pairs != nullptr && !first_c && n_next < (1u << kTailPairLabelBits) && m_r >= a.dedup_min &&
