@@ -677,6 +677,81 @@ struct CopyChunks {
   cudaEvent_t ev[kMax];
 };
 
+// ---- retirement bookkeeping (kernels.cuh "retirement"), shared by the
+// single-device and the sharded loops: one bitmap region per retiring light
+// round (sized by the host's bound on n_r), the last region kept for the
+// final one; at the light phase's end the regions are ranked and the level
+// maps composed top-down into final labels.
+struct RetireState {
+  static constexpr uint64_t kRegions = 5;
+  uint32_t* bits = nullptr;
+  uint64_t region = 0;  // words of one region (bound)
+  uint64_t used = 0;
+  std::vector<std::pair<int, uint64_t>> woff;  // (round, first word) of each retiring round
+
+  void init(Workspace& ws, uint32_t n, bool on) {
+    woff.clear();
+    used = 0;
+    region = ((uint64_t)n + 31) / 32 + 1;
+    bits = on ? ws.get<uint32_t>("ret_bits", kRegions * region) : nullptr;
+  }
+  bool active() const { return !woff.empty(); }
+  // round r's region (cleared), or nullptr when retirement is off or full
+  uint32_t* take(cudaStream_t s, int r, uint64_t n_bound) {
+    const uint64_t need = (n_bound + 31) / 32;
+    if (!bits || used + need + region > kRegions * region) return nullptr;
+    uint32_t* rb = bits + used;
+    MST_CUDA_CHECK(cudaMemsetAsync(rb, 0, need * 4, s));
+    woff.push_back({r, used});
+    used += need;
+    return rb;
+  }
+  void drop_from(int P) {
+    while (!woff.empty() && woff.back().first >= P) woff.pop_back();
+  }
+  // Final labels of the light phase ending at round P: every level map of
+  // `levels` (buffer, round; level 1 first) becomes vertex/component -> final
+  // label, n[P] the number of final components, and `heavy_min` (the heavy
+  // filter's table) is cleared for them. Returns the launches.
+  uint32_t finalize(Workspace& ws, cudaStream_t s, DevCounters* d_ctr, int P,
+                    const std::vector<std::pair<uint32_t*, int>>& levels, const DevCounters& snap,
+                    unsigned long long* heavy_min) {
+    const int dev = ws.device;
+    const uint64_t woff_final = used;  // after every region handed out (dropped rounds' are zero)
+    MST_CUDA_CHECK(cudaMemsetAsync(bits + woff_final, 0, region * 4, s));
+    launch_k(k_ret_fill_final, (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(region / 256 + 1, 4096)), 256, s,
+             bits + woff_final, (const DevCounters*)d_ctr, P);
+    const uint64_t W = woff_final + region;
+    uint32_t* prefix = ws.get<uint32_t>("ret_prefix", W);
+    launch_k(k_ret_popc, (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(W / 256 + 1, (uint64_t)sm_count(dev) * 8)),
+             256, s, (const uint32_t*)bits, W, prefix);
+    unsigned long long* st = ws.status_array((W + kScanTile - 1) / kScanTile + 1);
+    launch_k(k_scan_counts<kScanDense>,
+             (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((W + kScanTile - 1) / kScanTile, (uint64_t)sm_count(dev))),
+             kScanBlock, s, prefix, W, d_ctr, P, st, ws.next_epoch(), 0, 0);
+    for (int k = (int)levels.size() - 1; k >= 0; --k) {
+      uint64_t wo = 0;
+      for (const auto& rw : woff)
+        if (rw.first == levels[k].second) wo = rw.second;
+      const uint32_t* Lnext = k + 1 < (int)levels.size() ? levels[k + 1].first : nullptr;
+      const unsigned g = (unsigned)std::max<uint64_t>(
+          1, std::min<uint64_t>((snap.n[levels[k].second] + 1023) / 1024, (uint64_t)sm_count(dev) * 8));
+      launch_k(k_compose_ret, g, 256, s, levels[k].first, Lnext, (const uint32_t*)bits, (const uint32_t*)prefix, wo,
+               woff_final, (const DevCounters*)d_ctr, levels[k].second);
+    }
+    launch_k(k_fill_keys, (unsigned)(sm_count(dev) * 8), 256, s, heavy_min, (const DevCounters*)d_ctr, P);
+    return 5 + (uint32_t)levels.size();
+  }
+};
+
+// n[P] on the host (one sync): the component count after a retiring light
+// phase exists on the device only.
+uint32_t read_count(Workspace& ws, cudaStream_t s, const DevCounters* d_ctr, int P) {
+  MST_CUDA_CHECK(cudaMemcpyAsync(ws.h_u32, &d_ctr->n[P], sizeof(unsigned int), cudaMemcpyDeviceToHost, s));
+  MST_CUDA_CHECK(cudaStreamSynchronize(s));
+  return ws.h_u32[0];
+}
+
 // `enqueue_after` (optional) is enqueued on the stream right behind the last
 // round, before the one host sync that reads the verdict: the sorted output
 // and its copy-back need no host decision, so they follow the MST without a
@@ -693,8 +768,8 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   uint32_t* parent = ws.get<uint32_t>("parent", n);
   uint32_t* rootlabel = ws.get<uint32_t>("rootlabel", n);
   uint32_t* L = ws.get<uint32_t>("label", n);
-  // single GPU: the sorted output comes from the per-edge flags, so no MST
-  // slot array is written (the sharded loop keeps one, see Shard::mst)
+  // the sorted output comes from the per-edge flags (the sharded loop too:
+  // every rank sets the flags of every hooked component), no MST slot array
   uint32_t* mst = nullptr;
   uint4* E[2] = {ws.get<uint4>("E0", m), ws.get<uint4>("E1", m)};
   unsigned long long* st = ws.status_array(std::max(tiles_of(m), tiles_of(n)));
@@ -765,12 +840,8 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   // round (sized by the host's bound on n_r), then the final region. R-MAT's
   // light phase: 44 M of c4's 67 M vertices have no light edge, so from round
   // 2 on the per-component tables cover ~5 M instead of ~49 M components.
-  const bool retire_ok = filter && knob_i(kKnobRetire) != 0 && n < (1u << 31);
-  const uint64_t ret_region = ((uint64_t)n + 31) / 32 + 1;  // words: one region's bound
-  constexpr uint64_t kRetRegions = 5;
-  uint32_t* ret_bits = retire_ok ? ws.get<uint32_t>("ret_bits", kRetRegions * ret_region) : nullptr;
-  std::vector<std::pair<int, uint64_t>> ret_woff;  // (round, first word) of each retiring round
-  uint64_t ret_used = 0;
+  RetireState ret;
+  ret.init(ws, n, filter && knob_i(kKnobRetire) != 0 && n < (1u << 31));
   uint64_t n_bound = n, m_bound = m;
   int r = 1, loop_start = 1;
   int phase_end = 0;
@@ -836,36 +907,10 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       return false;
     }
     while (!levels.empty() && levels.back().second >= phase_end) levels.pop_back();
-    while (!ret_woff.empty() && ret_woff.back().first >= phase_end) ret_woff.pop_back();
-    const bool retired = !ret_woff.empty() && !levels.empty();
+    ret.drop_from(phase_end);
+    const bool retired = ret.active() && !levels.empty();
     if (retired) {
-      // final region: one bit per component labelled at the phase end; the
-      // rank of a bit over all regions is the final label; the total is n[P]
-      const int P = phase_end;
-      const uint64_t woff_final = ret_used;  // after every region handed out (dropped rounds' are zero)
-      MST_CUDA_CHECK(cudaMemsetAsync(ret_bits + woff_final, 0, ret_region * 4, s));
-      launch_k(k_ret_fill_final, (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ret_region / 256 + 1, 4096)), 256,
-               s, ret_bits + woff_final, d_ctr, P);
-      const uint64_t W = woff_final + ret_region;
-      uint32_t* prefix = ws.get<uint32_t>("ret_prefix", W);
-      launch_k(k_ret_popc, (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(W / 256 + 1, (uint64_t)sm_count(dev) * 8)),
-               256, s, (const uint32_t*)ret_bits, W, prefix);
-      launch_k(k_scan_counts<kScanDense>,
-               (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((W + kScanTile - 1) / kScanTile, (uint64_t)sm_count(dev))),
-               kScanBlock, s, prefix, W, d_ctr, P, st, ws.next_epoch(), 0, 0);
-      for (int k = (int)levels.size() - 1; k >= 0; --k) {
-        uint64_t woff = 0;
-        for (const auto& rw : ret_woff)
-          if (rw.first == levels[k].second) woff = rw.second;
-        const uint32_t* Lnext = k + 1 < (int)levels.size() ? levels[k + 1].first : nullptr;
-        const unsigned g = (unsigned)std::max<uint64_t>(
-            1, std::min<uint64_t>((snap.n[levels[k].second] + 1023) / 1024, (uint64_t)sm_count(dev) * 8));
-        launch_k(k_compose_ret, g, 256, s, levels[k].first, Lnext, (const uint32_t*)ret_bits, (const uint32_t*)prefix,
-                 woff, woff_final, d_ctr, levels[k].second);
-      }
-      // the heavy filter offers into this table for all n[P] components
-      launch_k(k_fill_keys, (unsigned)(sm_count(dev) * 8), 256, s, minb[(P - 1) & 1], d_ctr, P);
-      launches += 5 + (uint32_t)levels.size();
+      launches += ret.finalize(ws, s, d_ctr, phase_end, levels, snap, minb[(phase_end - 1) & 1]);
     } else {
       for (int k = (int)levels.size() - 2; k >= 0; --k) {
         const unsigned g = (unsigned)std::max<uint64_t>(
@@ -887,12 +932,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     r = R1;
     loop_start = R1;
     // retirement: n[R1] (all final components) was counted on the device
-    n_bound = snap.n[R1];
-    if (retired) {
-      MST_CUDA_CHECK(cudaMemcpyAsync(ws.h_u32, &d_ctr->n[R1], sizeof(unsigned int), cudaMemcpyDeviceToHost, s));
-      MST_CUDA_CHECK(cudaStreamSynchronize(s));
-      n_bound = ws.h_u32[0];
-    }
+    n_bound = retired ? read_count(ws, s, d_ctr, R1) : snap.n[R1];
     m_bound = m;
     return true;
   };
@@ -916,7 +956,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     // few of them can still carry millions of edges, which the round
     // kernels' pair dedup collapses and the tail would not (c3: 4 tail
     // rounds over ~9 M edges, +0.8 ms), so the small-n rule stays off there
-    const bool retiring = light && !ret_woff.empty();
+    const bool retiring = light && ret.active();
     // round 1 of the light phase: the split keeps ~beta*n edges (the pivot's
     // target), a better bound than m before its count is known
     const uint64_t m_est = (light && r == 1) ? std::min<uint64_t>(m_bound, (uint64_t)(1.1 * light_target)) : m_bound;
@@ -951,7 +991,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       TailArgs ta{{E[0], E[1]}, {minb[0], minb[1]}, parent, rootlabel, L, mst, broots, bkept, tmasks, twpref, M, flags,
                   trace, 0, nullptr, nullptr, nullptr, 0, d_ctr, n, r, (int)light};
       ta.start_c = tail_c_pending ? 1 : 0;
-      ta.retired = (light && !ret_woff.empty()) ? 1 : 0;
+      ta.retired = (light && ret.active()) ? 1 : 0;
       ta.c_soa = (tail_c_pending && r == 1) ? 1 : 0;
       if (knob_i(kKnobTailTiny)) {
         // three rotating min tables for the one-sync rounds (k_tail "tiny")
@@ -1028,15 +1068,8 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       const HookSrc src = hook_src(r);
       // a light round retires its isolated components into its own region
       // (the last region is kept for the final one)
-      rb = nullptr;
-      const uint64_t need = (n_bound + 31) / 32;
-      if (ret_bits && light && ret_used + need + ret_region <= kRetRegions * ret_region) {
-        rb = ret_bits + ret_used;
-        MST_CUDA_CHECK(cudaMemsetAsync(rb, 0, need * 4, s));
-        ret_woff.push_back({r, ret_used});
-        ret_used += need;
-      }
-      const int hphase = (light && !ret_woff.empty()) ? (int)kPhaseLightRetire : (int)light;
+      rb = light ? ret.take(s, r, n_bound) : nullptr;
+      const int hphase = (light && ret.active()) ? (int)kPhaseLightRetire : (int)light;
       auto launch_hook = [&](auto view) {
         auto kd = k_hook_decide<decltype(view)>;
         launch_k(kd, (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ht, (uint64_t)sm_count(dev) * blocks_per_sm(kd))),
@@ -1393,7 +1426,9 @@ struct Shard {
   SoaView in{};
   unsigned long long* minb[2]{};
   unsigned long long *xch = nullptr, *own = nullptr;
-  uint32_t *parent = nullptr, *rootlabel = nullptr, *L = nullptr, *partner = nullptr, *mst = nullptr;
+  uint32_t *parent = nullptr, *rootlabel = nullptr, *L = nullptr, *partner = nullptr;
+  uint8_t* flags = nullptr;  // MST flag per global edge id (replicated: every rank sets every flag)
+  RetireState ret;           // light-phase retirement (replicated decisions)
   uint32_t* hist = nullptr;  // Filter-Borůvka: weight histogram (summed across shards)
   uint32_t* errw = nullptr;  // error bits as counts (summed across shards)
   uint4* E[2]{};
@@ -1526,6 +1561,8 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, uint6
     MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
     init_counters(*s.ws, s.d_ctr, n, s.m);
     MST_CUDA_CHECK(cudaMemsetAsync(s.minb[0], 0xFF, (size_t)n * 8, s.ws->stream));
+    MST_CUDA_CHECK(cudaMemsetAsync(s.flags, 0, m_total + 16, s.ws->stream));
+    s.ret.init(*s.ws, n, filter && knob_i(kKnobRetire) != 0 && n < (1u << 31));
   }
   if (filter) {
     // pivot from the summed histogram of every shard's weight sample
@@ -1640,13 +1677,14 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, uint6
       cudaStream_t st = ws.stream;
       const uint64_t ht = tiles_of(n_bound);
       const int hfused = ht <= kFusedScanMaxTiles ? 1 : 0;
-      const int phase = light ? (int)kPhaseLight : (int)kPhasePlain;
+      uint32_t* rb = light ? s.ret.take(st, r, n_bound) : nullptr;  // same decision on every shard
+      const int phase = light ? (s.ret.active() ? (int)kPhaseLightRetire : (int)kPhaseLight) : (int)kPhasePlain;
       uint32_t* hcounts = ws.get<uint32_t>("hook_counts", tiles_of(n));
       uint32_t* hmasks = ws.get<uint32_t>("hook_masks", tiles_of(n) * kItems * kWarps);
       uint32_t* hslot = ws.get<uint32_t>("hook_slotpref", tiles_of(n) * kItems * kWarps);
       auto kd = k_hook_decide<PartnerView, true>;
       launch_k(kd, persistent_grid(kd, dev, ht), kBlock, st, PartnerView{s.partner}, s.xch, s.parent, s.rootlabel, hmasks,
-               hcounts, s.d_ctr, r, hfused, phase, hslot, (uint8_t*)nullptr, (uint32_t*)nullptr);
+               hcounts, s.d_ctr, r, hfused, phase, hslot, s.flags, rb);
       if (!hfused)
         launch_k(k_scan_counts<kScanRoots>,
                  (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((ht + kScanTile - 1) / kScanTile, (uint64_t)sm_count(dev))),
@@ -1654,8 +1692,8 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, uint6
       unsigned long long* mnext = s.minb[r & 1];
       uint32_t* Lr = light ? ws.get<uint32_t>("Llvl" + std::to_string(r), n_bound) : s.L;
       launch_k(k_label2, persistent_grid(k_label2, dev, ht), kBlock, st, s.parent, s.rootlabel, hmasks, hslot, hcounts, Lr,
-               mnext, s.mst, (uint8_t*)nullptr, n, s.d_ctr, r, (unsigned long long*)nullptr, 0ull, 0u, 4u,
-               (const uint32_t*)nullptr);
+               mnext, (uint32_t*)nullptr, (uint8_t*)nullptr, n, s.d_ctr, r, (unsigned long long*)nullptr, 0ull, 0u,
+               4u | (8u << 16), (const uint32_t*)rb);
       const CompactBufs cb{ws.get<uint32_t>("tile_counts", tiles_c(s.m)),
                            ws.get<uint32_t>("tile_masks", tiles_c(s.m) * kCItems * kWarps), s.st,
                            ws.get<uint4>("stage", tiles_c(s.m) * kCTile)};
@@ -1704,15 +1742,24 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, uint6
         }
         while (!levels.empty() && levels.back() >= pe) levels.pop_back();
         R1 = pe;
+        bool retired = false;
         for (auto& s : sh) {
           MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
           Workspace& ws = *s.ws;
-          for (int k = (int)levels.size() - 2; k >= 0; --k) {
-            const unsigned gk = (unsigned)std::max<uint64_t>(
-                1, std::min<uint64_t>((snap.n[levels[k]] + 255) / 256, (uint64_t)sm_count(ws.device) * 8));
-            launch_k(k_compose, gk, 256, ws.stream, ws.get<uint32_t>("Llvl" + std::to_string(levels[k]), 1),
-                     (const uint32_t*)ws.get<uint32_t>("Llvl" + std::to_string(levels[k + 1]), 1), s.d_ctr, levels[k]);
-            ++launches;
+          s.ret.drop_from(pe);
+          retired = s.ret.active() && !levels.empty();
+          if (retired) {
+            std::vector<std::pair<uint32_t*, int>> lv;
+            for (int lr : levels) lv.push_back({ws.get<uint32_t>("Llvl" + std::to_string(lr), 1), lr});
+            launches += s.ret.finalize(ws, ws.stream, s.d_ctr, pe, lv, snap, s.minb[(pe - 1) & 1]);
+          } else {
+            for (int k = (int)levels.size() - 2; k >= 0; --k) {
+              const unsigned gk = (unsigned)std::max<uint64_t>(
+                  1, std::min<uint64_t>((snap.n[levels[k]] + 255) / 256, (uint64_t)sm_count(ws.device) * 8));
+              launch_k(k_compose, gk, 256, ws.stream, ws.get<uint32_t>("Llvl" + std::to_string(levels[k]), 1),
+                       (const uint32_t*)ws.get<uint32_t>("Llvl" + std::to_string(levels[k + 1]), 1), s.d_ctr, levels[k]);
+              ++launches;
+            }
           }
           const uint32_t* vlabel = levels.empty() ? nullptr : ws.get<uint32_t>("Llvl" + std::to_string(levels[0]), 1);
           MST_CUDA_CHECK(cudaMemsetAsync(&s.d_ctr->phase_end, 0xFF, sizeof(unsigned int), ws.stream));
@@ -1726,7 +1773,8 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, uint6
           launches += 2;
         }
         light = false;
-        n_bound = snap.n[R1];
+        // after retirement n[R1] exists on the devices only (identical on every shard)
+        n_bound = retired ? read_count(*sh[0].ws, sh[0].ws->stream, sh[0].d_ctr, R1) : snap.n[R1];
         for (int g = 0; g < G; ++g) m_bound[g] = sh[g].m;
         r = R1;
         loop_start = R1;
@@ -1834,7 +1882,7 @@ RunOut run_sharded(const std::vector<PartSpec>& parts, Exchanger& ex, uint32_t n
     s.rootlabel = ws.get<uint32_t>("rootlabel", n);
     s.L = ws.get<uint32_t>("label", n);
     s.partner = ws.get<uint32_t>("partner", n);
-    s.mst = ws.get<uint32_t>("mst", n);
+    s.flags = ws.get<uint8_t>("mst_flags", m_total + 16);
     s.E[0] = ws.get<uint4>("E0", s.m);
     s.E[1] = ws.get<uint4>("E1", s.m);
     s.d_ctr = ws.get<DevCounters>("ctr", 1);
@@ -1850,7 +1898,7 @@ RunOut run_sharded(const std::vector<PartSpec>& parts, Exchanger& ex, uint32_t n
   Workspace& ws0 = *sh[0].ws;
   MST_CUDA_CHECK(cudaSetDevice(ws0.device));
   uint32_t* d_sorted = device_out ? out_ids : ws0.get<uint32_t>("sorted", n);
-  o.launches += sort_ids(ws0, sh[0].mst, o.count, std::max<uint64_t>(m_total, 1), d_sorted, sh[0].d_ctr);
+  o.launches += sort_from_flags(ws0, sh[0].flags, std::max<uint64_t>(m_total, 1), d_sorted, sh[0].d_ctr);
   MST_CUDA_CHECK(cudaEventRecord(e2, ws0.stream));
   if (o.count && out_ids && !device_out)
     copy_d2h(ws0, out_ids, d_sorted, o.count * 4);
