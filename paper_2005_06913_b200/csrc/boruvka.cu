@@ -152,7 +152,7 @@ constexpr KnobDef kKnobDefs[kKnobCount] = {
     {"MST_DEDUP_MIN_RATIO", 8},  {"MST_DEDUP_CAP_LOG2", 25},
     {"MST_LAZY_ROUND1", 1},      {"MST_PIPELINE_H2D", 0},        {"MST_PIPELINE_CHUNKS", 16},
     {"MST_DEBUG_ROUNDS", 0},     {"MST_L2_FETCH", 0},         {"MST_OFFER_CACHED", 15},
-    {"MST_RETIRE", 1},                      {"MST_TIMELINE", 0}};
+    {"MST_RETIRE", 1},           {"MST_TIMELINE", 0}};
 
 std::atomic<double>* knob_table() {
   static std::atomic<double> t[kKnobCount];
@@ -522,7 +522,7 @@ uint32_t sort_from_flags(Workspace& ws, const uint8_t* flags, uint64_t m, uint32
   const uint64_t tiles = (m + kFlagTile - 1) / kFlagTile;
   uint32_t* counts = ws.get<uint32_t>("sort_counts", std::max<uint64_t>(tiles, 1));
   const int fused = tiles <= kFusedScanMaxTiles ? 1 : 0;
-  MST_CUDA_CHECK(cudaMemsetAsync(&d_ctr->done[0][kSlotSort], 0, sizeof(unsigned int), ws.stream));
+  // done[0][kSlotSort] is zero: cleared at the run's start, re-armed by every fused scan
   const unsigned g = (unsigned)std::max<uint64_t>(
       1, std::min<uint64_t>(tiles, (uint64_t)sm_count(ws.device) * blocks_per_sm(k_flags_count)));
   launch_k(k_flags_count, g, kBlock, ws.stream, flags, m, counts, d_ctr, fused);
@@ -781,10 +781,10 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   uint32_t* hmasks = ws.get<uint32_t>("hook_masks", tiles_of(n) * kItems * kWarps);
   uint32_t* hslot = ws.get<uint32_t>("hook_slotpref", tiles_of(n) * kItems * kWarps);
 
-  init_counters(ws, d_ctr, n, m);
-  MST_CUDA_CHECK(cudaMemsetAsync(minb[0], 0xFF, (size_t)n * 8, s));
+  // counters, the first min table and the MST flags in one launch (three
+  // stream operations cost c1 ~20 us before its first kernel)
   uint8_t* flags = ws.get<uint8_t>("mst_flags", m + 16);
-  MST_CUDA_CHECK(cudaMemsetAsync(flags, 0, m + 16, s));
+  launch_k(k_init_run, (unsigned)(sm_count(dev) * 4), 256, s, d_ctr, n, m, minb[0], (uint4*)flags, (m + 16) / 16);
   timeline_mark(nullptr, s);
   uint32_t launches = 0;
   int tix = 0;
@@ -887,6 +887,10 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   const bool start_c_ok = tail_on && !filter && std::is_same<InView, SoaView>::value &&
                           knob_i(kKnobTailStartC) != 0 && m <= (32ull << 20) && n <= (16u << 20);
   bool tail_c_pending = false;
+  auto tail_grid = [&]() -> unsigned {
+    const int bps = std::max(1, std::min(blocks_per_sm(k_tail, 0), knob_i(kKnobTailBps)));
+    return std::min<unsigned>(kTailMaxBlocks, (unsigned)(sm_count(dev) * bps));
+  };
   const bool lazy1 = !start_c_ok && !filter && knob_i(kKnobLazyRound1) != 0 &&
                      !(tail_on && (m <= tail_edges() || (uint64_t)n <= tail_small_n) && (uint64_t)n <= tail_comps);
   const uint4* P1 = lazy1 ? reinterpret_cast<const uint4*>(ws.get<uint2>("pairs1", m)) : E[1];
@@ -976,8 +980,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       }
       auto kt = k_tail;
       const size_t tail_smem = 0;  // all static (< 48 KB)
-      const int bps = std::max(1, std::min(blocks_per_sm(kt, tail_smem), knob_i(kKnobTailBps)));
-      const unsigned G = std::min<unsigned>(kTailMaxBlocks, (unsigned)(sm_count(dev) * bps));
+      const unsigned G = tail_grid();
       uint32_t* broots = ws.get<uint32_t>("tail_broots", G);
       uint32_t* bkept = ws.get<uint32_t>("tail_bkept", G);
       uint32_t* tmasks = ws.get<uint32_t>("tail_masks", n_bound / 32 + 64);
@@ -1154,8 +1157,10 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     }
     ++r;
   }
-  MST_CUDA_CHECK(cudaMemcpyAsync(&out.ctr, d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
+  // the sort first: the counter read-back is a copy-engine operation in
+  // the stream that the sort kernels would otherwise queue behind
   if (enqueue_after) (*enqueue_after)();
+  MST_CUDA_CHECK(cudaMemcpyAsync(&out.ctr, d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
   MST_CUDA_CHECK(cudaStreamSynchronize(s));
   const DevCounters& c = out.ctr;
   out.err = c.err;

@@ -2198,9 +2198,9 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
         for (uint32_t c = threadIdx.x; c < n_next; c += kBlock) s_min[c] = kNoKey;
         __syncthreads();
       }
-      const uint64_t seg_hi = seg_lo + seg_len;
       uint64_t out = seg_lo;
       const uint32_t lt = lanemask_lt();
+      const uint64_t seg_hi = seg_lo + seg_len;
       for (uint64_t base = seg_lo; base < seg_hi; base += 32 * kItems) {
         uint4 e[kItems];
         bool live[kItems];
@@ -2295,6 +2295,30 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
 __global__ void k_err_words(const DevCounters* ctr, uint32_t* __restrict__ out) {
   pdl_prologue();
   if (blockIdx.x == 0 && threadIdx.x < 2) out[threadIdx.x] = (ctr->err >> threadIdx.x) & 1u;
+}
+
+// A run's start: zeroed counters with n[1] = n, m[0] = m[1] = m and no
+// verdict (block 0), the first min table all "no key", the MST flags clear.
+__global__ void k_init_run(DevCounters* ctr, uint32_t n, uint64_t m, unsigned long long* __restrict__ minb0,
+                           uint4* __restrict__ flags16, uint64_t flag_vecs) {
+  pdl_prologue();
+  if (blockIdx.x == 0) {
+    static_assert(sizeof(DevCounters) % 4 == 0, "DevCounters is word-sized");
+    uint32_t* cw = reinterpret_cast<uint32_t*>(ctr);
+    for (uint32_t i = threadIdx.x; i < sizeof(DevCounters) / 4; i += blockDim.x) cw[i] = 0u;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      ctr->n[1] = n;
+      ctr->m[0] = m;
+      ctr->m[1] = m;
+      ctr->stop_round = kNoStop;
+      ctr->phase_end = kNoStop;
+      ctr->pivot = 0xFFFFFFFFu;
+    }
+  }
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = tid; i < n; i += stride) minb0[i] = kNoKey;
+  for (uint64_t i = tid; i < flag_vecs; i += stride) flags16[i] = make_uint4(0, 0, 0, 0);
 }
 
 __global__ void k_iota(uint32_t* __restrict__ x, uint64_t count) {
