@@ -132,6 +132,7 @@ enum Knob {
   kKnobL2Fetch,           // cudaLimitMaxL2FetchGranularity in bytes (0: leave the device default)
   kKnobOfferCached,       // offer filter reads through L1 (bit kFiltCached) at these sites (bitmask of OfferSite)
   kKnobRetire,            // light phase: retire isolated components (tables sized by components with edges)
+  kKnobGiantBits,         // relabel rounds with more components than this: giant bits (0 off)
   kKnobTimeline,          // tools only: an event after every launch, per-launch stream times on stderr
   kKnobCount
 };
@@ -152,7 +153,7 @@ constexpr KnobDef kKnobDefs[kKnobCount] = {
     {"MST_DEDUP_MIN_RATIO", 8},  {"MST_DEDUP_CAP_LOG2", 25},
     {"MST_LAZY_ROUND1", 1},      {"MST_PIPELINE_H2D", 0},        {"MST_PIPELINE_CHUNKS", 16},
     {"MST_DEBUG_ROUNDS", 0},     {"MST_L2_FETCH", 0},         {"MST_OFFER_CACHED", 15},
-    {"MST_RETIRE", 1},           {"MST_TIMELINE", 0}};
+    {"MST_RETIRE", 1},           {"MST_GIANT_BITS", 16e6},    {"MST_TIMELINE", 0}};
 
 std::atomic<double>* knob_table() {
   static std::atomic<double> t[kKnobCount];
@@ -617,7 +618,7 @@ template <class View, int kMode>
 void launch_two_pass(Workspace& ws, const CompactBufs& cb, View in, uint4* relabeled, const uint32_t* L, uint4* out,
                      unsigned long long* min_next, DevCounters* d_ctr, int r, uint64_t m_bound, uint32_t n_orig,
                      int slot, int light, int filt, PairTable pt = PairTable{nullptr, nullptr, 0},
-                     bool emit = true) {
+                     bool emit = true, const uint32_t* gbits = nullptr) {
   const int dev = ws.device;
   const uint64_t tiles = tiles_c(m_bound);
   const int fused = tiles <= kFusedScanMaxTiles ? 1 : 0;  // small: the last count block scans
@@ -628,12 +629,12 @@ void launch_two_pass(Workspace& ws, const CompactBufs& cb, View in, uint4* relab
   // armed: this launch relabels + inserts pairs if the device chose dedup
   // (decided and table cleared by k_label2), the kModeDedup pass counts
   launch_k(kcnt, gc, kBlock, ws.stream, in, kMode == kModeRelabel ? relabeled : cb.stage, L, cb.masks, cb.counts, n_orig,
-           d_ctr, r, fused, slot, light, pt, min_next, filt);
+           d_ctr, r, fused, slot, light, pt, min_next, filt, gbits);
   if constexpr (!View::kOriginal) {
     if (armed) {
       auto kdc = k_count<PackedView, kModeDedup>;
       launch_k(kdc, gc, kBlock, ws.stream, PackedView{relabeled}, cb.stage, L, cb.masks, cb.counts, n_orig, d_ctr, r,
-               fused, slot, light, pt, min_next, filt);
+               fused, slot, light, pt, min_next, filt, (const uint32_t*)nullptr);
     }
   }
   if (!fused) {
@@ -1135,8 +1136,22 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
                                         const_cast<uint4*>(P1), Lr, Eout, mnext, d_ctr, r, m, n, kSlotCompact,
                                         (int)light, filt_for(n_bound, kSiteCount, filter));
     } else {
+      // a round with a huge component count (phase D's first on R-MAT):
+      // most endpoints join one giant, whose label the compaction takes from
+      // a bitmap (kernels.cuh k_giant_bits)
+      const uint32_t* gb = nullptr;
+      const double giant_min = knob(kKnobGiantBits);
+      if (giant_min > 0 && !light && (double)n_bound >= giant_min) {
+        uint32_t* bits = ws.get<uint32_t>("giant_bits", (n_bound + 31) / 32 + 1);
+        launch_k(k_pick_giant, 1, 1024, s, (const uint4*)E[r & 1], (const uint32_t*)Lr, d_ctr, r);
+        launch_k(k_giant_bits, (unsigned)(sm_count(dev) * 8), 256, s, (const uint32_t*)Lr, (const DevCounters*)d_ctr, r,
+                 bits);
+        gb = bits;
+        launches += 2;
+      }
       launch_two_pass<PackedView, kModeRelabel>(ws, cb, PackedView{E[r & 1]}, E[r & 1], Lr, Eout, mnext, d_ctr,
-                                                r, m_bound, n, kSlotCompact, (int)light, filt_for(n_bound, kSiteCount, filter), pt);
+                                                r, m_bound, n, kSlotCompact, (int)light, filt_for(n_bound, kSiteCount, filter), pt,
+                                                true, gb);
     }
     tmark();
     launches += 5;

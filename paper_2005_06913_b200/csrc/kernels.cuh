@@ -97,6 +97,7 @@ struct DevCounters {
   unsigned int pair_count[kMaxR];  // distinct pairs inserted
   unsigned int pair_abort[kMaxR];  // table overflowed: keep every edge this round
   unsigned int dedup_fail;         // some dedup attempt overflowed (sticky, see k_label2)
+  unsigned int giant;              // k_pick_giant: the most frequent next-round label of a round's endpoints
 };
 
 
@@ -623,6 +624,73 @@ __global__ void k_fill_keys(unsigned long long* __restrict__ t, const DevCounter
     t[i] = kNoKey;
 }
 
+// Giant bits for a relabel round with a huge component count (phase D's
+// first round on R-MAT: 47 M components, most of which its hooks join into
+// one giant). The most frequent next-round label among the endpoints of
+// kGiantSamples evenly spaced list edges becomes ctr->giant, and
+// gbits[c / 32] marks the components c with L[c] == giant: the round's
+// compaction then relabels those endpoints from an L2-resident bitmap (6 MB)
+// instead of gathering from the DRAM-sized map. Any choice is exact; ties
+// go to the smaller label (deterministic).
+constexpr int kGiantSamples = 8192;
+constexpr int kGiantSlots = 4096;
+__global__ void __launch_bounds__(1024) k_pick_giant(const uint4* __restrict__ E, const uint32_t* __restrict__ L,
+                                                     DevCounters* ctr, int r) {
+  pdl_prologue();
+  __shared__ uint32_t s_key[kGiantSlots];
+  __shared__ uint32_t s_cnt[kGiantSlots];
+  __shared__ unsigned long long s_best[32];
+  if ((uint32_t)r + 1 >= ctr->stop_round) return;
+  const uint64_t m_r = ctr->m[r];
+  for (int i = threadIdx.x; i < kGiantSlots; i += blockDim.x) {
+    s_key[i] = kNone;
+    s_cnt[i] = 0;
+  }
+  __syncthreads();
+  const uint64_t step = m_r / kGiantSamples > 0 ? m_r / kGiantSamples : 1;
+  for (int k = threadIdx.x; k < 2 * kGiantSamples; k += blockDim.x) {
+    const uint64_t i = (uint64_t)(k >> 1) * step;
+    if (i >= m_r) continue;
+    const uint4 e = __ldg(E + i);
+    const uint32_t lab = __ldg(L + ((k & 1) ? e.y : e.x));
+    uint32_t h = (lab * 2654435761u) & (kGiantSlots - 1);
+    for (int probe = 0; probe < 64; ++probe) {
+      const uint32_t cur = atomicCAS(s_key + h, kNone, lab);
+      if (cur == kNone || cur == lab) {
+        atomicAdd(s_cnt + h, 1u);
+        break;
+      }
+      h = (h + 1) & (kGiantSlots - 1);
+    }
+  }
+  __syncthreads();
+  unsigned long long best = 0;  // (count, ~label): max count, then min label
+  for (int i = threadIdx.x; i < kGiantSlots; i += blockDim.x)
+    if (s_cnt[i]) best = max(best, ((unsigned long long)s_cnt[i] << 32) | (uint32_t)~s_key[i]);
+  for (int d = 16; d > 0; d >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, d));
+  if ((threadIdx.x & 31) == 0) s_best[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    best = threadIdx.x < blockDim.x / 32 ? s_best[threadIdx.x] : 0ull;
+    for (int d = 16; d > 0; d >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, d));
+    if (threadIdx.x == 0) ctr->giant = best ? ~(uint32_t)best : kNone;
+  }
+}
+
+__global__ void k_giant_bits(const uint32_t* __restrict__ L, const DevCounters* ctr, int r,
+                             uint32_t* __restrict__ gbits) {
+  pdl_prologue();
+  if ((uint32_t)r + 1 >= ctr->stop_round) return;
+  const uint32_t n_r = ctr->n[r], g = ctr->giant;
+  const uint32_t words = (n_r + 31) / 32;
+  const uint32_t lane = lane_id();
+  for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < words; w += (gridDim.x * blockDim.x) >> 5) {
+    const uint32_t c = w * 32 + lane;
+    const unsigned gb = __ballot_sync(0xffffffffu, c < n_r && __ldcs(L + c) == g);
+    if (lane == 0) gbits[w] = gb;
+  }
+}
+
 // ------------------------------ scan helpers -------------------------------
 //   kScanEdges : m[r+1] = kept; none kept -> stop (or light-phase end)
 //   kScanRoots : n[r+1] = roots; <= 1 -> stop; == n[r] -> stop (or light end)
@@ -838,7 +906,8 @@ __global__ void MST_LB_(MST_MINB_COUNT) k_count(View in, uint4* __restrict__ rel
                                                   uint32_t* __restrict__ masks, uint32_t* __restrict__ counts,
                                                   uint32_t n_orig, DevCounters* ctr, int r, int fused, int slot,
                                                   int light_phase, PairTable pt,
-                                                  unsigned long long* __restrict__ min_next, int filt) {
+                                                  unsigned long long* __restrict__ min_next, int filt,
+                                                  const uint32_t* __restrict__ gbits) {
   pdl_prologue();
   __shared__ uint32_t s_cnt[kWarps];
   __shared__ uint32_t s_slot[kCItems * kWarps];
@@ -855,6 +924,10 @@ __global__ void MST_LB_(MST_MINB_COUNT) k_count(View in, uint4* __restrict__ rel
   const unsigned long long pmask = kMode == kModeDedup ? ctr->pair_mask[r] : 0ull;
   const bool pabort = kMode == kModeDedup && ctr->pair_abort[r] != 0;
   const uint32_t pivot = ctr->pivot;
+  // giant bits (relabel rounds of huge component counts, see k_giant_bits):
+  // an endpoint whose bit is set takes the giant's label without a gather
+  constexpr bool kGiant = kMode == kModeRelabel && !View::kOriginal;
+  const uint32_t giant = (kGiant && gbits) ? ctr->giant : 0u;
   const uint32_t ntiles = (uint32_t)((m_r + kCTile - 1) / kCTile);
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -864,6 +937,15 @@ __global__ void MST_LB_(MST_MINB_COUNT) k_count(View in, uint4* __restrict__ rel
       const uint64_t i = (uint64_t)tile * kCTile + k * kBlock + threadIdx.x;
       e[k] = EdgeRec{0, 0, 0, 0, false};
       if (i < m_r) e[k] = in.stream(i);
+    }
+    uint32_t gwa[kCItems], gwb[kCItems];  // giant words of the endpoints, all in flight first
+    if (kGiant && gbits) {
+#pragma unroll
+      for (int k = 0; k < kCItems; ++k) {
+        const uint64_t i = (uint64_t)tile * kCTile + k * kBlock + threadIdx.x;
+        gwa[k] = i < m_r ? __ldg(gbits + (e[k].a >> 5)) : 0u;
+        gwb[k] = i < m_r ? __ldg(gbits + (e[k].b >> 5)) : 0u;
+      }
     }
     uint32_t err = 0, cnt = 0;
     bool keep[kCItems];
@@ -899,8 +981,13 @@ __global__ void MST_LB_(MST_MINB_COUNT) k_count(View in, uint4* __restrict__ rel
         } else if (View::kMayBeDead && e[k].a == e[k].b) {
           // dead since an earlier round: no gather, no write (stays a == b)
         } else if (ok) {
-          ox = __ldg(L + e[k].a);
-          oy = __ldg(L + e[k].b);
+          if (kGiant && gbits) {
+            ox = ((gwa[k] >> (e[k].a & 31)) & 1u) ? giant : __ldg(L + e[k].a);
+            oy = ((gwb[k] >> (e[k].b & 31)) & 1u) ? giant : __ldg(L + e[k].b);
+          } else {
+            ox = __ldg(L + e[k].a);
+            oy = __ldg(L + e[k].b);
+          }
           keep[k] = ox != oy;
           if (View::kOriginal)
             __stcs(reinterpret_cast<uint2*>(relabeled) + i, make_uint2(ox, oy));

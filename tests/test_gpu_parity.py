@@ -49,6 +49,9 @@ MODES = [dict(MST_FILTER=0), dict(MST_FILTER=1, MST_FILTER_BETA=0.3),
          dict(MST_FILTER=0, MST_TAIL=0, MST_OFFER_MIN1=0, MST_OFFER_COUNT=0),
          # offer filter reads through L2 only (the default reads through L1), light phase without retirement
          dict(MST_FILTER=1, MST_TAIL=0, MST_OFFER_CACHED=0, MST_RETIRE=0),
+         # giant bits in every relabel round (default: >= 16 M components only)
+         dict(MST_FILTER=1, MST_TAIL=0, MST_GIANT_BITS=1),
+         dict(MST_FILTER=0, MST_TAIL=0, MST_GIANT_BITS=1, MST_LAZY_ROUND1=0),
          # the light phase's pair dedup from its second round with a large table
          dict(MST_FILTER=1, MST_TAIL=0, MST_DEDUP_MIN_EDGES=0, MST_DEDUP_ACTIVE=1e9, MST_DEDUP_MIN_RATIO=1,
               MST_DEDUP_TABLE_DIV=1, MST_DEDUP_CAP_LOG2=27)]
