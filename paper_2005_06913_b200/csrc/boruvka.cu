@@ -617,7 +617,7 @@ struct CompactBufs {
 template <class View, int kMode>
 void launch_two_pass(Workspace& ws, const CompactBufs& cb, View in, uint4* relabeled, const uint32_t* L, uint4* out,
                      unsigned long long* min_next, DevCounters* d_ctr, int r, uint64_t m_bound, uint32_t n_orig,
-                     int slot, int light, int filt, PairTable pt = PairTable{nullptr, nullptr, 0},
+                     int slot, int light, int filt, PairTable pt = PairTable{nullptr, 0},
                      bool emit = true, const uint32_t* gbits = nullptr) {
   const int dev = ws.device;
   const uint64_t tiles = tiles_c(m_bound);
@@ -767,11 +767,9 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   unsigned long long* minb[2] = {ws.get<unsigned long long>("minA", n),
                                  ws.get<unsigned long long>("minB", n)};
   uint32_t* parent = ws.get<uint32_t>("parent", n);
-  uint32_t* rootlabel = ws.get<uint32_t>("rootlabel", n);
   uint32_t* L = ws.get<uint32_t>("label", n);
   // the sorted output comes from the per-edge flags (the sharded loop too:
   // every rank sets the flags of every hooked component), no MST slot array
-  uint32_t* mst = nullptr;
   uint4* E[2] = {ws.get<uint4>("E0", m), ws.get<uint4>("E1", m)};
   unsigned long long* st = ws.status_array(std::max(tiles_of(m), tiles_of(n)));
   const int dev = ws.device;
@@ -983,7 +981,6 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       const size_t tail_smem = 0;  // all static (< 48 KB)
       const unsigned G = tail_grid();
       uint32_t* broots = ws.get<uint32_t>("tail_broots", G);
-      uint32_t* bkept = ws.get<uint32_t>("tail_bkept", G);
       uint32_t* tmasks = ws.get<uint32_t>("tail_masks", n_bound / 32 + 64);
       uint32_t* twpref = ws.get<uint32_t>("tail_wpref", n_bound / 32 + 64);
       unsigned long long* trace = nullptr;
@@ -992,7 +989,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
         MST_CUDA_CHECK(cudaMemsetAsync(trace, 0, 512 * 8, s));
       }
       const HookSrc src = hook_src(r);
-      TailArgs ta{{E[0], E[1]}, {minb[0], minb[1]}, parent, rootlabel, L, mst, broots, bkept, tmasks, twpref, M, flags,
+      TailArgs ta{{E[0], E[1]}, {minb[0], minb[1]}, parent, L, broots, tmasks, twpref, M, flags,
                   trace, 0, nullptr, nullptr, nullptr, 0, d_ctr, n, r, (int)light};
       ta.start_c = tail_c_pending ? 1 : 0;
       ta.retired = (light && ret.active()) ? 1 : 0;
@@ -1077,7 +1074,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       auto launch_hook = [&](auto view) {
         auto kd = k_hook_decide<decltype(view)>;
         launch_k(kd, (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ht, (uint64_t)sm_count(dev) * blocks_per_sm(kd))),
-                 kBlock, s, view, mcur, parent, rootlabel, hmasks, hcounts, d_ctr, r, hfused, hphase, hslot, flags, rb);
+                 kBlock, s, view, mcur, parent, hmasks, hcounts, d_ctr, r, hfused, hphase, hslot, flags, rb);
       };
       if (src.kind == kSrcIn)
         launch_hook(in);
@@ -1097,7 +1094,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       levels.push_back({Lr, r});
     }
     // pair dedup is armed for big rounds; k_label2 decides on the device
-    PairTable pt{nullptr, nullptr, 0};
+    PairTable pt{nullptr, 0};
     const bool lazy2 = lazy1 && r == 2;  // round 2 over round 1's uncompacted pairs
     // phase D's first round (Filter-Boruvka): hook + label here, then the
     // tail starts at its phase C over the heavy survivors in place (the host
@@ -1110,14 +1107,14 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       const unsigned long long cap = std::min<unsigned long long>(1ull << std::max(10, std::min(30, knob_i(kKnobDedupCapLog2))),
                                                                    next_pow2(m_bound / 2));
       unsigned long long* tab = ws.get<unsigned long long>("pair_table", 2 * cap);
-      pt = PairTable{tab, nullptr, cap};
+      pt = PairTable{tab, cap};
       launches += 2;
     }
     {
       const unsigned g = (unsigned)std::max<uint64_t>(
           1, std::min<uint64_t>(tiles_of(n_bound), (uint64_t)sm_count(dev) * blocks_per_sm(k_label2)));
-      launch_k(k_label2, g, kBlock, s, parent, rootlabel, hmasks, hslot, hcounts, Lr, mnext, mst, flags, n, d_ctr, r,
-               pt.pairs, pt.cap, dedup_active, pair_div, (const uint32_t*)rb);
+      launch_k(k_label2, g, kBlock, s, parent, hmasks, hslot, hcounts, Lr, mnext, d_ctr, r, pt.pairs, pt.cap,
+               dedup_active, pair_div, (const uint32_t*)rb);
     }
     if ((original_in && start_c_ok) || d_start_c) {  // this round's compaction: the tail's first phase C
       tail_c_pending = true;
@@ -1129,7 +1126,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       // round 2's list), else compacted into E[0]
       launch_two_pass<InView, kModeRelabel>(ws, cb, in, const_cast<uint4*>(P1), Lr, Eout, mnext, d_ctr, r, m_bound, n,
                                             kSlotCompact, (int)light, filt_for(n_bound, kSiteCount, filter),
-                                            PairTable{nullptr, nullptr, 0}, !lazy1);
+                                            PairTable{nullptr, 0}, !lazy1);
     } else if (lazy2) {
       using PV = PairsInView<InView>;
       launch_two_pass<PV, kModeRelabel>(ws, cb, PV{reinterpret_cast<const uint2*>(P1), in, in.base},
@@ -1446,7 +1443,7 @@ struct Shard {
   SoaView in{};
   unsigned long long* minb[2]{};
   unsigned long long *xch = nullptr, *own = nullptr;
-  uint32_t *parent = nullptr, *rootlabel = nullptr, *L = nullptr, *partner = nullptr;
+  uint32_t *parent = nullptr, *L = nullptr, *partner = nullptr;
   uint8_t* flags = nullptr;  // MST flag per global edge id (replicated: every rank sets every flag)
   RetireState ret;           // light-phase retirement (replicated decisions)
   uint32_t* hist = nullptr;  // Filter-Borůvka: weight histogram (summed across shards)
@@ -1703,7 +1700,7 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, uint6
       uint32_t* hmasks = ws.get<uint32_t>("hook_masks", tiles_of(n) * kItems * kWarps);
       uint32_t* hslot = ws.get<uint32_t>("hook_slotpref", tiles_of(n) * kItems * kWarps);
       auto kd = k_hook_decide<PartnerView, true>;
-      launch_k(kd, persistent_grid(kd, dev, ht), kBlock, st, PartnerView{s.partner}, s.xch, s.parent, s.rootlabel, hmasks,
+      launch_k(kd, persistent_grid(kd, dev, ht), kBlock, st, PartnerView{s.partner}, s.xch, s.parent, hmasks,
                hcounts, s.d_ctr, r, hfused, phase, hslot, s.flags, rb);
       if (!hfused)
         launch_k(k_scan_counts<kScanRoots>,
@@ -1711,9 +1708,8 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, uint6
                  kScanBlock, st, hcounts, ht, s.d_ctr, r, s.st, ws.next_epoch(), phase, 0);
       unsigned long long* mnext = s.minb[r & 1];
       uint32_t* Lr = light ? ws.get<uint32_t>("Llvl" + std::to_string(r), n_bound) : s.L;
-      launch_k(k_label2, persistent_grid(k_label2, dev, ht), kBlock, st, s.parent, s.rootlabel, hmasks, hslot, hcounts, Lr,
-               mnext, (uint32_t*)nullptr, (uint8_t*)nullptr, n, s.d_ctr, r, (unsigned long long*)nullptr, 0ull, 0u,
-               4u | (8u << 16), (const uint32_t*)rb);
+      launch_k(k_label2, persistent_grid(k_label2, dev, ht), kBlock, st, s.parent, hmasks, hslot, hcounts, Lr, mnext,
+               s.d_ctr, r, (unsigned long long*)nullptr, 0ull, 0u, 4u | (8u << 16), (const uint32_t*)rb);
       const CompactBufs cb{ws.get<uint32_t>("tile_counts", tiles_c(s.m)),
                            ws.get<uint32_t>("tile_masks", tiles_c(s.m) * kCItems * kWarps), s.st,
                            ws.get<uint4>("stage", tiles_c(s.m) * kCTile)};
@@ -1899,7 +1895,6 @@ RunOut run_sharded(const std::vector<PartSpec>& parts, Exchanger& ex, uint32_t n
     s.xch = ws.get<unsigned long long>("xch", n);
     s.own = ws.get<unsigned long long>("own", n);
     s.parent = ws.get<uint32_t>("parent", n);
-    s.rootlabel = ws.get<uint32_t>("rootlabel", n);
     s.L = ws.get<uint32_t>("label", n);
     s.partner = ws.get<uint32_t>("partner", n);
     s.flags = ws.get<uint8_t>("mst_flags", m_total + 16);

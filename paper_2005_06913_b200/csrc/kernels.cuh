@@ -825,8 +825,7 @@ enum { kModeRelabel = 0, kModeLight = 1, kModeHeavy = 2, kModeDedup = 3 };
 // (active[r]/2)^2/2; dedup when that is < m_r/4.
 struct PairTable {
   unsigned long long* pairs;  // slot i = {pair, min key} at pairs[2i], pairs[2i+1]: one sector
-  unsigned long long* mins;   // unused (layout kept for the launch signature)
-  unsigned long long cap;  // power of two, allocated slots
+  unsigned long long cap;     // power of two, allocated slots
 };
 constexpr unsigned long long kNoPair = ~0ull;
 constexpr int kPairProbes = 64;
@@ -1328,20 +1327,20 @@ __global__ void __launch_bounds__(kBlock) k_shard_partner(const unsigned long lo
 
 // ------------------------------ hook ---------------------------------------
 // k_hook_decide: per component, the partner along its lightest edge, the
-// mutual-pair root rule, parent[], the MST edge id stashed in rootlabel[],
-// a root bitmask, in-tile root prefixes and per-tile root counts; k_label2
-// turns the scanned counts into dense root labels and MST slots.
+// mutual-pair root rule, parent[], the MST flag of the edge, a root bitmask,
+// in-tile root prefixes and per-tile root counts; k_label2 turns the scanned
+// counts into dense root labels.
 // kExchanged: the sharded loop. minimum[c] holds the all-reduced global
 // key (w << 32 | global edge id) and E.partner[c] the other endpoint's label
 // of that edge (all-reduced too), so nothing is gathered from an edge list.
 template <class View, bool kExchanged = false>
 __global__ void MST_LB_(MST_MINB_HOOK) k_hook_decide(View E, const unsigned long long* __restrict__ minimum,
-                                                        uint32_t* __restrict__ parent, uint32_t* __restrict__ rootlabel,
+                                                        uint32_t* __restrict__ parent,
                                                         uint32_t* __restrict__ masks, uint32_t* __restrict__ counts,
                                                         DevCounters* ctr, int r, int fused, int light_phase,
                                                         uint32_t* __restrict__ slotpref,
-                                                        uint8_t* __restrict__ flags = nullptr,
-                                                        uint32_t* __restrict__ rbits = nullptr) {
+                                                        uint8_t* __restrict__ flags,
+                                                        uint32_t* __restrict__ rbits) {
   pdl_prologue();
   __shared__ uint32_t s_cnt[kWarps];
   __shared__ uint32_t s_slot[kItems * kWarps];
@@ -1394,12 +1393,7 @@ __global__ void MST_LB_(MST_MINB_HOOK) k_hook_decide(View E, const unsigned long
           parent[c] = isroot ? (uint32_t)c : o;
           ++active;
           if (!isroot) {
-            // single GPU: the MST flag right here; the sharded loop stashes
-            // the id for its MST slot (placed by k_label2)
-            if (flags)
-              flags[e[k].eid] = 1;
-            else
-              rootlabel[c] = e[k].eid;
+            flags[e[k].eid] = 1;  // the MST edge (global id in the sharded loop)
             wsum += (uint32_t)(key[k] >> 32);
           }
         }
@@ -1455,12 +1449,11 @@ __global__ void MST_LB_(MST_MINB_HOOK) k_hook_decide(View E, const unsigned long
   }
 }
 
-// ------------------------------ label (fused with the MST slots) -------------------
+// ------------------------------ label --------------------------------------
 // The dense label of a root is the number of roots before it; with the
 // hook's root masks, per-tile offsets (scanned counts) and in-tile slot
-// prefixes it is three small loads, so no separate kernel has to write
-// rootlabel[] first: k_label2 writes the MST slots and the relabel in one
-// pass.
+// prefixes it is three small loads, so k_label2 finds every component's
+// root and writes its next-round label in one pass.
 __device__ __forceinline__ uint32_t roots_before(uint32_t x, const uint32_t* __restrict__ masks,
                                                  const uint32_t* __restrict__ slotpref,
                                                  const uint32_t* __restrict__ offsets) {
@@ -1471,23 +1464,20 @@ __device__ __forceinline__ uint32_t roots_before(uint32_t x, const uint32_t* __r
   return __ldg(offsets + t) + __ldg(slotpref + (uint64_t)t * 32 + slot) + __popc(m & ((1u << lane) - 1u));
 }
 
-__global__ void MST_LB_(MST_MINB_LABEL) k_label2(uint32_t* __restrict__ parent, const uint32_t* __restrict__ stash,
+__global__ void MST_LB_(MST_MINB_LABEL) k_label2(uint32_t* __restrict__ parent,
                                                    const uint32_t* __restrict__ masks,
                                                    const uint32_t* __restrict__ slotpref,
                                                    const uint32_t* __restrict__ offsets, uint32_t* __restrict__ L,
-                                                   unsigned long long* __restrict__ min_next,
-                                                   uint32_t* __restrict__ mst, uint8_t* __restrict__ flags,
-                                                   uint32_t n_orig, DevCounters* ctr, int r,
+                                                   unsigned long long* __restrict__ min_next, DevCounters* ctr, int r,
                                                    unsigned long long* pair_keys, unsigned long long pair_cap,
                                                    unsigned int dedup_active, unsigned int pair_div,
                                                    const uint32_t* __restrict__ rbits = nullptr) {
   pdl_prologue();
   if ((uint32_t)r >= ctr->stop_round || (uint32_t)r >= ctr->phase_end) return;
-  const bool labels = (uint32_t)r + 1 < ctr->stop_round;  // the last hook round only emits MST slots
+  if ((uint32_t)r + 1 >= ctr->stop_round) return;  // the last hook round: its MST flags are all set
   const uint32_t n_r = ctr->n[r];
   const uint32_t n_next = ctr->n[r + 1];
-  const uint32_t mst_base = n_orig - n_r;
-  if (labels && pair_keys) {
+  if (pair_keys) {
     // pair dedup decision for this round's compaction + table clear (see
     // "pair dedup"); tried when few active components carry many edges each
     const unsigned long long K = ctr->active[r];
@@ -1535,14 +1525,6 @@ __global__ void MST_LB_(MST_MINB_LABEL) k_label2(uint32_t* __restrict__ parent, 
       own[k] = toff + __ldg(slotpref + (uint64_t)tile * 32 + slot) + __popc(m & lt);
       iso[k] = rbits != nullptr && v[k] && ((__ldg(rbits + (c[k] >> 5)) >> lane) & 1u);
     }
-#pragma unroll
-    for (int k = 0; k < kItems; ++k) {
-      if (!mst || !v[k] || isroot[k]) continue;  // single GPU: flags set by the hook
-      const uint32_t eid = __ldg(stash + c[k]);
-      mst[mst_base + (c[k] - own[k])] = eid;  // the sharded loop's slots
-      if (flags) flags[eid] = 1;
-    }
-    if (!labels) continue;
     bool walk[kItems];
 #pragma unroll
     for (int k = 0; k < kItems; ++k) walk[k] = v[k] && !isroot[k] && !iso[k];
@@ -1591,11 +1573,8 @@ struct TailArgs {
   uint4* E[2];
   unsigned long long* minb[2];
   uint32_t* parent;
-  uint32_t* rootlabel;  // MST edge id of each hooked component (stash)
   uint32_t* L;
-  uint32_t* mst;
   uint32_t* broots;     // [gridDim.x] roots per block chunk (A -> B)
-  uint32_t* bkept;      // unused (the segmented list needs no per-block counts)
   uint32_t* masks;      // root bitmask, one word per 32 components
   uint32_t* wpref;      // roots of the block's chunk before each word
   uint32_t* M;          // light phase: entry-label -> current-label map (n[r0] entries)
@@ -1885,7 +1864,6 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
     // edges kept by round r-1 (C's atomics, complete at the last grid.sync);
     // issued here, first used after A
     const uint64_t m_r = r > a.r0 ? __ldcg(reinterpret_cast<const unsigned long long*>(&a.ctr->m[r])) : m_entry;
-    const uint32_t mst_base = a.n_orig - n_r;
     // ternaries, not a dynamic index: keeps TailArgs out of local memory
     const unsigned long long* mcur = (r & 1) ? a.minb[0] : a.minb[1];
     unsigned long long* mnext = (r & 1) ? a.minb[1] : a.minb[0];
@@ -1944,7 +1922,7 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
               isroot = s_min[o] == key[k] && c < o;
               s_par[c] = isroot ? c : o;
               if (!isroot && b == 0) {  // block 0 records the MST edge (flags, weight)
-                if (a.flags) a.flags[e[k].w] = 1;
+                a.flags[e[k].w] = 1;
                 wsum += (uint32_t)(key[k] >> 32);
               }
             }
@@ -2103,10 +2081,7 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
               isroot = okey[k] == key[k] && c < o;
               a.parent[c] = isroot ? c : o;
               if (!isroot) {
-                if (a.flags)
-                  a.flags[e[k].w] = 1;  // the MST edge
-                else
-                  a.rootlabel[c] = e[k].w;  // the MST edge id, placed in B
+                a.flags[e[k].w] = 1;  // the MST edge
                 wsum += (uint32_t)(key[k] >> 32);
               }
             }
@@ -2192,16 +2167,6 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
         v[k] = c[k] < n_r;
         isroot[k] = v[k] && ((__ldcg(a.masks + (c[k] >> 5)) >> (c[k] & 31)) & 1u);
         walk[k] = v[k] && !isroot[k] && !stop_now;
-      }
-#pragma unroll
-      for (int k = 0; k < kItems; ++k) {
-        if (!a.mst || !v[k] || isroot[k]) continue;  // flags: set in A
-        const uint32_t x = c[k], w = x >> 5;
-        const uint32_t before = s_bpre[x / cs] + __ldcg(a.wpref + w) +
-                                __popc(__ldcg(a.masks + w) & ((1u << (x & 31)) - 1u));
-        const uint32_t eid = __ldcg(a.rootlabel + x);
-        a.mst[mst_base + (x - before)] = eid;
-        if (a.flags) a.flags[eid] = 1;
       }
       if (stop_now) continue;
       find_roots<kItems>(a.parent, c, walk, root);

@@ -401,3 +401,55 @@ def test_pipelined_host_copy(mst, oracle_mod):
                     r = P.boruvka_gpu(g, info=info)
                     assert np.array_equal(r.mst_edges, k.ids.astype(np.int64)) and r.total_weight == k.total_weight
                     assert info.ms_h2d > 0 and info.ms_device > 0
+
+
+def _retire_cases(seed=5):
+    """Graphs whose light phase retires components in several rounds (round
+    kernels only, MST_TAIL=0): a light perfect matching under a heavy path
+    (every component is isolated in light round 2: the phase ends on zero
+    components with edges), a light star forest, and a small R-MAT."""
+    rng = np.random.default_rng(seed)
+    out = []
+    k = 30000
+    n = 2 * k
+    # matching (2i, 2i+1) light, a Hamiltonian path over a permutation heavy
+    perm = rng.permutation(n).astype(np.uint32)
+    src = np.concatenate([np.arange(0, n, 2, dtype=np.uint32), perm[:-1]])
+    dst = np.concatenate([np.arange(1, n, 2, dtype=np.uint32), perm[1:]])
+    w = np.concatenate([rng.permutation(k).astype(np.uint32),
+                        (np.uint32(1 << 28) + rng.permutation(n - 1).astype(np.uint32))])
+    out.append(("matching", n, src, dst, w))
+    # stars: 2000 centres, each with 20 light leaves; centres chained heavily
+    c, leaves = 2000, 20
+    n2 = c * (leaves + 1)
+    centre = np.repeat(np.arange(c, dtype=np.uint32), leaves)
+    leaf = (c + np.arange(c * leaves)).astype(np.uint32)
+    src2 = np.concatenate([centre, np.arange(c - 1, dtype=np.uint32)])
+    dst2 = np.concatenate([leaf, np.arange(1, c, dtype=np.uint32)])
+    w2 = np.concatenate([rng.permutation(c * leaves).astype(np.uint32),
+                         (np.uint32(1 << 29) + rng.permutation(c - 1).astype(np.uint32))])
+    out.append(("stars", n2, src2, dst2, w2))
+    return out
+
+
+@pytest.mark.parametrize("beta", [0.25, 0.5, 1.5])
+def test_light_phase_retirement(mst, oracle_mod, beta):
+    """Retirement of isolated light components (kernels.cuh "retirement"):
+    same MST with and without it, equal to the oracle, for graphs whose
+    light phase ends with every component retired."""
+    from paper_2005_06913_b200 import configs as C
+    P, O = mst, oracle_mod
+    cases = _retire_cases()
+    g = C.generate_host(C.rmat(14, 8, seed=9))
+    cases.append(("rmat14", g.n, g.src, g.dst, g.w))
+    for name, n, src, dst, w in cases:
+        k = O.kruskal(n, src, dst, w)
+        G = P.Graph(n, src, dst, w)
+        for retire in (1, 0):
+            with _env(MST_FILTER=1, MST_TAIL=0, MST_FILTER_BETA=beta, MST_RETIRE=retire, MST_DEDUP_MIN_EDGES=0):
+                r = P.boruvka_gpu(G)
+                e = P.boruvka_gpu_emulated(G, 2)
+            assert r.mst_edges.tolist() == k.ids.tolist(), f"{name} beta={beta} retire={retire}: edge set differs"
+            assert r.total_weight == k.total_weight
+            assert e.mst_edges.tolist() == k.ids.tolist() and e.total_weight == k.total_weight, \
+                f"{name} beta={beta} retire={retire}: 2-shard edge set differs"
