@@ -518,57 +518,30 @@ void launch_k(void (*kernel)(KArgs...), unsigned grid, unsigned block, cudaStrea
   timeline_mark(reinterpret_cast<const void*>(kernel), s);
 }
 
-// Sorted id list from the per-edge flags the hook kernels set.
-uint32_t sort_from_flags(Workspace& ws, const uint8_t* flags, uint64_t m, uint32_t* d_sorted, DevCounters* d_ctr) {
-  const uint64_t tiles = (m + kFlagTile - 1) / kFlagTile;
+// Sorted id list (ascending) from the MST bitmap the hook kernels set.
+// words = (m + 31) / 32; the bitmap buffer is allocated with mst_bits_words(m).
+uint64_t mst_bits_words(uint64_t m) { return ((m + 31) / 32 + 3) & ~3ull; }  // whole uint4 vectors
+uint32_t sort_from_bits(Workspace& ws, const uint32_t* bits, uint64_t m, uint32_t* d_sorted, DevCounters* d_ctr) {
+  const uint64_t words = (m + 31) / 32;
+  const uint64_t tiles = tiles_of(words);
   uint32_t* counts = ws.get<uint32_t>("sort_counts", std::max<uint64_t>(tiles, 1));
   const int fused = tiles <= kFusedScanMaxTiles ? 1 : 0;
   // done[0][kSlotSort] is zero: cleared at the run's start, re-armed by every fused scan
   const unsigned g = (unsigned)std::max<uint64_t>(
-      1, std::min<uint64_t>(tiles, (uint64_t)sm_count(ws.device) * blocks_per_sm(k_flags_count)));
-  launch_k(k_flags_count, g, kBlock, ws.stream, flags, m, counts, d_ctr, fused);
+      1, std::min<uint64_t>(tiles, (uint64_t)sm_count(ws.device) * blocks_per_sm(k_bitmap_count)));
+  launch_k(k_bitmap_count, g, kBlock, ws.stream, bits, words, counts, d_ctr, fused);
   uint32_t launches = 2;
   if (!fused) {
     unsigned long long* st = ws.status_array(tiles);
-    launch_k(k_scan_counts<kScanPlain>, (unsigned)std::max<uint64_t>(
-                                    1, std::min<uint64_t>((tiles + kScanTile - 1) / kScanTile, (uint64_t)sm_count(ws.device))), kScanBlock, ws.stream, counts, tiles, d_ctr, 0, st, ws.next_epoch(), 0, 0);
+    launch_k(k_scan_counts<kScanPlain>,
+             (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((tiles + kScanTile - 1) / kScanTile, (uint64_t)sm_count(ws.device))),
+             kScanBlock, ws.stream, counts, tiles, d_ctr, 0, st, ws.next_epoch(), 0, 0);
     ++launches;
   }
-  // the emit's own residency (more registers + 16 KB of staging per block)
+  // the emit's own residency (32 KB of staging per block)
   const unsigned ge = (unsigned)std::max<uint64_t>(
-      1, std::min<uint64_t>(tiles, (uint64_t)sm_count(ws.device) * blocks_per_sm(k_flags_emit)));
-  launch_k(k_flags_emit, ge, kBlock, ws.stream, flags, m, counts, d_sorted);
-  MST_CUDA_CHECK(cudaGetLastError());
-  return launches;
-}
-
-// Sorted id list (ascending) of `count` distinct ids < m_total, via a bitmap.
-uint32_t sort_ids(Workspace& ws, const uint32_t* d_ids, uint64_t count, uint64_t m_total,
-                  uint32_t* d_sorted, DevCounters* d_ctr) {
-  const uint64_t words = (m_total + 31) / 32;
-  uint32_t* bits = ws.get<uint32_t>("bitmap", words);
-  MST_CUDA_CHECK(cudaMemsetAsync(bits, 0, words * sizeof(uint32_t), ws.stream));
-  uint32_t launches = 0;
-  if (count) {
-    const unsigned g = (unsigned)std::min<uint64_t>((count + 255) / 256, (uint64_t)sm_count(ws.device) * 8);
-    launch_k(k_mark, g, 256, ws.stream, d_ids, (uint32_t)count, bits, m_total);
-    ++launches;
-  }
-  const uint64_t tiles = tiles_of(words);
-  uint32_t* counts = ws.get<uint32_t>("sort_counts", tiles);
-  const int fused = tiles <= kFusedScanMaxTiles ? 1 : 0;
-  MST_CUDA_CHECK(cudaMemsetAsync(&d_ctr->done[0][kSlotSort], 0, sizeof(unsigned int), ws.stream));
-  const unsigned g = (unsigned)std::max<uint64_t>(
-      1, std::min<uint64_t>(tiles, (uint64_t)sm_count(ws.device) * blocks_per_sm(k_bitmap_count)));
-  launch_k(k_bitmap_count, g, kBlock, ws.stream, bits, words, counts, d_ctr, fused);
-  if (!fused) {
-    unsigned long long* st = ws.status_array(tiles_of(words));
-    launch_k(k_scan_counts<kScanPlain>, (unsigned)std::max<uint64_t>(
-                                    1, std::min<uint64_t>((tiles + kScanTile - 1) / kScanTile, (uint64_t)sm_count(ws.device))), kScanBlock, ws.stream, counts, tiles, d_ctr, 0, st, ws.next_epoch(), 0, 0);
-    ++launches;
-  }
-  launch_k(k_bitmap_emit, g, kBlock, ws.stream, bits, words, counts, d_sorted);
-  launches += 2;
+      1, std::min<uint64_t>(tiles, (uint64_t)sm_count(ws.device) * blocks_per_sm(k_bitmap_emit)));
+  launch_k(k_bitmap_emit, ge, kBlock, ws.stream, bits, words, counts, d_sorted);
   MST_CUDA_CHECK(cudaGetLastError());
   return launches;
 }
@@ -782,8 +755,8 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
 
   // counters, the first min table and the MST flags in one launch (three
   // stream operations cost c1 ~20 us before its first kernel)
-  uint8_t* flags = ws.get<uint8_t>("mst_flags", m + 16);
-  launch_k(k_init_run, (unsigned)(sm_count(dev) * 4), 256, s, d_ctr, n, m, minb[0], (uint4*)flags, (m + 16) / 16);
+  uint32_t* flags = ws.get<uint32_t>("mst_bits", mst_bits_words(m));
+  launch_k(k_init_run, (unsigned)(sm_count(dev) * 4), 256, s, d_ctr, n, m, minb[0], (uint4*)flags, mst_bits_words(m) / 4);
   timeline_mark(nullptr, s);
   uint32_t launches = 0;
   int tix = 0;
@@ -1384,14 +1357,14 @@ RunOut run_single(const SingleArgs& a, mst_stats_t* stats) {
   RunOut o;
   uint32_t* d_sorted = a.device_out ? a.out_ids : ws.get<uint32_t>("sorted", std::max<uint32_t>(a.n, 1));
   auto* d_ctr = ws.get<DevCounters>("ctr", 1);
-  uint8_t* d_flags = ws.get<uint8_t>("mst_flags", a.m + 16);
+  uint32_t* d_flags = ws.get<uint32_t>("mst_bits", mst_bits_words(a.m));
   // the sorted ids and their copy-back, enqueued behind the last round: a
   // spanning tree has n - 1 edges, so n - 1 ids are copied (a forest's
   // shorter list is followed by stale slots, which the caller's n - 1
   // capacity holds and the returned count excludes)
   uint32_t sort_launches = 0;
   const std::function<void()> after = [&]() {
-    sort_launches = sort_from_flags(ws, d_flags, std::max<uint64_t>(a.m, 1), d_sorted, d_ctr);
+    sort_launches = sort_from_bits(ws, d_flags, std::max<uint64_t>(a.m, 1), d_sorted, d_ctr);
     MST_CUDA_CHECK(cudaEventRecord(e2, s));
     if (!a.device_out && a.n > 1) copy_d2h(ws, a.out_ids, d_sorted, (uint64_t)(a.n - 1) * 4);
     MST_CUDA_CHECK(cudaEventRecord(e3, s));
@@ -1444,7 +1417,7 @@ struct Shard {
   unsigned long long* minb[2]{};
   unsigned long long *xch = nullptr, *own = nullptr;
   uint32_t *parent = nullptr, *L = nullptr, *partner = nullptr;
-  uint8_t* flags = nullptr;  // MST flag per global edge id (replicated: every rank sets every flag)
+  uint32_t* flags = nullptr;  // MST bitmap over global edge ids (replicated: every rank sets every bit)
   RetireState ret;           // light-phase retirement (replicated decisions)
   uint32_t* hist = nullptr;  // Filter-Borůvka: weight histogram (summed across shards)
   uint32_t* errw = nullptr;  // error bits as counts (summed across shards)
@@ -1578,7 +1551,7 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, uint6
     MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
     init_counters(*s.ws, s.d_ctr, n, s.m);
     MST_CUDA_CHECK(cudaMemsetAsync(s.minb[0], 0xFF, (size_t)n * 8, s.ws->stream));
-    MST_CUDA_CHECK(cudaMemsetAsync(s.flags, 0, m_total + 16, s.ws->stream));
+    MST_CUDA_CHECK(cudaMemsetAsync(s.flags, 0, mst_bits_words(m_total) * 4, s.ws->stream));
     s.ret.init(*s.ws, n, filter && knob_i(kKnobRetire) != 0 && n < (1u << 31));
   }
   if (filter) {
@@ -1897,7 +1870,7 @@ RunOut run_sharded(const std::vector<PartSpec>& parts, Exchanger& ex, uint32_t n
     s.parent = ws.get<uint32_t>("parent", n);
     s.L = ws.get<uint32_t>("label", n);
     s.partner = ws.get<uint32_t>("partner", n);
-    s.flags = ws.get<uint8_t>("mst_flags", m_total + 16);
+    s.flags = ws.get<uint32_t>("mst_bits", mst_bits_words(m_total));
     s.E[0] = ws.get<uint4>("E0", s.m);
     s.E[1] = ws.get<uint4>("E1", s.m);
     s.d_ctr = ws.get<DevCounters>("ctr", 1);
@@ -1913,7 +1886,7 @@ RunOut run_sharded(const std::vector<PartSpec>& parts, Exchanger& ex, uint32_t n
   Workspace& ws0 = *sh[0].ws;
   MST_CUDA_CHECK(cudaSetDevice(ws0.device));
   uint32_t* d_sorted = device_out ? out_ids : ws0.get<uint32_t>("sorted", n);
-  o.launches += sort_from_flags(ws0, sh[0].flags, std::max<uint64_t>(m_total, 1), d_sorted, sh[0].d_ctr);
+  o.launches += sort_from_bits(ws0, sh[0].flags, std::max<uint64_t>(m_total, 1), d_sorted, sh[0].d_ctr);
   MST_CUDA_CHECK(cudaEventRecord(e2, ws0.stream));
   if (o.count && out_ids && !device_out)
     copy_d2h(ws0, out_ids, d_sorted, o.count * 4);

@@ -220,6 +220,13 @@ struct PairsInView {
 
 // ------------------------------ primitives ---------------------------------
 
+// The MST output: one bit per edge id (c4: 143 MB, mostly L2-resident, where
+// a byte per edge was 1.14 GB of partial-sector writes), set by a
+// fire-and-forget RED.OR from the hook of the edge's component.
+__device__ __forceinline__ void mst_set(uint32_t* bits, uint32_t eid) {
+  atomicOr(bits + (eid >> 5), 1u << (eid & 31));
+}
+
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
@@ -1339,7 +1346,7 @@ __global__ void MST_LB_(MST_MINB_HOOK) k_hook_decide(View E, const unsigned long
                                                         uint32_t* __restrict__ masks, uint32_t* __restrict__ counts,
                                                         DevCounters* ctr, int r, int fused, int light_phase,
                                                         uint32_t* __restrict__ slotpref,
-                                                        uint8_t* __restrict__ flags,
+                                                        uint32_t* __restrict__ mst_bits,
                                                         uint32_t* __restrict__ rbits) {
   pdl_prologue();
   __shared__ uint32_t s_cnt[kWarps];
@@ -1393,7 +1400,7 @@ __global__ void MST_LB_(MST_MINB_HOOK) k_hook_decide(View E, const unsigned long
           parent[c] = isroot ? (uint32_t)c : o;
           ++active;
           if (!isroot) {
-            flags[e[k].eid] = 1;  // the MST edge (global id in the sharded loop)
+            mst_set(mst_bits, e[k].eid);  // the MST edge (global id in the sharded loop)
             wsum += (uint32_t)(key[k] >> 32);
           }
         }
@@ -1578,7 +1585,7 @@ struct TailArgs {
   uint32_t* masks;      // root bitmask, one word per 32 components
   uint32_t* wpref;      // roots of the block's chunk before each word
   uint32_t* M;          // light phase: entry-label -> current-label map (n[r0] entries)
-  uint8_t* flags;       // MST edge flags (sorted output)
+  uint32_t* mst_bits;   // MST edge bitmap (sorted output)
   unsigned long long* trace;  // optional: globaltimer stamps at phase boundaries (block 0)
   // the list the entry round's keys index (kTailSrc*): a packed list, round
   // 1's label pairs with the caller's weights, or the caller's SoA / AoS list
@@ -1922,7 +1929,7 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
               isroot = s_min[o] == key[k] && c < o;
               s_par[c] = isroot ? c : o;
               if (!isroot && b == 0) {  // block 0 records the MST edge (flags, weight)
-                a.flags[e[k].w] = 1;
+                mst_set(a.mst_bits, e[k].w);
                 wsum += (uint32_t)(key[k] >> 32);
               }
             }
@@ -2081,7 +2088,7 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
               isroot = okey[k] == key[k] && c < o;
               a.parent[c] = isroot ? c : o;
               if (!isroot) {
-                a.flags[e[k].w] = 1;  // the MST edge
+                mst_set(a.mst_bits, e[k].w);  // the MST edge
                 wsum += (uint32_t)(key[k] >> 32);
               }
             }
@@ -2350,9 +2357,9 @@ __global__ void k_err_words(const DevCounters* ctr, uint32_t* __restrict__ out) 
 }
 
 // A run's start: zeroed counters with n[1] = n, m[0] = m[1] = m and no
-// verdict (block 0), the first min table all "no key", the MST flags clear.
+// verdict (block 0), the first min table all "no key", the MST bitmap clear.
 __global__ void k_init_run(DevCounters* ctr, uint32_t n, uint64_t m, unsigned long long* __restrict__ minb0,
-                           uint4* __restrict__ flags16, uint64_t flag_vecs) {
+                           uint4* __restrict__ bits16, uint64_t bit_vecs) {
   pdl_prologue();
   if (blockIdx.x == 0) {
     static_assert(sizeof(DevCounters) % 4 == 0, "DevCounters is word-sized");
@@ -2370,7 +2377,7 @@ __global__ void k_init_run(DevCounters* ctr, uint32_t n, uint64_t m, unsigned lo
   }
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = tid; i < n; i += stride) minb0[i] = kNoKey;
-  for (uint64_t i = tid; i < flag_vecs; i += stride) flags16[i] = make_uint4(0, 0, 0, 0);
+  for (uint64_t i = tid; i < bit_vecs; i += stride) bits16[i] = make_uint4(0, 0, 0, 0);
 }
 
 __global__ void k_iota(uint32_t* __restrict__ x, uint64_t count) {
@@ -2403,15 +2410,6 @@ __global__ void k_shard_min(ShardPtrs<T, 8> bufs, int shards, uint64_t count) {
   }
 }
 
-__global__ void k_mark(const uint32_t* __restrict__ ids, uint32_t count, uint32_t* __restrict__ bits,
-                       uint64_t m) {
-  pdl_prologue();
-  const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
-    const uint32_t e = ids[i];
-    if (e < m) atomicOr(bits + (e >> 5), 1u << (e & 31));
-  }
-}
 
 // Sorted id list from the bitmap: popc per word, ordered scan with look-back,
 // then each word writes its set bits in ascending order.
@@ -2448,11 +2446,16 @@ __global__ void __launch_bounds__(kBlock) k_bitmap_count(const uint32_t* __restr
   }
 }
 
+// Ascending MST ids from the bitmap: a warp's ids for item k come from 32
+// consecutive words, one contiguous run of <= 1024, staged in shared memory
+// and stored coalesced (lane-by-lane stores from the bit loops would touch
+// one sector per lane).
 __global__ void __launch_bounds__(kBlock) k_bitmap_emit(const uint32_t* __restrict__ bits, uint64_t words,
                                                         const uint32_t* __restrict__ offsets,
                                                         uint32_t* __restrict__ out) {
   pdl_prologue();
   __shared__ uint32_t s_scan[32];
+  __shared__ uint32_t s_stage[kWarps][32 * 32];
   const uint32_t ntiles = (uint32_t)((words + kTile - 1) / kTile);
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -2475,105 +2478,15 @@ __global__ void __launch_bounds__(kBlock) k_bitmap_emit(const uint32_t* __restri
     const uint32_t prefix = __ldg(offsets + tile);
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
-      const uint64_t i = (uint64_t)tile * kTile + k * kBlock + threadIdx.x;
-      uint32_t pos = prefix + s_scan[k * kWarps + warp] + incl[k] - cnt[k];
-      uint32_t x = wv[k];
-      while (x) {
-        const int bit = __ffs(x) - 1;
-        x &= x - 1;
-        out[pos++] = (uint32_t)(i * 32 + bit);
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// Sorted output from per-edge flags set by the hook kernels (no atomics):
-// count set flags per tile of kTile x 16 bytes, scan, emit ids ascending.
-constexpr int kFlagTile = kTile * 16;
-
-__global__ void __launch_bounds__(kBlock) k_flags_count(const uint8_t* __restrict__ flags, uint64_t m,
-                                                        uint32_t* __restrict__ counts, DevCounters* ctr, int fused) {
-  pdl_prologue();
-  __shared__ uint32_t s_cnt[kWarps];
-  const uint32_t ntiles = (uint32_t)((m + kFlagTile - 1) / kFlagTile);
-  const uint64_t nvec = (m + 15) / 16;
-  const uint4* v4 = reinterpret_cast<const uint4*>(flags);
-  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    uint32_t c = 0;
-#pragma unroll
-    for (int k = 0; k < kItems; ++k) {
-      const uint64_t i = (uint64_t)tile * kTile + k * kBlock + threadIdx.x;
-      if (i < nvec) {
-        const uint4 v = __ldcs(v4 + i);
-        c += ((v.x * 0x01010101u) >> 24) + ((v.y * 0x01010101u) >> 24) + ((v.z * 0x01010101u) >> 24) +
-             ((v.w * 0x01010101u) >> 24);
-      }
-    }
-    c = warp_sum<uint32_t>(c);
-    if (lane_id() == 0) s_cnt[threadIdx.x >> 5] = c;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint32_t t = 0;
-      for (int w = 0; w < kWarps; ++w) t += s_cnt[w];
-      counts[tile] = t;
-    }
-    __syncthreads();
-  }
-  if (fused) {
-    __shared__ uint32_t s_warp[kWarps + 1], s_flag;
-    fused_scan_if_last<kScanPlain>(counts, ntiles, ctr, 0, kSlotSort, 0, s_warp, &s_flag);
-  }
-}
-
-__global__ void __launch_bounds__(kBlock) k_flags_emit(const uint8_t* __restrict__ flags, uint64_t m,
-                                                       const uint32_t* __restrict__ offsets,
-                                                       uint32_t* __restrict__ out) {
-  pdl_prologue();
-  __shared__ uint32_t s_scan[32];
-  __shared__ uint32_t s_stage[kWarps][32 * 16];
-  const uint32_t ntiles = (uint32_t)((m + kFlagTile - 1) / kFlagTile);
-  const uint64_t nvec = (m + 15) / 16;
-  const uint4* v4 = reinterpret_cast<const uint4*>(flags);
-  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    uint4 v[kItems];
-    uint32_t cnt[kItems], incl[kItems];
-#pragma unroll
-    for (int k = 0; k < kItems; ++k) {
-      const uint64_t i = (uint64_t)tile * kTile + k * kBlock + threadIdx.x;
-      v[k] = i < nvec ? __ldcs(v4 + i) : make_uint4(0, 0, 0, 0);
-      cnt[k] = ((v[k].x * 0x01010101u) >> 24) + ((v[k].y * 0x01010101u) >> 24) + ((v[k].z * 0x01010101u) >> 24) +
-               ((v[k].w * 0x01010101u) >> 24);
-      incl[k] = warp_incl_scan(cnt[k]);
-      if (lane == 31) s_scan[k * kWarps + warp] = incl[k];
-    }
-    __syncthreads();
-    if (warp == 0) {
-      const uint32_t x = s_scan[lane];
-      const uint32_t in = warp_incl_scan(x);
-      s_scan[lane] = in - x;
-    }
-    __syncthreads();
-    const uint32_t prefix = __ldg(offsets + tile);
-#pragma unroll
-    for (int k = 0; k < kItems; ++k) {
-      // a warp's ids for item k are one contiguous run of <= 512: stage them
-      // in shared memory, then store the run coalesced (lane-by-lane stores
-      // from the bit loop hit one sector per lane per store)
       const uint32_t wtot = __shfl_sync(0xffffffffu, incl[k], 31);
       if (!wtot) continue;
       const uint64_t i = (uint64_t)tile * kTile + k * kBlock + threadIdx.x;
       uint32_t pos = incl[k] - cnt[k];
-      const uint32_t words[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint32_t wd = words[q];
-        while (wd) {
-          const int byte = (__ffs(wd) - 1) >> 3;
-          wd &= ~(0xFFu << (byte * 8));
-          s_stage[warp][pos++] = (uint32_t)(i * 16 + q * 4 + byte);
-        }
+      uint32_t x = wv[k];
+      while (x) {
+        const int bit = __ffs(x) - 1;
+        x &= x - 1;
+        s_stage[warp][pos++] = (uint32_t)(i * 32 + bit);
       }
       __syncwarp();
       uint32_t* dst = out + prefix + s_scan[k * kWarps + warp];
@@ -2583,5 +2496,6 @@ __global__ void __launch_bounds__(kBlock) k_flags_emit(const uint8_t* __restrict
     __syncthreads();
   }
 }
+
 
 }  // namespace mstgpu

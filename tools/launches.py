@@ -14,7 +14,7 @@ for r in rows:
         d = dict(zip(hdr, r))
         nm = d['Kernel Name'].split('(')[0].replace('void ', '').replace('mstgpu::', '').replace('<unnamed>::', '')
         out.append((nm[:60], float(d['Metric Value'])))
-ends = [i for i, (k, _) in enumerate(out) if k.startswith(('k_bitmap_emit', 'k_flags_emit'))]
+ends = [i for i, (k, _) in enumerate(out) if k.startswith(("k_bitmap_emit", "k_flags_emit"))]
 start = ends[-2] + 1 if len(ends) >= 2 else 0
 last = out[start:ends[-1] + 1]
 tot = sum(v for _, v in last)
