@@ -868,7 +868,7 @@ __device__ __forceinline__ void dedup_insert(uint4* __restrict__ E, const uint32
       const uint64_t i = base + k * kBlock + threadIdx.x;
       if (i >= m_r) continue;
       const uint32_t x = __ldg(L + e[k].x), y = __ldg(L + e[k].y);
-      *reinterpret_cast<uint2*>(E + i) = make_uint2(x, y);
+      E[i] = make_uint4(x, y, e[k].z, e[k].w);  // whole entry (see k_count)
       if (x == y || aborted) continue;
       const unsigned long long pair = ((unsigned long long)min(x, y) << 32) | max(x, y);
       const unsigned long long key = ((unsigned long long)e[k].z << 32) | (uint32_t)i;
@@ -998,7 +998,9 @@ __global__ void MST_LB_(MST_MINB_COUNT) k_count(View in, uint4* __restrict__ rel
           if (View::kOriginal)
             __stcs(reinterpret_cast<uint2*>(relabeled) + i, make_uint2(ox, oy));
           else
-            __stcs(reinterpret_cast<uint2*>(relabeled + i), make_uint2(ox, oy));
+            // the whole 16 B entry: an 8 B store into it is a partial-sector
+            // write, merged in L2 (or read back from DRAM once evicted)
+            __stcs(relabeled + i, make_uint4(ox, oy, e[k].w, e[k].eid));
         } else if (View::kOriginal && kMode == kModeRelabel) {
           __stcs(reinterpret_cast<uint2*>(relabeled) + i, make_uint2(0, 0));  // rejected edge: a self-loop
         }
