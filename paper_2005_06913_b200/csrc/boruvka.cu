@@ -521,6 +521,34 @@ void launch_k(void (*kernel)(KArgs...), unsigned grid, unsigned block, cudaStrea
 // Sorted id list (ascending) from the MST bitmap the hook kernels set.
 // words = (m + 31) / 32; the bitmap buffer is allocated with mst_bits_words(m).
 uint64_t mst_bits_words(uint64_t m) { return ((m + 31) / 32 + 3) & ~3ull; }  // whole uint4 vectors
+// The single-GPU output's words: one byte per edge up to kMstBytesMax edges
+// (kernels.cuh mst_mark), else the bitmap.
+bool mst_out_bytes(uint64_t m) { return m <= kMstBytesMax; }
+uint64_t mst_out_words(uint64_t m) { return mst_out_bytes(m) ? ((m + 16 + 15) / 16) * 4 : mst_bits_words(m); }
+
+// Sorted id list from one flag byte per edge (small lists, see mst_mark).
+uint32_t sort_from_bytes(Workspace& ws, const uint8_t* flags, uint64_t m, uint32_t* d_sorted, DevCounters* d_ctr) {
+  const uint64_t tiles = (m + kFlagTile - 1) / kFlagTile;
+  uint32_t* counts = ws.get<uint32_t>("sort_counts", std::max<uint64_t>(tiles, 1));
+  const int fused = tiles <= kFusedScanMaxTiles ? 1 : 0;
+  // done[0][kSlotSort] is zero: cleared at the run's start, re-armed by every fused scan
+  const unsigned g = (unsigned)std::max<uint64_t>(
+      1, std::min<uint64_t>(tiles, (uint64_t)sm_count(ws.device) * blocks_per_sm(k_flags_count)));
+  launch_k(k_flags_count, g, kBlock, ws.stream, flags, m, counts, d_ctr, fused);
+  uint32_t launches = 2;
+  if (!fused) {
+    unsigned long long* st = ws.status_array(tiles);
+    launch_k(k_scan_counts<kScanPlain>,
+             (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((tiles + kScanTile - 1) / kScanTile, (uint64_t)sm_count(ws.device))),
+             kScanBlock, ws.stream, counts, tiles, d_ctr, 0, st, ws.next_epoch(), 0, 0);
+    ++launches;
+  }
+  const unsigned ge = (unsigned)std::max<uint64_t>(
+      1, std::min<uint64_t>(tiles, (uint64_t)sm_count(ws.device) * blocks_per_sm(k_flags_emit)));
+  launch_k(k_flags_emit, ge, kBlock, ws.stream, flags, m, counts, d_sorted);
+  MST_CUDA_CHECK(cudaGetLastError());
+  return launches;
+}
 uint32_t sort_from_bits(Workspace& ws, const uint32_t* bits, uint64_t m, uint32_t* d_sorted, DevCounters* d_ctr) {
   const uint64_t words = (m + 31) / 32;
   const uint64_t tiles = tiles_of(words);
@@ -755,8 +783,9 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
 
   // counters, the first min table and the MST flags in one launch (three
   // stream operations cost c1 ~20 us before its first kernel)
-  uint32_t* flags = ws.get<uint32_t>("mst_bits", mst_bits_words(m));
-  launch_k(k_init_run, (unsigned)(sm_count(dev) * 4), 256, s, d_ctr, n, m, minb[0], (uint4*)flags, mst_bits_words(m) / 4);
+  uint32_t* flags = ws.get<uint32_t>("mst_bits", mst_out_words(m));
+  const int mst_bytes = mst_out_bytes(m) ? 1 : 0;
+  launch_k(k_init_run, (unsigned)(sm_count(dev) * 4), 256, s, d_ctr, n, m, minb[0], (uint4*)flags, mst_out_words(m) / 4);
   timeline_mark(nullptr, s);
   uint32_t launches = 0;
   int tix = 0;
@@ -965,6 +994,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       TailArgs ta{{E[0], E[1]}, {minb[0], minb[1]}, parent, L, broots, tmasks, twpref, M, flags,
                   trace, 0, nullptr, nullptr, nullptr, 0, d_ctr, n, r, (int)light};
       ta.start_c = tail_c_pending ? 1 : 0;
+      ta.mst_bytes = mst_bytes;
       ta.retired = (light && ret.active()) ? 1 : 0;
       ta.c_soa = (tail_c_pending && r == 1) ? 1 : 0;
       if (knob_i(kKnobTailTiny)) {
@@ -1047,7 +1077,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       auto launch_hook = [&](auto view) {
         auto kd = k_hook_decide<decltype(view)>;
         launch_k(kd, (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ht, (uint64_t)sm_count(dev) * blocks_per_sm(kd))),
-                 kBlock, s, view, mcur, parent, hmasks, hcounts, d_ctr, r, hfused, hphase, hslot, flags, rb);
+                 kBlock, s, view, mcur, parent, hmasks, hcounts, d_ctr, r, hfused, hphase, hslot, flags, mst_bytes, rb);
       };
       if (src.kind == kSrcIn)
         launch_hook(in);
@@ -1357,14 +1387,17 @@ RunOut run_single(const SingleArgs& a, mst_stats_t* stats) {
   RunOut o;
   uint32_t* d_sorted = a.device_out ? a.out_ids : ws.get<uint32_t>("sorted", std::max<uint32_t>(a.n, 1));
   auto* d_ctr = ws.get<DevCounters>("ctr", 1);
-  uint32_t* d_flags = ws.get<uint32_t>("mst_bits", mst_bits_words(a.m));
+  uint32_t* d_flags = ws.get<uint32_t>("mst_bits", mst_out_words(a.m));
   // the sorted ids and their copy-back, enqueued behind the last round: a
   // spanning tree has n - 1 edges, so n - 1 ids are copied (a forest's
   // shorter list is followed by stale slots, which the caller's n - 1
   // capacity holds and the returned count excludes)
   uint32_t sort_launches = 0;
   const std::function<void()> after = [&]() {
-    sort_launches = sort_from_bits(ws, d_flags, std::max<uint64_t>(a.m, 1), d_sorted, d_ctr);
+    sort_launches = mst_out_bytes(a.m)
+                        ? sort_from_bytes(ws, reinterpret_cast<const uint8_t*>(d_flags), std::max<uint64_t>(a.m, 1),
+                                          d_sorted, d_ctr)
+                        : sort_from_bits(ws, d_flags, std::max<uint64_t>(a.m, 1), d_sorted, d_ctr);
     MST_CUDA_CHECK(cudaEventRecord(e2, s));
     if (!a.device_out && a.n > 1) copy_d2h(ws, a.out_ids, d_sorted, (uint64_t)(a.n - 1) * 4);
     MST_CUDA_CHECK(cudaEventRecord(e3, s));
@@ -1674,7 +1707,7 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, uint6
       uint32_t* hslot = ws.get<uint32_t>("hook_slotpref", tiles_of(n) * kItems * kWarps);
       auto kd = k_hook_decide<PartnerView, true>;
       launch_k(kd, persistent_grid(kd, dev, ht), kBlock, st, PartnerView{s.partner}, s.xch, s.parent, hmasks,
-               hcounts, s.d_ctr, r, hfused, phase, hslot, s.flags, rb);
+               hcounts, s.d_ctr, r, hfused, phase, hslot, s.flags, 0, rb);
       if (!hfused)
         launch_k(k_scan_counts<kScanRoots>,
                  (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((ht + kScanTile - 1) / kScanTile, (uint64_t)sm_count(dev))),

@@ -69,6 +69,7 @@ constexpr int kCTile = kBlock * kCItems;
 constexpr int kMaxR = MST_MAX_ROUNDS + 2;
 constexpr uint64_t kNoKey = ~0ull;
 constexpr int kFiltCached = 8;  // offer filter reads through L1 (see offer)
+constexpr uint64_t kMstBytesMax = 64ull << 20;  // output as bytes (not bits) up to this many edges
 constexpr uint32_t kRetFlag = 0x80000000u;  // level-map entry of a retired component: kRetFlag | own index
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr uint32_t kErrRange = 1u;
@@ -225,6 +226,17 @@ struct PairsInView {
 // fire-and-forget RED.OR from the hook of the edge's component.
 __device__ __forceinline__ void mst_set(uint32_t* bits, uint32_t eid) {
   atomicOr(bits + (eid >> 5), 1u << (eid & 31));
+}
+// The output for a caller's list small enough that one byte per edge stays
+// in L2 (<= kMstBytesMax edges): plain byte stores. Grids hook neighbouring
+// components along neighbouring edges, ~16 MST edges per bitmap word, whose
+// REDs queue on the same word (c1 round-1 hook: 57 us with the bitmap, 39 us
+// with bytes).
+__device__ __forceinline__ void mst_mark(uint32_t* out, int bytes, uint32_t eid) {
+  if (bytes)
+    reinterpret_cast<uint8_t*>(out)[eid] = 1;
+  else
+    mst_set(out, eid);
 }
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
@@ -1348,7 +1360,7 @@ __global__ void MST_LB_(MST_MINB_HOOK) k_hook_decide(View E, const unsigned long
                                                         uint32_t* __restrict__ masks, uint32_t* __restrict__ counts,
                                                         DevCounters* ctr, int r, int fused, int light_phase,
                                                         uint32_t* __restrict__ slotpref,
-                                                        uint32_t* __restrict__ mst_bits,
+                                                        uint32_t* __restrict__ mst_bits, int mst_bytes,
                                                         uint32_t* __restrict__ rbits) {
   pdl_prologue();
   __shared__ uint32_t s_cnt[kWarps];
@@ -1402,7 +1414,7 @@ __global__ void MST_LB_(MST_MINB_HOOK) k_hook_decide(View E, const unsigned long
           parent[c] = isroot ? (uint32_t)c : o;
           ++active;
           if (!isroot) {
-            mst_set(mst_bits, e[k].eid);  // the MST edge (global id in the sharded loop)
+            mst_mark(mst_bits, mst_bytes, e[k].eid);  // the MST edge (global id in the sharded loop)
             wsum += (uint32_t)(key[k] >> 32);
           }
         }
@@ -1587,7 +1599,7 @@ struct TailArgs {
   uint32_t* masks;      // root bitmask, one word per 32 components
   uint32_t* wpref;      // roots of the block's chunk before each word
   uint32_t* M;          // light phase: entry-label -> current-label map (n[r0] entries)
-  uint32_t* mst_bits;   // MST edge bitmap (sorted output)
+  uint32_t* mst_bits;   // MST output: bitmap, or one byte per edge (mst_bytes)
   unsigned long long* trace;  // optional: globaltimer stamps at phase boundaries (block 0)
   // the list the entry round's keys index (kTailSrc*): a packed list, round
   // 1's label pairs with the caller's weights, or the caller's SoA / AoS list
@@ -1617,6 +1629,7 @@ struct TailArgs {
   // light phase after retiring round kernels: components outside the tail's
   // label space exist, so one component left ends the light phase, not the MST
   int retired;
+  int mst_bytes;
 };
 
 constexpr uint32_t kTailSmemMin = 2048;  // block-local min table entries (16 KB); tiny rounds up to this
@@ -1931,7 +1944,7 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
               isroot = s_min[o] == key[k] && c < o;
               s_par[c] = isroot ? c : o;
               if (!isroot && b == 0) {  // block 0 records the MST edge (flags, weight)
-                mst_set(a.mst_bits, e[k].w);
+                mst_mark(a.mst_bits, a.mst_bytes, e[k].w);
                 wsum += (uint32_t)(key[k] >> 32);
               }
             }
@@ -2090,7 +2103,7 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
               isroot = okey[k] == key[k] && c < o;
               a.parent[c] = isroot ? c : o;
               if (!isroot) {
-                mst_set(a.mst_bits, e[k].w);  // the MST edge
+                mst_mark(a.mst_bits, a.mst_bytes, e[k].w);  // the MST edge
                 wsum += (uint32_t)(key[k] >> 32);
               }
             }
@@ -2418,6 +2431,102 @@ __global__ void k_shard_min(ShardPtrs<T, 8> bufs, int shards, uint64_t count) {
 // Sorted output, two passes like the compactions: popcount per tile of
 // bitmap words (+ fused or separate scan), then each word writes its set
 // bits at their final positions in ascending order.
+// Sorted output from per-edge flags set by the hook kernels (no atomics):
+// count set flags per tile of kTile x 16 bytes, scan, emit ids ascending.
+constexpr int kFlagTile = kTile * 16;
+
+__global__ void __launch_bounds__(kBlock) k_flags_count(const uint8_t* __restrict__ flags, uint64_t m,
+                                                        uint32_t* __restrict__ counts, DevCounters* ctr, int fused) {
+  pdl_prologue();
+  __shared__ uint32_t s_cnt[kWarps];
+  const uint32_t ntiles = (uint32_t)((m + kFlagTile - 1) / kFlagTile);
+  const uint64_t nvec = (m + 15) / 16;
+  const uint4* v4 = reinterpret_cast<const uint4*>(flags);
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      const uint64_t i = (uint64_t)tile * kTile + k * kBlock + threadIdx.x;
+      if (i < nvec) {
+        const uint4 v = __ldcs(v4 + i);
+        c += ((v.x * 0x01010101u) >> 24) + ((v.y * 0x01010101u) >> 24) + ((v.z * 0x01010101u) >> 24) +
+             ((v.w * 0x01010101u) >> 24);
+      }
+    }
+    c = warp_sum<uint32_t>(c);
+    if (lane_id() == 0) s_cnt[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t t = 0;
+      for (int w = 0; w < kWarps; ++w) t += s_cnt[w];
+      counts[tile] = t;
+    }
+    __syncthreads();
+  }
+  if (fused) {
+    __shared__ uint32_t s_warp[kWarps + 1], s_flag;
+    fused_scan_if_last<kScanPlain>(counts, ntiles, ctr, 0, kSlotSort, 0, s_warp, &s_flag);
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) k_flags_emit(const uint8_t* __restrict__ flags, uint64_t m,
+                                                       const uint32_t* __restrict__ offsets,
+                                                       uint32_t* __restrict__ out) {
+  pdl_prologue();
+  __shared__ uint32_t s_scan[32];
+  __shared__ uint32_t s_stage[kWarps][32 * 16];
+  const uint32_t ntiles = (uint32_t)((m + kFlagTile - 1) / kFlagTile);
+  const uint64_t nvec = (m + 15) / 16;
+  const uint4* v4 = reinterpret_cast<const uint4*>(flags);
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    uint4 v[kItems];
+    uint32_t cnt[kItems], incl[kItems];
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      const uint64_t i = (uint64_t)tile * kTile + k * kBlock + threadIdx.x;
+      v[k] = i < nvec ? __ldcs(v4 + i) : make_uint4(0, 0, 0, 0);
+      cnt[k] = ((v[k].x * 0x01010101u) >> 24) + ((v[k].y * 0x01010101u) >> 24) + ((v[k].z * 0x01010101u) >> 24) +
+               ((v[k].w * 0x01010101u) >> 24);
+      incl[k] = warp_incl_scan(cnt[k]);
+      if (lane == 31) s_scan[k * kWarps + warp] = incl[k];
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t x = s_scan[lane];
+      const uint32_t in = warp_incl_scan(x);
+      s_scan[lane] = in - x;
+    }
+    __syncthreads();
+    const uint32_t prefix = __ldg(offsets + tile);
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      // a warp's ids for item k are one contiguous run of <= 512: stage them
+      // in shared memory, then store the run coalesced (lane-by-lane stores
+      // from the bit loop hit one sector per lane per store)
+      const uint32_t wtot = __shfl_sync(0xffffffffu, incl[k], 31);
+      if (!wtot) continue;
+      const uint64_t i = (uint64_t)tile * kTile + k * kBlock + threadIdx.x;
+      uint32_t pos = incl[k] - cnt[k];
+      const uint32_t words[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t wd = words[q];
+        while (wd) {
+          const int byte = (__ffs(wd) - 1) >> 3;
+          wd &= ~(0xFFu << (byte * 8));
+          s_stage[warp][pos++] = (uint32_t)(i * 16 + q * 4 + byte);
+        }
+      }
+      __syncwarp();
+      uint32_t* dst = out + prefix + s_scan[k * kWarps + warp];
+      for (uint32_t j = lane; j < wtot; j += 32) __stcs(dst + j, s_stage[warp][j]);
+      __syncwarp();
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(kBlock) k_bitmap_count(const uint32_t* __restrict__ bits, uint64_t words,
                                                          uint32_t* __restrict__ counts, DevCounters* ctr,
                                                          int fused) {
