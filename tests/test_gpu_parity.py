@@ -429,6 +429,20 @@ def _retire_cases(seed=5):
     w2 = np.concatenate([rng.permutation(c * leaves).astype(np.uint32),
                          (np.uint32(1 << 29) + rng.permutation(c - 1).astype(np.uint32))])
     out.append(("stars", n2, src2, dst2, w2))
+    # a light random tree over half the vertices (the light phase ends with
+    # one component plus the retired other half), heavy random edges over all
+    n3, half = 100000, 50000
+    parent = (rng.random(half - 1) * np.arange(1, half)).astype(np.uint32)
+    src3 = np.concatenate([np.arange(1, half, dtype=np.uint32), rng.integers(0, n3, 300000, dtype=np.uint32),
+                           np.arange(half, n3, dtype=np.uint32)])
+    dst3 = np.concatenate([parent, rng.integers(0, n3, 300000, dtype=np.uint32),
+                           rng.integers(0, half, n3 - half, dtype=np.uint32)])
+    keep = src3 != dst3
+    src3, dst3 = src3[keep], dst3[keep]
+    w3 = np.empty(src3.size, dtype=np.uint32)
+    w3[: half - 1] = rng.permutation(half - 1)
+    w3[half - 1:] = np.uint32(1 << 28) + rng.permutation(src3.size - (half - 1)).astype(np.uint32)
+    out.append(("half_tree", n3, src3, dst3, w3))
     return out
 
 
@@ -445,11 +459,37 @@ def test_light_phase_retirement(mst, oracle_mod, beta):
     for name, n, src, dst, w in cases:
         k = O.kruskal(n, src, dst, w)
         G = P.Graph(n, src, dst, w)
-        for retire in (1, 0):
-            with _env(MST_FILTER=1, MST_TAIL=0, MST_FILTER_BETA=beta, MST_RETIRE=retire, MST_DEDUP_MIN_EDGES=0):
+        for retire, tail in ((1, 0), (0, 0), (1, 1)):
+            # tail on: light rounds past the round kernels run in the tail with
+            # TailArgs.retired (one component left ends the light phase there)
+            with _env(MST_FILTER=1, MST_TAIL=tail, MST_TAIL_EDGES=20000, MST_FILTER_BETA=beta, MST_RETIRE=retire,
+                      MST_DEDUP_MIN_EDGES=0):
                 r = P.boruvka_gpu(G)
                 e = P.boruvka_gpu_emulated(G, 2)
-            assert r.mst_edges.tolist() == k.ids.tolist(), f"{name} beta={beta} retire={retire}: edge set differs"
+            assert r.mst_edges.tolist() == k.ids.tolist(), f"{name} beta={beta} retire={retire} tail={tail}: edge set differs"
             assert r.total_weight == k.total_weight
             assert e.mst_edges.tolist() == k.ids.tolist() and e.total_weight == k.total_weight, \
                 f"{name} beta={beta} retire={retire}: 2-shard edge set differs"
+
+
+@pytest.mark.parametrize("mode", [dict(MST_FILTER=1, MST_TAIL=0), dict(MST_FILTER=1), dict(MST_FILTER=0)])
+def test_disconnected_large_forest(mst, oracle_mod, mode):
+    """Two disjoint R-MAT graphs plus isolated vertices: the minimum spanning
+    forest through Filter-Boruvka with retirement (components retired in the
+    light phase must stay separate trees) and the plain loop."""
+    from paper_2005_06913_b200 import configs as C
+    P, O = mst, oracle_mod
+    g = C.generate_host(C.rmat(14, 8, seed=21))
+    n1 = g.n
+    src = np.concatenate([g.src, g.src + np.uint32(n1)])
+    dst = np.concatenate([g.dst, g.dst + np.uint32(n1)])
+    rng = np.random.default_rng(4)
+    w = rng.permutation(src.size).astype(np.uint32)
+    n = 2 * n1 + 1000  # 1000 isolated vertices
+    k = O.kruskal(n, src, dst, w)
+    with _env(**mode):
+        with pytest.raises(P.GraphError) as ei:
+            P.boruvka_gpu(P.Graph(n, src, dst, w))
+    assert ei.value.kind == "Disconnected"
+    f = ei.value.forest
+    assert f.mst_edges.tolist() == k.ids.tolist() and f.total_weight == k.total_weight
