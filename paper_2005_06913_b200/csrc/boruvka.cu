@@ -133,6 +133,8 @@ enum Knob {
   kKnobOfferCached,       // offer filter reads through L1 (bit kFiltCached) at these sites (bitmask of OfferSite)
   kKnobRetire,            // light phase: retire isolated components (tables sized by components with edges)
   kKnobGiantBits,         // relabel rounds with more components than this: giant bits (0 off)
+  kKnobRangeOffers,       // split / heavy filter offers in range passes over L2-sized table slices
+  kKnobRangeMB,           // ... slice size
   kKnobTimeline,          // tools only: an event after every launch, per-launch stream times on stderr
   kKnobCount
 };
@@ -153,7 +155,8 @@ constexpr KnobDef kKnobDefs[kKnobCount] = {
     {"MST_DEDUP_MIN_RATIO", 8},  {"MST_DEDUP_CAP_LOG2", 25},
     {"MST_LAZY_ROUND1", 1},      {"MST_PIPELINE_H2D", 0},        {"MST_PIPELINE_CHUNKS", 16},
     {"MST_DEBUG_ROUNDS", 0},     {"MST_L2_FETCH", 0},         {"MST_OFFER_CACHED", 15},
-    {"MST_RETIRE", 1},           {"MST_GIANT_BITS", 16e6},    {"MST_TIMELINE", 0}};
+    {"MST_RETIRE", 1},           {"MST_GIANT_BITS", 16e6},   {"MST_RANGE_OFFERS", 1},
+    {"MST_RANGE_MB", 128},    {"MST_TIMELINE", 0}};
 
 std::atomic<double>* knob_table() {
   static std::atomic<double> t[kKnobCount];
@@ -619,7 +622,7 @@ template <class View, int kMode>
 void launch_two_pass(Workspace& ws, const CompactBufs& cb, View in, uint4* relabeled, const uint32_t* L, uint4* out,
                      unsigned long long* min_next, DevCounters* d_ctr, int r, uint64_t m_bound, uint32_t n_orig,
                      int slot, int light, int filt, PairTable pt = PairTable{nullptr, 0},
-                     bool emit = true, const uint32_t* gbits = nullptr) {
+                     bool emit = true, const uint32_t* gbits = nullptr, uint64_t range_table = 0) {
   const int dev = ws.device;
   const uint64_t tiles = tiles_c(m_bound);
   const int fused = tiles <= kFusedScanMaxTiles ? 1 : 0;  // small: the last count block scans
@@ -659,7 +662,18 @@ void launch_two_pass(Workspace& ws, const CompactBufs& cb, View in, uint4* relab
     launch_k(kem, ge, kBlock, ws.stream, in, relabeled, L, cb.masks, cb.counts, out, d_ctr, r, armed ? 1 : 0, n_orig);
   } else {
     auto kes = (filt & 3) == 2 ? k_emit_staged<kMode, true> : k_emit_staged<kMode, false>;
-    launch_k(kes, ge, kBlock, ws.stream, cb.stage, cb.counts, out, min_next, d_ctr, r, filt);
+    // range passes (kernels.cuh k_range_offers) for a table of range_table
+    // entries larger than the slice: the emit only copies
+    const uint64_t slice = (uint64_t)(knob(kKnobRangeMB) * 1048576.0 / 8.0);
+    const bool ranged = (kMode == kModeHeavy || kMode == kModeLight) && knob_i(kKnobRangeOffers) && slice > 0 &&
+                        range_table > slice;
+    launch_k(kes, ge, kBlock, ws.stream, cb.stage, cb.counts, out, ranged ? nullptr : min_next, d_ctr, r, filt);
+    if (ranged) {
+      const unsigned gr = (unsigned)(sm_count(dev) * blocks_per_sm(k_range_offers));
+      for (uint64_t lo = 0; lo < range_table; lo += slice)
+        launch_k(k_range_offers, gr, kBlock, ws.stream, (const uint4*)out, (const DevCounters*)d_ctr, r, min_next,
+                 (uint32_t)lo, (uint32_t)std::min<uint64_t>(range_table, lo + slice), filt);
+    }
   }
   MST_CUDA_CHECK(cudaGetLastError());
 }
@@ -814,7 +828,8 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     launches += 2;
     hot_begin(kHotSplit, 0, true);
     launch_two_pass<InView, kModeLight>(ws, cb, in, nullptr, nullptr, E[1], minb[0], d_ctr, 0, m, n,
-                                        kSlotCompact, 0, filt_for(n, kSiteSplit));
+                                        kSlotCompact, 0, filt_for(n, kSiteSplit), PairTable{nullptr, 0}, true,
+                                        nullptr, n);
     tmark();
     launches += 2;
   } else {
@@ -927,17 +942,19 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     const uint32_t* vlabel = levels.empty() ? nullptr : levels[0].first;
     MST_CUDA_CHECK(cudaMemsetAsync(&d_ctr->phase_end, 0xFF, sizeof(unsigned int), s));
     const int R1 = phase_end;
+    // retirement: n[R1] (all final components) was counted on the device
+    const uint64_t n_heavy = retired ? read_count(ws, s, d_ctr, R1) : snap.n[R1];
     hot_begin(kHotHeavy, R1, false);
     // launched as round R1-1's producer: it writes m[R1] and E/min of round R1
     launch_two_pass<InView, kModeHeavy>(ws, cb, in, nullptr, vlabel, E[R1 & 1], minb[(R1 - 1) & 1], d_ctr,
-                                        R1 - 1, m, n, kSlotFilter, 0, filt_for(snap.n[R1], kSiteHeavy));
+                                        R1 - 1, m, n, kSlotFilter, 0, filt_for(snap.n[R1], kSiteHeavy),
+                                        PairTable{nullptr, 0}, true, nullptr, n_heavy);
     tmark();
     launches += 2;
     light = false;
     r = R1;
     loop_start = R1;
-    // retirement: n[R1] (all final components) was counted on the device
-    n_bound = retired ? read_count(ws, s, d_ctr, R1) : snap.n[R1];
+    n_bound = n_heavy;
     m_bound = m;
     return true;
   };

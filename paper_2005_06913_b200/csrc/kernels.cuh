@@ -1195,7 +1195,7 @@ __global__ void __launch_bounds__(kBlock) k_emit_staged(const uint4* __restrict_
         const bool v = j < cnt;
         const uint4 e = v ? __ldcs(stage + (uint64_t)tile * kCTile + j) : make_uint4(0, 0, 0, 0);
         if (v) __stcs(out + off + j, e);
-        if (kMode == kModeHeavy || kMode == kModeLight) {
+        if ((kMode == kModeHeavy || kMode == kModeLight) && min_next) {  // null: k_range_offers does them
           const unsigned long long key = ((unsigned long long)e.z << 32) | (off + j);
           offer(min_next, e.x, key, v, filt);
           offer(min_next, e.y, key, v, filt);
@@ -1221,8 +1221,52 @@ __global__ void __launch_bounds__(kBlock) k_emit_staged(const uint4* __restrict_
           y[k] = e[k].y;
           key[k] = ((unsigned long long)e[k].z << 32) | (off + j);
         }
-        if (kMode == kModeHeavy || kMode == kModeLight) offer_both<kCItems>(min_next, x, y, key, v, 2 | (filt & kFiltCached));
+        if ((kMode == kModeHeavy || kMode == kModeLight) && min_next)
+          offer_both<kCItems>(min_next, x, y, key, v, 2 | (filt & kFiltCached));
       }
+    }
+  }
+}
+
+// Range passes (the split's and the heavy filter's offers): their min tables
+// are DRAM-sized (c4: 537 / 376 MB), so an offer straight from the emit
+// costs a 64 B DRAM fetch. Instead the emit only copies, and the output list
+// is streamed once per slice [lo, hi) of the table (128 MB by default):
+// each pass offers the endpoints whose label falls in its slice, keyed by
+// list position exactly like the emit would. The list itself is read with
+// evict-first loads, so the slice stays in L2. The minimum does not depend
+// on the order of the offers.
+__global__ void __launch_bounds__(kBlock) k_range_offers(const uint4* __restrict__ E, const DevCounters* ctr, int r,
+                                                         unsigned long long* __restrict__ table, uint32_t lo,
+                                                         uint32_t hi, int filt) {
+  pdl_prologue();
+  if ((uint32_t)r >= ctr->phase_end || (uint32_t)r + 1 >= ctr->stop_round) return;  // as the emit
+  const uint64_t m = ctr->m[r + 1];
+  const uint32_t span = hi - lo;
+  constexpr int kU = 4;
+  for (uint64_t base = (uint64_t)blockIdx.x * kBlock * kU; base < m; base += (uint64_t)gridDim.x * kBlock * kU) {
+    uint4 e[kU];
+#pragma unroll
+    for (int k = 0; k < kU; ++k) {
+      const uint64_t i = base + k * kBlock + threadIdx.x;
+      e[k] = i < m ? __ldcs(E + i) : make_uint4(0, 0, 0, 0);
+    }
+    uint32_t x[kU], y[kU];
+    unsigned long long key[kU];
+    bool vx[kU], vy[kU];
+#pragma unroll
+    for (int k = 0; k < kU; ++k) {
+      const uint64_t i = base + k * kBlock + threadIdx.x;
+      x[k] = e[k].x;
+      y[k] = e[k].y;
+      key[k] = ((unsigned long long)e[k].z << 32) | (uint32_t)i;
+      vx[k] = i < m && (x[k] - lo) < span;
+      vy[k] = i < m && (y[k] - lo) < span;
+    }
+#pragma unroll
+    for (int k = 0; k < kU; ++k) {
+      offer(table, x[k], key[k], vx[k], filt);
+      offer(table, y[k], key[k], vy[k], filt);
     }
   }
 }
