@@ -1631,7 +1631,8 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, uint6
                            ws.get<uint32_t>("tile_masks", tiles_c(s.m) * kCItems * kWarps), s.st,
                            ws.get<uint4>("stage", tiles_c(s.m) * kCTile)};
       launch_two_pass<SoaView, kModeLight>(ws, cb, s.in, nullptr, nullptr, s.E[1], s.minb[0], s.d_ctr, 0, s.m, n,
-                                           kSlotCompact, (int)kPhaseSharded, filt_for(n, kSiteSplit));
+                                           kSlotCompact, (int)kPhaseSharded, filt_for(n, kSiteSplit),
+                                           PairTable{nullptr, 0}, true, nullptr, n);
       launches += 4;
     }
   } else {
@@ -1741,9 +1742,24 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, uint6
         launch_two_pass<SoaView, kModeRelabel>(ws, cb, s.in, s.E[1], Lr, Eout, mnext, s.d_ctr, r, m_bound[g], n,
                                                kSlotCompact, (int)kPhaseSharded, filt_for(n_bound, kSiteCount, filter));
       else
+      {
+        // giant bits for huge rounds (phase D's first): each shard picks its
+        // own giant from its own list; any choice is exact
+        const uint32_t* gb = nullptr;
+        const double giant_min = knob(kKnobGiantBits);
+        if (giant_min > 0 && !light && (double)n_bound >= giant_min && s.m) {
+          uint32_t* bits = ws.get<uint32_t>("giant_bits", (n_bound + 31) / 32 + 1);
+          launch_k(k_pick_giant, 1, 1024, st, (const uint4*)s.E[r & 1], (const uint32_t*)Lr, s.d_ctr, r);
+          launch_k(k_giant_bits, (unsigned)(sm_count(dev) * 8), 256, st, (const uint32_t*)Lr,
+                   (const DevCounters*)s.d_ctr, r, bits);
+          gb = bits;
+          launches += 2;
+        }
         launch_two_pass<PackedView, kModeRelabel>(ws, cb, PackedView{s.E[r & 1]}, s.E[r & 1], Lr, Eout, mnext,
                                                   s.d_ctr, r, m_bound[g], n, kSlotCompact, (int)kPhaseSharded,
-                                                  filt_for(n_bound, kSiteCount, filter));
+                                                  filt_for(n_bound, kSiteCount, filter), PairTable{nullptr, 0}, true,
+                                                  gb);
+      }
       launches += 5;
       MST_CUDA_CHECK(cudaGetLastError());
       MST_CUDA_CHECK(cudaMemcpyAsync(&ws.h_snap[r], s.d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, st));
@@ -1800,20 +1816,26 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, uint6
               ++launches;
             }
           }
-          const uint32_t* vlabel = levels.empty() ? nullptr : ws.get<uint32_t>("Llvl" + std::to_string(levels[0]), 1);
           MST_CUDA_CHECK(cudaMemsetAsync(&s.d_ctr->phase_end, 0xFF, sizeof(unsigned int), ws.stream));
+        }
+        // after retirement n[R1] exists on the devices only (identical on every shard)
+        const uint64_t n_heavy = retired ? read_count(*sh[0].ws, sh[0].ws->stream, sh[0].d_ctr, R1) : snap.n[R1];
+        for (auto& s : sh) {
+          MST_CUDA_CHECK(cudaSetDevice(s.ws->device));
+          Workspace& ws = *s.ws;
+          const uint32_t* vlabel = levels.empty() ? nullptr : ws.get<uint32_t>("Llvl" + std::to_string(levels[0]), 1);
           const CompactBufs cb{ws.get<uint32_t>("tile_counts", tiles_c(s.m)),
                                ws.get<uint32_t>("tile_masks", tiles_c(s.m) * kCItems * kWarps), s.st,
                                ws.get<uint4>("stage", tiles_c(s.m) * kCTile)};
           // launched as round R1-1's producer: m[R1], E and the min table of round R1
           launch_two_pass<SoaView, kModeHeavy>(ws, cb, s.in, nullptr, vlabel, s.E[R1 & 1], s.minb[(R1 - 1) & 1],
                                                s.d_ctr, R1 - 1, s.m, n, kSlotFilter, (int)kPhaseSharded,
-                                               filt_for(snap.n[R1], kSiteHeavy));
+                                               filt_for(snap.n[R1], kSiteHeavy), PairTable{nullptr, 0}, true,
+                                               nullptr, n_heavy);
           launches += 2;
         }
         light = false;
-        // after retirement n[R1] exists on the devices only (identical on every shard)
-        n_bound = retired ? read_count(*sh[0].ws, sh[0].ws->stream, sh[0].d_ctr, R1) : snap.n[R1];
+        n_bound = n_heavy;
         for (int g = 0; g < G; ++g) m_bound[g] = sh[g].m;
         r = R1;
         loop_start = R1;
