@@ -505,8 +505,13 @@ void timeline_print(cudaEvent_t start) {
   t_timeline.clear();
 }
 
+// Kernels launched by the calling thread (GpuRunInfo::kernel_launches is
+// the difference over a call).
+thread_local uint64_t t_launches = 0;
+
 template <typename... KArgs, typename... Args>
 void launch_k(void (*kernel)(KArgs...), unsigned grid, unsigned block, cudaStream_t s, Args... args) {
+  ++t_launches;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
@@ -1055,6 +1060,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
       void* args[] = {&ta};
       hot_begin(kHotTail, r, light);
       MST_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)kt, G, kBlock, args, tail_smem, s));
+      ++t_launches;
       timeline_mark((const void*)kt, s);
       ++launches;
       tmark();
@@ -1321,6 +1327,7 @@ void apply_l2_fetch(int dev) {
 
 RunOut run_single(const SingleArgs& a, mst_stats_t* stats) {
   const auto t_start = Clock::now();
+  const uint64_t launches0 = t_launches;
   const int dev = current_device_checked();
   apply_l2_fetch(dev);
   Workspace& ws = workspace(dev, 0);
@@ -1429,7 +1436,8 @@ RunOut run_single(const SingleArgs& a, mst_stats_t* stats) {
     run_single_impl<AosView>(ws, v, wb, 4, a.n, a.m, o, a.time_hot, filter_mode(a.n, a.m), nullptr, &after);
   }
   check_err_bits(o.err);
-  o.launches += sort_launches;
+  o.launches = (uint32_t)(t_launches - launches0);  // every kernel of the call, counted at launch
+  (void)sort_launches;
   if (join_legacy) {
     MST_CUDA_CHECK(cudaEventRecord(ws.join_out, s));
     MST_CUDA_CHECK(cudaStreamWaitEvent(cudaStreamLegacy, ws.join_out, 0));
@@ -1490,6 +1498,7 @@ struct EmulatedExchanger : Exchanger {
     if (sh.size() == 1 || count == 0) return;
     ShardPtrs<T, 8> p{};
     for (size_t i = 0; i < sh.size(); ++i) p.p[i] = sh[i].*buf;
+    ++t_launches;
     k_shard_min<T, kSum><<<(unsigned)std::min<uint64_t>((count + 255) / 256, 4096), 256, 0, sh[0].ws->stream>>>(
         p, (int)sh.size(), count);
     MST_CUDA_CHECK(cudaGetLastError());
@@ -1891,6 +1900,7 @@ RunOut run_sharded(const std::vector<PartSpec>& parts, Exchanger& ex, uint32_t n
                    uint32_t* out_ids, mst_stats_t* stats, bool device_out = false,
                    cudaStream_t user_stream = nullptr) {
   const auto t_start = Clock::now();
+  const uint64_t launches0 = t_launches;
   std::vector<Shard> sh(parts.size());
   std::vector<std::unique_lock<std::mutex>> locks;
   struct Restore {
@@ -1958,7 +1968,8 @@ RunOut run_sharded(const std::vector<PartSpec>& parts, Exchanger& ex, uint32_t n
   Workspace& ws0 = *sh[0].ws;
   MST_CUDA_CHECK(cudaSetDevice(ws0.device));
   uint32_t* d_sorted = device_out ? out_ids : ws0.get<uint32_t>("sorted", n);
-  o.launches += sort_from_bits(ws0, sh[0].flags, std::max<uint64_t>(m_total, 1), d_sorted, sh[0].d_ctr);
+  sort_from_bits(ws0, sh[0].flags, std::max<uint64_t>(m_total, 1), d_sorted, sh[0].d_ctr);
+  o.launches = (uint32_t)(t_launches - launches0);  // every kernel of the call (all shards), counted at launch
   MST_CUDA_CHECK(cudaEventRecord(e2, ws0.stream));
   if (o.count && out_ids && !device_out)
     copy_d2h(ws0, out_ids, d_sorted, o.count * 4);
