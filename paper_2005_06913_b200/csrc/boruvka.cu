@@ -135,6 +135,7 @@ enum Knob {
   kKnobGiantBits,         // relabel rounds with more components than this: giant bits (0 off)
   kKnobRangeOffers,       // split / heavy filter offers in range passes over L2-sized table slices
   kKnobRangeMB,           // ... slice size
+  kKnobBytesMax,          // MST output as bytes up to this many edges, a bitmap above
   kKnobTimeline,          // tools only: an event after every launch, per-launch stream times on stderr
   kKnobCount
 };
@@ -156,7 +157,7 @@ constexpr KnobDef kKnobDefs[kKnobCount] = {
     {"MST_LAZY_ROUND1", 1},      {"MST_PIPELINE_H2D", 0},        {"MST_PIPELINE_CHUNKS", 16},
     {"MST_DEBUG_ROUNDS", 0},     {"MST_L2_FETCH", 0},         {"MST_OFFER_CACHED", 15},
     {"MST_RETIRE", 1},           {"MST_GIANT_BITS", 16e6},   {"MST_RANGE_OFFERS", 1},
-    {"MST_RANGE_MB", 128},    {"MST_TIMELINE", 0}};
+    {"MST_RANGE_MB", 128},       {"MST_BYTES_MAX", 67108864},    {"MST_TIMELINE", 0}};
 
 std::atomic<double>* knob_table() {
   static std::atomic<double> t[kKnobCount];
@@ -529,9 +530,9 @@ void launch_k(void (*kernel)(KArgs...), unsigned grid, unsigned block, cudaStrea
 // Sorted id list (ascending) from the MST bitmap the hook kernels set.
 // words = (m + 31) / 32; the bitmap buffer is allocated with mst_bits_words(m).
 uint64_t mst_bits_words(uint64_t m) { return ((m + 31) / 32 + 3) & ~3ull; }  // whole uint4 vectors
-// The single-GPU output's words: one byte per edge up to kMstBytesMax edges
+// The single-GPU output's words: one byte per edge up to MST_BYTES_MAX edges
 // (kernels.cuh mst_mark), else the bitmap.
-bool mst_out_bytes(uint64_t m) { return m <= kMstBytesMax; }
+bool mst_out_bytes(uint64_t m) { return (double)m <= knob(kKnobBytesMax); }
 uint64_t mst_out_words(uint64_t m) { return mst_out_bytes(m) ? ((m + 16 + 15) / 16) * 4 : mst_bits_words(m); }
 
 // Sorted id list from one flag byte per edge (small lists, see mst_mark).

@@ -69,7 +69,6 @@ constexpr int kCTile = kBlock * kCItems;
 constexpr int kMaxR = MST_MAX_ROUNDS + 2;
 constexpr uint64_t kNoKey = ~0ull;
 constexpr int kFiltCached = 8;  // offer filter reads through L1 (see offer)
-constexpr uint64_t kMstBytesMax = 64ull << 20;  // output as bytes (not bits) up to this many edges
 constexpr uint32_t kRetFlag = 0x80000000u;  // level-map entry of a retired component: kRetFlag | own index
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr uint32_t kErrRange = 1u;
@@ -228,7 +227,7 @@ __device__ __forceinline__ void mst_set(uint32_t* bits, uint32_t eid) {
   atomicOr(bits + (eid >> 5), 1u << (eid & 31));
 }
 // The output for a caller's list small enough that one byte per edge stays
-// in L2 (<= kMstBytesMax edges): plain byte stores. Grids hook neighbouring
+// in L2 (<= MST_BYTES_MAX edges, 64 Mi): plain byte stores. Grids hook neighbouring
 // components along neighbouring edges, ~16 MST edges per bitmap word, whose
 // REDs queue on the same word (c1 round-1 hook: 57 us with the bitmap, 39 us
 // with bytes).

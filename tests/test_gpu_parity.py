@@ -52,6 +52,9 @@ MODES = [dict(MST_FILTER=0), dict(MST_FILTER=1, MST_FILTER_BETA=0.3),
          # the split's / heavy filter's offers as range passes over tiny table slices
          dict(MST_FILTER=1, MST_TAIL=0, MST_RANGE_MB=0.01),
          dict(MST_FILTER=1, MST_RANGE_MB=0.05, MST_OFFER_SPLIT=2, MST_OFFER_HEAVY=2),
+         # the MST bitmap output (default above 64 Mi edges)
+         dict(MST_FILTER=1, MST_TAIL=0, MST_BYTES_MAX=0),
+         dict(MST_FILTER=0, MST_BYTES_MAX=0),
          # giant bits in every relabel round (default: >= 16 M components only)
          dict(MST_FILTER=1, MST_TAIL=0, MST_GIANT_BITS=1),
          dict(MST_FILTER=0, MST_TAIL=0, MST_GIANT_BITS=1, MST_LAZY_ROUND1=0),
