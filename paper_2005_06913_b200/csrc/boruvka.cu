@@ -137,6 +137,7 @@ enum Knob {
   kKnobRangeMB,           // ... slice size
   kKnobBytesMax,          // MST output as bytes up to this many edges, a bitmap above
   kKnobTimeline,          // tools only: an event after every launch, per-launch stream times on stderr
+  kKnobEmitSparse,        // warp-per-32-tiles copy for the split's / heavy filter's staged survivors
   kKnobCount
 };
 struct KnobDef {
@@ -157,7 +158,8 @@ constexpr KnobDef kKnobDefs[kKnobCount] = {
     {"MST_LAZY_ROUND1", 1},      {"MST_PIPELINE_H2D", 0},        {"MST_PIPELINE_CHUNKS", 16},
     {"MST_DEBUG_ROUNDS", 0},     {"MST_L2_FETCH", 0},         {"MST_OFFER_CACHED", 15},
     {"MST_RETIRE", 1},           {"MST_GIANT_BITS", 16e6},   {"MST_RANGE_OFFERS", 1},
-    {"MST_RANGE_MB", 128},       {"MST_BYTES_MAX", 67108864},    {"MST_TIMELINE", 0}};
+    {"MST_RANGE_MB", 128},       {"MST_BYTES_MAX", 67108864},    {"MST_TIMELINE", 0},
+    {"MST_EMIT_SPARSE", 1}};
 
 std::atomic<double>* knob_table() {
   static std::atomic<double> t[kKnobCount];
@@ -673,7 +675,14 @@ void launch_two_pass(Workspace& ws, const CompactBufs& cb, View in, uint4* relab
     const uint64_t slice = (uint64_t)(knob(kKnobRangeMB) * 1048576.0 / 8.0);
     const bool ranged = (kMode == kModeHeavy || kMode == kModeLight) && knob_i(kKnobRangeOffers) && slice > 0 &&
                         range_table > slice;
-    launch_k(kes, ge, kBlock, ws.stream, cb.stage, cb.counts, out, ranged ? nullptr : min_next, d_ctr, r, filt);
+    if (ranged && knob_i(kKnobEmitSparse)) {
+      const uint64_t groups = (tiles + 31) / 32;
+      const unsigned gw = (unsigned)std::max<uint64_t>(
+          1, std::min<uint64_t>((groups + kWarps - 1) / kWarps, (uint64_t)sm_count(dev) * blocks_per_sm(k_emit_sparse)));
+      launch_k(k_emit_sparse, gw, kBlock, ws.stream, (const uint4*)cb.stage, (const uint32_t*)cb.counts, out, d_ctr, r);
+    } else {
+      launch_k(kes, ge, kBlock, ws.stream, cb.stage, cb.counts, out, ranged ? nullptr : min_next, d_ctr, r, filt);
+    }
     if (ranged) {
       const unsigned gr = (unsigned)(sm_count(dev) * blocks_per_sm(k_range_offers));
       for (uint64_t lo = 0; lo < range_table; lo += slice)
