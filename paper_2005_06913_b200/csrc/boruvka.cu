@@ -138,6 +138,7 @@ enum Knob {
   kKnobBytesMax,          // MST output as bytes up to this many edges, a bitmap above
   kKnobTimeline,          // tools only: an event after every launch, per-launch stream times on stderr
   kKnobEmitSparse,        // warp-per-32-tiles copy for the split's / heavy filter's staged survivors
+  kKnobInterleave,        // count passes walk the list in this many interleaved segments (<= 1 off)
   kKnobCount
 };
 struct KnobDef {
@@ -159,7 +160,7 @@ constexpr KnobDef kKnobDefs[kKnobCount] = {
     {"MST_DEBUG_ROUNDS", 0},     {"MST_L2_FETCH", 0},         {"MST_OFFER_CACHED", 15},
     {"MST_RETIRE", 1},           {"MST_GIANT_BITS", 16e6},   {"MST_RANGE_OFFERS", 1},
     {"MST_RANGE_MB", 128},       {"MST_BYTES_MAX", 67108864},    {"MST_TIMELINE", 0},
-    {"MST_EMIT_SPARSE", 1}};
+    {"MST_EMIT_SPARSE", 1},      {"MST_INTERLEAVE", 128}};
 
 std::atomic<double>* knob_table() {
   static std::atomic<double> t[kKnobCount];
@@ -641,12 +642,13 @@ void launch_two_pass(Workspace& ws, const CompactBufs& cb, View in, uint4* relab
   // armed: this launch relabels + inserts pairs if the device chose dedup
   // (decided and table cleared by k_label2), the kModeDedup pass counts
   launch_k(kcnt, gc, kBlock, ws.stream, in, kMode == kModeRelabel ? relabeled : cb.stage, L, cb.masks, cb.counts, n_orig,
-           d_ctr, r, fused, slot, light, pt, min_next, filt, gbits);
+           d_ctr, r, fused, slot, light, pt, min_next, filt, gbits, (uint32_t)std::max(0, knob_i(kKnobInterleave)));
   if constexpr (!View::kOriginal) {
     if (armed) {
       auto kdc = k_count<PackedView, kModeDedup>;
       launch_k(kdc, gc, kBlock, ws.stream, PackedView{relabeled}, cb.stage, L, cb.masks, cb.counts, n_orig, d_ctr, r,
-               fused, slot, light, pt, min_next, filt, (const uint32_t*)nullptr);
+               fused, slot, light, pt, min_next, filt, (const uint32_t*)nullptr,
+               (uint32_t)std::max(0, knob_i(kKnobInterleave)));
     }
   }
   if (!fused) {

@@ -924,7 +924,7 @@ __global__ void MST_LB_(MST_MINB_COUNT) k_count(View in, uint4* __restrict__ rel
                                                   uint32_t n_orig, DevCounters* ctr, int r, int fused, int slot,
                                                   int light_phase, PairTable pt,
                                                   unsigned long long* __restrict__ min_next, int filt,
-                                                  const uint32_t* __restrict__ gbits) {
+                                                  const uint32_t* __restrict__ gbits, uint32_t ileave) {
   pdl_prologue();
   __shared__ uint32_t s_cnt[kWarps];
   __shared__ uint32_t s_slot[kCItems * kWarps];
@@ -947,7 +947,18 @@ __global__ void MST_LB_(MST_MINB_COUNT) k_count(View in, uint4* __restrict__ rel
   const uint32_t giant = (kGiant && gbits) ? ctr->giant : 0u;
   const uint32_t ntiles = (uint32_t)((m_r + kCTile - 1) / kCTile);
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  // Interleaved tile order: the list is cut into S equal segments and the
+  // grid walks them round-robin, so regions of a different character are in
+  // flight together instead of one after the other (the BASELINE generators
+  // put the uniform-random spanning tree first: its label gathers are
+  // DRAM-random-bound, the R-MAT block's are L1-request-bound). Per-tile
+  // outputs are indexed by the tile itself, so nothing else changes.
+  const uint32_t S = (View::kOriginal && ileave > 1 && ntiles >= 64 * ileave) ? ileave : 1u;
+  const uint32_t seg = (ntiles + S - 1) / S;
+  const uint32_t nvt = seg * S;
+  for (uint32_t vt = blockIdx.x; vt < nvt; vt += gridDim.x) {
+    const uint32_t tile = S > 1 ? (vt % S) * seg + vt / S : vt;
+    if (tile >= ntiles) continue;
     EdgeRec e[kCItems];
 #pragma unroll
     for (int k = 0; k < kCItems; ++k) {
