@@ -953,7 +953,7 @@ __global__ void MST_LB_(MST_MINB_COUNT) k_count(View in, uint4* __restrict__ rel
   // put the uniform-random spanning tree first: its label gathers are
   // DRAM-random-bound, the R-MAT block's are L1-request-bound). Per-tile
   // outputs are indexed by the tile itself, so nothing else changes.
-  const uint32_t S = (View::kOriginal && ileave > 1 && ntiles >= 64 * ileave) ? ileave : 1u;
+  const uint32_t S = (View::kOriginal && ileave > 1 && ntiles >= 4 * ileave) ? ileave : 1u;
   const uint32_t seg = (ntiles + S - 1) / S;
   const uint32_t nvt = seg * S;
   for (uint32_t vt = blockIdx.x; vt < nvt; vt += gridDim.x) {

@@ -62,7 +62,12 @@ MODES = [dict(MST_FILTER=0), dict(MST_FILTER=1, MST_FILTER_BETA=0.3),
          dict(MST_FILTER=1, MST_TAIL=0, MST_DEDUP_MIN_EDGES=0, MST_DEDUP_ACTIVE=1e9, MST_DEDUP_MIN_RATIO=1,
               MST_DEDUP_TABLE_DIV=1, MST_DEDUP_CAP_LOG2=27),
          # ranged offers with the block-per-tile staged copy (default: warp per 32 tiles)
-         dict(MST_FILTER=1, MST_RANGE_MB=0.01, MST_EMIT_SPARSE=0)]
+         dict(MST_FILTER=1, MST_RANGE_MB=0.01, MST_EMIT_SPARSE=0),
+         # the caller's list walked in 2 / 3 interleaved segments (default 128, lists of >= 512 tiles),
+         # and front to back
+         dict(MST_FILTER=1, MST_INTERLEAVE=2, MST_TAIL=0), dict(MST_FILTER=0, MST_INTERLEAVE=3, MST_TAIL=0,
+                                                                MST_LAZY_ROUND1=0),
+         dict(MST_FILTER=1, MST_INTERLEAVE=0)]
 
 
 def _check(P, n, src, dst, w, ids, total, shards=(2, 3), modes=MODES):
