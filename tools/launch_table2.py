@@ -44,12 +44,16 @@ for k, v in d.items():
            "l1_ld_requests_M": v.get("l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum", 0) / 1e6,
            "l1_wavefronts_M": wf / 1e6, "wavefronts_per_sm_cycle": wf / cyc if cyc else 0,
            "warps_active_pct": v.get("sm__warps_active.avg.pct_of_peak_sustained_active", 0),
-           "registers": v.get("launch__registers_per_thread", 0)}
+           "registers": v.get("launch__registers_per_thread", 0),
+           # sectors the L1 fetched from L2 (its miss path: ~1 per SM-cycle at most, tools/gather_bench.cu)
+           "l1_miss_Msectors": v.get("l1tex__m_xbar2l1tex_read_sectors.sum", 0) / 1e6,
+           "l1_miss_sectors_per_sm_cycle": v.get("l1tex__m_xbar2l1tex_read_sectors.sum", 0) / cyc if cyc else 0}
     out.append(rec)
     print(f"{k:>4} {rec['kernel']:40s} {t:8.1f} {rd / 1e6:9.1f} {wr / 1e6:9.1f} {rec['dram_GBs']:6.0f} "
           f"{rec['l2_hit_pct']:6.1f} {rec['l2_read_Msectors']:9.1f} {rec['l2_red_Msectors']:8.1f} "
           f"{rec['l2_atom_Msectors']:9.1f} {rec['l1_ld_requests_M']:8.1f} {wf / 1e6:7.1f} "
-          f"{rec['wavefronts_per_sm_cycle']:8.2f} {rec['warps_active_pct']:5.1f} {rec['registers']:4.0f}")
+          f"{rec['wavefronts_per_sm_cycle']:8.2f} {rec['warps_active_pct']:5.1f} {rec['registers']:4.0f} "
+          f"{rec['l1_miss_Msectors']:11.1f} {rec['l1_miss_sectors_per_sm_cycle']:9.2f}")
 print(f"total (generator excluded): {tot / 1e3:.3f} ms (ncu, serialised, cold L2 per launch)")
 if "--json" in sys.argv:
     json.dump({"source": sys.argv[1], "launches": out, "total_ms": tot / 1e3},
