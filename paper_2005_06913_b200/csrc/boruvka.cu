@@ -139,6 +139,7 @@ enum Knob {
   kKnobTimeline,          // tools only: an event after every launch, per-launch stream times on stderr
   kKnobEmitSparse,        // warp-per-32-tiles copy for the split's / heavy filter's staged survivors
   kKnobInterleave,        // count passes walk the list in this many interleaved segments (<= 1 off)
+  kKnobDedupGuarantee,    // dedup a round only when the next round's components can form <= m_r / this pairs (0: off)
   kKnobCount
 };
 struct KnobDef {
@@ -160,7 +161,8 @@ constexpr KnobDef kKnobDefs[kKnobCount] = {
     {"MST_DEBUG_ROUNDS", 0},     {"MST_L2_FETCH", 0},         {"MST_OFFER_CACHED", 15},
     {"MST_RETIRE", 1},           {"MST_GIANT_BITS", 16e6},   {"MST_RANGE_OFFERS", 1},
     {"MST_RANGE_MB", 128},       {"MST_BYTES_MAX", 67108864},    {"MST_TIMELINE", 0},
-    {"MST_EMIT_SPARSE", 1},      {"MST_INTERLEAVE", 128}};
+    {"MST_EMIT_SPARSE", 1},      {"MST_INTERLEAVE", 128},
+    {"MST_DEDUP_GUARANTEE", 4}};
 
 std::atomic<double>* knob_table() {
   static std::atomic<double> t[kKnobCount];
@@ -891,7 +893,8 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   // 16-23: the minimum edges-per-active-component ratio of a dedup round
   const unsigned int pair_div = (unsigned int)std::max(1, std::min(255, knob_i(kKnobDedupTableDiv))) |
                                 (knob_i(kKnobDedupRetry) ? 0x100u : 0u) |
-                                ((unsigned int)std::max(1, std::min(255, knob_i(kKnobDedupMinRatio))) << 16);
+                                ((unsigned int)std::max(1, std::min(255, knob_i(kKnobDedupMinRatio))) << 16) |
+                                ((unsigned int)std::max(0, std::min(255, knob_i(kKnobDedupGuarantee))) << 24);
   // Tail entry (m_bound is the host's one-round-stale edge bound). Measured
   // (tools/sweep_tail.sh, tools/sweep_tail2.sh): the plain loop and phase D
   // gain from entering early (12 M: c1's round 2 with 5.1 M edges runs in

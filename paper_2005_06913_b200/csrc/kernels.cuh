@@ -1606,7 +1606,16 @@ __global__ void MST_LB_(MST_MINB_LABEL) k_label2(uint32_t* __restrict__ parent,
     // try again only once K(K-1)/2 pairs guarantee an 8x reduction;
     // R-MAT's repeated hub pairs keep succeeding and are not held back
     const bool doubtful = ctr->dedup_fail && K * (K - 1) / 2 > m_r / 8 && !(pair_div & 0x100u);
-    const bool use = K <= dedup_active && m_r >= ((pair_div >> 16) & 0xFFu) * K && m_r >= 4096 && !doubtful;
+    // bits 24-31 of pair_div: only when the n_next components of the next
+    // round can form at most m_r / g distinct pairs, i.e. the dedup is
+    // guaranteed to shrink the list g-fold. (Uniform graphs: c3's light round
+    // 4 has 148 K active components, 9.4 M edges and almost as many distinct
+    // pairs; the attempt overflowed its table and cost 0.4 ms.)
+    const unsigned long long gfac = (pair_div >> 24) & 0xFFu;
+    const unsigned long long pairs_next = (unsigned long long)n_next * (n_next > 0 ? n_next - 1 : 0) / 2;
+    const bool guaranteed = gfac == 0 || pairs_next <= m_r / gfac;
+    const bool use = K <= dedup_active && m_r >= ((pair_div >> 16) & 0xFFu) * K && m_r >= 4096 && !doubtful &&
+                     guaranteed;
     // table >= m_r / div slots, but no more than twice the pairs the next
     // round's n_next components can form (after retirement they are few: c4
     // round 3, 825 components, 1 M slots in L2 instead of 32 M in DRAM:
