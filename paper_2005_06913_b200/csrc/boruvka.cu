@@ -147,7 +147,7 @@ struct KnobDef {
   double dflt;
 };
 constexpr KnobDef kKnobDefs[kKnobCount] = {
-    {"MST_FILTER", -1},          {"MST_FILTER_BETA", 1.5},       {"MST_PIVOT_SAMPLES", 262144},
+    {"MST_FILTER", -1},          {"MST_FILTER_BETA", 1.25},       {"MST_PIVOT_SAMPLES", 262144},
     {"MST_FILTER_TABLE_MB", 1e7}, {"MST_OFFER_MIN1", -1},         {"MST_OFFER_SPLIT", -1},
     {"MST_OFFER_COUNT", -1},     {"MST_OFFER_HEAVY", -1},        {"MST_PDL", 1},
     {"MST_TAIL", 1},             {"MST_TAIL_EDGES", 0},          {"MST_TAIL_COMPS", 8e6},
