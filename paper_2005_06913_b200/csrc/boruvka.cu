@@ -153,7 +153,7 @@ constexpr KnobDef kKnobDefs[kKnobCount] = {
     {"MST_TAIL", 1},             {"MST_TAIL_EDGES", 0},          {"MST_TAIL_COMPS", 8e6},
     {"MST_TAIL_SMALL_N", 65536}, {"MST_TAIL_BPS", MST_TAIL_MINB}, {"MST_TAIL_TINY", 1},
     {"MST_TAIL_TRACE", 0},       {"MST_TAIL_START_C", 1},        {"MST_TAIL_START_C_D", 1},
-    {"MST_TAIL_START_C_D_EDGES", 1e12}, {"MST_TAIL_DEDUP", 0},   {"MST_TAIL_DEDUP_RATIO", 4},
+    {"MST_TAIL_START_C_D_EDGES", 3.2e7}, {"MST_TAIL_DEDUP", 0},   {"MST_TAIL_DEDUP_RATIO", 4},
     {"MST_TAIL_DEDUP_MIN", 16384}, {"MST_DEDUP", 1},             {"MST_DEDUP_MIN_EDGES", 2e6},
     {"MST_DEDUP_ACTIVE", 262144}, {"MST_DEDUP_TABLE_DIV", 4},    {"MST_DEDUP_RETRY", 0},
     {"MST_DEDUP_MIN_RATIO", 8},  {"MST_DEDUP_CAP_LOG2", 25},
@@ -1139,8 +1139,11 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
     const bool lazy2 = lazy1 && r == 2;  // round 2 over round 1's uncompacted pairs
     // phase D's first round (Filter-Boruvka): hook + label here, then the
     // tail starts at its phase C over the heavy survivors in place (the host
-    // knows only m here, not the survivor count: bounded by components;
-    // c2 3.04 -> 2.97 ms, c3 neutral, c4's 47 M components excluded)
+    // knows only m here, not the survivor count: bounded by components and
+    // by m <= 32 M: measured across sizes (tools/knob_ab_sizes.py) the
+    // hand-off gains 2 % on lists of <= 18 M edges and loses 1-3 % from 64 M
+    // on, where the round kernels' full-occupancy compaction wins; c4's 47 M
+    // components are excluded either way)
     const bool d_start_c = tail_on && !light && phase_end && r == phase_end && knob_i(kKnobTailStartCD) != 0 &&
                            m_bound <= (uint64_t)knob(kKnobTailStartCDEdges) &&
                            n_bound <= (16u << 20);
