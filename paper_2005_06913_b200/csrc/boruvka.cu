@@ -96,7 +96,7 @@ NcclApi& nccl() {
 // Values are read per use with relaxed atomics, so a knob set before a call
 // holds for the whole call.
 enum Knob {
-  kKnobFilter,            // -1 auto (m >= 5n), 0 plain loop, 1 Filter-Boruvka
+  kKnobFilter,            // -1 auto (filter_mode: m >= 5n, or m >= 2.5n once m >= 24 M), 0 plain loop, 1 Filter-Boruvka
   kKnobFilterBeta,        // light edges ~ beta * n
   kKnobPivotSamples,      // sampled weights for the pivot
   kKnobFilterTableMB,     // read-first filter off for min tables above this size
@@ -593,7 +593,7 @@ uint32_t sort_from_bits(Workspace& ws, const uint32_t* bits, uint64_t m, uint32_
 // the winning edge directly. The host runs one round ahead of the device;
 // kernels of rounds past a stop early-exit on the device counters.
 //
-// Filter-Boruvka (default when m >= 5n): a sampled weight pivot splits the
+// Filter-Boruvka (default for dense or large lists, filter_mode): a sampled weight pivot splits the
 // edges; the round loop first runs on the light edges alone (phase B), then
 // one pass drops every heavy edge inside a light component (cycle property,
 // exact) and the loop continues on the survivors (phase D). Uniform and
@@ -615,7 +615,15 @@ bool filter_mode(uint32_t n, uint64_t m) {
   // m/n = 4 plain 0.65 vs filter 0.97 ms (c0), m/n = 6 0.92 vs 1.01, m/n = 8
   // 4.25 vs 1.05; R-MAT m/n = 5 1.41 vs 1.23. (The light phase of a sparse
   // graph stalls on the parallel light edges of a few active components.)
-  return m >= (uint64_t)5 * n && m >= (1u << 16);
+  // Large lists gain from the filter at lower densities too (round 2,
+  // tools/knob_ab_sizes.py --plain, profiles/r2s4/filter_rule_sparse.log):
+  // from m >= 2.5 n once m >= 24 M (uniform n = 16 M, m = 64 M: 12.3 -> 5.6
+  // ms; R-MAT 24 ef 2: 6.0 -> 4.4; a 256^3 grid: 3.1 -> 2.8; an 8-neighbour
+  // 4096^2 grid: 3.06 -> 2.83), while 4-neighbour grids (m = 2 n: +46-83 %
+  // with the filter) and lists under ~17 M edges (8-neighbour 2048^2 grid,
+  // 128^3 grid: +40 %; c0: +11 %) stay on the plain loop.
+  if (m >= (uint64_t)5 * n) return m >= (1u << 16);
+  return 2 * m >= (uint64_t)5 * n && m >= (24ull << 20);
 }
 
 
