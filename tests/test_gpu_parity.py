@@ -270,6 +270,30 @@ def test_baseline_configs_full_size(mst, oracle_mod, cfg):
     assert np.array_equal(e.mst_edges, r.mst_edges)
 
 
+@pytest.mark.parametrize("kind", ["uniform", "rmat"])
+def test_sparse_large_graphs_take_the_filter(mst, oracle_mod, kind):
+    """Sparse lists of >= 24 M edges with 2.5 <= m/n < 5 run Filter-Boruvka by
+    default (filter_mode's second clause): default arm = forced plain loop =
+    the oracle's Kruskal, single GPU and 2 emulated shards."""
+    from paper_2005_06913_b200 import configs as C
+    P, O = mst, oracle_mod
+    spec = C.uniform(1 << 23, 26 << 20, seed=9) if kind == "uniform" else C.rmat(23, 3, seed=9)
+    g = C.generate_host(spec)
+    assert g.src.size >= (24 << 20) and 2 * g.src.size >= 5 * g.n and g.src.size < 5 * g.n
+    k = O.kruskal(g.n, g.src, g.dst, g.w)
+    info = P.GpuRunInfo()
+    r = P.boruvka_gpu(g, info=info)
+    assert np.array_equal(r.mst_edges, k.ids.astype(np.int64)) and r.total_weight == k.total_weight
+    assert info.final_components == 1
+    with _env(MST_FILTER=0):
+        info0 = P.GpuRunInfo()
+        r0 = P.boruvka_gpu(g, info=info0)
+    assert np.array_equal(r0.mst_edges, r.mst_edges) and r0.total_weight == r.total_weight
+    assert info.rounds != info0.rounds or info.kernel_launches != info0.kernel_launches  # the arms differ
+    e = P.boruvka_gpu_emulated(g, 2)
+    assert np.array_equal(e.mst_edges, r.mst_edges) and e.total_weight == r.total_weight
+
+
 def test_c3_full_size(mst, oracle_mod):
     """268 M edges from the host API: plain loop = Filter-Boruvka = the
     oracle's answer, plus the restated verify_mst's structural checks."""
