@@ -129,7 +129,10 @@ SURVEY_B_ALG_GB = {"c0": 0.725, "c1": 0.679, "c2": 8.90, "c3": 66.4, "c4": 152.4
 CPU_SAMPLE_EDGES = 20_000_000  # above this the CPU legs time a scaled instance (10-30 s of work per run)
 
 
-def cpu_sample(spec):
+REFERENCE_ARM_BUDGET_S = 240.0  # --impl reference: K + W runs of the sample should end within about this
+
+
+def cpu_sample(spec, shrink: int = 0):
     """(spec, description) of the graph the CPU legs time: the workload itself
     when it is small, else the same generator family, parameters and seed
     scaled to ~16-17 M edges. The unchanged reference CAS scans every edge in
@@ -142,13 +145,14 @@ def cpu_sample(spec):
     if m is not None and m <= CPU_SAMPLE_EDGES:
         return spec, f"the full {spec.name} graph (m={m})"
     if spec.kind == 0:
-        n2 = 1 << 20
+        n2 = 1 << max(14, 20 - shrink)
         sub = C.uniform(n2, n2 * (spec.m // spec.n), seed=spec.seed, name=f"{spec.name}_sample_n{n2}")
         return sub, (f"scaled {spec.name}: uniform n={n2}, m={sub.m} (same density {spec.m // spec.n}, "
                      f"generator and seed)")
     if spec.kind == 2:
-        sub = C.rmat(20, spec.edgefactor, seed=spec.seed, name=f"{spec.name}_sample_s20")
-        return sub, (f"scaled {spec.name}: R-MAT scale 20, edgefactor {spec.edgefactor} (same generator, "
+        sc = max(14, 20 - shrink)
+        sub = C.rmat(sc, spec.edgefactor, seed=spec.seed, name=f"{spec.name}_sample_s{sc}")
+        return sub, (f"scaled {spec.name}: R-MAT scale {sc}, edgefactor {spec.edgefactor} (same generator, "
                      f"a/b/c/d and seed)")
     return spec, f"the full {spec.name} graph"
 
@@ -182,11 +186,12 @@ def cpu_baseline_sweep(spec):
     m = int(src.size)
     hw, omp = O.hardware_threads(), O.omp_max_threads()
     rows = {}
-    seq = O.ref_solve(n, src, dst, w, O.ALGO_SEQ, threads=1)
+    rg = O.RefGraph(n, src, dst, w)  # the adapter runs once, outside every timed run
+    seq = rg.solve(O.ALGO_SEQ, threads=1)
     rows["boruvka_seq T=1"] = {"ms": seq.elapsed_ms, "edges_per_s": m / (seq.elapsed_ms / 1e3), "rounds": seq.rounds}
     cas = None
     for t in thread_sweep(hw):
-        cas = O.ref_solve(n, src, dst, w, O.ALGO_CAS, threads=t)
+        cas = rg.solve(O.ALGO_CAS, threads=t)
         rows[f"boruvka_cas T={t}"] = {"ms": cas.elapsed_ms, "edges_per_s": m / (cas.elapsed_ms / 1e3),
                                       "rounds": cas.rounds}
     return {"value": m / (cas.elapsed_ms / 1e3), "unit": UNIT, "cores": hw, "kind": "reference",
@@ -223,12 +228,32 @@ def run_reference(args):
     n, src, dst, w = host_graph(cspec)
     m = int(src.size)
     threads = O.hardware_threads()
-    for _ in range(args.warmup):
-        O.ref_solve(n, src, dst, w, O.ALGO_CAS, threads=threads)
+    # One calibration run (it doubles as the first warm-up): if K + W runs of
+    # this sample would not end within the budget on this host, halve the
+    # sample (same generator family and seed) until they do, and say so.
+    runs = args.steps + args.warmup
+    rg = O.RefGraph(n, src, dst, w)  # the adapter (sort, collapse, build_graph) runs once, outside the runs
+    t0 = time.perf_counter()
+    rg.solve(O.ALGO_CAS, threads=threads)
+    cal_s = time.perf_counter() - t0
+    est = cal_s * runs
+    warm_done = 1
+    if est > REFERENCE_ARM_BUDGET_S and cspec is not spec:
+        shrink = int(np.ceil(np.log2(est / REFERENCE_ARM_BUDGET_S)))
+        cspec, sample = cpu_sample(spec, shrink)
+        sample += (f"; halved {shrink}x after a calibration run of {cal_s:.1f} s so that "
+                   f"{runs} runs fit ~{REFERENCE_ARM_BUDGET_S:.0f} s")
+        n, src, dst, w = host_graph(cspec)
+        m = int(src.size)
+        rg.close()
+        rg = O.RefGraph(n, src, dst, w)
+        warm_done = 0
+    for _ in range(max(0, args.warmup - warm_done)):
+        rg.solve(O.ALGO_CAS, threads=threads)
     times = []
     r = None
     for _ in range(args.steps):
-        r = O.ref_solve(n, src, dst, w, O.ALGO_CAS, threads=threads)
+        r = rg.solve(O.ALGO_CAS, threads=threads)
         times.append(r.elapsed_ms)
     ms = float(np.mean(times))
     value = m / (ms / 1e3)

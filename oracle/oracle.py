@@ -74,6 +74,12 @@ def _load_ref():
         lib.ref_generate_graph.argtypes = [_u32, ctypes.c_int, _u64, _vp, _vp, _vp, _u64p]
         lib.ref_solve.argtypes = [ctypes.c_int, ctypes.c_int, _u32, _u64, _vp, _vp, _vp, _vp,
                                   _u64p, _u64p, ctypes.POINTER(ctypes.c_double), _u32p, _u64p]
+        if hasattr(lib, "ref_prepare"):  # (a library built before the split has ref_solve only)
+            lib.ref_prepare.restype = ctypes.c_void_p
+            lib.ref_prepare.argtypes = [_u32, _u64, _vp, _vp, _vp, ctypes.POINTER(ctypes.c_int)]
+            lib.ref_run.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, _vp, _u64p, _u64p,
+                                    ctypes.POINTER(ctypes.c_double), _u32p, _u64p]
+            lib.ref_release.argtypes = [ctypes.c_void_p]
         lib.ref_save_generated.argtypes = [_u32, ctypes.c_int, _u64, ctypes.c_char_p]
         lib.ref_load_graph.argtypes = [ctypes.c_char_p, _u32p, _u64p, _vp, _vp, _vp, _u64]
         _ref = lib
@@ -220,6 +226,48 @@ def ref_solve(n: int, src, dst, w, algo: int = ALGO_KRUSKAL, threads: int = 1) -
         raise ValueError(f"ref_solve status {rc}: {lib.ref_last_error().decode()}")
     return OracleResult(ids[: cnt.value].copy(), int(tot.value), int(rounds.value), float(ms.value),
                         int(mp.value))
+
+
+class RefGraph:
+    """One input list through the §8(c) adapter, built once (sort, collapse,
+    the reference's build_graph) and solved any number of times by the
+    unchanged reference algorithms: the CPU legs of bench.py time several runs
+    of one sample, and the adapter is not part of any of them."""
+
+    def __init__(self, n: int, src, dst, w):
+        self._lib = _load_ref()
+        self.n = int(n)
+        self._h = None
+        self._arrays = None
+        if not hasattr(self._lib, "ref_prepare"):
+            self._arrays = _arrs(src, dst, w)  # old library: every solve re-runs the adapter
+            return
+        src, dst, w = _arrs(src, dst, w)
+        st = ctypes.c_int(0)
+        self._h = self._lib.ref_prepare(self.n, src.size, _p(src), _p(dst), _p(w), ctypes.byref(st))
+        if not self._h:
+            raise ValueError(f"ref_prepare status {st.value}: {self._lib.ref_last_error().decode()}")
+
+    def solve(self, algo: int = ALGO_KRUSKAL, threads: int = 1) -> OracleResult:
+        if self._h is None:
+            return ref_solve(self.n, *self._arrays, algo, threads)
+        ids = np.empty(max(self.n - 1, 1), dtype=np.uint32)
+        cnt, tot, mp = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        ms, rounds = ctypes.c_double(), ctypes.c_uint32()
+        rc = self._lib.ref_run(self._h, algo, threads, _p(ids), ctypes.byref(cnt), ctypes.byref(tot),
+                               ctypes.byref(ms), ctypes.byref(rounds), ctypes.byref(mp))
+        if rc:
+            raise ValueError(f"ref_run status {rc}: {self._lib.ref_last_error().decode()}")
+        return OracleResult(ids[: cnt.value].copy(), int(tot.value), int(rounds.value), float(ms.value),
+                            int(mp.value))
+
+    def close(self) -> None:
+        if self._h:
+            self._lib.ref_release(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
 
 
 def omp_max_threads() -> int:

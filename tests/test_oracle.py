@@ -77,6 +77,13 @@ def test_oracle_matches_reference_on_random_multigraphs(oracle_mod):
         assert np.array_equal(k.ids, r.ids) and k.total_weight == r.total_weight
         c = oracle_mod.ref_solve(n, src, dst, w, oracle_mod.ALGO_CAS, threads=3)
         assert np.array_equal(c.ids, r.ids)
+        # the adapter built once, solved repeatedly (bench.py's CPU legs)
+        rg = oracle_mod.RefGraph(n, src, dst, w)
+        for algo, t in ((oracle_mod.ALGO_KRUSKAL, 1), (oracle_mod.ALGO_SEQ, 1), (oracle_mod.ALGO_CAS, 2),
+                        (oracle_mod.ALGO_CAS, 4)):
+            x = rg.solve(algo, threads=t)
+            assert np.array_equal(x.ids, r.ids) and x.total_weight == r.total_weight and x.m_prime == r.m_prime
+        rg.close()
 
 
 def test_min_edges_table(oracle_mod):
