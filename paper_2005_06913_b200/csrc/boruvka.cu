@@ -458,6 +458,7 @@ struct RunOut {
   double ms_hot = 0;
   uint32_t hot_launches = 0;
   uint64_t hot_bytes = 0;
+  uint32_t phase_end = 0;  // Filter-Boruvka: the first round past the light phase (0: the plain loop)
   DevCounters ctr{};
 };
 
@@ -1233,6 +1234,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   const int stop = (int)c.stop_round;
   if (c.stop_round == kNoStop) throw MstError{MST_ERR_STALL, "round loop ended without a stop verdict"};
   out.rounds = (uint32_t)stop - 1;
+  out.phase_end = (uint32_t)phase_end;
   out.final_components = c.n[stop];
   out.count = (uint64_t)n - out.final_components;
   out.total_weight = c.total_weight;
@@ -1270,12 +1272,21 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   }
 }
 
-uint64_t alg_bytes_from(const DevCounters& c, uint32_t rounds) {
-  // 12 m + 32 sum k_r + 32 sum n_r.
-  uint64_t b = 12ull * c.m[1];
-  for (uint32_t r = 1; r <= rounds; ++r) {
-    b += 32ull * c.n[r];
-    if (r + 1 <= rounds) b += 32ull * c.m[r + 1];
+uint64_t alg_bytes_from(const DevCounters& c, uint32_t rounds, uint32_t phase_end) {
+  // SURVEY.md §8(d)'s units: 12 B per caller edge read, 16 B per packed edge
+  // read, 16 B per kept edge written, 32 B per live component.
+  // Plain loop: 12 m + 32 sum k_r + 32 sum n_r (its formula).
+  // Filter-Boruvka: the caller's list is streamed twice (split, heavy
+  // filter: 2 x 12 m[0]) and every round list m[r] -- the split's output,
+  // each emit's, the heavy survivors' -- is written once and read once.
+  uint64_t b = 0;
+  for (uint32_t r = 1; r <= rounds; ++r) b += 32ull * c.n[r];
+  if (phase_end == 0) {
+    b += 12ull * c.m[1];
+    for (uint32_t r = 2; r <= rounds; ++r) b += 32ull * c.m[r];
+  } else {
+    b += 24ull * c.m[0];
+    for (uint32_t r = 1; r <= rounds; ++r) b += 32ull * c.m[r];
   }
   return b;
 }
@@ -1284,7 +1295,7 @@ void fill_stats(mst_stats_t* st, const RunOut& o) {
   if (!st) return;
   st->rounds = o.rounds;
   st->final_components = o.final_components;
-  st->alg_bytes = alg_bytes_from(o.ctr, o.rounds);
+  st->alg_bytes = alg_bytes_from(o.ctr, o.rounds, o.phase_end);
   for (int r = 0; r < MST_MAX_ROUNDS; ++r) {
     const bool live = (uint32_t)(r + 1) <= o.rounds;
     st->live_edges[r] = live ? o.ctr.m[r + 1] : 0;
@@ -1903,6 +1914,7 @@ void run_sharded_rounds(std::vector<Shard>& sh, Exchanger& ex, uint32_t n, uint6
   if (c.stop_round == kNoStop) throw MstError{MST_ERR_STALL, "sharded loop ended without a stop verdict"};
   const int stop = (int)c.stop_round;
   out.rounds = (uint32_t)stop - 1;
+  out.phase_end = (uint32_t)R1;
   out.final_components = c.n[stop];
   out.count = (uint64_t)n - out.final_components;
   out.total_weight = c.total_weight;
@@ -2394,7 +2406,7 @@ int mst_gpu_boruvka_device(const mst_edges_soa_t* edges, uint32_t* d_out_ids, vo
     if (ms_hot) *ms_hot = o.ms_hot;
     if (hot_launches) *hot_launches = o.hot_launches;
     if (stats) stats->hot_bytes = o.hot_bytes;
-    if (stats) stats->alg_bytes = alg_bytes_from(o.ctr, o.rounds);
+    if (stats) stats->alg_bytes = alg_bytes_from(o.ctr, o.rounds, o.phase_end);
     return finish_status(o, out_count, out_total_weight);
   });
 }
