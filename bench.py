@@ -91,7 +91,37 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
 
+    _NVML_BITS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+                  0x4: "sw_power_cap"}
+
+    def _run_nvml(self) -> bool:
+        """NVML directly (one sample per ~10 ms; an nvidia-smi process takes
+        ~0.5 s, longer than a short timed region). False when unavailable."""
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            get_reasons = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                N.nvmlDeviceGetCurrentClocksThrottleReasons
+            get_reasons(h)
+        except Exception:
+            return False
+        while not self._stop.is_set():
+            try:
+                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                bits = int(get_reasons(h))
+                names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+                active = {v for b, v in self._NVML_BITS.items() if bits & b}
+                self.samples.append([str(sm), str(mx)] + ["Active" if nm in active else "Not Active" for nm in names])
+            except Exception:
+                pass
+            self._stop.wait(0.01)
+        return True
+
     def _run(self):
+        if self._run_nvml():
+            return
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
