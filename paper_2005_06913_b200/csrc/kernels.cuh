@@ -12,13 +12,19 @@
 //                        halving over the hook forest (the reference's find
 //                        walk, union_find.cpp:28-35), dense relabel, clears
 //                        the next min table.
-//   k_count       (m_r)  relabels both endpoints, drops intra-component
-//                        edges (the covered flags, graph.hpp:62-67), counts
-//                        the kept edges per tile.
-//   k_emit        (m_r)  writes the kept edges in order and offers each to
-//                        both endpoint components of round r+1 with a
-//                        filtered 64-bit atomicMin (the edge scan + offer,
-//                        boruvka_parallel.cpp:150-167).
+//   k_count       (m_r)  relabels both endpoints in place, drops
+//                        intra-component edges (the covered flags,
+//                        graph.hpp:62-67), counts the kept edges per tile and
+//                        offers each kept edge to both endpoint components of
+//                        round r+1 with a filtered 64-bit atomicMin keyed by
+//                        its position in this list (the edge scan + offer,
+//                        boruvka_parallel.cpp:150-167). The caller's list is
+//                        walked in interleaved segments (MST_INTERLEAVE).
+//   k_emit        (m_r)  writes the kept edges in order (a pure copy). The
+//                        light split and the heavy filter stage their sparse
+//                        survivors per tile instead (k_emit_sparse copies
+//                        them) and make their offers in range passes over
+//                        L2-sized table slices (k_range_offers).
 //
 // Round 1 reads the caller's edge list directly (k_min_round1 + the count
 // pass over the original view; in the plain loop its label pairs are round
