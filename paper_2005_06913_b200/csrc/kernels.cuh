@@ -1941,8 +1941,8 @@ __device__ __forceinline__ void offer_batch(unsigned long long* table, const uin
   unsigned long long cx[kItems], cy[kItems];
 #pragma unroll
   for (int k = 0; k < kItems; ++k) {
-    cx[k] = f[k] ? __ldcg(table + e[k].x) : 0ull;
-    cy[k] = f[k] ? __ldcg(table + e[k].y) : 0ull;
+    cx[k] = f[k] ? __ldca(table + e[k].x) : 0ull;
+    cy[k] = f[k] ? __ldca(table + e[k].y) : 0ull;
   }
 #pragma unroll
   for (int k = 0; k < kItems; ++k) {
@@ -2201,7 +2201,7 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
         for (int k = 0; k < kItems; ++k) {
           const uint32_t c = base + k * kBlock + threadIdx.x;
           const uint32_t o = (e[k].x == c) ? e[k].y : e[k].x;
-          okey[k] = key[k] != kNoKey ? __ldcg(mcur + o) : kNoKey;
+          okey[k] = key[k] != kNoKey ? __ldca(mcur + o) : kNoKey;
         }
         unsigned bal[kItems];
 #pragma unroll
@@ -2310,7 +2310,7 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
       for (int k = 0; k < kItems; ++k) {
         if (!v[k]) continue;
         const uint32_t x = isroot[k] ? c[k] : root[k], w = x >> 5;
-        a.L[c[k]] = s_bpre[x / cs] + __ldcg(a.wpref + w) + __popc(__ldcg(a.masks + w) & ((1u << (x & 31)) - 1u));
+        a.L[c[k]] = s_bpre[x / cs] + __ldca(a.wpref + w) + __popc(__ldca(a.masks + w) & ((1u << (x & 31)) - 1u));
         if (c[k] < n_next) mnext[c[k]] = kNoKey;
       }
     }
@@ -2326,7 +2326,7 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
         for (int k = 0; k < 4; ++k) x[k] = base + k * kBlock < n_entry ? __ldcg(a.M + base + k * kBlock) : 0u;
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          if (base + k * kBlock < n_entry) x[k] = __ldcg(a.L + x[k]);
+          if (base + k * kBlock < n_entry) x[k] = __ldca(a.L + x[k]);
 #pragma unroll
         for (int k = 0; k < 4; ++k)
           if (base + k * kBlock < n_entry) a.M[base + k * kBlock] = x[k];
@@ -2355,8 +2355,8 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
           const uint64_t i = base + k * 32 + lane;
-          x[k] = i < seg_lo + seg_len ? __ldcg(a.L + e[k].x) : 0u;
-          y[k] = i < seg_lo + seg_len ? __ldcg(a.L + e[k].y) : 0u;
+          x[k] = i < seg_lo + seg_len ? __ldca(a.L + e[k].x) : 0u;
+          y[k] = i < seg_lo + seg_len ? __ldca(a.L + e[k].y) : 0u;
         }
         unsigned long long pw[kItems], key[kItems];
         bool v[kItems];
@@ -2416,8 +2416,8 @@ __global__ void __launch_bounds__(kBlock, MST_TAIL_MINB) k_tail(TailArgs a) {
 #pragma unroll
           for (int k = 0; k < kItems; ++k) {
             if (live[k]) {
-              e[k].x = __ldcg(a.L + e[k].x);
-              e[k].y = __ldcg(a.L + e[k].y);
+              e[k].x = __ldca(a.L + e[k].x);
+              e[k].y = __ldca(a.L + e[k].y);
             }
           }
         }
