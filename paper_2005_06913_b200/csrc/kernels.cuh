@@ -396,7 +396,10 @@ __device__ __forceinline__ void find_roots(uint32_t* parent, const uint32_t (&c)
   while (true) {
     uint32_t gp[kU];
 #pragma unroll
-    for (int k = 0; k < kU; ++k) gp[k] = (live[k] && px[k] != x[k]) ? __ldcg(parent + px[k]) : px[k];
+    // through L1: the roots' entries are read by every walk that ends there
+    // (the giant's root: millions of reads of one line, which serialise on
+    // its L2 slice with ld.cg). A stale line only shows an older ancestor.
+    for (int k = 0; k < kU; ++k) gp[k] = (live[k] && px[k] != x[k]) ? __ldca(parent + px[k]) : px[k];
     bool any = false;
 #pragma unroll
     for (int k = 0; k < kU; ++k) {
@@ -416,7 +419,7 @@ __device__ __forceinline__ void find_roots(uint32_t* parent, const uint32_t (&c)
     if (!any) break;
 #pragma unroll
     for (int k = 0; k < kU; ++k)
-      if (live[k]) px[k] = __ldcg(parent + x[k]);
+      if (live[k]) px[k] = __ldca(parent + x[k]);
   }
 }
 
@@ -891,11 +894,13 @@ __device__ __forceinline__ void dedup_insert(uint4* __restrict__ E, const uint32
       const unsigned long long key = ((unsigned long long)e[k].z << 32) | (uint32_t)i;
       unsigned long long h = pair_hash(pair) & mask;
       for (int probe = 0; probe < kPairProbes; ++probe) {
-        const unsigned long long cur = __ldcg(t.pairs + 2 * h);
+        // through L1 (hot pairs: the giant's): a claimed slot never changes, a
+        // stale empty one is settled by the CAS, a stale key only costs an atomic
+        const unsigned long long cur = __ldca(t.pairs + 2 * h);
         const unsigned long long got = cur == pair ? pair : atomicCAS(t.pairs + 2 * h, kNoPair, pair);
         if (got == kNoPair || got == pair) {
           fresh += got == kNoPair;
-          if (key < __ldcg(t.pairs + 2 * h + 1)) atomicMin(t.pairs + 2 * h + 1, key);
+          if (key < __ldca(t.pairs + 2 * h + 1)) atomicMin(t.pairs + 2 * h + 1, key);
           break;
         }
         h = (h + 1) & mask;  // a failed insert keeps the edge (see pair_keep)
@@ -914,7 +919,7 @@ __device__ __forceinline__ bool pair_keep(const PairTable& t, unsigned long long
   const unsigned long long pair = ((unsigned long long)min(x, y) << 32) | max(x, y);
   unsigned long long h = pair_hash(pair) & mask;
   for (int probe = 0; probe < kPairProbes; ++probe) {
-    const ulonglong2 slot = __ldcg(reinterpret_cast<const ulonglong2*>(t.pairs) + h);
+    const ulonglong2 slot = __ldca(reinterpret_cast<const ulonglong2*>(t.pairs) + h);  // read-only in this pass
     const unsigned long long cur = slot.x;
     if (cur == pair) return key <= slot.y;
     if (cur == kNoPair) return true;
