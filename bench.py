@@ -94,33 +94,43 @@ class ClockSampler:
     _NVML_BITS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
                   0x4: "sw_power_cap"}
 
-    def _run_nvml(self) -> bool:
+    def _nvml_open(self) -> bool:
         """NVML directly (one sample per ~10 ms; an nvidia-smi process takes
-        ~0.5 s, longer than a short timed region). False when unavailable."""
+        ~0.5 s, longer than a short timed region). Opened in __enter__, before
+        the timed region, so that even a few-millisecond region is sampled."""
         try:
             import pynvml as N
             N.nvmlInit()
-            h = N.nvmlDeviceGetHandleByIndex(self.index)
-            mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
-            get_reasons = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            self._N = N
+            self._h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self._mx = N.nvmlDeviceGetMaxClockInfo(self._h, N.NVML_CLOCK_SM)
+            self._reasons = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
                 N.nvmlDeviceGetCurrentClocksThrottleReasons
-            get_reasons(h)
+            self._reasons(self._h)
+            return True
         except Exception:
+            self._N = None
             return False
-        while not self._stop.is_set():
-            try:
-                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
-                bits = int(get_reasons(h))
-                names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-                active = {v for b, v in self._NVML_BITS.items() if bits & b}
-                self.samples.append([str(sm), str(mx)] + ["Active" if nm in active else "Not Active" for nm in names])
-            except Exception:
-                pass
-            self._stop.wait(0.01)
-        return True
+
+    def sample_now(self) -> None:
+        """One NVML sample from the calling thread (bench.py calls it with the
+        timed steps enqueued and the GPU busy)."""
+        if getattr(self, "_N", None) is None:
+            return
+        try:
+            sm = self._N.nvmlDeviceGetClockInfo(self._h, self._N.NVML_CLOCK_SM)
+            bits = int(self._reasons(self._h))
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            active = {v for b, v in self._NVML_BITS.items() if bits & b}
+            self.samples.append([str(sm), str(self._mx)] + ["Active" if nm in active else "Not Active" for nm in names])
+        except Exception:
+            pass
 
     def _run(self):
-        if self._run_nvml():
+        if getattr(self, "_N", None) is not None:
+            while not self._stop.is_set():
+                self.sample_now()
+                self._stop.wait(0.01)
             return
         while not self._stop.is_set():
             try:
@@ -134,6 +144,7 @@ class ClockSampler:
             self._stop.wait(0.1)
 
     def __enter__(self):
+        self._nvml_open()
         self._t.start()
         return self
 
@@ -369,6 +380,7 @@ def run_ours(args):
                 hot_launch += hot["launches"]
                 hot_b += hot["bytes"]
             launches += info.kernel_launches
+            clk.sample_now()  # this step's kernels are enqueued or running
         barrier()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     t_local = float(np.sum(step_ms))
