@@ -827,7 +827,7 @@ void run_single_impl(Workspace& ws, InView in, const uint32_t* wbase, uint32_t w
   // stream operations cost c1 ~20 us before its first kernel)
   uint32_t* flags = ws.get<uint32_t>("mst_bits", mst_out_words(m));
   const int mst_bytes = mst_out_bytes(m) ? 1 : 0;
-  launch_k(k_init_run, (unsigned)(sm_count(dev) * 4), 256, s, d_ctr, n, m, minb[0], (uint4*)flags, mst_out_words(m) / 4);
+  launch_k(k_init_run, (unsigned)(sm_count(dev) * 8), 256, s, d_ctr, n, m, minb[0], (uint4*)flags, mst_out_words(m) / 4);
   timeline_mark(nullptr, s);
   uint32_t launches = 0;
   int tix = 0;

@@ -2510,7 +2510,10 @@ __global__ void k_init_run(DevCounters* ctr, uint32_t n, uint64_t m, unsigned lo
     }
   }
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = tid; i < n; i += stride) minb0[i] = kNoKey;
+  // 16 B stores (the table comes from cudaMalloc: 256 B aligned)
+  ulonglong2* m2 = reinterpret_cast<ulonglong2*>(minb0);
+  for (uint64_t i = tid; i < n / 2; i += stride) m2[i] = make_ulonglong2(kNoKey, kNoKey);
+  if (tid == 0 && (n & 1u)) minb0[n - 1] = kNoKey;
   for (uint64_t i = tid; i < bit_vecs; i += stride) bits16[i] = make_uint4(0, 0, 0, 0);
 }
 
